@@ -1,0 +1,350 @@
+// ref_driver: test infrastructure only (never shipped, never on the product
+// path). Links the UNMODIFIED reference core built by oracle/Makefile from
+// /root/reference sources and drives it through its public API, mirroring the
+// reference's own timing harness `measure_distance_phase`
+// (proj/core/src/cli.cpp:308-350) and the server steps 3 and 8 of `run_round`
+// (proj/core/src/protocol.cpp:430-432, 492-493).
+//
+//   ref_driver gen   <options> --out DIR   dump keys, inputs, outputs, counters
+//   ref_driver bench <options> --reps R    time build_distance_matrix + masked_aggregate
+//
+// Options: --N --depth --clients --dim --k --seed --rule krum|multi_krum|median
+//          --select i,j,... --secure 0|1 --lazy 0|1 --inter 0|1
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <fstream>
+#include <map>
+#include <sstream>
+#include <string>
+#include <vector>
+
+#include "lancelot/aggregation.hpp"
+#include "lancelot/ckks.hpp"
+#include "lancelot/distance.hpp"
+#include "lancelot/threading.hpp"
+
+using namespace lancelot;
+
+namespace {
+
+struct Opts {
+  std::string cmd;
+  std::size_t N = 256;
+  int depth = 3;
+  std::size_t clients = 4;
+  std::size_t dim = 300;
+  std::size_t k = 1;
+  u64 seed = 1;
+  std::string rule = "krum";
+  std::vector<std::size_t> select{0};
+  bool secure = false;
+  bool lazy = true;
+  bool inter = true;
+  std::size_t reps = 3;
+  std::string out = ".";
+};
+
+Opts parse(int argc, char** argv) {
+  Opts o;
+  if (argc < 2) throw std::runtime_error("usage: ref_driver gen|bench [opts]");
+  o.cmd = argv[1];
+  for (int i = 2; i + 1 < argc; i += 2) {
+    std::string k = argv[i], v = argv[i + 1];
+    if (k == "--N") o.N = std::stoull(v);
+    else if (k == "--depth") o.depth = std::stoi(v);
+    else if (k == "--clients") o.clients = std::stoull(v);
+    else if (k == "--dim") o.dim = std::stoull(v);
+    else if (k == "--k") o.k = std::stoull(v);
+    else if (k == "--seed") o.seed = std::stoull(v);
+    else if (k == "--rule") o.rule = v;
+    else if (k == "--secure") o.secure = v == "1";
+    else if (k == "--lazy") o.lazy = v == "1";
+    else if (k == "--inter") o.inter = v == "1";
+    else if (k == "--reps") o.reps = std::stoull(v);
+    else if (k == "--out") o.out = v;
+    else if (k == "--select") {
+      o.select.clear();
+      std::stringstream ss(v);
+      std::string t;
+      while (std::getline(ss, t, ',')) o.select.push_back(std::stoull(t));
+    } else {
+      throw std::runtime_error("unknown option " + k);
+    }
+  }
+  return o;
+}
+
+void dump_poly(std::ofstream& f, const PolyRns& p) {
+  for (std::size_t r = 0; r < p.row_count(); ++r) {
+    f.write(reinterpret_cast<const char*>(p.row(r).data()),
+            static_cast<std::streamsize>(p.row(r).size() * sizeof(u64)));
+  }
+}
+
+void dump_ct(const std::string& path, const std::vector<const Ciphertext*>& cts) {
+  std::ofstream f(path, std::ios::binary);
+  for (const Ciphertext* c : cts) {
+    dump_poly(f, c->c0);
+    dump_poly(f, c->c1);
+  }
+}
+
+void dump_ternary(const std::string& path, const TernaryCiphertext& t) {
+  std::ofstream f(path, std::ios::binary);
+  dump_poly(f, t.d0);
+  dump_poly(f, t.d1);
+  dump_poly(f, t.d2);
+}
+
+void dump_key(const std::string& path, const KeySwitchKey& k) {
+  std::ofstream f(path, std::ios::binary);
+  for (const auto& d : k.digits) {
+    dump_poly(f, d.first);
+    dump_poly(f, d.second);
+  }
+}
+
+std::string counts_json(const OpCounts& c) {
+  char buf[512];
+  std::snprintf(buf, sizeof buf,
+                "{\"encryptions\": %llu, \"additions\": %llu, \"multiplications\": %llu, "
+                "\"relinearizations\": %llu, \"rescales\": %llu, \"rotations\": %llu, "
+                "\"mod_ups\": %llu}",
+                (unsigned long long)c.encryptions, (unsigned long long)c.additions,
+                (unsigned long long)c.multiplications,
+                (unsigned long long)c.relinearizations,
+                (unsigned long long)c.rescales, (unsigned long long)c.rotations,
+                (unsigned long long)c.mod_ups);
+  return buf;
+}
+
+std::string dbl(double v) {
+  char buf[64];
+  std::snprintf(buf, sizeof buf, "%.17g", v);
+  return buf;
+}
+
+SelectionRule rule_of(const std::string& s) {
+  if (s == "krum") return SelectionRule::krum;
+  if (s == "multi_krum") return SelectionRule::multi_krum;
+  if (s == "median") return SelectionRule::median;
+  throw std::runtime_error("bad rule");
+}
+
+struct System {
+  std::unique_ptr<CkksContext> ctx;
+  HoistPlan plan;
+  KeyBundle keys;
+  std::vector<std::size_t> steps;
+  std::vector<PackedWeights> packed;
+  SelectionMask mask;
+};
+
+System setup(const Opts& o) {
+  System s;
+  CkksParams p;
+  p.ring_degree = o.N;
+  p.depth = o.depth;
+  p.security = o.secure ? SecurityLevel::bits128 : SecurityLevel::none;
+  s.ctx = std::make_unique<CkksContext>(p);
+  const CkksContext& ctx = *s.ctx;
+  const std::size_t width = std::bit_ceil(std::min(o.dim, ctx.slot_count()));
+  // make_system with a fixed unfold factor (protocol.cpp:255-287).
+  s.plan = fixed_plan(HoistMode::off, width);
+  s.plan.k = o.k;
+  s.steps = slot_reduce_steps(width, o.k);
+  Sampler key_rng(derive_seed(o.seed, 5));
+  s.keys = ctx.generate_keys(key_rng, s.steps);
+  // measure_distance_phase input generation (cli.cpp:316-329).
+  Sampler rng(derive_seed(o.seed, 0xAB1A7Eu));
+  s.packed.resize(o.clients);
+  for (std::size_t i = 0; i < o.clients; ++i) {
+    std::vector<double> w(o.dim);
+    for (double& x : w) x = rng.uniform_real() - 0.5;
+    s.packed[i] = pack_and_encrypt(ctx, w, s.keys.pk, rng);
+  }
+  SelectionResult sel{rule_of(o.rule), o.select, o.select.size()};
+  Sampler mask_rng(derive_seed(o.seed, 0x3000000000000000ull));
+  s.mask = build_mask(ctx, sel, o.clients, s.keys.pk, mask_rng);
+  return s;
+}
+
+int cmd_gen(const Opts& o) {
+  System s = setup(o);
+  const CkksContext& ctx = *s.ctx;
+  const std::string d = o.out;
+  {
+    std::ofstream f(d + "/sk.bin", std::ios::binary);
+    dump_poly(f, s.keys.sk.s);
+  }
+  dump_key(d + "/relin.bin", s.keys.relin.key);
+  for (const auto& [step, key] : s.keys.rotations.steps) {
+    dump_key(d + "/rot_" + std::to_string(step) + ".bin", key);
+  }
+  for (std::size_t i = 0; i < o.clients; ++i) {
+    std::vector<const Ciphertext*> v;
+    for (const auto& c : s.packed[i].chunks) v.push_back(&c);
+    dump_ct(d + "/client_" + std::to_string(i) + ".bin", v);
+    dump_ct(d + "/sel_" + std::to_string(i) + ".bin", {&s.mask.client_selectors[i]});
+  }
+
+  DistanceOptions dopt;
+  dopt.lazy_relin = o.lazy;
+  dopt.reduce_on_server = true;
+  ctx.counters().reset();
+  const EncryptedDistanceMatrix m =
+      build_distance_matrix(ctx, s.packed, s.keys.relin, s.plan,
+                            DistanceMode::per_pair, s.keys.rotations, dopt);
+  const OpCounts dist_ops = ctx.counters().snapshot();
+  ctx.counters().reset();
+  const PackedWeights agg =
+      masked_aggregate(ctx, s.packed, s.mask, rule_of(o.rule), s.keys.relin);
+  const OpCounts agg_ops = ctx.counters().snapshot();
+
+  std::ostringstream js;
+  js << "{\n";
+  const RnsBasis& b = *ctx.basis();
+  js << "  \"N\": " << o.N << ", \"depth\": " << o.depth << ", \"slots\": "
+     << ctx.slot_count() << ",\n";
+  js << "  \"primes\": [";
+  for (std::size_t i = 0; i < b.prime_count(); ++i) js << (i ? ", " : "") << b.prime(i).value;
+  js << "], \"special\": " << b.special().value << ",\n";
+  js << "  \"psi\": [";
+  for (std::size_t i = 0; i <= b.prime_count(); ++i)
+    js << (i ? ", " : "") << b.tables_or_special(i).psi;
+  js << "],\n";
+  js << "  \"width\": " << s.plan.n << ", \"k\": " << s.plan.k << ", \"steps\": [";
+  for (std::size_t i = 0; i < s.steps.size(); ++i) js << (i ? ", " : "") << s.steps[i];
+  js << "],\n  \"rot_keys\": [";
+  {
+    bool first = true;
+    for (const auto& [step, key] : s.keys.rotations.steps) {
+      js << (first ? "" : ", ") << step;
+      first = false;
+    }
+  }
+  js << "],\n";
+  js << "  \"chunks\": " << s.packed[0].chunk_count() << ", \"client_scale\": "
+     << dbl(s.packed[0].chunks[0].scale) << ", \"client_level\": "
+     << s.packed[0].chunks[0].level() << ",\n";
+  js << "  \"dist_ops\": " << counts_json(dist_ops) << ",\n";
+  js << "  \"agg_ops\": " << counts_json(agg_ops) << ",\n";
+
+  // Outputs.
+  js << "  \"dist\": [";
+  bool first = true;
+  for (const auto& [key, ct] : m.entries) {
+    dump_ct(d + "/dist_" + std::to_string(key.first) + "_" + std::to_string(key.second) + ".bin",
+            {&ct});
+    const auto slots = ctx.decrypt_values(ct, s.keys.sk);
+    js << (first ? "" : ", ") << "{\"i\": " << key.first << ", \"j\": " << key.second
+       << ", \"level\": " << ct.level() << ", \"scale\": " << dbl(ct.scale)
+       << ", \"slot0\": " << dbl(slots[0]) << "}";
+    first = false;
+  }
+  js << "],\n";
+  {
+    std::vector<const Ciphertext*> v;
+    for (const auto& c : agg.chunks) v.push_back(&c);
+    dump_ct(d + "/agg.bin", v);
+    const std::vector<double> w = decrypt_weights(ctx, agg, s.keys.sk);
+    js << "  \"agg_level\": " << agg.chunks[0].level() << ", \"agg_scale\": "
+       << dbl(agg.chunks[0].scale) << ", \"agg_head\": [";
+    for (std::size_t i = 0; i < std::min<std::size_t>(8, w.size()); ++i)
+      js << (i ? ", " : "") << dbl(w[i]);
+    js << "],\n";
+  }
+  // Plaintext oracle for the distances (cli input generation replayed).
+  {
+    Sampler rng(derive_seed(o.seed, 0xAB1A7Eu));
+    std::vector<std::vector<double>> ws(o.clients);
+    // Replay is not possible without re-encrypting (the stream is shared), so
+    // the plaintext weights are recovered by decryption instead.
+    js << "  \"plain_dist\": [";
+    for (std::size_t i = 0; i < o.clients; ++i) ws[i] = decrypt_weights(ctx, s.packed[i], s.keys.sk);
+    bool f2 = true;
+    for (std::size_t i = 0; i < o.clients; ++i)
+      for (std::size_t j = i + 1; j < o.clients; ++j) {
+        double acc = 0;
+        for (std::size_t t = 0; t < o.dim; ++t) acc += (ws[i][t] - ws[j][t]) * (ws[i][t] - ws[j][t]);
+        js << (f2 ? "" : ", ") << dbl(acc);
+        f2 = false;
+      }
+    js << "]";
+  }
+
+  if (o.inter) {
+    // Intermediates of pair (0,1): the lazy ternary accumulator, relin, rescale
+    // and every hoisted / iterative rotation of slot_reduce.
+    const PackedWeights& a = s.packed[0];
+    const PackedWeights& bb = s.packed[1];
+    TernaryCiphertext acc = ctx.hsquare(ctx.hsub(a.chunks[0], bb.chunks[0]));
+    for (std::size_t c = 1; c < a.chunk_count(); ++c)
+      ctx.lazy_accumulate(acc, ctx.hsquare(ctx.hsub(a.chunks[c], bb.chunks[c])));
+    dump_ternary(d + "/p01_acc.bin", acc);
+    const Ciphertext rl = ctx.relinearize(acc, s.keys.relin);
+    dump_ct(d + "/p01_relin.bin", {&rl});
+    const Ciphertext rs = ctx.rescale(rl);
+    dump_ct(d + "/p01_rescale.bin", {&rs});
+    // Each rotation key applied once to the rescaled ciphertext.
+    for (const auto& [step, key] : s.keys.rotations.steps) {
+      const Ciphertext r = ctx.rotate(rs, step, s.keys.rotations);
+      dump_ct(d + "/p01_rot_" + std::to_string(step) + ".bin", {&r});
+    }
+    // Aggregate chunk 0 pieces.
+    TernaryCiphertext t = ctx.hmult_triple(s.packed[0].chunks[0], s.mask.client_selectors[0]);
+    for (std::size_t i = 1; i < o.clients; ++i)
+      ctx.lazy_accumulate(t, ctx.hmult_triple(s.packed[i].chunks[0], s.mask.client_selectors[i]));
+    dump_ternary(d + "/agg0_acc.bin", t);
+  }
+  js << "\n}\n";
+  std::ofstream(d + "/meta.json") << js.str();
+  return 0;
+}
+
+int cmd_bench(const Opts& o) {
+  const auto t0 = std::chrono::steady_clock::now();
+  System s = setup(o);
+  const double setup_s =
+      std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  const CkksContext& ctx = *s.ctx;
+  DistanceOptions dopt;
+  dopt.lazy_relin = o.lazy;
+  dopt.reduce_on_server = true;
+  std::printf("{\"setup_s\": %.3f, \"threads\": %zu, \"reps\": [", setup_s, worker_count());
+  for (std::size_t r = 0; r < o.reps; ++r) {
+    const auto a = std::chrono::steady_clock::now();
+    const EncryptedDistanceMatrix m =
+        build_distance_matrix(ctx, s.packed, s.keys.relin, s.plan,
+                              DistanceMode::per_pair, s.keys.rotations, dopt);
+    const auto b = std::chrono::steady_clock::now();
+    const PackedWeights agg =
+        masked_aggregate(ctx, s.packed, s.mask, rule_of(o.rule), s.keys.relin);
+    const auto c = std::chrono::steady_clock::now();
+    std::printf("%s{\"distance_s\": %.6f, \"aggregate_s\": %.6f}", r ? ", " : "",
+                std::chrono::duration<double>(b - a).count(),
+                std::chrono::duration<double>(c - b).count());
+    std::fflush(stdout);
+    (void)m;
+    (void)agg;
+  }
+  std::printf("]}\n");
+  return 0;
+}
+
+}  // namespace
+
+int main(int argc, char** argv) {
+  try {
+    const Opts o = parse(argc, argv);
+    if (o.cmd == "gen") return cmd_gen(o);
+    if (o.cmd == "bench") return cmd_bench(o);
+    std::fprintf(stderr, "unknown command %s\n", o.cmd.c_str());
+    return 2;
+  } catch (const std::exception& e) {
+    std::fprintf(stderr, "error: %s\n", e.what());
+    return 1;
+  }
+}
