@@ -1,0 +1,158 @@
+/*
+ * lancelot_b200.h — C-ABI of the B200-native Lancelot server path.
+ *
+ * Drop-in boundary for the server half of Lancelot (arXiv 2408.06197): the
+ * encrypted pairwise squared-distance matrix and the encrypted masked
+ * aggregate, plus the CKKS evaluator primitives they are built from. Every
+ * entry point replaces one function of the reference C++ API (paths relative
+ * to /root/reference/proj/core) and is bit-exact with it:
+ *
+ *   lcl_context_create       CkksContext::CkksContext + make_basis     ckks.cpp:77-93, 164-167
+ *   lcl_upload_*_key         KeyBundle relin / rotation keys           ckks.hpp:73-97
+ *   lcl_ntt_forward/inverse  PolyRns::ntt_forward / ntt_inverse        rns.cpp:282-302
+ *   lcl_hadd / lcl_hsub      CkksContext::hadd / hsub                  ckks.cpp:395-415
+ *   lcl_relinearize          CkksContext::relinearize                  ckks.cpp:522-534
+ *   lcl_rescale              CkksContext::rescale                      ckks.cpp:536-547
+ *   lcl_rotate               CkksContext::rotate                       ckks.cpp:560-580
+ *   lcl_hoisted_rotations    CkksContext::hoisted_rotations            ckks.cpp:582-612
+ *   lcl_slot_reduce          slot_reduce                               distance.cpp:214-240
+ *   lcl_pairwise_distance    encrypted_pairwise_distance               distance.cpp:107-142
+ *   lcl_distance_matrix      build_distance_matrix (per_pair)          distance.cpp:242-300
+ *   lcl_masked_aggregate     masked_aggregate                          aggregation.cpp:188-229
+ *   lcl_get_counts           OpCounters::snapshot                      ckks.cpp:134-156
+ *
+ * Conventions
+ *   - Plain pointers and sizes only. Buffers named d_* are DEVICE pointers on
+ *     the context's device; h_* are host pointers.
+ *   - Layouts are the reference's (LCLT-compatible): little-endian u64,
+ *     limb-major. A ciphertext at `count` live q-limbs is [2][count][N]
+ *     (c0 rows then c1 rows); a ternary is [3][count][N]; a switch key is
+ *     [full][2][full+1][N] (digit j: k0 rows then k1 rows, special row last).
+ *     Client weights are [n][chunks][2][full][N]; selectors [n][2][full][N].
+ *   - Every call returns an lcl_status; the codes map 1:1 onto the reference
+ *     exception types (errors.hpp:27-104). lcl_last_error() gives the message.
+ *   - Work is enqueued on the context's stream (lcl_set_stream; default: the
+ *     legacy default stream) and is asynchronous unless stated otherwise.
+ *   - Op counters advance exactly as the reference's OpCounters do.
+ *   - There is no CPU fallback: without a CUDA device every compute call
+ *     fails with LCL_CUDA_ERROR.
+ */
+#ifndef LANCELOT_B200_H
+#define LANCELOT_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  LCL_OK = 0,
+  LCL_PARAMETER_ERROR = 1,  /* ParameterError      */
+  LCL_BASIS_MISMATCH = 2,   /* BasisMismatchError  */
+  LCL_DOMAIN_ERROR = 3,     /* DomainError         */
+  LCL_ALIGNMENT_ERROR = 4,  /* AlignmentError      */
+  LCL_KEY_ERROR = 5,        /* KeyError            */
+  LCL_DEPTH_EXHAUSTED = 6,  /* DepthExhaustedError */
+  LCL_CAPACITY_ERROR = 7,   /* CapacityError       */
+  LCL_SHAPE_ERROR = 8,      /* ShapeError          */
+  LCL_WIDTH_ERROR = 9,      /* WidthError          */
+  LCL_INFEASIBLE_ERROR = 10,/* InfeasibleError     */
+  LCL_DATA_ERROR = 11,      /* DataError           */
+  LCL_USAGE_ERROR = 12,     /* UsageError          */
+  LCL_CUDA_ERROR = 100      /* device failure (no reference counterpart) */
+} lcl_status;
+
+typedef struct lcl_context lcl_context;
+
+typedef struct {
+  uint64_t encryptions, additions, multiplications, relinearizations, rescales, rotations,
+      mod_ups;
+} lcl_counts;
+
+/* ------------------------------------------------------------ context */
+/* CkksParams{ring_degree = degree, depth, security}: scale 2^40, q0 44 bits,
+ * scale primes 40 bits, special prime 54 bits (ckks.hpp:39-55). */
+int lcl_context_create(size_t degree, int depth, int secure, int device, lcl_context** out);
+int lcl_context_destroy(lcl_context* ctx);
+const char* lcl_last_error(void);
+/* primes[0..full-1] = q chain, primes[full] = special. */
+int lcl_context_primes(const lcl_context* ctx, uint64_t* primes, size_t* full);
+int lcl_set_stream(lcl_context* ctx, void* cuda_stream);
+int lcl_synchronize(lcl_context* ctx);
+int lcl_get_counts(const lcl_context* ctx, lcl_counts* out);
+int lcl_reset_counts(lcl_context* ctx);
+/* Number of kernel launches issued so far (instrumentation for bench.py). */
+uint64_t lcl_launch_count(const lcl_context* ctx);
+
+/* ------------------------------------------------------------ keys */
+/* Host key in the reference layout [full][2][full+1][N]; words must equal
+ * full * 2 * (full+1) * N. Keys stay resident in HBM. */
+int lcl_upload_relin_key(lcl_context* ctx, const uint64_t* h_key, size_t words);
+int lcl_upload_rotation_key(lcl_context* ctx, size_t step, const uint64_t* h_key, size_t words);
+int lcl_has_rotation_key(const lcl_context* ctx, size_t step);
+
+/* ------------------------------------------------------------ device memory */
+int lcl_device_alloc(lcl_context* ctx, size_t bytes, void** d_ptr);
+int lcl_device_free(lcl_context* ctx, void* d_ptr);
+int lcl_copy_h2d(lcl_context* ctx, void* d_dst, const void* h_src, size_t bytes);
+int lcl_copy_d2h(lcl_context* ctx, void* h_dst, const void* d_src, size_t bytes);
+
+/* ------------------------------------------------------------ primitives */
+/* Batched negacyclic NTT, in place, over `items` polys of `count` q rows
+ * (+ the special row last when with_special). Eval order = reference's. */
+int lcl_ntt_forward(lcl_context* ctx, uint64_t* d_polys, size_t items, size_t count,
+                    int with_special);
+int lcl_ntt_inverse(lcl_context* ctx, uint64_t* d_polys, size_t items, size_t count,
+                    int with_special);
+/* hadd / hsub (ckks.cpp:395-415) over [batch][2][count][N]; out may alias a. */
+int lcl_hadd(lcl_context* ctx, const uint64_t* d_a, const uint64_t* d_b, size_t batch,
+             size_t count, uint64_t* d_out);
+int lcl_hsub(lcl_context* ctx, const uint64_t* d_a, const uint64_t* d_b, size_t batch,
+             size_t count, uint64_t* d_out);
+/* batch ternaries [batch][3][count][N] -> ciphertexts [batch][2][count][N]. */
+int lcl_relinearize(lcl_context* ctx, const uint64_t* d_tern, size_t batch, size_t count,
+                    uint64_t* d_out);
+/* [batch][2][count][N] -> [batch][2][count-1][N]; DEPTH_EXHAUSTED at count 1. */
+int lcl_rescale(lcl_context* ctx, const uint64_t* d_ct, size_t batch, size_t count,
+                uint64_t* d_out);
+int lcl_rotate(lcl_context* ctx, const uint64_t* d_ct, size_t batch, size_t count, size_t step,
+               uint64_t* d_out);
+/* outs: [nsteps][batch][2][count][N]; one decomposition for all steps. */
+int lcl_hoisted_rotations(lcl_context* ctx, const uint64_t* d_ct, size_t batch, size_t count,
+                          const size_t* h_steps, size_t nsteps, uint64_t* d_outs);
+/* HoistPlan{k, n = width}: first min(k-1, log2 width) levels hoisted. */
+int lcl_slot_reduce(lcl_context* ctx, const uint64_t* d_ct, size_t batch, size_t count,
+                    size_t width, size_t k, uint64_t* d_out);
+/* ct x pt with a plaintext encoded on the host at (value, scale, level). */
+int lcl_mult_plain_const(lcl_context* ctx, const uint64_t* d_ct, size_t batch, size_t count,
+                         double value, double pt_scale, uint64_t* d_out);
+
+/* ------------------------------------------------------------ hot path */
+/* a, b: [chunks][2][full][N]; out: [2][full-1][N]. lazy != 0 -> one relin. */
+int lcl_pairwise_distance(lcl_context* ctx, const uint64_t* d_a, const uint64_t* d_b,
+                          size_t chunks, int lazy, uint64_t* d_out);
+/* clients [n][chunks][2][full][N] at scale in_scale -> out [pairs][2][full-1][N]
+ * in (i<j) row-major order; width/k = HoistPlan n/k; reduce = reduce_on_server.
+ * *out_scale receives the output scale (host double bookkeeping). */
+int lcl_distance_matrix(lcl_context* ctx, const uint64_t* d_clients, size_t n, size_t chunks,
+                        double in_scale, size_t width, size_t k, int lazy, int reduce,
+                        uint64_t* d_out, double* out_scale);
+/* selectors [n][2][full][N]; average = (rule == multi_krum && l > 1);
+ * out [chunks][2][full-1 (or full-2 when averaging)][N]. */
+int lcl_masked_aggregate(lcl_context* ctx, const uint64_t* d_clients, const uint64_t* d_sel,
+                         size_t n, size_t chunks, double w_scale, double sel_scale, size_t l,
+                         int average, uint64_t* d_out, double* out_scale);
+/* Host-buffer variant of the server round used by the end-to-end benchmark:
+ * H2D of clients + selectors, distance matrix, masked aggregate, D2H of both
+ * outputs, synchronised before returning. */
+int lcl_server_round_host(lcl_context* ctx, const uint64_t* h_clients, const uint64_t* h_sel,
+                          size_t n, size_t chunks, double in_scale, size_t width, size_t k,
+                          size_t l, int average, uint64_t* h_dist, uint64_t* h_agg);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* LANCELOT_B200_H */

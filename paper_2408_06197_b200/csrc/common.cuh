@@ -1,0 +1,152 @@
+// Shared device arithmetic for the Lancelot server path on sm_100a.
+//
+// All residues are u64 in [0, q) at every observable boundary; inside kernels
+// values may be kept lazily in [0, 2q) or [0, 4q) (Harvey butterflies). Every
+// prime of the chain is < 2^55 (q0 44 bits, scale primes 40 bits, special 54
+// bits: CkksParams defaults, reference ckks.hpp:39-55), so 4q < 2^57 never
+// overflows a word. Results are bit-identical to the reference because the
+// arithmetic is exact modular arithmetic: any evaluation order yields the same
+// fully reduced residue.
+#pragma once
+
+#include <cstdint>
+
+typedef uint64_t u64;
+typedef unsigned int u32;
+
+#define LCL_MAXP 16  // q primes + special supported by one context
+
+// Per-prime constants, resident in __constant__ memory of every module.
+struct PrimeConst {
+  u64 q;
+  u64 two_q;
+  u64 ratio_lo, ratio_hi;  // floor((2^128 - 1) / q): exact 128-bit Barrett (modmath.hpp:62-73)
+  u64 one_shoup;           // floor(2^64 / q): 64-bit reduction via Shoup with w = 1
+  u64 half;                // q >> 1: centred-lift threshold (rns.cpp:370-378)
+  u64 n_inv, n_inv_shoup;  // N^-1 mod q
+};
+
+// Row addressing for batched transforms. Row r of a launch is row
+// sub = r % rows_per_item of item = r / rows_per_item; items come in groups of
+// items_per_group (e.g. the (c0, c1) halves of one ciphertext):
+//   base + (item / ipg) * group_stride + (item % ipg) * item_stride + sub * row_stride
+// and uses prime prime_of[sub].
+struct RowMap {
+  u64* base;
+  u64 group_stride;
+  u64 item_stride;
+  u64 row_stride;
+  u32 rows_per_item;
+  u32 items_per_group;
+  unsigned char prime_of[LCL_MAXP * 2];
+};
+
+__device__ __forceinline__ u64* row_ptr(const RowMap& m, u32 r) {
+  const u32 item = r / m.rows_per_item;
+  const u32 sub = r - item * m.rows_per_item;
+  const u32 g = item / m.items_per_group;
+  const u32 h = item - g * m.items_per_group;
+  return m.base + (u64)g * m.group_stride + (u64)h * m.item_stride + (u64)sub * m.row_stride;
+}
+__device__ __forceinline__ u32 row_prime(const RowMap& m, u32 r) {
+  return m.prime_of[r % m.rows_per_item];
+}
+
+// ---------------------------------------------------------------- scalar ops
+__device__ __forceinline__ u64 add_mod(u64 a, u64 b, u64 q) {
+  u64 s = a + b;
+  return s >= q ? s - q : s;
+}
+__device__ __forceinline__ u64 sub_mod(u64 a, u64 b, u64 q) {
+  return a >= b ? a - b : a + q - b;
+}
+__device__ __forceinline__ u64 csub(u64 a, u64 q) { return a >= q ? a - q : a; }
+
+// Shoup product a*w mod q for fixed w with ws = floor(w * 2^64 / q).
+// Any a < 2^64 is accepted; the result lies in [0, 2q).
+__device__ __forceinline__ u64 mul_shoup_lazy(u64 a, u64 w, u64 ws, u64 q) {
+  const u64 hi = __umul64hi(a, ws);
+  return a * w - hi * q;
+}
+__device__ __forceinline__ u64 mul_shoup(u64 a, u64 w, u64 ws, u64 q) {
+  return csub(mul_shoup_lazy(a, w, ws, q), q);
+}
+// a mod q for any 64-bit a.
+__device__ __forceinline__ u64 reduce64(u64 a, const PrimeConst& p) {
+  return csub(a - __umul64hi(a, p.one_shoup) * p.q, p.q);
+}
+
+// Exact reduction of the 128-bit value (hi, lo) mod q (modmath.hpp:62-73).
+__device__ __forceinline__ u64 reduce128(u64 lo, u64 hi, const PrimeConst& p) {
+  // q_hat = floor(x * ratio / 2^128), computed from the three upper partial
+  // products exactly as the reference does, in 64-bit halves.
+  const u64 c0_hi = __umul64hi(lo, p.ratio_lo);
+  const u64 c1_lo = lo * p.ratio_hi;
+  const u64 c1_hi = __umul64hi(lo, p.ratio_hi);
+  // c1 = lo*rhi + c0_hi  (128-bit)
+  const u64 c1l = c1_lo + c0_hi;
+  const u64 c1h = c1_hi + (c1l < c1_lo ? 1ull : 0ull);
+  // c2 = hi*rlo + c1l   (only the high word is needed)
+  const u64 c2_lo = hi * p.ratio_lo;
+  const u64 c2_hi = __umul64hi(hi, p.ratio_lo);
+  const u64 c2l = c2_lo + c1l;
+  const u64 c2h = c2_hi + (c2l < c2_lo ? 1ull : 0ull);
+  const u64 q_hat = hi * p.ratio_hi + c1h + c2h;
+  return csub(lo - q_hat * p.q, p.q);
+}
+
+__device__ __forceinline__ u64 mul_mod(u64 a, u64 b, const PrimeConst& p) {
+  return reduce128(a * b, __umul64hi(a, b), p);
+}
+
+// 128-bit accumulate (lo, hi) += a * b.
+__device__ __forceinline__ void mac128(u64& lo, u64& hi, u64 a, u64 b) {
+  asm("mad.lo.cc.u64 %0, %2, %3, %0;\n\tmadc.hi.u64 %1, %2, %3, %1;"
+      : "+l"(lo), "+l"(hi)
+      : "l"(a), "l"(b));
+}
+
+// ------------------------------------------------ split-23 product sums
+// Operands below 2^46 are split into 23-bit halves x = x1*2^23 + x0. A product
+// then needs four 32x32->64 multiply-adds into three 64-bit partial sums
+//   s0 += x0*y0, s1 += x0*y1 + x1*y0, s2 += x1*y1     (each term < 2^47)
+// that cannot overflow for fewer than 2^16 accumulated products. The value
+// is s0 + s1*2^23 + s2*2^46 and is reduced once at the end.
+struct Split {
+  u32 lo, hi;
+};
+__device__ __forceinline__ Split split23(u64 x) {
+  Split s;
+  s.lo = (u32)x & 0x7FFFFFu;
+  s.hi = (u32)(x >> 23);
+  return s;
+}
+__device__ __forceinline__ u64 wmul(u32 a, u32 b) { return (u64)a * (u64)b; }
+
+struct Acc3 {
+  u64 s0, s1, s2;
+  __device__ __forceinline__ void zero() { s0 = s1 = s2 = 0; }
+  __device__ __forceinline__ void mac(Split x, Split y) {
+    s0 += wmul(x.lo, y.lo);
+    s1 += wmul(x.lo, y.hi);
+    s1 += wmul(x.hi, y.lo);
+    s2 += wmul(x.hi, y.hi);
+  }
+  __device__ __forceinline__ void sq(Split x) {  // x^2 with the cross term halved
+    s0 += wmul(x.lo, x.lo);
+    s1 += wmul(x.lo, x.hi) << 1;
+    s2 += wmul(x.hi, x.hi);
+  }
+  // Fully reduced value mod q.
+  __device__ __forceinline__ u64 reduce(const PrimeConst& p) const {
+    // v = s0 + s1*2^23 + s2*2^46 as a 128-bit (lo, hi).
+    u64 lo = s0, hi = 0;
+    const u64 a = s1 << 23, ah = s1 >> 41;
+    lo += a;
+    hi += ah + (lo < a ? 1ull : 0ull);
+    const u64 b = s2 << 46, bh = s2 >> 18;
+    lo += b;
+    hi += bh + (lo < b ? 1ull : 0ull);
+    return reduce128(lo, hi, p);
+  }
+};

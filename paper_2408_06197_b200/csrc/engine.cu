@@ -1,0 +1,1159 @@
+// Host runtime + C-ABI of the B200-native Lancelot server path.
+//
+// Everything below the C-ABI is native: basis construction (prime search,
+// psi, twiddle and Shoup tables), key residency in HBM, a grow-only device
+// workspace, and the batched orchestration of the reference's server
+// functions as level-synchronous kernel sequences on one CUDA stream.
+//
+// Reference call structure mirrored here (paths under /root/reference/proj/core):
+//   build_distance_matrix      distance.cpp:242-300
+//   encrypted_pairwise_distance distance.cpp:107-142
+//   slot_reduce                distance.cpp:214-240
+//   masked_aggregate           aggregation.cpp:188-229
+//   relinearize / rescale / rotate / hoisted_rotations   ckks.cpp:522-612
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <complex>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/lancelot_b200.h"
+#include "common.cuh"
+#include "kernels.cuh"
+#include "ntt.cuh"
+
+using namespace lcl;
+
+typedef unsigned __int128 u128;
+
+namespace {
+
+// ------------------------------------------------------------ errors
+thread_local std::string g_last_error;
+
+struct Status {
+  int code;
+  std::string msg;
+};
+
+struct LclError {
+  int code;
+  std::string msg;
+};
+
+[[noreturn]] void fail(int code, const std::string& msg) { throw LclError{code, msg}; }
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) fail(LCL_CUDA_ERROR, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+// ------------------------------------------------------------ host modular math
+// Setup-time only (basis construction); restates modmath.cpp:24-132.
+u64 h_mulmod(u64 a, u64 b, u64 q) { return (u64)((u128)a * b % q); }
+u64 h_powmod(u64 b, u64 e, u64 q) {
+  u64 r = 1;
+  b %= q;
+  while (e) {
+    if (e & 1) r = h_mulmod(r, b, q);
+    b = h_mulmod(b, b, q);
+    e >>= 1;
+  }
+  return r;
+}
+u64 h_invmod(u64 a, u64 q) { return h_powmod(a % q, q - 2, q); }
+bool h_is_prime(u64 n) {
+  static const u64 small[12] = {2, 3, 5, 7, 11, 13, 17, 19, 23, 29, 31, 37};
+  if (n < 2) return false;
+  for (u64 p : small) {
+    if (n == p) return true;
+    if (n % p == 0) return false;
+  }
+  u64 d = n - 1;
+  int s = 0;
+  while (!(d & 1)) d >>= 1, ++s;
+  for (u64 a : small) {
+    u64 x = h_powmod(a, d, n);
+    if (x == 1 || x == n - 1) continue;
+    bool comp = true;
+    for (int i = 1; i < s; ++i) {
+      x = h_mulmod(x, x, n);
+      if (x == n - 1) {
+        comp = false;
+        break;
+      }
+    }
+    if (comp) return false;
+  }
+  return true;
+}
+std::vector<u64> h_ntt_primes(int bits, u64 degree, size_t count, const std::vector<u64>& avoid) {
+  const u64 step = 2 * degree, lo = 1ull << (bits - 1);
+  u64 cand = (1ull << bits) - step + 1;
+  std::vector<u64> out;
+  while (out.size() < count && cand > lo) {
+    if (h_is_prime(cand) && std::find(avoid.begin(), avoid.end(), cand) == avoid.end() &&
+        std::find(out.begin(), out.end(), cand) == out.end())
+      out.push_back(cand);
+    cand -= step;
+  }
+  if (out.size() < count) fail(LCL_PARAMETER_ERROR, "prime search exhausted the requested bit range");
+  return out;
+}
+u64 h_root_2n(u64 n, u64 q) {
+  const u64 quot = (q - 1) / (2 * n);
+  for (u64 g = 2; g < q; ++g) {
+    const u64 r = h_powmod(g, quot, q);
+    if (h_powmod(r, n, q) == q - 1) return r;
+  }
+  fail(LCL_PARAMETER_ERROR, "no primitive root found");
+}
+u64 h_shoup(u64 w, u64 q) { return (u64)(((u128)w << 64) / q); }
+size_t h_brv(size_t x, int bits) {
+  size_t r = 0;
+  for (int i = 0; i < bits; ++i, x >>= 1) r = (r << 1) | (x & 1);
+  return r;
+}
+
+// ------------------------------------------------------------ canonical embedding
+// Host encode of a plaintext (ckks.cpp:263-307 with encoding.cpp:37-116),
+// compiled without FP contraction so it reproduces the reference's default
+// x86-64 build word for word. Used only for the 1/l plaintext of Multi-Krum
+// averaging, which the reference also encodes on the host.
+std::vector<long long> h_encode_rounded(const std::vector<double>& values, size_t degree,
+                                        double scale) {
+  const size_t h = degree / 2;
+  const int logh = __builtin_ctzll(h);
+  std::vector<double> br(h, 0.0), bi(h, 0.0);
+  u64 g = 1;
+  const u64 two_n = 2 * degree;
+  for (size_t j = 0; j < values.size(); ++j) {
+    br[(g - 1) / 4] = values[j];
+    g = (g * 5) % two_n;
+  }
+  for (size_t i = 0; i < h; ++i) {
+    const size_t r = h_brv(i, logh);
+    if (i < r) {
+      std::swap(br[i], br[r]);
+      std::swap(bi[i], bi[r]);
+    }
+  }
+  const double pi = 3.141592653589793238462643383279502884;
+  for (size_t len = 2; len <= h; len <<= 1) {
+    const size_t stride = h / len;
+    for (size_t st = 0; st < h; st += len) {
+      for (size_t k = 0; k < len / 2; ++k) {
+        const double ang = 2.0 * pi * (double)(k * stride) / (double)h;
+        const double wr = std::cos(ang), wi = -std::sin(ang);  // inverse: conj
+        const size_t u = st + k, v = st + k + len / 2;
+        const double xr = br[v], xi = bi[v];
+        const double vr = xr * wr - xi * wi, vi = xr * wi + xi * wr;
+        const double ur = br[u], ui = bi[u];
+        br[u] = ur + vr;
+        bi[u] = ui + vi;
+        br[v] = ur - vr;
+        bi[v] = ui - vi;
+      }
+    }
+  }
+  const double s = 1.0 / (double)h;
+  for (size_t i = 0; i < h; ++i) {
+    br[i] *= s;
+    bi[i] *= s;
+  }
+  std::vector<long long> rounded(degree);
+  for (size_t i = 0; i < h; ++i) {
+    const double ang = pi * (double)i / (double)degree;
+    const double tr = std::cos(ang), ti = -std::sin(ang);
+    const double re = br[i] * tr - bi[i] * ti;
+    const double im = br[i] * ti + bi[i] * tr;
+    const double x0 = re * scale, x1 = im * scale;
+    if (std::fabs(x0) >= 4.6e18 || std::fabs(x1) >= 4.6e18)
+      fail(LCL_CAPACITY_ERROR, "scaled coefficient overflows 62 bits");
+    rounded[i] = std::llround(x0);
+    rounded[i + h] = std::llround(x1);
+  }
+  return rounded;
+}
+
+// ------------------------------------------------------------ device buffers
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  u64* get(size_t need_words) {
+    const size_t need = need_words * 8;
+    if (need > bytes) {
+      if (p) cudaFree(p);
+      p = nullptr;
+      bytes = 0;
+      cuda_check(cudaMalloc(&p, need), "workspace alloc");
+      bytes = need;
+    }
+    return static_cast<u64*>(p);
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+};
+
+RowMap make_map(const u64* base, u32 rpi, u64 row_stride, u64 item_stride, u32 ipg,
+                u64 group_stride, const std::vector<u32>& primes) {
+  RowMap m;
+  std::memset(&m, 0, sizeof m);
+  m.base = const_cast<u64*>(base);
+  m.rows_per_item = rpi;
+  m.row_stride = row_stride;
+  m.item_stride = item_stride;
+  m.items_per_group = ipg;
+  m.group_stride = group_stride;
+  for (u32 i = 0; i < rpi && i < 2 * LCL_MAXP; ++i) m.prime_of[i] = (unsigned char)primes[i];
+  return m;
+}
+
+RowMap null_map() {
+  RowMap m;
+  std::memset(&m, 0, sizeof m);
+  m.rows_per_item = 1;
+  m.items_per_group = 1;
+  return m;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------ context
+struct lcl_context {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  size_t n = 0;
+  int logn = 0;
+  u32 full = 0;  // q primes; special at index full
+  std::vector<u64> primes;
+  double scale = 0;
+  PrimeConst* d_primes = nullptr;
+  ulonglong2* d_tw = nullptr;
+  ulonglong2* d_itw = nullptr;
+  u64* d_smod = nullptr;
+  ulonglong2* d_pinv = nullptr;  // [(full+1) * (full+1)]: (q_div^-1 mod q_dst, shoup)
+  u32* d_pairs = nullptr;
+  size_t pairs_cap = 0;
+  u64* d_relin = nullptr;
+  std::map<size_t, u64*> d_rot;
+  std::map<size_t, u32*> d_perm;
+  lcl_counts counts{};
+  u64 launches = 0;
+  // workspace
+  DevBuf ws_coef, ws_digits, ws_acc, ws_coefsp, ws_mid, ws_tern, ws_ctA, ws_ctB, ws_ctC, ws_pt;
+  DevBuf ws_io_in, ws_io_sel, ws_io_dist, ws_io_agg;
+
+  u32 P() const { return full + 1; }
+  u64 N() const { return (u64)n; }
+  std::vector<u32> primes_0(u32 count) const {
+    std::vector<u32> v(count);
+    for (u32 i = 0; i < count; ++i) v[i] = i;
+    return v;
+  }
+};
+
+namespace {
+
+void count_launch(lcl_context* c, u64 k = 1) { c->launches += k; }
+
+void post_launch(lcl_context* c, u64 k = 1) {
+  count_launch(c, k);
+  cuda_check(cudaGetLastError(), "kernel launch");
+}
+
+// ------------------------------------------------------------ NTT launchers
+RowMap mid_map(lcl_context* c, u32 rows, const RowMap& pm) {
+  u64* mid = c->ws_mid.get((u64)rows * c->N());
+  RowMap m = pm;
+  m.base = mid;
+  m.row_stride = c->N();
+  m.item_stride = (u64)pm.rows_per_item * c->N();
+  m.items_per_group = 1;
+  m.group_stride = 0;
+  return m;
+}
+
+template <class K>
+void allow_smem(K kernel, size_t bytes) {
+  if (bytes > 48 * 1024)
+    cuda_check(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes),
+               "smem attribute");
+}
+
+template <int LOGN1, int E, class Loader, class Epi>
+void fwd2(lcl_context* c, u32 rows, const RowMap& mid, const Loader& ld, const Epi& epi) {
+  constexpr int N1 = 1 << LOGN1;
+  constexpr size_t smem = (size_t)N1 * 16 * 8;
+  static bool once = (allow_smem(ntt_col_fwd<LOGN1, E, Loader>, smem), true);
+  (void)once;
+  const u32 groups = (u32)(c->n >> LOGN1) >> 4;
+  ntt_col_fwd<LOGN1, E, Loader><<<rows * groups, 16 * (N1 / E), smem, c->stream>>>(
+      mid, ld, c->d_tw, c->d_primes, c->logn);
+  ntt_blk_fwd<LOGN1, Epi><<<rows * N1 / 4, 64, 0, c->stream>>>(mid, epi, c->d_tw, c->d_primes,
+                                                               c->logn);
+  post_launch(c, 2);
+}
+
+template <int LOGN1, int E, class Epi>
+void inv2(lcl_context* c, u32 rows, const RowMap& in, const RowMap& mid, const Epi& epi) {
+  constexpr int N1 = 1 << LOGN1;
+  constexpr size_t smem = (size_t)N1 * 16 * 8;
+  static bool once = (allow_smem(ntt_col_inv<LOGN1, E, Epi>, smem), true);
+  (void)once;
+  const u32 groups = (u32)(c->n >> LOGN1) >> 4;
+  ntt_blk_inv<LOGN1><<<rows * N1 / 4, 64, 0, c->stream>>>(in, mid, c->d_itw, c->d_primes,
+                                                          c->logn);
+  ntt_col_inv<LOGN1, E, Epi><<<rows * groups, 16 * (N1 / E), smem, c->stream>>>(
+      mid, epi, c->d_itw, c->d_primes, c->logn);
+  post_launch(c, 2);
+}
+
+// Forward NTT of `rows` rows whose prime layout is pm; the loader supplies
+// coefficient-domain inputs and the epilogue consumes fully reduced outputs.
+template <class Loader, class Epi>
+void launch_fwd(lcl_context* c, u32 rows, const RowMap& pm, const Loader& ld, const Epi& epi) {
+  if (rows == 0) return;
+  if (c->logn <= 12) {
+    ntt_small<false, Loader, Epi><<<rows, 256, c->n * 8, c->stream>>>(ld, epi, pm, c->d_tw,
+                                                                     c->d_primes, c->logn);
+    post_launch(c);
+    return;
+  }
+  const RowMap mid = mid_map(c, rows, pm);
+  switch (c->logn) {
+    case 13: fwd2<5, 16>(c, rows, mid, ld, epi); break;
+    case 14: fwd2<6, 16>(c, rows, mid, ld, epi); break;
+    case 15: fwd2<7, 16>(c, rows, mid, ld, epi); break;
+    case 16: fwd2<8, 16>(c, rows, mid, ld, epi); break;
+    case 17: fwd2<9, 32>(c, rows, mid, ld, epi); break;
+    default: fail(LCL_PARAMETER_ERROR, "ring degree outside 2^3..2^17");
+  }
+}
+
+template <class Epi>
+void launch_inv(lcl_context* c, u32 rows, const RowMap& in, const Epi& epi) {
+  if (rows == 0) return;
+  if (c->logn <= 12) {
+    ntt_small<true, PlainLoad, Epi><<<rows, 256, c->n * 8, c->stream>>>(
+        PlainLoad{in}, epi, in, c->d_itw, c->d_primes, c->logn);
+    post_launch(c);
+    return;
+  }
+  const RowMap mid = mid_map(c, rows, in);
+  switch (c->logn) {
+    case 13: inv2<5, 16>(c, rows, in, mid, epi); break;
+    case 14: inv2<6, 16>(c, rows, in, mid, epi); break;
+    case 15: inv2<7, 16>(c, rows, in, mid, epi); break;
+    case 16: inv2<8, 16>(c, rows, in, mid, epi); break;
+    case 17: inv2<9, 32>(c, rows, in, mid, epi); break;
+    default: fail(LCL_PARAMETER_ERROR, "ring degree outside 2^3..2^17");
+  }
+}
+
+LiftLoad lift_from(lcl_context* c, const RowMap& src, u32 rows_per_item, u32 fan) {
+  LiftLoad l;
+  l.src = src;
+  l.rows_per_item = rows_per_item;
+  l.fan = fan;
+  l.nprimes = c->P();
+  l.primes = c->d_primes;
+  l.smod = c->d_smod;
+  return l;
+}
+
+// ------------------------------------------------------------ key switching
+// decompose_for_keyswitch (ckks.cpp:464-481): the c1 / d2 rows of B items
+// (map `in`, rows_per_item = m) -> digits [B][m][m+1][N] in HBM.
+u64* ks_decompose(lcl_context* c, const RowMap& in, u32 B, u32 m) {
+  const u64 N = c->N();
+  u64* coef = c->ws_coef.get((u64)B * m * N);
+  const RowMap coef_map = make_map(coef, m, N, m * N, 1, 0, c->primes_0(m));
+  launch_inv(c, B * m, in, PlainStore{coef_map});
+  u64* dig = c->ws_digits.get((u64)B * m * (m + 1) * N);
+  std::vector<u32> dp(m * (m + 1));
+  for (u32 j = 0; j < m; ++j)
+    for (u32 t = 0; t <= m; ++t) dp[j * (m + 1) + t] = t < m ? t : c->full;
+  const RowMap dig_map = make_map(dig, m * (m + 1), N, (u64)m * (m + 1) * N, 1, 0, dp);
+  launch_fwd(c, B * m * (m + 1), dig_map, lift_from(c, coef_map, m * (m + 1), m + 1),
+             PlainStore{dig_map});
+  return dig;
+}
+
+u64* ks_ip(lcl_context* c, const u64* dig, u32 B, u32 m, const u64* key,
+                      const u32* perm) {
+  const u64 N = c->N();
+  u64* acc = c->ws_acc.get((u64)B * 2 * (m + 1) * N);
+  const u64 threads = (u64)(m + 1) * N;
+  lcl::ks_inner_product<<<(u32)((threads + 255) / 256), 256, 0, c->stream>>>(
+      dig, B, m, key, c->full, perm, acc, c->logn, c->d_primes);
+  post_launch(c);
+  return acc;
+}
+
+// ModDown of acc [B][2][m+1][N] into `out` (items (b, x), rows_per_item m,
+// 2 items per group) with the fused output additions.
+void ks_moddown(lcl_context* c, const u64* acc, u32 B, u32 m, const RowMap& out,
+                const RowMap& add1, const RowMap& add2, const u32* perm) {
+  const u64 N = c->N();
+  u64* csp = c->ws_coefsp.get((u64)B * 2 * N);
+  const RowMap sp_in = make_map(acc + (u64)m * N, 1, N, (m + 1) * N, 1, 0, {c->full});
+  const RowMap sp_map = make_map(csp, 1, N, N, 1, 0, {c->full});
+  launch_inv(c, 2 * B, sp_in, PlainStore{sp_map});
+  DivRoundStore epi;
+  epi.out = out;
+  epi.x = make_map(acc, m, N, (m + 1) * N, 1, 0, c->primes_0(m));
+  epi.add1 = add1;
+  epi.add2 = add2;
+  epi.perm = perm;
+  epi.pinv = c->d_pinv + (u64)c->full * c->P();
+  launch_fwd(c, 2 * B * m, out, lift_from(c, sp_map, m, m), epi);
+}
+
+RowMap ct_map(const u64* base, u32 m, u64 N, u64 ct_stride) {
+  std::vector<u32> p(m);
+  for (u32 i = 0; i < m; ++i) p[i] = i;
+  return make_map(base, m, N, (u64)m * N, 2, ct_stride, p);
+}
+
+// relinearize (ckks.cpp:522-534) over a batch of ternaries [B][3][m][N].
+void relinearize_batch(lcl_context* c, const u64* tern, u32 B, u32 m, u64* out) {
+  if (!c->d_relin) fail(LCL_KEY_ERROR, "no relinearization key uploaded");
+  const u64 N = c->N();
+  const RowMap d2 = make_map(tern + 2ull * m * N, m, N, 3ull * m * N, 1, 0, c->primes_0(m));
+  u64* dig = ks_decompose(c, d2, B, m);
+  u64* acc = ks_ip(c, dig, B, m, c->d_relin, nullptr);
+  ks_moddown(c, acc, B, m, ct_map(out, m, N, 2ull * m * N), ct_map(tern, m, N, 3ull * m * N),
+             null_map(), nullptr);
+  c->counts.relinearizations += B;
+  c->counts.mod_ups += B;
+}
+
+// rescale (ckks.cpp:536-547): [B][2][m] -> [B][2][m-1] (in and out may not alias).
+void rescale_batch(lcl_context* c, const u64* ct, u32 B, u32 m, u64* out) {
+  if (m < 2) fail(LCL_DEPTH_EXHAUSTED, "no prime left to rescale by");
+  const u64 N = c->N();
+  u64* last = c->ws_coefsp.get((u64)B * 2 * N);
+  const RowMap last_in = make_map(ct + (u64)(m - 1) * N, 1, N, (u64)m * N, 2, 2ull * m * N, {m - 1});
+  const RowMap last_map = make_map(last, 1, N, N, 1, 0, {m - 1});
+  launch_inv(c, 2 * B, last_in, PlainStore{last_map});
+  DivRoundStore epi;
+  epi.out = ct_map(out, m - 1, N, 2ull * (m - 1) * N);
+  epi.x = ct_map(ct, m - 1, N, 2ull * m * N);
+  epi.x.item_stride = (u64)m * N;
+  epi.add1 = null_map();
+  epi.add2 = null_map();
+  epi.perm = nullptr;
+  epi.pinv = c->d_pinv + (u64)(m - 1) * c->P();
+  launch_fwd(c, 2 * B * (m - 1), epi.out, lift_from(c, last_map, m - 1, m - 1), epi);
+  c->counts.rescales += B;
+}
+
+const u64* rot_key(lcl_context* c, size_t step) {
+  auto it = c->d_rot.find(step);
+  if (it == c->d_rot.end()) fail(LCL_KEY_ERROR, "no rotation key for the requested step");
+  return it->second;
+}
+
+// out = in + rotate(in, step) over B ciphertexts (one slot_reduce level,
+// distance.cpp:235-237), or plain rotate when accumulate == false.
+void rotate_level(lcl_context* c, const u64* in, u32 B, u32 m, size_t step, u64* out,
+                  bool accumulate) {
+  const u64 N = c->N();
+  const u64* key = rot_key(c, step);
+  const u32* perm = c->d_perm.at(step);
+  const RowMap c1 = make_map(in + (u64)m * N, m, N, 2ull * m * N, 1, 0, c->primes_0(m));
+  u64* dig = ks_decompose(c, c1, B, m);
+  u64* acc = ks_ip(c, dig, B, m, key, perm);
+  const RowMap inm = ct_map(in, m, N, 2ull * m * N);
+  ks_moddown(c, acc, B, m, ct_map(out, m, N, 2ull * m * N), accumulate ? inm : null_map(), inm,
+             perm);
+  c->counts.rotations += B;
+  c->counts.mod_ups += B;
+  if (accumulate) c->counts.additions += B;
+}
+
+size_t norm_step(lcl_context* c, size_t step) { return step % (c->n / 2); }
+
+// slot_reduce (distance.cpp:214-240) over B ciphertexts; in and out may alias.
+void slot_reduce_batch(lcl_context* c, const u64* in, u32 B, u32 m, size_t width, size_t k,
+                       u64* out) {
+  if (width == 0 || (width & (width - 1))) fail(LCL_WIDTH_ERROR, "reduction width must be a power of two");
+  if (width > c->n / 2) fail(LCL_WIDTH_ERROR, "reduction width exceeds the slot count");
+  if (k == 0) fail(LCL_PARAMETER_ERROR, "unfold factor starts at 1");
+  const u64 N = c->N();
+  const u64 words = (u64)B * 2 * m * N;
+  if (width == 1) {
+    if (out != in) cudaMemcpyAsync(out, in, words * 8, cudaMemcpyDeviceToDevice, c->stream);
+    return;
+  }
+  const size_t levels = __builtin_ctzll(width);
+  const size_t unf = std::min(k - 1, levels);
+  // validate keys up front (the reference raises KeyError before any work
+  // lands in the output for the first missing step)
+  for (size_t u = 1; unf >= 1 && u < (size_t{1} << unf); ++u) rot_key(c, norm_step(c, u));
+  for (size_t j = unf; j < levels; ++j) rot_key(c, norm_step(c, size_t{1} << j));
+  u64* bufs[2] = {c->ws_ctB.get(words), c->ws_ctC.get(words)};
+  int cur = -1;  // -1: current value lives in `in`
+  auto cur_ptr = [&]() -> const u64* { return cur < 0 ? in : bufs[cur]; };
+  if (unf >= 1) {
+    // hoisted batch: one decomposition of in.c1, every step reuses it.
+    const RowMap c1 = make_map(in + (u64)m * N, m, N, 2ull * m * N, 1, 0, c->primes_0(m));
+    u64* dig = ks_decompose(c, c1, B, m);
+    c->counts.mod_ups += B;
+    const RowMap base = ct_map(in, m, N, 2ull * m * N);
+    for (size_t u = 1; u < (size_t{1} << unf); ++u) {
+      const size_t st = norm_step(c, u);
+      const int nxt = cur < 0 ? 0 : 1 - cur;
+      u64* acc = ks_ip(c, dig, B, m, rot_key(c, st), c->d_perm.at(st));
+      ks_moddown(c, acc, B, m, ct_map(bufs[nxt], m, N, 2ull * m * N),
+                 ct_map(cur_ptr(), m, N, 2ull * m * N), base, c->d_perm.at(st));
+      cur = nxt;
+      c->counts.rotations += B;
+      c->counts.additions += B;
+    }
+  }
+  for (size_t j = unf; j < levels; ++j) {
+    const int nxt = cur < 0 ? 0 : 1 - cur;
+    rotate_level(c, cur_ptr(), B, m, norm_step(c, size_t{1} << j), bufs[nxt], true);
+    cur = nxt;
+  }
+  cudaMemcpyAsync(out, cur_ptr(), words * 8, cudaMemcpyDeviceToDevice, c->stream);
+}
+
+void ensure_pairs(lcl_context* c, u32 n) {
+  const size_t np = (size_t)n * (n - 1) / 2;
+  std::vector<u32> h;
+  h.reserve(np);
+  for (u32 i = 0; i < n; ++i)
+    for (u32 j = i + 1; j < n; ++j) h.push_back(i | (j << 16));
+  if (np > c->pairs_cap) {
+    if (c->d_pairs) cudaFree(c->d_pairs);
+    cuda_check(cudaMalloc(&c->d_pairs, np * 4), "pairs alloc");
+    c->pairs_cap = np;
+  }
+  cuda_check(cudaMemcpy(c->d_pairs, h.data(), np * 4, cudaMemcpyHostToDevice), "pairs upload");
+}
+
+constexpr int kPP = 4;
+
+// Lazy ternary accumulators for pairs [p0, p1) over chunks [c0, c1).
+void pair_accumulate_launch(lcl_context* c, const u64* clients, u32 n, u32 chunks, u32 c0,
+                            u32 c1, u32 p0, u32 p1, u64* tern, bool accumulate) {
+  const u32 m = c->full;
+  const u32 warps = 8;
+  const u32 pairs = p1 - p0;
+  const u32 per_cta = warps * kPP;
+  dim3 grid((u32)(m * c->n / 32), (pairs + per_cta - 1) / per_cta);
+  const size_t smem = (size_t)n * 64 * 8;
+  pair_accumulate<kPP><<<grid, warps * 32, smem, c->stream>>>(
+      clients, n, c0, c1, chunks, m, c->logn, c->d_pairs, p0, p1, tern, accumulate ? 1 : 0,
+      c->d_primes);
+  post_launch(c);
+}
+
+void hadd_into(lcl_context* c, u64* acc, const u64* x, u32 B, u32 m) {
+  const u64 N = c->N();
+  const RowMap a = ct_map(acc, m, N, 2ull * m * N);
+  const RowMap b = ct_map(x, m, N, 2ull * m * N);
+  const u32 rows = B * 2 * m;
+  rows_addsub<false><<<(u32)(((u64)rows * N + 255) / 256), 256, 0, c->stream>>>(
+      a, a, b, rows, c->logn, c->d_primes);
+  post_launch(c);
+  c->counts.additions += B;
+}
+
+// Sub-batch size for the key-switch chain: bounds the digit workspace.
+u32 sub_batch(lcl_context* c, u32 m) {
+  const u64 per_item = (u64)m * (m + 1) * c->N() * 8 * 2;  // digits + mid
+  const u64 budget = 8ull << 30;
+  return (u32)std::max<u64>(1, std::min<u64>(1024, budget / per_item));
+}
+
+// build_distance_matrix per_pair (distance.cpp:242-300), pairs in i<j order.
+void distance_matrix(lcl_context* c, const u64* clients, u32 n, u32 chunks, size_t width,
+                     size_t k, bool lazy, bool reduce, u64* out) {
+  if (n < 2) fail(LCL_SHAPE_ERROR, "pairwise distances need at least two clients");
+  if (n > 65535) fail(LCL_SHAPE_ERROR, "too many clients");
+  const u32 m = c->full;
+  if (m < 2) fail(LCL_DEPTH_EXHAUSTED, "no prime left to rescale by");
+  const u64 N = c->N();
+  ensure_pairs(c, n);
+  const u32 P = n * (n - 1) / 2;
+  const u32 SB = sub_batch(c, m);
+  const u64 out_stride = 2ull * (m - 1) * N;
+  for (u32 p0 = 0; p0 < P; p0 += SB) {
+    const u32 p1 = std::min(P, p0 + SB), B = p1 - p0;
+    u64* o = out + (u64)p0 * out_stride;
+    u64* ctA = c->ws_ctA.get((u64)B * 2 * m * N);
+    if (lazy) {
+      u64* tern = c->ws_tern.get((u64)B * 3 * m * N);
+      for (u32 cb = 0; cb < chunks; cb += 32768) {
+        pair_accumulate_launch(c, clients, n, chunks, cb, std::min(chunks, cb + 32768), p0, p1,
+                               tern, cb > 0);
+      }
+      relinearize_batch(c, tern, B, m, ctA);
+      rescale_batch(c, ctA, B, m, o);
+    } else {
+      u64* tern = c->ws_tern.get((u64)B * 3 * m * N);
+      u64* part = c->ws_ctB.get((u64)B * 2 * (m - 1) * N);
+      for (u32 ch = 0; ch < chunks; ++ch) {
+        pair_accumulate_launch(c, clients, n, chunks, ch, ch + 1, p0, p1, tern, false);
+        relinearize_batch(c, tern, B, m, ctA);
+        rescale_batch(c, ctA, B, m, ch == 0 ? o : part);
+        if (ch) hadd_into(c, o, part, B, m - 1);
+      }
+    }
+    // counters of the pair loop (hsub + hsquare + lazy_accumulate per chunk)
+    c->counts.multiplications += (u64)B * chunks;
+    c->counts.additions += (u64)B * (2ull * chunks - 1) - (lazy ? 0 : (u64)B * (chunks - 1));
+    if (reduce) slot_reduce_batch(c, o, B, m - 1, width, k, o);
+  }
+}
+
+void masked_aggregate(lcl_context* c, const u64* clients, const u64* sel, u32 n, u32 chunks,
+                      size_t l, bool average, u64* out) {
+  if (n == 0) fail(LCL_SHAPE_ERROR, "no client weights to aggregate");
+  const u32 m = c->full;
+  const u64 N = c->N();
+  const u32 SB = sub_batch(c, m);
+  const u32 mo = average ? m - 2 : m - 1;
+  if (m < 2 || (average && m < 3)) fail(LCL_DEPTH_EXHAUSTED, "no prime left to rescale by");
+  std::vector<u64> pt_h;
+  u64* d_pt = nullptr;
+  if (average) {
+    // encode(1/l at scale, level of the rescaled chunk) on the host (aggregation.cpp:221-223)
+    std::vector<double> v(c->n / 2, 1.0 / (double)l);
+    const std::vector<long long> rounded = h_encode_rounded(v, c->n, c->scale);
+    pt_h.resize((u64)(m - 1) * N);
+    for (u32 r = 0; r < m - 1; ++r) {
+      const u64 q = c->primes[r];
+      for (u64 i = 0; i < N; ++i) {
+        const long long x = rounded[i];
+        const u64 mag = (u64)(x < 0 ? -x : x) % q;
+        pt_h[r * N + i] = x < 0 ? (mag == 0 ? 0 : q - mag) : mag;
+      }
+    }
+    d_pt = c->ws_pt.get(pt_h.size());
+    cuda_check(cudaMemcpyAsync(d_pt, pt_h.data(), pt_h.size() * 8, cudaMemcpyHostToDevice,
+                               c->stream),
+               "pt upload");
+    const RowMap ptm = make_map(d_pt, m - 1, N, (u64)(m - 1) * N, 1, 0, c->primes_0(m - 1));
+    launch_fwd(c, m - 1, ptm, PlainLoad{ptm}, PlainStore{ptm});
+    cuda_check(cudaStreamSynchronize(c->stream), "pt encode");  // pt_h must outlive the copy
+  }
+  for (u32 c0 = 0; c0 < chunks; c0 += SB) {
+    const u32 c1 = std::min(chunks, c0 + SB), B = c1 - c0;
+    u64* tern = c->ws_tern.get((u64)B * 3 * m * N);
+    constexpr int CK = 4;
+    const u64 slots = (u64)m * N;
+    const u64 threads = ((B + CK - 1) / CK) * slots;
+    aggregate_tensor<CK><<<(u32)((threads + 255) / 256), 256, 0, c->stream>>>(
+        clients, sel, n, chunks, c0, B, m, c->logn, tern, c->d_primes);
+    post_launch(c);
+    u64* ctA = c->ws_ctA.get((u64)B * 2 * m * N);
+    relinearize_batch(c, tern, B, m, ctA);
+    u64* o = out + (u64)c0 * 2 * mo * N;
+    if (!average) {
+      rescale_batch(c, ctA, B, m, o);
+    } else {
+      u64* ctB = c->ws_ctB.get((u64)B * 2 * (m - 1) * N);
+      rescale_batch(c, ctA, B, m, ctB);
+      const u64 total = (u64)B * 2 * (m - 1) * N;
+      mult_plain<<<(u32)((total + 255) / 256), 256, 0, c->stream>>>(ctB, d_pt, B, m - 1, c->logn,
+                                                                    ctB, c->d_primes);
+      post_launch(c);
+      rescale_batch(c, ctB, B, m - 1, o);
+      c->counts.multiplications += B;
+    }
+    c->counts.multiplications += (u64)n * B;
+    c->counts.additions += (u64)(n - 1) * B;
+  }
+}
+
+}  // namespace
+
+// ============================================================ C-ABI
+namespace {
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return LCL_OK;
+  } catch (const LclError& e) {
+    g_last_error = e.msg;
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    g_last_error = "host allocation failed";
+    return LCL_CUDA_ERROR;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return LCL_PARAMETER_ERROR;
+  }
+}
+
+void need(bool ok, int code, const char* msg) {
+  if (!ok) fail(code, msg);
+}
+
+void build_context(lcl_context* c, size_t degree, int depth, int secure, int device) {
+  need(degree >= 8 && (degree & (degree - 1)) == 0, LCL_PARAMETER_ERROR,
+       "ring degree must be a power of two >= 8");
+  need(degree <= (1u << 17), LCL_PARAMETER_ERROR, "ring degree above 2^17 is not supported");
+  need(depth >= 0 && depth + 2 <= LCL_MAXP, LCL_PARAMETER_ERROR, "depth outside supported range");
+  int ndev = 0;
+  cuda_check(cudaGetDeviceCount(&ndev), "cudaGetDeviceCount");
+  need(device >= 0 && device < ndev, LCL_CUDA_ERROR, "no such CUDA device");
+  cuda_check(cudaSetDevice(device), "cudaSetDevice");
+  c->device = device;
+  c->n = degree;
+  c->logn = __builtin_ctzll(degree);
+  c->full = (u32)depth + 1;
+  c->scale = std::ldexp(1.0, 40);
+  // make_basis (ckks.cpp:77-93): q0 44 bits, depth x 40 bits, special 54 bits.
+  std::vector<u64> avoid;
+  std::vector<u64> chain = h_ntt_primes(44, degree, 1, avoid);
+  avoid.push_back(chain[0]);
+  if (depth > 0) {
+    for (u64 q : h_ntt_primes(40, degree, depth, avoid)) {
+      chain.push_back(q);
+      avoid.push_back(q);
+    }
+  }
+  const u64 special = h_ntt_primes(54, degree, 1, avoid)[0];
+  if (secure) {
+    static const std::map<size_t, double> budget = {
+        {1024, 27}, {2048, 54}, {4096, 109}, {8192, 218}, {16384, 438}, {32768, 881},
+        {65536, 1770}, {131072, 3540}};
+    auto it = budget.find(degree);
+    need(it != budget.end(), LCL_PARAMETER_ERROR, "no 128-bit budget entry for this ring degree");
+    double total = 0;
+    for (u64 q : chain) total += std::log2((double)q);
+    total += std::log2((double)special);
+    need(total <= it->second, LCL_PARAMETER_ERROR, "modulus chain exceeds the 128-bit budget");
+  }
+  c->primes = chain;
+  c->primes.push_back(special);
+  const u32 P = c->P();
+  const size_t n = degree;
+  std::vector<PrimeConst> pc(P);
+  std::vector<ulonglong2> tw(P * n), itw(P * n);
+  for (u32 i = 0; i < P; ++i) {
+    const u64 q = c->primes[i];
+    const u128 ratio = ~(u128)0 / q;
+    PrimeConst& k = pc[i];
+    k.q = q;
+    k.two_q = 2 * q;
+    k.ratio_lo = (u64)ratio;
+    k.ratio_hi = (u64)(ratio >> 64);
+    k.one_shoup = (u64)(((u128)1 << 64) / q);
+    k.half = q >> 1;
+    k.n_inv = h_invmod(n, q);
+    k.n_inv_shoup = h_shoup(k.n_inv, q);
+    // build_tables (rns.cpp:115-138): root[brv(i)] = psi^i, inverse likewise.
+    const u64 psi = h_root_2n(n, q), psi_inv = h_invmod(psi, q);
+    u64 f = 1, g = 1;
+    for (size_t t = 0; t < n; ++t) {
+      const size_t r = h_brv(t, c->logn);
+      tw[i * n + r] = make_ulonglong2(f, h_shoup(f, q));
+      itw[i * n + r] = make_ulonglong2(g, h_shoup(g, q));
+      f = h_mulmod(f, psi, q);
+      g = h_mulmod(g, psi_inv, q);
+    }
+  }
+  std::vector<u64> smod(P * P);
+  std::vector<ulonglong2> pinv(P * P);
+  for (u32 s = 0; s < P; ++s)
+    for (u32 d = 0; d < P; ++d) {
+      smod[s * P + d] = c->primes[s] % c->primes[d];
+      const u64 iv = s == d ? 0 : h_invmod(c->primes[s], c->primes[d]);
+      pinv[s * P + d] = make_ulonglong2(iv, h_shoup(iv, c->primes[d]));
+    }
+  cuda_check(cudaMalloc(&c->d_primes, P * sizeof(PrimeConst)), "alloc");
+  cuda_check(cudaMalloc(&c->d_tw, P * n * sizeof(ulonglong2)), "alloc");
+  cuda_check(cudaMalloc(&c->d_itw, P * n * sizeof(ulonglong2)), "alloc");
+  cuda_check(cudaMalloc(&c->d_smod, P * P * 8), "alloc");
+  cuda_check(cudaMalloc(&c->d_pinv, P * P * sizeof(ulonglong2)), "alloc");
+  cuda_check(cudaMemcpy(c->d_primes, pc.data(), P * sizeof(PrimeConst), cudaMemcpyHostToDevice), "upload");
+  cuda_check(cudaMemcpy(c->d_tw, tw.data(), P * n * sizeof(ulonglong2), cudaMemcpyHostToDevice), "upload");
+  cuda_check(cudaMemcpy(c->d_itw, itw.data(), P * n * sizeof(ulonglong2), cudaMemcpyHostToDevice), "upload");
+  cuda_check(cudaMemcpy(c->d_smod, smod.data(), P * P * 8, cudaMemcpyHostToDevice), "upload");
+  cuda_check(cudaMemcpy(c->d_pinv, pinv.data(), P * P * sizeof(ulonglong2), cudaMemcpyHostToDevice), "upload");
+}
+
+void free_context(lcl_context* c) {
+  cudaFree(c->d_primes);
+  cudaFree(c->d_tw);
+  cudaFree(c->d_itw);
+  cudaFree(c->d_smod);
+  cudaFree(c->d_pinv);
+  cudaFree(c->d_pairs);
+  cudaFree(c->d_relin);
+  for (auto& kv : c->d_rot) cudaFree(kv.second);
+  for (auto& kv : c->d_perm) cudaFree(kv.second);
+  for (DevBuf* b : {&c->ws_coef, &c->ws_digits, &c->ws_acc, &c->ws_coefsp, &c->ws_mid,
+                    &c->ws_tern, &c->ws_ctA, &c->ws_ctB, &c->ws_ctC, &c->ws_pt, &c->ws_io_in,
+                    &c->ws_io_sel, &c->ws_io_dist, &c->ws_io_agg})
+    b->release();
+}
+
+u64 key_words(const lcl_context* c) { return (u64)c->full * 2 * c->P() * c->N(); }
+
+u64* upload_key(lcl_context* c, const u64* h, size_t words) {
+  need(h != nullptr, LCL_KEY_ERROR, "null key");
+  need(words == key_words(c), LCL_KEY_ERROR, "switch key has the wrong shape");
+  u64* d = nullptr;
+  cuda_check(cudaMalloc(&d, words * 8), "key alloc");
+  cuda_check(cudaMemcpy(d, h, words * 8, cudaMemcpyHostToDevice), "key upload");
+  return d;
+}
+
+// galois_elt_for_rotation + make_galois_tables (rns.cpp:508-532).
+std::vector<u32> galois_perm(size_t n, int logn, size_t step) {
+  const u64 two_n = 2 * (u64)n;
+  u64 elt = 1;
+  for (size_t i = 0; i < step % (n / 2); ++i) elt = (elt * 5) % two_n;
+  std::vector<u32> p(n);
+  for (size_t i = 0; i < n; ++i) {
+    const u64 e = 2 * (u64)h_brv(i, logn) + 1;
+    const u64 t = (e * elt) % two_n;
+    p[i] = (u32)h_brv((size_t)((t - 1) / 2), logn);
+  }
+  return p;
+}
+
+void check_count(const lcl_context* c, size_t count) {
+  need(count >= 1 && count <= c->full, LCL_BASIS_MISMATCH, "prime count outside the basis");
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* lcl_last_error(void) { return g_last_error.c_str(); }
+
+int lcl_context_create(size_t degree, int depth, int secure, int device, lcl_context** out) {
+  return guarded([&] {
+    need(out != nullptr, LCL_USAGE_ERROR, "null output handle");
+    auto c = std::make_unique<lcl_context>();
+    try {
+      build_context(c.get(), degree, depth, secure, device);
+    } catch (...) {
+      free_context(c.get());
+      throw;
+    }
+    *out = c.release();
+  });
+}
+
+int lcl_context_destroy(lcl_context* ctx) {
+  return guarded([&] {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    cudaDeviceSynchronize();
+    free_context(ctx);
+    delete ctx;
+  });
+}
+
+int lcl_context_primes(const lcl_context* ctx, uint64_t* primes, size_t* full) {
+  return guarded([&] {
+    if (full) *full = ctx->full;
+    if (primes) std::copy(ctx->primes.begin(), ctx->primes.end(), primes);
+  });
+}
+
+int lcl_set_stream(lcl_context* ctx, void* s) {
+  return guarded([&] { ctx->stream = static_cast<cudaStream_t>(s); });
+}
+
+int lcl_synchronize(lcl_context* ctx) {
+  return guarded([&] { cuda_check(cudaStreamSynchronize(ctx->stream), "synchronize"); });
+}
+
+int lcl_get_counts(const lcl_context* ctx, lcl_counts* out) {
+  return guarded([&] { *out = ctx->counts; });
+}
+
+int lcl_reset_counts(lcl_context* ctx) {
+  return guarded([&] { ctx->counts = lcl_counts{}; });
+}
+
+uint64_t lcl_launch_count(const lcl_context* ctx) { return ctx ? ctx->launches : 0; }
+
+int lcl_upload_relin_key(lcl_context* ctx, const uint64_t* h_key, size_t words) {
+  return guarded([&] {
+    cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
+    u64* d = upload_key(ctx, h_key, words);
+    if (ctx->d_relin) cudaFree(ctx->d_relin);
+    ctx->d_relin = d;
+  });
+}
+
+int lcl_upload_rotation_key(lcl_context* ctx, size_t step, const uint64_t* h_key, size_t words) {
+  return guarded([&] {
+    cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
+    step %= ctx->n / 2;
+    need(step != 0, LCL_KEY_ERROR, "rotation step 0 needs no key");
+    u64* d = upload_key(ctx, h_key, words);
+    auto it = ctx->d_rot.find(step);
+    if (it != ctx->d_rot.end()) cudaFree(it->second);
+    ctx->d_rot[step] = d;
+    if (!ctx->d_perm.count(step)) {
+      const std::vector<u32> p = galois_perm(ctx->n, ctx->logn, step);
+      u32* dp = nullptr;
+      cuda_check(cudaMalloc(&dp, p.size() * 4), "perm alloc");
+      cuda_check(cudaMemcpy(dp, p.data(), p.size() * 4, cudaMemcpyHostToDevice), "perm upload");
+      ctx->d_perm[step] = dp;
+    }
+  });
+}
+
+int lcl_has_rotation_key(const lcl_context* ctx, size_t step) {
+  return ctx->d_rot.count(step % (ctx->n / 2)) ? 1 : 0;
+}
+
+int lcl_device_alloc(lcl_context* ctx, size_t bytes, void** d_ptr) {
+  return guarded([&] {
+    cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
+    cuda_check(cudaMalloc(d_ptr, bytes), "cudaMalloc");
+  });
+}
+
+int lcl_device_free(lcl_context* ctx, void* d_ptr) {
+  return guarded([&] { cuda_check(cudaFree(d_ptr), "cudaFree"); (void)ctx; });
+}
+
+int lcl_copy_h2d(lcl_context* ctx, void* d_dst, const void* h_src, size_t bytes) {
+  return guarded([&] {
+    cuda_check(cudaMemcpyAsync(d_dst, h_src, bytes, cudaMemcpyHostToDevice, ctx->stream), "h2d");
+    cuda_check(cudaStreamSynchronize(ctx->stream), "h2d sync");
+  });
+}
+
+int lcl_copy_d2h(lcl_context* ctx, void* h_dst, const void* d_src, size_t bytes) {
+  return guarded([&] {
+    cuda_check(cudaMemcpyAsync(h_dst, d_src, bytes, cudaMemcpyDeviceToHost, ctx->stream), "d2h");
+    cuda_check(cudaStreamSynchronize(ctx->stream), "d2h sync");
+  });
+}
+
+static int ntt_common(lcl_context* ctx, uint64_t* d, size_t items, size_t count, int sp, bool inv) {
+  return guarded([&] {
+    check_count(ctx, count);
+    const u32 rpi = (u32)count + (sp ? 1 : 0);
+    std::vector<u32> p(rpi);
+    for (u32 i = 0; i < rpi; ++i) p[i] = i < count ? i : ctx->full;
+    const RowMap m = make_map(d, rpi, ctx->N(), (u64)rpi * ctx->N(), 1, 0, p);
+    const u32 rows = (u32)(items * rpi);
+    if (inv)
+      launch_inv(ctx, rows, m, PlainStore{m});
+    else
+      launch_fwd(ctx, rows, m, PlainLoad{m}, PlainStore{m});
+  });
+}
+
+int lcl_ntt_forward(lcl_context* ctx, uint64_t* d, size_t items, size_t count, int sp) {
+  return ntt_common(ctx, d, items, count, sp, false);
+}
+int lcl_ntt_inverse(lcl_context* ctx, uint64_t* d, size_t items, size_t count, int sp) {
+  return ntt_common(ctx, d, items, count, sp, true);
+}
+
+static int addsub(lcl_context* ctx, const uint64_t* a, const uint64_t* b, size_t batch,
+                  size_t count, uint64_t* out, bool sub) {
+  return guarded([&] {
+    check_count(ctx, count);
+    const u32 m = (u32)count;
+    const u64 N = ctx->N();
+    const RowMap o = ct_map(out, m, N, 2ull * m * N), x = ct_map(a, m, N, 2ull * m * N),
+                 y = ct_map(b, m, N, 2ull * m * N);
+    const u32 rows = (u32)(batch * 2 * m);
+    const u32 grid = (u32)(((u64)rows * N + 255) / 256);
+    if (sub)
+      rows_addsub<true><<<grid, 256, 0, ctx->stream>>>(o, x, y, rows, ctx->logn, ctx->d_primes);
+    else
+      rows_addsub<false><<<grid, 256, 0, ctx->stream>>>(o, x, y, rows, ctx->logn, ctx->d_primes);
+    post_launch(ctx);
+    ctx->counts.additions += batch;
+  });
+}
+
+int lcl_hadd(lcl_context* ctx, const uint64_t* a, const uint64_t* b, size_t batch, size_t count,
+             uint64_t* out) {
+  return addsub(ctx, a, b, batch, count, out, false);
+}
+int lcl_hsub(lcl_context* ctx, const uint64_t* a, const uint64_t* b, size_t batch, size_t count,
+             uint64_t* out) {
+  return addsub(ctx, a, b, batch, count, out, true);
+}
+
+int lcl_relinearize(lcl_context* ctx, const uint64_t* d_tern, size_t batch, size_t count,
+                    uint64_t* d_out) {
+  return guarded([&] {
+    check_count(ctx, count);
+    relinearize_batch(ctx, d_tern, (u32)batch, (u32)count, d_out);
+  });
+}
+
+int lcl_rescale(lcl_context* ctx, const uint64_t* d_ct, size_t batch, size_t count,
+                uint64_t* d_out) {
+  return guarded([&] {
+    check_count(ctx, count);
+    rescale_batch(ctx, d_ct, (u32)batch, (u32)count, d_out);
+  });
+}
+
+int lcl_rotate(lcl_context* ctx, const uint64_t* d_ct, size_t batch, size_t count, size_t step,
+               uint64_t* d_out) {
+  return guarded([&] {
+    check_count(ctx, count);
+    step = norm_step(ctx, step);
+    const u64 words = (u64)batch * 2 * count * ctx->N();
+    if (step == 0) {
+      cuda_check(cudaMemcpyAsync(d_out, d_ct, words * 8, cudaMemcpyDeviceToDevice, ctx->stream), "copy");
+      return;
+    }
+    rotate_level(ctx, d_ct, (u32)batch, (u32)count, step, d_out, false);
+  });
+}
+
+int lcl_hoisted_rotations(lcl_context* ctx, const uint64_t* d_ct, size_t batch, size_t count,
+                          const size_t* h_steps, size_t nsteps, uint64_t* d_outs) {
+  return guarded([&] {
+    check_count(ctx, count);
+    const u32 B = (u32)batch, m = (u32)count;
+    const u64 N = ctx->N();
+    const u64 words = (u64)B * 2 * m * N;
+    u64* dig = nullptr;
+    for (size_t s = 0; s < nsteps; ++s) {
+      const size_t st = norm_step(ctx, h_steps[s]);
+      u64* o = d_outs + s * words;
+      if (st == 0) {
+        cuda_check(cudaMemcpyAsync(o, d_ct, words * 8, cudaMemcpyDeviceToDevice, ctx->stream), "copy");
+        continue;
+      }
+      const u64* key = rot_key(ctx, st);
+      if (!dig) {
+        const RowMap c1 = make_map(d_ct + (u64)m * N, m, N, 2ull * m * N, 1, 0, ctx->primes_0(m));
+        dig = ks_decompose(ctx, c1, B, m);
+        ctx->counts.mod_ups += B;
+      }
+      u64* acc = ks_ip(ctx, dig, B, m, key, ctx->d_perm.at(st));
+      ks_moddown(ctx, acc, B, m, ct_map(o, m, N, 2ull * m * N), null_map(),
+                 ct_map(d_ct, m, N, 2ull * m * N), ctx->d_perm.at(st));
+      ctx->counts.rotations += B;
+    }
+  });
+}
+
+int lcl_slot_reduce(lcl_context* ctx, const uint64_t* d_ct, size_t batch, size_t count,
+                    size_t width, size_t k, uint64_t* d_out) {
+  return guarded([&] {
+    check_count(ctx, count);
+    slot_reduce_batch(ctx, d_ct, (u32)batch, (u32)count, width, k, d_out);
+  });
+}
+
+int lcl_mult_plain_const(lcl_context* ctx, const uint64_t* d_ct, size_t batch, size_t count,
+                         double value, double pt_scale, uint64_t* d_out) {
+  return guarded([&] {
+    check_count(ctx, count);
+    const u32 m = (u32)count;
+    const u64 N = ctx->N();
+    std::vector<double> v(ctx->n / 2, value);
+    const std::vector<long long> rounded = h_encode_rounded(v, ctx->n, pt_scale);
+    std::vector<u64> pt((u64)m * N);
+    for (u32 r = 0; r < m; ++r) {
+      const u64 q = ctx->primes[r];
+      for (u64 i = 0; i < N; ++i) {
+        const long long x = rounded[i];
+        const u64 mag = (u64)(x < 0 ? -x : x) % q;
+        pt[r * N + i] = x < 0 ? (mag == 0 ? 0 : q - mag) : mag;
+      }
+    }
+    u64* d_pt = ctx->ws_pt.get(pt.size());
+    cuda_check(cudaMemcpyAsync(d_pt, pt.data(), pt.size() * 8, cudaMemcpyHostToDevice, ctx->stream), "pt");
+    const RowMap ptm = make_map(d_pt, m, N, (u64)m * N, 1, 0, ctx->primes_0(m));
+    launch_fwd(ctx, m, ptm, PlainLoad{ptm}, PlainStore{ptm});
+    const u64 total = (u64)batch * 2 * m * N;
+    mult_plain<<<(u32)((total + 255) / 256), 256, 0, ctx->stream>>>(d_ct, d_pt, (u32)batch, m,
+                                                                    ctx->logn, d_out, ctx->d_primes);
+    post_launch(ctx);
+    cuda_check(cudaStreamSynchronize(ctx->stream), "mult_plain");
+    ctx->counts.multiplications += batch;
+  });
+}
+
+int lcl_pairwise_distance(lcl_context* ctx, const uint64_t* d_a, const uint64_t* d_b,
+                          size_t chunks, int lazy, uint64_t* d_out) {
+  return guarded([&] {
+    // Two "clients" laid out as [2][chunks][...] are required by the pair
+    // kernel; stage them contiguously.
+    const u32 m = ctx->full;
+    const u64 ctw = 2ull * m * ctx->N();
+    u64* both = ctx->ws_io_in.get(2 * chunks * ctw);
+    cuda_check(cudaMemcpyAsync(both, d_a, chunks * ctw * 8, cudaMemcpyDeviceToDevice, ctx->stream), "copy");
+    cuda_check(cudaMemcpyAsync(both + chunks * ctw, d_b, chunks * ctw * 8, cudaMemcpyDeviceToDevice, ctx->stream), "copy");
+    distance_matrix(ctx, both, 2, (u32)chunks, 1, 1, lazy != 0, false, d_out);
+  });
+}
+
+int lcl_distance_matrix(lcl_context* ctx, const uint64_t* d_clients, size_t n, size_t chunks,
+                        double in_scale, size_t width, size_t k, int lazy, int reduce,
+                        uint64_t* d_out, double* out_scale) {
+  return guarded([&] {
+    need(chunks >= 1, LCL_SHAPE_ERROR, "empty weight vector");
+    distance_matrix(ctx, d_clients, (u32)n, (u32)chunks, width, k, lazy != 0, reduce != 0, d_out);
+    if (out_scale) *out_scale = (in_scale * in_scale) / (double)ctx->primes[ctx->full - 1];
+  });
+}
+
+int lcl_masked_aggregate(lcl_context* ctx, const uint64_t* d_clients, const uint64_t* d_sel,
+                         size_t n, size_t chunks, double w_scale, double sel_scale, size_t l,
+                         int average, uint64_t* d_out, double* out_scale) {
+  return guarded([&] {
+    need(chunks >= 1, LCL_SHAPE_ERROR, "empty weight vector");
+    masked_aggregate(ctx, d_clients, d_sel, (u32)n, (u32)chunks, l, average != 0, d_out);
+    if (out_scale) {
+      double s = (w_scale * sel_scale) / (double)ctx->primes[ctx->full - 1];
+      if (average) s = (s * ctx->scale) / (double)ctx->primes[ctx->full - 2];
+      *out_scale = s;
+    }
+  });
+}
+
+int lcl_server_round_host(lcl_context* ctx, const uint64_t* h_clients, const uint64_t* h_sel,
+                          size_t n, size_t chunks, double in_scale, size_t width, size_t k,
+                          size_t l, int average, uint64_t* h_dist, uint64_t* h_agg) {
+  return guarded([&] {
+    const u32 m = ctx->full;
+    const u64 N = ctx->N();
+    const u64 cw = (u64)n * chunks * 2 * m * N, sw = (u64)n * 2 * m * N;
+    const u64 dw = (u64)n * (n - 1) / 2 * 2 * (m - 1) * N;
+    const u64 aw = (u64)chunks * 2 * (average ? m - 2 : m - 1) * N;
+    u64* dc = ctx->ws_io_in.get(cw);
+    u64* ds = ctx->ws_io_sel.get(sw);
+    u64* dd = ctx->ws_io_dist.get(dw);
+    u64* da = ctx->ws_io_agg.get(aw);
+    cuda_check(cudaMemcpyAsync(dc, h_clients, cw * 8, cudaMemcpyHostToDevice, ctx->stream), "h2d");
+    cuda_check(cudaMemcpyAsync(ds, h_sel, sw * 8, cudaMemcpyHostToDevice, ctx->stream), "h2d");
+    distance_matrix(ctx, dc, (u32)n, (u32)chunks, width, k, true, true, dd);
+    masked_aggregate(ctx, dc, ds, (u32)n, (u32)chunks, l, average != 0, da);
+    cuda_check(cudaMemcpyAsync(h_dist, dd, dw * 8, cudaMemcpyDeviceToHost, ctx->stream), "d2h");
+    cuda_check(cudaMemcpyAsync(h_agg, da, aw * 8, cudaMemcpyDeviceToHost, ctx->stream), "d2h");
+    cuda_check(cudaStreamSynchronize(ctx->stream), "round sync");
+    (void)in_scale;
+  });
+}
+
+}  // extern "C"

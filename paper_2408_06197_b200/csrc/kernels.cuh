@@ -1,0 +1,222 @@
+// Tensor, accumulation and key inner-product kernels for the server path.
+#pragma once
+
+#include "common.cuh"
+
+namespace lcl {
+
+// ------------------------------------------------------------------------
+// Pairwise lazy accumulation (distance.cpp:107-127 lazy branch):
+//   for every pair (i, j) and chunk c:  e = a_i[c] - a_j[c]  (hsub)
+//   d0 += e0^2, d1 += 2 e0 e1, d2 += e1^2                   (hsquare + lazy_accumulate)
+// All C chunks of all pairs are folded into split-23 partial sums in
+// registers and reduced once, so the ternary accumulator is written once and
+// every client word is read once per CTA (client tile staged in shared memory
+// and reused by every pair in the CTA).
+//
+// CTA: 32 consecutive slots of one limb row r; warp w, lane e handles PP pairs
+// of that slot. Grid: x = m * N / 32 slot tiles, y = pair groups.
+// clients: [n][C][2][m][N]; tern out: [pairs][3][m][N] (pair p at out + (p - p0) * 3mN).
+template <int PP>
+__global__ void __launch_bounds__(256)
+    pair_accumulate(const u64* __restrict__ clients, u32 n, u32 c_begin, u32 c_end,
+                    u32 chunks_total, u32 m, u32 logn, const u32* __restrict__ pairs,
+                    u32 p_begin, u32 p_end, u64* __restrict__ tern, int accumulate,
+                    const PrimeConst* __restrict__ primes) {
+  extern __shared__ u64 tile[];  // [n][2][32]
+  const u32 N = 1u << logn;
+  const u32 tiles_per_row = N >> 5;
+  const u32 r = blockIdx.x / tiles_per_row;
+  const u32 a0 = (blockIdx.x - r * tiles_per_row) << 5;
+  const u32 lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const u32 nwarps = blockDim.x >> 5;
+  const PrimeConst P = primes[r];
+  const u64 q = P.q;
+  const u64 ct_words = 2ull * m * N;
+  const u32 pbase = p_begin + (blockIdx.y * nwarps + warp) * PP;
+
+  u32 pi[PP], pj[PP];
+#pragma unroll
+  for (int t = 0; t < PP; ++t) {
+    const u32 p = pbase + t;
+    const u32 pk = p < p_end ? __ldg(pairs + p) : 0u;
+    pi[t] = pk & 0xFFFFu;
+    pj[t] = pk >> 16;
+  }
+  Acc3 A00[PP], A01[PP], A11[PP];
+#pragma unroll
+  for (int t = 0; t < PP; ++t) {
+    A00[t].zero();
+    A01[t].zero();
+    A11[t].zero();
+  }
+  for (u32 c = c_begin; c < c_end; ++c) {
+    __syncthreads();
+    for (u32 v = threadIdx.x; v < n * 64; v += blockDim.x) {
+      const u32 cl = v >> 6, h = (v >> 5) & 1, e = v & 31;
+      tile[v] = __ldg(clients + ((u64)cl * chunks_total + c) * ct_words + (u64)h * m * N +
+                      (u64)r * N + a0 + e);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int t = 0; t < PP; ++t) {
+      const u64 x0 = tile[pi[t] * 64 + lane], x1 = tile[pi[t] * 64 + 32 + lane];
+      const u64 y0 = tile[pj[t] * 64 + lane], y1 = tile[pj[t] * 64 + 32 + lane];
+      const Split e0 = split23(x0 - y0 + q), e1 = split23(x1 - y1 + q);
+      A00[t].sq(e0);
+      A01[t].mac(e0, e1);
+      A11[t].sq(e1);
+    }
+  }
+#pragma unroll
+  for (int t = 0; t < PP; ++t) {
+    const u32 p = pbase + t;
+    if (p >= p_end) break;
+    u64* o = tern + (u64)(p - p_begin) * 3 * m * N + (u64)r * N + a0 + lane;
+    u64 d0 = A00[t].reduce(P);
+    u64 d1 = A01[t].reduce(P);
+    d1 = add_mod(d1, d1, q);
+    u64 d2 = A11[t].reduce(P);
+    if (accumulate) {
+      d0 = add_mod(d0, o[0], q);
+      d1 = add_mod(d1, o[(u64)m * N], q);
+      d2 = add_mod(d2, o[2ull * m * N], q);
+    }
+    o[0] = d0;
+    o[(u64)m * N] = d1;
+    o[2ull * m * N] = d2;
+  }
+}
+
+// ------------------------------------------------------------------------
+// Masked aggregation tensor (aggregation.cpp:205-219): per chunk ch,
+//   sum_i hmult_triple(w_i[ch], sel_i) with Karatsuba d1 = (w0+w1)(s0+s1) - d0 - d2,
+// lazily accumulated over the n clients, reduced once. A thread owns one slot
+// of one limb for CK consecutive chunks and reuses the selector words.
+// clients: [n][C][2][m][N]; sel: [n][2][m][N]; tern: [C][3][m][N].
+template <int CK>
+__global__ void __launch_bounds__(256)
+    aggregate_tensor(const u64* __restrict__ clients, const u64* __restrict__ sel, u32 n,
+                     u32 chunks_total, u32 c_begin, u32 chunks, u32 m, u32 logn,
+                     u64* __restrict__ tern, const PrimeConst* __restrict__ primes) {
+  const u32 N = 1u << logn;
+  const u64 gid = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  const u64 slots = (u64)m * N;
+  const u32 cgroup = (u32)(gid / slots);
+  const u32 rem = (u32)(gid - (u64)cgroup * slots);
+  const u32 r = rem >> logn, a = rem & (N - 1);
+  const u32 c0 = cgroup * CK;
+  if (c0 >= chunks) return;
+  const PrimeConst P = primes[r];
+  const u64 q = P.q;
+  const u64 ct_words = 2ull * m * N;
+  Acc3 D0[CK], D1[CK], D2[CK];
+#pragma unroll
+  for (int k = 0; k < CK; ++k) {
+    D0[k].zero();
+    D1[k].zero();
+    D2[k].zero();
+  }
+  for (u32 i = 0; i < n; ++i) {
+    const u64* s = sel + (u64)i * ct_words + (u64)r * N + a;
+    const u64 s0 = __ldg(s), s1 = __ldg(s + slots);
+    const Split S0 = split23(s0), S1 = split23(s1), SS = split23(s0 + s1);
+#pragma unroll
+    for (int k = 0; k < CK; ++k) {
+      if (c0 + k < chunks) {
+        const u64* w =
+            clients + ((u64)i * chunks_total + c_begin + c0 + k) * ct_words + (u64)r * N + a;
+        const u64 w0 = __ldg(w), w1 = __ldg(w + slots);
+        D0[k].mac(split23(w0), S0);
+        D2[k].mac(split23(w1), S1);
+        D1[k].mac(split23(w0 + w1), SS);
+      }
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < CK; ++k) {
+    if (c0 + k >= chunks) break;
+    u64* o = tern + (u64)(c0 + k) * 3 * slots + (u64)r * N + a;
+    const u64 d0 = D0[k].reduce(P), d2 = D2[k].reduce(P);
+    const u64 d1 = sub_mod(sub_mod(D1[k].reduce(P), d0, q), d2, q);
+    o[0] = d0;
+    o[slots] = d1;
+    o[2 * slots] = d2;
+  }
+}
+
+// ------------------------------------------------------------------------
+// Key inner product (ckks.cpp:490-518 without the ModDown):
+//   acc_x[b][r][a] = sum_j digit_j[b][r][g(a)] * key_x[j][kr][a],  g = perm or identity
+// digits: [B][m][m+1][N]; key: [full][2][full+1][N]; acc: [B][2][m+1][N].
+// A thread owns one slot of one target row and walks the batch, so every key
+// word is read once per launch (all B ciphertexts share the key).
+__global__ void __launch_bounds__(256)
+    ks_inner_product(const u64* __restrict__ digits, u32 B, u32 m, const u64* __restrict__ key,
+                     u32 full, const u32* __restrict__ perm, u64* __restrict__ acc, u32 logn,
+                     const PrimeConst* __restrict__ primes) {
+  const u32 N = 1u << logn;
+  const u32 gid = blockIdx.x * blockDim.x + threadIdx.x;
+  const u32 r = gid >> logn, a = gid & (N - 1);
+  if (r > m) return;
+  const u32 kr = r < m ? r : full;
+  const PrimeConst P = primes[kr];
+  const u64 kstride = (u64)(full + 1) * N;
+  u64 k0[LCL_MAXP], k1[LCL_MAXP];
+#pragma unroll
+  for (u32 j = 0; j < LCL_MAXP; ++j) {
+    if (j < m) {
+      k0[j] = __ldg(key + (2ull * j) * kstride + (u64)kr * N + a);
+      k1[j] = __ldg(key + (2ull * j + 1) * kstride + (u64)kr * N + a);
+    }
+  }
+  const u32 g = perm ? __ldg(perm + a) : a;
+  const u64 dstride = (u64)(m + 1) * N;
+  for (u32 b = 0; b < B; ++b) {
+    const u64* d = digits + (u64)b * m * dstride + (u64)r * N + g;
+    u64 l0 = 0, h0 = 0, l1 = 0, h1 = 0;
+#pragma unroll
+    for (u32 j = 0; j < LCL_MAXP; ++j) {
+      if (j < m) {
+        const u64 v = __ldg(d + j * dstride);
+        mac128(l0, h0, v, k0[j]);
+        mac128(l1, h1, v, k1[j]);
+      }
+    }
+    u64* o = acc + (u64)b * 2 * dstride + (u64)r * N + a;
+    o[0] = reduce128(l0, h0, P);
+    o[dstride] = reduce128(l1, h1, P);
+  }
+}
+
+// ------------------------------------------------------------------------
+// ct x pt (ckks.cpp:549-558): out[b][x][i][a] = ct[b][x][i][a] * pt[i][a].
+__global__ void __launch_bounds__(256)
+    mult_plain(const u64* __restrict__ ct, const u64* __restrict__ pt, u32 B, u32 m, u32 logn,
+               u64* __restrict__ out, const PrimeConst* __restrict__ primes) {
+  const u32 N = 1u << logn;
+  const u64 gid = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  const u64 total = (u64)B * 2 * m * N;
+  if (gid >= total) return;
+  const u32 a = (u32)(gid & (N - 1));
+  const u32 i = (u32)((gid >> logn) % m);
+  const PrimeConst P = primes[i];
+  out[gid] = mul_mod(__ldg(ct + gid), __ldg(pt + (u64)i * N + a), P);
+}
+
+// Elementwise add / sub over ciphertext batches with RowMap addressing.
+template <bool SUB>
+__global__ void __launch_bounds__(256)
+    rows_addsub(const __grid_constant__ RowMap out, const __grid_constant__ RowMap a,
+                const __grid_constant__ RowMap b, u32 rows, u32 logn,
+                const PrimeConst* __restrict__ primes) {
+  const u32 N = 1u << logn;
+  const u64 gid = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gid >= (u64)rows * N) return;
+  const u32 r = (u32)(gid >> logn), k = (u32)(gid & (N - 1));
+  const u64 q = primes[row_prime(out, r)].q;
+  const u64 x = row_ptr(a, r)[k], y = row_ptr(b, r)[k];
+  row_ptr(out, r)[k] = SUB ? sub_mod(x, y, q) : add_mod(x, y, q);
+}
+
+}  // namespace lcl

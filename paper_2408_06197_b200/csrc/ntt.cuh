@@ -1,0 +1,393 @@
+// Negacyclic NTT over 64-bit primes for sm_100a.
+//
+// Mathematically identical to the reference transforms
+// (proj/core/src/rns.cpp:140-181): forward = Cooley-Tukey with the
+// bit-reversed psi-power table root[m + i] (natural order in, bit-reversed
+// evaluation order out: index i holds a(psi^(2 brv(i) + 1))); inverse =
+// Gentleman-Sande with the inverse table, then x N^-1. Because every output
+// is fully reduced, the GPU factorisation below produces the same words.
+//
+// Factorisation for N = N1 * N2 (N2 = 256): element a = j + t*N2.
+//   * The first log2(N1) CT stages pair rows t, t + N1/(2m) of each column j
+//     with twiddle root[m + (t*m/N1)]: an N1-point NTT per column with the
+//     table prefix root[1 .. N1-1]                        -> col pass
+//   * The last log2(N2) stages stay inside block b = a / N2 and use
+//     root[m'(N1 + b) + i'] at local stage m'              -> block pass
+// The inverse runs the block pass first, then the column pass, fusing the
+// N^-1 scaling into the column pass's store.
+//
+// Arithmetic: Harvey lazy butterflies. Forward values live in [0, 4q),
+// inverse values in [0, 2q); twiddles are (w, floor(w 2^64 / q)) pairs.
+// One HBM round trip per pass; shared memory only carries the transpose
+// inside each pass. Loader / epilogue functors fuse the ModUp lift, the
+// ModDown / rescale divide-and-round and the key-switch output adds into the
+// first / last pass, so no standalone elementwise kernel touches HBM.
+#pragma once
+
+#include <type_traits>
+
+#include "common.cuh"
+
+namespace lcl {
+
+struct Tw {
+  u64 w, ws;
+};
+
+__device__ __forceinline__ Tw ldtw(const ulonglong2* t, u32 idx) {
+  const ulonglong2 v = __ldg(t + idx);
+  return Tw{v.x, v.y};
+}
+
+// Forward CT butterfly: x, y in [0, 4q) -> x', y' in [0, 4q).
+__device__ __forceinline__ void ct_bfly(u64& x, u64& y, Tw w, u64 q, u64 two_q) {
+  const u64 a = x >= two_q ? x - two_q : x;
+  const u64 t = mul_shoup_lazy(y, w.w, w.ws, q);
+  x = a + t;
+  y = a - t + two_q;
+}
+
+// Inverse GS butterfly: x, y in [0, 2q) -> x', y' in [0, 2q).
+__device__ __forceinline__ void gs_bfly(u64& x, u64& y, Tw w, u64 q, u64 two_q) {
+  const u64 a = x, b = y;
+  const u64 s = a + b;
+  x = s >= two_q ? s - two_q : s;
+  y = mul_shoup_lazy(a - b + two_q, w.w, w.ws, q);
+}
+
+__device__ __forceinline__ u64 reduce_4q(u64 x, u64 q, u64 two_q) {
+  x = x >= two_q ? x - two_q : x;
+  return x >= q ? x - q : x;
+}
+
+// ------------------------------------------------------------ loaders
+// Loader(r, a, dst_prime_index, dst) -> value in [0, q) (or any < 4q).
+struct PlainLoad {
+  RowMap in;
+  __device__ __forceinline__ u64 operator()(u32 r, u32 a, u32, const PrimeConst&) const {
+    return __ldg(row_ptr(in, r) + a);
+  }
+};
+
+// Centred lift of a coefficient-domain source row into the destination prime
+// (single-prime mod_up branch, rns.cpp:367-383; the lift inside
+// divide_and_round_by_last, rns.cpp:484-494). Destination row r of a launch
+// reads source row  (r / rows_per_item) * src_item_stride + ((r % rows_per_item) / fan) * n.
+struct LiftLoad {
+  RowMap src;                // source rows: rows_per_item / fan per destination item
+  u32 rows_per_item;         // destination rows per item
+  u32 fan;                   // destination rows per source row
+  u32 nprimes;               // full + 1
+  const PrimeConst* primes;  // device table
+  const u64* smod;           // smod[s * nprimes + d] = q_s mod q_d
+  __device__ __forceinline__ u64 operator()(u32 r, u32 a, u32 dpi, const PrimeConst& dst) const {
+    const u32 item = r / rows_per_item;
+    const u32 sub = (r - item * rows_per_item) / fan;
+    const u32 srow = item * (rows_per_item / fan) + sub;
+    const u32 sp = row_prime(src, srow);
+    const u64 v = __ldg(row_ptr(src, srow) + a);
+    u64 x = reduce64(v, dst);
+    if (v > __ldg(&primes[sp].half)) x = sub_mod(x, __ldg(smod + sp * nprimes + dpi), dst.q);
+    return x;
+  }
+};
+
+// ------------------------------------------------------------ epilogues
+// Epilogue(r, a, value in [0, q), dst_prime_index, dst)
+struct PlainStore {
+  RowMap out;
+  __device__ __forceinline__ void operator()(u32 r, u32 a, u64 v, u32, const PrimeConst&) const {
+    row_ptr(out, r)[a] = v;
+  }
+};
+
+// Divide-and-round output (rns.cpp:496-505) fused with the key-switch output
+// additions:  out = (x - lift) * p^-1  [+ add1[a]]  [+ add2[perm[a]] on the
+// first item of every group, i.e. the c0 half]. add2 must not alias out
+// (gathered reads); add1 may alias out (same thread reads then writes one word).
+struct DivRoundStore {
+  RowMap out;
+  RowMap x;
+  RowMap add1;  // base == nullptr: absent
+  RowMap add2;  // base == nullptr: absent
+  const u32* perm;  // gather for add2 (nullptr: identity)
+  const ulonglong2* pinv;  // indexed by destination prime: (p^-1 mod q, shoup)
+  __device__ __forceinline__ void operator()(u32 r, u32 a, u64 lift, u32 dpi,
+                                             const PrimeConst& P) const {
+    const ulonglong2 iv = __ldg(pinv + dpi);
+    const u64 xv = row_ptr(x, r)[a];
+    u64 v = mul_shoup(xv - lift + P.q, iv.x, iv.y, P.q);
+    if (add1.base) v = add_mod(v, row_ptr(add1, r)[a], P.q);
+    if (add2.base && ((r / out.rows_per_item) % out.items_per_group) == 0) {
+      const u32 src = perm ? __ldg(perm + a) : a;
+      v = add_mod(v, row_ptr(add2, r)[src], P.q);
+    }
+    row_ptr(out, r)[a] = v;
+  }
+};
+
+// ------------------------------------------------------------ stage helpers
+// Compile-time stage iteration: every register index below is a constant, so
+// the 16/32-element tiles stay in registers (no local-memory arrays).
+template <int I, int END, int STEP, class F>
+__device__ __forceinline__ void static_for(F&& f) {
+  if constexpr (I != END) {
+    f(std::integral_constant<int, I>{});
+    static_for<I + STEP, END, STEP>(f);
+  }
+}
+
+// One radix-2 stage over a register tile: groups of 2D consecutive elements,
+// butterflies (g*2D + e, g*2D + e + D); twf(g) gives the group's twiddle.
+template <int E, int D, class TwF>
+__device__ __forceinline__ void ct_stage(u64 (&x)[E], const TwF& twf, u64 q, u64 two_q) {
+#pragma unroll
+  for (int g = 0; g < E / (2 * D); ++g) {
+    const Tw w = twf(g);
+#pragma unroll
+    for (int e = 0; e < D; ++e) ct_bfly(x[g * 2 * D + e], x[g * 2 * D + e + D], w, q, two_q);
+  }
+}
+template <int E, int D, class TwF>
+__device__ __forceinline__ void gs_stage(u64 (&x)[E], const TwF& twf, u64 q, u64 two_q) {
+#pragma unroll
+  for (int g = 0; g < E / (2 * D); ++g) {
+    const Tw w = twf(g);
+#pragma unroll
+    for (int e = 0; e < D; ++e) gs_bfly(x[g * 2 * D + e], x[g * 2 * D + e + D], w, q, two_q);
+  }
+}
+
+// ------------------------------------------------------------ kernels
+// Column pass, forward. CTA = 16 consecutive columns x N1 rows of one row-poly.
+// Thread (c, k): column c, rows k + R e (phase 1, log2 E stages in registers),
+// then rows k E + e (phase 2, log2 R stages) after one shared transpose.
+template <int LOGN1, int E, class Loader>
+__global__ void __launch_bounds__(16 * ((1 << LOGN1) / E))
+    ntt_col_fwd(const __grid_constant__ RowMap out, const __grid_constant__ Loader ld,
+                const ulonglong2* __restrict__ tw_all, const PrimeConst* __restrict__ primes,
+                u32 logn) {
+  constexpr int N1 = 1 << LOGN1;
+  constexpr int R = N1 / E;
+  constexpr int LOGE = __builtin_ctz(E);
+  extern __shared__ u64 sm[];  // [N1][16]
+  const u32 n = 1u << logn;
+  const u32 n2 = n >> LOGN1;
+  const u32 groups = n2 >> 4;
+  const u32 r = blockIdx.x / groups;
+  const u32 g = blockIdx.x - r * groups;
+  const u32 c = threadIdx.x & 15, k = threadIdx.x >> 4;
+  const u32 j = (g << 4) + c;
+  const u32 pi = row_prime(out, r);
+  const PrimeConst P = primes[pi];
+  const ulonglong2* tw = tw_all + (u64)pi * n;
+  u64 x[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) x[e] = ld(r, j + (k + R * e) * n2, pi, P);
+  // phase 1: m = 1 .. E/2; group g of a stage is twiddle root[m + g]
+  static_for<0, LOGE, 1>([&](auto LM) {
+    constexpr int lm = decltype(LM)::value;
+    ct_stage<E, (E >> (lm + 1))>(x, [&](int gi) { return ldtw(tw, (1 << lm) + gi); }, P.q, P.two_q);
+  });
+#pragma unroll
+  for (int e = 0; e < E; ++e) sm[(k + R * e) * 16 + c] = x[e];
+  __syncthreads();
+#pragma unroll
+  for (int e = 0; e < E; ++e) x[e] = sm[(k * E + e) * 16 + c];
+  // phase 2: m = E .. N1/2 on rows t = kE + e; distance N1/(2m) < R <= E
+  static_for<LOGE, LOGN1, 1>([&](auto LM) {
+    constexpr int lm = decltype(LM)::value;
+    constexpr int d = N1 >> (lm + 1);
+    ct_stage<E, d>(x, [&](int gi) { return ldtw(tw, (1 << lm) + ((k * E + gi * 2 * d) >> (LOGN1 - lm))); },
+                   P.q, P.two_q);
+  });
+  u64* o = row_ptr(out, r);
+#pragma unroll
+  for (int e = 0; e < E; ++e) o[j + (k * E + e) * n2] = x[e];
+}
+
+// Block pass, forward: 256-point blocks, 16 threads per block, 16 elements per
+// thread, 4 blocks per CTA. Phase 1 on s = l + 16 e, phase 2 on s = 16 l + e.
+template <int LOGN1, class Epi>
+__global__ void __launch_bounds__(64)
+    ntt_blk_fwd(const __grid_constant__ RowMap in, const __grid_constant__ Epi epi,
+                const ulonglong2* __restrict__ tw_all, const PrimeConst* __restrict__ primes,
+                u32 logn) {
+  constexpr int N1 = 1 << LOGN1;
+  __shared__ u64 sm[4][256 + 16];
+  const u32 n = 1u << logn;
+  const u32 l = threadIdx.x & 15, bw = threadIdx.x >> 4;
+  const u32 blk_global = blockIdx.x * 4 + bw;
+  const u32 r = blk_global / N1;
+  const u32 b = blk_global - r * N1;
+  const u32 pi = row_prime(in, r);
+  const PrimeConst P = primes[pi];
+  const ulonglong2* tw = tw_all + (u64)pi * n;
+  const u64* src = row_ptr(in, r) + (b << 8);
+  u64 x[16];
+#pragma unroll
+  for (int e = 0; e < 16; ++e) x[e] = src[l + 16 * e];
+  static_for<0, 4, 1>([&](auto LM) {
+    constexpr int lm = decltype(LM)::value;
+    ct_stage<16, (16 >> (lm + 1))>(x, [&](int gi) { return ldtw(tw, (N1 + b) * (1 << lm) + gi); },
+                                   P.q, P.two_q);
+  });
+  u64* s = sm[bw];
+#pragma unroll
+  for (int e = 0; e < 16; ++e) s[l + 16 * e + e] = x[e];
+  __syncwarp();
+#pragma unroll
+  for (int e = 0; e < 16; ++e) x[e] = s[16 * l + e + l];
+  static_for<4, 8, 1>([&](auto LM) {
+    constexpr int lm = decltype(LM)::value;
+    constexpr int d = 256 >> (lm + 1);
+    ct_stage<16, d>(x,
+                    [&](int gi) { return ldtw(tw, (N1 + b) * (1 << lm) + ((16 * l + gi * 2 * d) >> (8 - lm))); },
+                    P.q, P.two_q);
+  });
+  __syncwarp();
+#pragma unroll
+  for (int e = 0; e < 16; ++e) s[16 * l + e + l] = reduce_4q(x[e], P.q, P.two_q);
+  __syncwarp();
+#pragma unroll
+  for (int e = 0; e < 16; ++e) epi(r, (b << 8) + l + 16 * e, s[l + 16 * e + e], pi, P);
+}
+
+// Block pass, inverse: GS stages m = N/2 .. N1 (local m' = 128 .. 1).
+template <int LOGN1>
+__global__ void __launch_bounds__(64)
+    ntt_blk_inv(const __grid_constant__ RowMap in, const __grid_constant__ RowMap out,
+                const ulonglong2* __restrict__ itw_all, const PrimeConst* __restrict__ primes,
+                u32 logn) {
+  constexpr int N1 = 1 << LOGN1;
+  __shared__ u64 sm[4][256 + 16];
+  const u32 n = 1u << logn;
+  const u32 l = threadIdx.x & 15, bw = threadIdx.x >> 4;
+  const u32 blk_global = blockIdx.x * 4 + bw;
+  const u32 r = blk_global / N1;
+  const u32 b = blk_global - r * N1;
+  const u32 pi = row_prime(in, r);
+  const PrimeConst P = primes[pi];
+  const ulonglong2* tw = itw_all + (u64)pi * n;
+  const u64* src = row_ptr(in, r) + (b << 8);
+  u64* s = sm[bw];
+  u64 x[16];
+#pragma unroll
+  for (int e = 0; e < 16; ++e) s[l + 16 * e + e] = src[l + 16 * e];
+  __syncwarp();
+#pragma unroll
+  for (int e = 0; e < 16; ++e) x[e] = s[16 * l + e + l];
+  static_for<7, 3, -1>([&](auto LM) {
+    constexpr int lm = decltype(LM)::value;
+    constexpr int d = 256 >> (lm + 1);
+    gs_stage<16, d>(x,
+                    [&](int gi) { return ldtw(tw, (N1 + b) * (1 << lm) + ((16 * l + gi * 2 * d) >> (8 - lm))); },
+                    P.q, P.two_q);
+  });
+  __syncwarp();
+#pragma unroll
+  for (int e = 0; e < 16; ++e) s[16 * l + e + l] = x[e];
+  __syncwarp();
+#pragma unroll
+  for (int e = 0; e < 16; ++e) x[e] = s[l + 16 * e + e];
+  static_for<3, -1, -1>([&](auto LM) {
+    constexpr int lm = decltype(LM)::value;
+    gs_stage<16, (16 >> (lm + 1))>(x, [&](int gi) { return ldtw(tw, (N1 + b) * (1 << lm) + gi); },
+                                   P.q, P.two_q);
+  });
+  u64* dst = row_ptr(out, r) + (b << 8);
+#pragma unroll
+  for (int e = 0; e < 16; ++e) dst[l + 16 * e] = x[e];
+}
+
+// Column pass, inverse: GS stages m = N1/2 .. 1, then x N^-1 and a full
+// reduction; the result goes through the epilogue.
+template <int LOGN1, int E, class Epi>
+__global__ void __launch_bounds__(16 * ((1 << LOGN1) / E))
+    ntt_col_inv(const __grid_constant__ RowMap in, const __grid_constant__ Epi epi,
+                const ulonglong2* __restrict__ itw_all, const PrimeConst* __restrict__ primes,
+                u32 logn) {
+  constexpr int N1 = 1 << LOGN1;
+  constexpr int R = N1 / E;
+  constexpr int LOGE = __builtin_ctz(E);
+  extern __shared__ u64 sm[];  // [N1][16]
+  const u32 n = 1u << logn;
+  const u32 n2 = n >> LOGN1;
+  const u32 groups = n2 >> 4;
+  const u32 r = blockIdx.x / groups;
+  const u32 g = blockIdx.x - r * groups;
+  const u32 c = threadIdx.x & 15, k = threadIdx.x >> 4;
+  const u32 j = (g << 4) + c;
+  const u32 pi = row_prime(in, r);
+  const PrimeConst P = primes[pi];
+  const ulonglong2* tw = itw_all + (u64)pi * n;
+  const u64* src = row_ptr(in, r);
+  u64 x[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) x[e] = src[j + (k * E + e) * n2];
+  static_for<LOGN1 - 1, LOGE - 1, -1>([&](auto LM) {
+    constexpr int lm = decltype(LM)::value;
+    constexpr int d = N1 >> (lm + 1);
+    gs_stage<E, d>(x, [&](int gi) { return ldtw(tw, (1 << lm) + ((k * E + gi * 2 * d) >> (LOGN1 - lm))); },
+                   P.q, P.two_q);
+  });
+#pragma unroll
+  for (int e = 0; e < E; ++e) sm[(k * E + e) * 16 + c] = x[e];
+  __syncthreads();
+#pragma unroll
+  for (int e = 0; e < E; ++e) x[e] = sm[(k + R * e) * 16 + c];
+  static_for<LOGE - 1, -1, -1>([&](auto LM) {
+    constexpr int lm = decltype(LM)::value;
+    gs_stage<E, (E >> (lm + 1))>(x, [&](int gi) { return ldtw(tw, (1 << lm) + gi); }, P.q, P.two_q);
+  });
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const u64 v = mul_shoup(x[e], P.n_inv, P.n_inv_shoup, P.q);
+    epi(r, j + (k + R * e) * n2, v, pi, P);
+  }
+}
+
+// Single-CTA transform for small rings (N <= 4096): the whole row in shared
+// memory, reference stage order.
+template <bool INV, class Loader, class Epi>
+__global__ void __launch_bounds__(256)
+    ntt_small(const __grid_constant__ Loader ld, const __grid_constant__ Epi epi,
+              const __grid_constant__ RowMap rows, const ulonglong2* __restrict__ tw_all,
+              const PrimeConst* __restrict__ primes, u32 logn) {
+  extern __shared__ u64 smem[];
+  const u32 n = 1u << logn;
+  const u32 r = blockIdx.x;
+  const u32 pi = row_prime(rows, r);
+  const PrimeConst P = primes[pi];
+  const ulonglong2* tw = tw_all + (u64)pi * n;
+  for (u32 a = threadIdx.x; a < n; a += blockDim.x) smem[a] = ld(r, a, pi, P);
+  __syncthreads();
+  if (!INV) {
+    u32 half = n;
+    for (u32 m = 1; m < n; m <<= 1) {
+      half >>= 1;
+      for (u32 bt = threadIdx.x; bt < n / 2; bt += blockDim.x) {
+        const u32 i = bt / half, jj = bt - i * half;
+        const u32 a0 = 2 * i * half + jj;
+        ct_bfly(smem[a0], smem[a0 + half], ldtw(tw, m + i), P.q, P.two_q);
+      }
+      __syncthreads();
+    }
+    for (u32 a = threadIdx.x; a < n; a += blockDim.x) epi(r, a, reduce_4q(smem[a], P.q, P.two_q), pi, P);
+  } else {
+    u32 half = 1;
+    for (u32 m = n >> 1; m >= 1; m >>= 1) {
+      for (u32 bt = threadIdx.x; bt < n / 2; bt += blockDim.x) {
+        const u32 i = bt / half, jj = bt - i * half;
+        const u32 a0 = 2 * i * half + jj;
+        gs_bfly(smem[a0], smem[a0 + half], ldtw(tw, m + i), P.q, P.two_q);
+      }
+      __syncthreads();
+      half <<= 1;
+    }
+    for (u32 a = threadIdx.x; a < n; a += blockDim.x)
+      epi(r, a, mul_shoup(smem[a], P.n_inv, P.n_inv_shoup, P.q), pi, P);
+  }
+}
+
+}  // namespace lcl

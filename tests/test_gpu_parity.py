@@ -1,0 +1,223 @@
+"""GPU parity: every sm_100a kernel path, called through the C-ABI, against
+the oracle port (which is itself pinned to the reference by
+tests/test_oracle_golden.py) and against the reference's golden digests."""
+import numpy as np
+import pytest
+
+from oracle.oracle import Oracle, slot_reduce_steps
+from tests.golden_util import Rig, sha
+
+pytestmark = pytest.mark.gpu
+
+
+def _L():
+    import paper_2408_06197_b200.lancelot as L
+    return L
+
+
+_CTX = {}
+
+
+def gpu_ctx(N, secure=False):
+    L = _L()
+    key = (N, secure)
+    if key not in _CTX:
+        _CTX[key] = L.CkksContext(L.CkksParams(
+            ring_degree=N, security=L.SecurityLevel.bits128 if secure else L.SecurityLevel.none))
+    return _CTX[key]
+
+
+@pytest.mark.parametrize("N", [256, 1024, 4096, 8192, 16384, 32768, 65536, 131072])
+def test_ntt_matches_oracle(N):
+    L = _L()
+    import torch
+    orc = Oracle(N, secure=False, threads=1)
+    ctx = gpu_ctx(N)
+    assert ctx.primes == orc.primes and ctx.special == orc.special
+    rng = np.random.default_rng(N)
+    P = orc.full + 1
+    items = 3
+    rows = np.zeros((items, P, N), np.uint64)
+    qs = orc.primes + [orc.special]
+    for r in range(P):
+        rows[:, r] = rng.integers(0, qs[r], size=(items, N), dtype=np.uint64)
+    rows[0, 0, :] = 0
+    rows[0, 1, :] = np.uint64(qs[1] - 1)
+    want_f = np.stack([[orc.ntt_forward(rows[i, r], r) for r in range(P)] for i in range(items)])
+    d = L.to_device(rows)
+    L._check(L.lib().lcl_ntt_forward(ctx.h, L._ptr(d), items, orc.full, 1))
+    torch.cuda.synchronize()
+    got_f = L.to_host(d)
+    assert np.array_equal(got_f, want_f)
+    L._check(L.lib().lcl_ntt_inverse(ctx.h, L._ptr(d), items, orc.full, 1))
+    torch.cuda.synchronize()
+    assert np.array_equal(L.to_host(d), rows)
+    want_i = np.stack([[orc.ntt_inverse(rows[i, r], r) for r in range(P)] for i in range(items)])
+    d = L.to_device(rows)
+    L._check(L.lib().lcl_ntt_inverse(ctx.h, L._ptr(d), items, orc.full, 1))
+    torch.cuda.synchronize()
+    assert np.array_equal(L.to_host(d), want_i)
+
+
+@pytest.fixture(scope="module", params=[1024, 8192])
+def evalrig(request):
+    N = request.param
+    orc = Oracle(N, secure=False, threads=4)
+    steps = [1, 2, 3, 4, 7, 8, 16, 64]
+    orc.keygen(1, steps)
+    clients = orc.make_clients(1, 3, N)  # two chunks each
+    return N, orc, steps, clients
+
+
+def test_evaluator_matches_oracle(evalrig):
+    L = _L()
+    N, orc, steps, clients = evalrig
+    ctx = gpu_ctx(N)
+    rk = L.RelinKey(orc.relin_key())
+    keys = L.RotationKeySet({s: orc.rotation_key(s) for s in steps})
+    s = orc.scale
+    a = L.Ciphertext(L.to_device(clients[0, 0]), s)
+    b = L.Ciphertext(L.to_device(clients[1, 0]), s)
+    assert np.array_equal(L.to_host(ctx.hsub(a, b).data), orc.hsub(clients[0, 0], clients[1, 0]))
+    assert np.array_equal(L.to_host(ctx.hadd(a, b).data), orc.hadd(clients[0, 0], clients[1, 0]))
+    t = orc.hsquare(orc.hsub(clients[0, 0], clients[1, 0]))
+    tern = L.TernaryCiphertext(L.to_device(t), s * s)
+    rl = ctx.relinearize(tern, rk)
+    want_rl = orc.relinearize(t)
+    assert np.array_equal(L.to_host(rl.data), want_rl)
+    rs = ctx.rescale(rl)
+    want_rs = orc.rescale(want_rl)
+    assert np.array_equal(L.to_host(rs.data), want_rs)
+    assert rs.scale == (s * s) / float(orc.primes[3])
+    for st in steps:
+        got = ctx.rotate(rs, st, keys)
+        assert np.array_equal(L.to_host(got.data), orc.rotate(want_rs, st)), st
+    hs = [1, 2, 3, 0, 7]
+    got = ctx.hoisted_rotations(rs, hs, keys)
+    want = orc.hoisted_rotations(want_rs, hs)
+    for i in range(len(hs)):
+        assert np.array_equal(L.to_host(got[i].data), want[i]), hs[i]
+    for width, k in [(128, 1), (128, 3), (8, 4), (64, 2), (1, 1)]:
+        got = L.slot_reduce(ctx, rs, L.HoistPlan(k=k, n=width), keys)
+        assert np.array_equal(L.to_host(got.data), orc.slot_reduce(want_rs, width, k)), (width, k)
+    # fresh-level (m = 4) rotation and rescale chain down to level 0
+    top = L.Ciphertext(L.to_device(clients[2, 1]), s)
+    assert np.array_equal(L.to_host(ctx.rotate(top, 3, keys).data), orc.rotate(clients[2, 1], 3))
+    x, xw = top, clients[2, 1]
+    for _ in range(3):
+        x, xw = ctx.rescale(x), orc.rescale(xw)
+        assert np.array_equal(L.to_host(x.data), xw)
+    with pytest.raises(L.DepthExhaustedError):
+        ctx.rescale(x)
+    with pytest.raises(L.KeyError):
+        ctx.rotate(rs, 5, keys)
+
+
+def test_mult_plain_matches_oracle(evalrig):
+    L = _L()
+    N, orc, steps, clients = evalrig
+    ctx = gpu_ctx(N)
+    ct = orc.rescale(clients[0, 0])
+    for l in (2, 3, 7, 25):
+        got = ctx.mult_plain_const(L.Ciphertext(L.to_device(ct), 1.0), 1.0 / l, orc.scale)
+        want = orc.mult_plain_inv_l(ct, l)  # includes the rescale
+        assert np.array_equal(L.to_host(ctx.rescale(got).data), want), l
+
+
+GOLDEN = ["tiny_krum", "tiny_hoist_multikrum", "tiny_eager", "tiny_fullhoist", "cfg1", "cfg2"]
+
+
+@pytest.fixture(scope="module", params=GOLDEN)
+def golden(request):
+    return Rig(request.param, threads=8)
+
+
+def _packed(L, rig):
+    dev = L.to_device(rig.clients)
+    return [L.PackedWeights(dev[i], rig.dim, 1.0, rig.oracle.scale) for i in range(rig.n)]
+
+
+def test_distance_matrix_bit_exact_vs_reference(golden):
+    L = _L()
+    rig = golden
+    ctx = gpu_ctx(rig.N, secure=bool(rig.meta["options"]["secure"]))
+    rk = L.RelinKey(rig.oracle.relin_key())
+    keys = L.RotationKeySet({s: rig.oracle.rotation_key(s) for s in rig.meta["rot_keys"]})
+    pw = _packed(L, rig)
+    ctx.reset_counters()
+    dm = L.build_distance_matrix(ctx, pw, rk, L.HoistPlan(k=rig.k, n=rig.width),
+                                 L.DistanceMode.per_pair, keys,
+                                 L.DistanceOptions(lazy_relin=rig.lazy))
+    got = L.to_host(dm.batch)
+    counts = ctx.counters()
+    for p, (i, j) in enumerate(dm.keys):
+        assert sha(got[p]) == rig.meta["sha256"][f"dist_{i}_{j}"], (i, j)
+    assert counts == rig.meta["dist_ops"]
+    e0 = rig.meta["dist"][0]
+    assert dm.scale == e0["scale"]
+    assert dm.value_scale == 1.0
+
+
+def test_masked_aggregate_bit_exact_vs_reference(golden):
+    L = _L()
+    rig = golden
+    ctx = gpu_ctx(rig.N, secure=bool(rig.meta["options"]["secure"]))
+    rk = L.RelinKey(rig.oracle.relin_key())
+    pw = _packed(L, rig)
+    mask = L.SelectionMask(rig.n, len(rig.selected), L.to_device(rig.selectors), rig.oracle.scale)
+    rule = {"krum": L.SelectionRule.krum, "multi_krum": L.SelectionRule.multi_krum,
+            "median": L.SelectionRule.median}[rig.rule]
+    ctx.reset_counters()
+    agg = L.masked_aggregate(ctx, pw, mask, rule, rk)
+    assert sha(L.to_host(agg.chunks)) == rig.meta["sha256"]["agg"]
+    assert ctx.counters() == rig.meta["agg_ops"]
+    assert agg.scale == rig.meta["agg_scale"]
+
+
+def test_decrypted_results_within_ckks_tolerance(golden):
+    """Decrypt the GPU outputs with the oracle: distances within rel 1e-5 of
+    the reference's decryption (same words => identical), and within the
+    reference's own 1e-3 of the plaintext distances."""
+    L = _L()
+    rig = golden
+    if rig.N > 8192:
+        pytest.skip("decryption check on small rings only")
+    ctx = gpu_ctx(rig.N, secure=bool(rig.meta["options"]["secure"]))
+    rk = L.RelinKey(rig.oracle.relin_key())
+    keys = L.RotationKeySet({s: rig.oracle.rotation_key(s) for s in rig.meta["rot_keys"]})
+    dm = L.build_distance_matrix(ctx, _packed(L, rig), rk, L.HoistPlan(k=rig.k, n=rig.width),
+                                 L.DistanceMode.per_pair, keys,
+                                 L.DistanceOptions(lazy_relin=rig.lazy))
+    got = L.to_host(dm.batch)
+    for p, e in enumerate(rig.meta["dist"]):
+        v = rig.oracle.decrypt_values(got[p], dm.scale)[0]
+        assert abs(v - e["slot0"]) <= 1e-5 * max(1.0, abs(e["slot0"]))
+        plain = rig.meta["plain_dist"][p]
+        assert abs(v - plain) <= 1e-3 * max(1.0, abs(plain))
+
+
+def test_shape_and_width_errors():
+    L = _L()
+    orc = Oracle(256, secure=False, threads=1)
+    orc.keygen(1, [1, 2, 4])
+    ctx = gpu_ctx(256)
+    cl = orc.make_clients(1, 3, 200)
+    dev = L.to_device(cl)
+    rk = L.RelinKey(orc.relin_key())
+    keys = L.RotationKeySet({s: orc.rotation_key(s) for s in (1, 2, 4)})
+    pw = [L.PackedWeights(dev[i], 200, 1.0, orc.scale) for i in range(3)]
+    with pytest.raises(L.ShapeError):
+        L.build_distance_matrix(ctx, pw[:1], rk, L.HoistPlan(k=1, n=128), L.DistanceMode.per_pair,
+                                keys)
+    with pytest.raises(L.WidthError):
+        L.build_distance_matrix(ctx, pw, rk, L.HoistPlan(k=1, n=64), L.DistanceMode.per_pair, keys)
+    with pytest.raises(L.KeyError):  # width 128 needs steps up to 64
+        L.build_distance_matrix(ctx, pw, rk, L.HoistPlan(k=1, n=128), L.DistanceMode.per_pair,
+                                keys)
+    bad = L.PackedWeights(dev[2], 199, 1.0, orc.scale)
+    with pytest.raises(L.ShapeError):
+        L.build_distance_matrix(ctx, pw[:2] + [bad], rk, L.HoistPlan(k=1, n=128),
+                                L.DistanceMode.per_pair, keys)
+    with pytest.raises(L.ShapeError):
+        L.masked_aggregate(ctx, pw, L.SelectionMask(2, 1, L.to_device(cl[:2, 0]), orc.scale),
+                           L.SelectionRule.krum, rk)
