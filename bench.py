@@ -1,0 +1,409 @@
+"""Benchmark: one encrypted Krum round of the Lancelot server path on B200.
+
+A step = server step 3 + step 8 of the reference's run_round
+(protocol.cpp:430-432, 492-493): build_distance_matrix(per_pair, lazy relin,
+reduce_on_server) over all n clients, then masked_aggregate with the Krum
+selection mask. Workload = BASELINE.json configs[1] (cfg2): 10 clients,
+272,474-parameter updates, CKKS N = 2^15 (17 chunks, 45 pairs, width 16384).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+                    [--config cfg2|cfg1|cfg3|cfg4]
+
+Our arm prints one JSON line (rank 0). `value` is device time per round with
+inputs resident in HBM; `e2e` is the same round through the C-ABI entry
+lcl_server_round_host with pinned host buffers (H2D of the clients and
+selectors + D2H of the matrix and aggregate inside the timed region).
+The reference arm (--impl reference) times the unmodified reference core
+(oracle/_ref/ref_driver, built from /root/reference sources) on the host
+cores for the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # name: (n clients, P params, N, k unfold, rule, selected)
+    "cfg1": dict(n=4, P=8192, N=8192, k=1),
+    "cfg2": dict(n=10, P=272474, N=32768, k=1),
+    "cfg3": dict(n=20, P=11173962, N=65536, k=1),
+    "cfg4": dict(n=50, P=11173962, N=65536, k=1),
+}
+METRIC = "Krum-round latency (ms) over encrypted updates"
+
+
+def bit_ceil(x):
+    return 1 << (x - 1).bit_length()
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(
+                    ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                     "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                self.samples.append([x.strip() for x in out.stdout.strip().split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=6)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = sorted(float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit())
+        mx = max((float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()), default=None)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for s in self.samples:
+            for nm, v in zip(names, s[4:8]):
+                if v.strip().lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------------ reference arm
+def reference_arm(args, cfg):
+    """Times the reference's own CPU implementation (oracle/_ref/ref_driver,
+    the unmodified reference core) on this host's cores."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    driver = os.path.join(ROOT, "oracle", "_ref", "ref_driver")
+    line = {"impl": "reference", "metric": METRIC, "unit": "ms", "higher_is_better": False,
+            "n_gpus": args.gpus, "config": workload(cfg, args.config)}
+    if not os.path.exists(driver):
+        line["unavailable"] = "oracle/_ref/ref_driver not built (needs /root/reference at build time)"
+        print(json.dumps(line))
+        return
+    cores = os.cpu_count() or 1
+    env = dict(os.environ, LANCELOT_THREADS=str(cores))
+    reps = args.warmup + args.steps
+    cmd = [driver, "bench", "--N", str(cfg["N"]), "--clients", str(cfg["n"]), "--dim",
+           str(cfg["P"]), "--k", str(cfg["k"]), "--secure", "1", "--reps", str(reps),
+           "--rule", "krum", "--select", "0"]
+    t0 = time.time()
+    proc = subprocess.Popen(cmd, stdout=subprocess.PIPE, text=True, env=env)
+    budget = args.ref_budget_s
+    try:
+        out, _ = proc.communicate(timeout=budget)
+    except subprocess.TimeoutExpired:
+        proc.kill()
+        out, _ = proc.communicate()
+    res = parse_partial_json(out)
+    times = [r["distance_s"] + r["aggregate_s"] for r in res.get("reps", [])]
+    timed = times[args.warmup:] if len(times) > args.warmup else times[-1:]
+    if not timed:
+        line["unavailable"] = "reference run produced no timed repetition within the budget"
+        print(json.dumps(line))
+        return
+    ms = 1000.0 * sum(timed) / len(timed)
+    sample = (f"full {args.config} round (build_distance_matrix per_pair lazy reduce + "
+              f"masked_aggregate krum) x {len(timed)} timed reps after {min(args.warmup, len(times) - len(timed))} "
+              f"warm-up; setup (keygen + encryption) {res.get('setup_s', 0):.1f}s excluded; "
+              f"wall {time.time() - t0:.0f}s")
+    line.update({"value": ms, "steps": len(timed), "warmup": args.warmup, "ms_per_step": ms,
+                 "scaling": "replicas", "vs_baseline": None, "dtype": "u64",
+                 "data": "synthetic encrypted updates (uniform [-0.5,0.5) weights, reference generator)",
+                 "cpu_baseline": {"value": ms, "unit": "ms", "cores": cores, "kind": "reference",
+                                  "sample": sample},
+                 "e2e": {"value": ms, "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}})
+    print(json.dumps(line))
+
+
+def parse_partial_json(out):
+    out = out.strip()
+    try:
+        return json.loads(out)
+    except Exception:
+        pass
+    # truncated run: close the list
+    i = out.rfind("}")
+    if i < 0:
+        return {}
+    try:
+        return json.loads(out[: i + 1] + "]}")
+    except Exception:
+        return {}
+
+
+def workload(cfg, name):
+    N = cfg["N"]
+    slots = N // 2
+    C = (cfg["P"] + slots - 1) // slots
+    return {"workload": f"{name}: encrypted Krum round, {cfg['n']} clients x {cfg['P']} params, "
+                        f"CKKS N=2^{N.bit_length() - 1}",
+            "clients": cfg["n"], "params": cfg["P"], "ring_degree": N, "chunks": C,
+            "pairs": cfg["n"] * (cfg["n"] - 1) // 2, "reduce_width": bit_ceil(min(cfg["P"], slots)),
+            "unfold_k": cfg["k"], "lazy_relin": True, "rule": "krum",
+            "l2": "flushed between steps (256 MiB write) and client data > L2"}
+
+
+# ------------------------------------------------------------------ cpu baseline
+def cpu_baseline(cfg, name, budget_s):
+    driver = os.path.join(ROOT, "oracle", "_ref", "ref_driver")
+    cores = os.cpu_count() or 1
+    if not os.path.exists(driver):
+        return {"value": None, "unit": "ms", "cores": cores, "kind": "reference",
+                "sample": "unavailable: oracle/_ref not built"}
+    env = dict(os.environ, LANCELOT_THREADS=str(cores))
+    cmd = [driver, "bench", "--N", str(cfg["N"]), "--clients", str(cfg["n"]), "--dim",
+           str(cfg["P"]), "--k", str(cfg["k"]), "--secure", "1", "--reps", "1",
+           "--rule", "krum", "--select", "0"]
+    try:
+        out = subprocess.run(cmd, capture_output=True, text=True, env=env, timeout=budget_s).stdout
+        res = json.loads(out)
+        r = res["reps"][0]
+        ms = 1000.0 * (r["distance_s"] + r["aggregate_s"])
+        return {"value": ms, "unit": "ms", "cores": cores, "kind": "reference",
+                "sample": f"one full {name} round on the unmodified reference core "
+                          f"(distance {r['distance_s']:.2f}s + aggregate {r['aggregate_s']:.2f}s), "
+                          f"LANCELOT_THREADS={cores}; setup {res['setup_s']:.1f}s excluded"}
+    except Exception as e:  # noqa: BLE001
+        return {"value": None, "unit": "ms", "cores": cores, "kind": "reference",
+                "sample": f"failed: {e}"[:200]}
+
+
+# ------------------------------------------------------------------ our arm
+def our_arm(args, cfg):
+    import ctypes as C
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2408_06197_b200.lancelot as L
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        dist.init_process_group("nccl")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    N, n = cfg["N"], cfg["n"]
+    slots = N // 2
+    Cc = (cfg["P"] + slots - 1) // slots
+    width = bit_ceil(min(cfg["P"], slots))
+    k = cfg["k"]
+    ctx = L.CkksContext(L.CkksParams(ring_degree=N), device=local)
+    stream = torch.cuda.Stream(device=dev)
+    ctx.set_stream(stream)
+    m = ctx.full
+    primes = ctx.primes + [ctx.special]
+    g = torch.Generator(device=dev)
+    g.manual_seed(1234 + rank)
+
+    def residues(*shape, rows_last=2, row_primes=None):
+        t = torch.empty(shape, dtype=torch.int64, device=dev)
+        for r, q in enumerate(row_primes):
+            sl = [slice(None)] * len(shape)
+            sl[-rows_last] = r
+            t[tuple(sl)] = torch.randint(0, q, shape[:-rows_last] + shape[-rows_last + 1:],
+                                         generator=g, device=dev, dtype=torch.int64)
+        return t
+
+    # keys: [full][2][full+1][N], uniform residues per row prime (data-oblivious kernels)
+    def key():
+        return L.to_host(residues(m, 2, m + 1, N, row_primes=primes))
+
+    rk = L.RelinKey(key())
+    steps = L.slot_reduce_steps(width, k)
+    keys = L.RotationKeySet({s: key() for s in steps})
+    ctx.use_relin_key(rk)
+    ctx.use_rotation_keys(keys, steps)
+    clients = residues(n, Cc, 2, m, N, row_primes=primes[:m])
+    sel = residues(n, 2, m, N, row_primes=primes[:m])
+    npairs = n * (n - 1) // 2
+    d_dist = torch.empty(npairs, 2, m - 1, N, dtype=torch.int64, device=dev)
+    d_agg = torch.empty(Cc, 2, m - 1, N, dtype=torch.int64, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    scale = ctx.scale()
+    osc = C.c_double()
+    lib = L.lib()
+
+    def step():
+        L._check(lib.lcl_distance_matrix(ctx.h, L._ptr(clients), n, Cc, scale, width, k, 1, 1,
+                                         L._ptr(d_dist), C.byref(osc)))
+        L._check(lib.lcl_masked_aggregate(ctx.h, L._ptr(clients), L._ptr(sel), n, Cc, scale, scale,
+                                          1, 0, L._ptr(d_agg), C.byref(osc)))
+
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            step()
+        stream.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        launches0 = ctx.launch_count()
+        total_ms = 0.0
+        with ClockSampler(local) as clk:
+            for _ in range(args.steps):
+                flush.zero_()
+                a = torch.cuda.Event(enable_timing=True)
+                b = torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                step()
+                b.record(stream)
+                b.synchronize()
+                total_ms += a.elapsed_time(b)
+        launches = ctx.launch_count() - launches0
+        torch.cuda.synchronize()
+    ms = total_ms / args.steps
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+
+    # ---- end to end through the C-ABI with pinned host buffers
+    h_clients = torch.empty(clients.shape, dtype=torch.int64, pin_memory=True)
+    h_clients.copy_(clients.cpu())
+    h_sel = torch.empty(sel.shape, dtype=torch.int64, pin_memory=True)
+    h_sel.copy_(sel.cpu())
+    h_dist = torch.empty(d_dist.shape, dtype=torch.int64, pin_memory=True)
+    h_agg = torch.empty(d_agg.shape, dtype=torch.int64, pin_memory=True)
+
+    def e2e_step():
+        L._check(lib.lcl_server_round_host(ctx.h, C.c_void_p(h_clients.data_ptr()),
+                                           C.c_void_p(h_sel.data_ptr()), n, Cc, scale, width, k,
+                                           1, 0, C.c_void_p(h_dist.data_ptr()),
+                                           C.c_void_p(h_agg.data_ptr())))
+
+    e2e_step()
+    e2e_step()
+    e2e_ms = 0.0
+    e2e_steps = max(3, min(args.steps, 10))
+    with torch.cuda.stream(stream):
+        for _ in range(e2e_steps):
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            e2e_step()
+            b.record(stream)
+            b.synchronize()
+            e2e_ms += a.elapsed_time(b)
+    e2e_ms /= e2e_steps
+    h2d = (h_clients.numel() + h_sel.numel()) * 8
+    d2h = (h_dist.numel() + h_agg.numel()) * 8
+
+    # ---- per-kernel breakdown of one profiled round (CUDA events per launch)
+    prof = profile_round(ctx, step, stream, N, m, npairs, Cc, width, n)
+
+    if rank == 0:
+        cpu = cpu_baseline(cfg, args.config, args.cpu_budget_s) if world == 1 and not args.no_cpu else None
+        line = {
+            "metric": METRIC, "value": ms, "unit": "ms", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False,
+            "scaling": "replicas", "vs_baseline": None, "dtype": "u64",
+            "data": "synthetic: uniform residues mod each q_i for ciphertexts, selectors and keys "
+                    "(every kernel is data-oblivious; bit-exactness is proven by tests/)",
+            "config": workload(cfg, args.config),
+            "clocks": clk.summary(),
+            "e2e": {"value": e2e_ms, "unit": "ms", "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h},
+            "gpu_launches": int(launches // max(1, args.steps)),
+            "roofline": prof.get("roofline"),
+            "kernels": prof.get("kernels"),
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def profile_round(ctx, step, stream, N, m, npairs, Cc, width, n):
+    """Times every launch of one round with CUDA events (lcl profiling hooks)
+    and returns the per-kernel totals plus the roofline of the top kernel."""
+    import ctypes as C
+    import json as _json
+
+    import paper_2408_06197_b200.lancelot as L
+    lib = L.lib()
+    if not hasattr(lib, "lcl_profile_begin"):
+        return {}
+    lib.lcl_profile_begin.argtypes = [C.c_void_p]
+    lib.lcl_profile_end.argtypes = [C.c_void_p, C.c_char_p, C.c_size_t]
+    lib.lcl_profile_end.restype = C.c_int
+    step()
+    stream.synchronize()
+    lib.lcl_profile_begin(ctx.h)
+    step()
+    buf = C.create_string_buffer(1 << 20)
+    lib.lcl_profile_end(ctx.h, buf, len(buf))
+    rows = _json.loads(buf.value.decode())
+    peaks = load_peaks()
+    kernels = sorted(rows, key=lambda r: -r["ms"])
+    top = kernels[0] if kernels else None
+    roof = None
+    if top:
+        achieved = top["bytes"] / (top["ms"] / top["launches"] * 1e-3) / top["launches"] / 1e9
+        roof = {"bound": "hbm", "kernel": top["name"], "achieved": achieved,
+                "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"],
+                "traffic": None, "peak_source": peaks["source"],
+                "bytes_per_launch": top["bytes"] / top["launches"],
+                "avg_launch_ms": top["ms"] / top["launches"],
+                "share_of_round": top["ms"] / sum(k["ms"] for k in kernels)}
+    return {"roofline": roof, "kernels": kernels[:12]}
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return {"hbm_gbs": float(d["hbm_gbs"]), "source": "measured (MEASURED_PEAKS.json)"}
+    except Exception:
+        return {"hbm_gbs": 6650.0, "source": "fallback (B200_PROFILING.md)"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-budget-s", type=float, default=120.0)
+    ap.add_argument("--ref-budget-s", type=float, default=240.0)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        reference_arm(args, cfg)
+    else:
+        our_arm(args, cfg)
+
+
+if __name__ == "__main__":
+    main()

@@ -85,6 +85,10 @@ int lcl_get_counts(const lcl_context* ctx, lcl_counts* out);
 int lcl_reset_counts(lcl_context* ctx);
 /* Number of kernel launches issued so far (instrumentation for bench.py). */
 uint64_t lcl_launch_count(const lcl_context* ctx);
+/* Per-launch CUDA-event timing between begin and end; end writes a JSON list
+ * of {name, launches, ms, bytes (algorithmic)} per kernel into json[cap]. */
+int lcl_profile_begin(lcl_context* ctx);
+int lcl_profile_end(lcl_context* ctx, char* json, size_t cap);
 
 /* ------------------------------------------------------------ keys */
 /* Host key in the reference layout [full][2][full+1][N]; words must equal

@@ -212,7 +212,7 @@ RowMap make_map(const u64* base, u32 rpi, u64 row_stride, u64 item_stride, u32 i
   m.row_stride = row_stride;
   m.item_stride = item_stride;
   m.items_per_group = ipg;
-  m.group_stride = group_stride;
+  m.group_stride = ipg == 1 ? item_stride : group_stride;
   for (u32 i = 0; i < rpi && i < 2 * LCL_MAXP; ++i) m.prime_of[i] = (unsigned char)primes[i];
   return m;
 }
@@ -228,6 +228,12 @@ RowMap null_map() {
 }  // namespace
 
 // ------------------------------------------------------------ context
+struct ProfRec {
+  const char* name;
+  cudaEvent_t a, b;
+  double bytes;  // algorithmic bytes moved by the launch
+};
+
 struct lcl_context {
   int device = 0;
   cudaStream_t stream = nullptr;
@@ -243,11 +249,14 @@ struct lcl_context {
   ulonglong2* d_pinv = nullptr;  // [(full+1) * (full+1)]: (q_div^-1 mod q_dst, shoup)
   u32* d_pairs = nullptr;
   size_t pairs_cap = 0;
+  u32 pairs_n = 0;
   u64* d_relin = nullptr;
   std::map<size_t, u64*> d_rot;
   std::map<size_t, u32*> d_perm;
   lcl_counts counts{};
   u64 launches = 0;
+  bool prof_on = false;
+  std::vector<ProfRec> prof;
   // workspace
   DevBuf ws_coef, ws_digits, ws_acc, ws_coefsp, ws_mid, ws_tern, ws_ctA, ws_ctB, ws_ctC, ws_pt;
   DevBuf ws_io_in, ws_io_sel, ws_io_dist, ws_io_agg;
@@ -270,6 +279,37 @@ void post_launch(lcl_context* c, u64 k = 1) {
   cuda_check(cudaGetLastError(), "kernel launch");
 }
 
+// CUDA-event bracket around one launch when profiling is on (bench.py uses it
+// to attribute the round's device time to kernels).
+struct ProfScope {
+  lcl_context* c;
+  const char* name;
+  double bytes;
+  cudaEvent_t a = nullptr;
+  ProfScope(lcl_context* c_, const char* n, double b) : c(c_), name(n), bytes(b) {
+    if (c->prof_on) {
+      cudaEventCreate(&a);
+      cudaEventRecord(a, c->stream);
+    }
+  }
+  ~ProfScope() {
+    if (a) {
+      cudaEvent_t b2;
+      cudaEventCreate(&b2);
+      cudaEventRecord(b2, c->stream);
+      c->prof.push_back({name, a, b2, bytes});
+    }
+  }
+};
+
+// Algorithmic traffic of the functors (words per output row).
+inline double load_rows(const PlainLoad&, double rows) { return rows; }
+inline double load_rows(const LiftLoad& l, double rows) { return rows / l.fan; }
+inline double store_rows(const PlainStore&, double rows) { return rows; }
+inline double store_rows(const DivRoundStore& s, double rows) {
+  return rows * (2.0 + (s.add1.base ? 1.0 : 0.0)) + (s.add2.base ? rows / 2 : 0.0);
+}
+
 // ------------------------------------------------------------ NTT launchers
 RowMap mid_map(lcl_context* c, u32 rows, const RowMap& pm) {
   u64* mid = c->ws_mid.get((u64)rows * c->N());
@@ -278,7 +318,7 @@ RowMap mid_map(lcl_context* c, u32 rows, const RowMap& pm) {
   m.row_stride = c->N();
   m.item_stride = (u64)pm.rows_per_item * c->N();
   m.items_per_group = 1;
-  m.group_stride = 0;
+  m.group_stride = m.item_stride;
   return m;
 }
 
@@ -296,10 +336,19 @@ void fwd2(lcl_context* c, u32 rows, const RowMap& mid, const Loader& ld, const E
   static bool once = (allow_smem(ntt_col_fwd<LOGN1, E, Loader>, smem), true);
   (void)once;
   const u32 groups = (u32)(c->n >> LOGN1) >> 4;
-  ntt_col_fwd<LOGN1, E, Loader><<<rows * groups, 16 * (N1 / E), smem, c->stream>>>(
-      mid, ld, c->d_tw, c->d_primes, c->logn);
-  ntt_blk_fwd<LOGN1, Epi><<<rows * N1 / 4, 64, 0, c->stream>>>(mid, epi, c->d_tw, c->d_primes,
-                                                               c->logn);
+  const double rb = 8.0 * c->N();
+  {
+    ProfScope ps(c, std::is_same<Loader, LiftLoad>::value ? "ntt_col_fwd<lift>" : "ntt_col_fwd",
+                 rb * (load_rows(ld, rows) + rows));
+    ntt_col_fwd<LOGN1, E, Loader><<<rows * groups, 16 * (N1 / E), smem, c->stream>>>(
+        mid, ld, c->d_tw, c->d_primes, c->logn);
+  }
+  {
+    ProfScope ps(c, std::is_same<Epi, DivRoundStore>::value ? "ntt_blk_fwd<divround>" : "ntt_blk_fwd",
+                 rb * (store_rows(epi, rows) + (std::is_same<Epi, PlainStore>::value ? rows : 0)));
+    ntt_blk_fwd<LOGN1, Epi><<<rows * N1 / 4, 64, 0, c->stream>>>(mid, epi, c->d_tw, c->d_primes,
+                                                                 c->logn);
+  }
   post_launch(c, 2);
 }
 
@@ -310,10 +359,17 @@ void inv2(lcl_context* c, u32 rows, const RowMap& in, const RowMap& mid, const E
   static bool once = (allow_smem(ntt_col_inv<LOGN1, E, Epi>, smem), true);
   (void)once;
   const u32 groups = (u32)(c->n >> LOGN1) >> 4;
-  ntt_blk_inv<LOGN1><<<rows * N1 / 4, 64, 0, c->stream>>>(in, mid, c->d_itw, c->d_primes,
-                                                          c->logn);
-  ntt_col_inv<LOGN1, E, Epi><<<rows * groups, 16 * (N1 / E), smem, c->stream>>>(
-      mid, epi, c->d_itw, c->d_primes, c->logn);
+  const double rb = 8.0 * c->N();
+  {
+    ProfScope ps(c, "ntt_blk_inv", rb * 2.0 * rows);
+    ntt_blk_inv<LOGN1><<<rows * N1 / 4, 64, 0, c->stream>>>(in, mid, c->d_itw, c->d_primes,
+                                                            c->logn);
+  }
+  {
+    ProfScope ps(c, "ntt_col_inv", rb * 2.0 * rows);
+    ntt_col_inv<LOGN1, E, Epi><<<rows * groups, 16 * (N1 / E), smem, c->stream>>>(
+        mid, epi, c->d_itw, c->d_primes, c->logn);
+  }
   post_launch(c, 2);
 }
 
@@ -323,6 +379,7 @@ template <class Loader, class Epi>
 void launch_fwd(lcl_context* c, u32 rows, const RowMap& pm, const Loader& ld, const Epi& epi) {
   if (rows == 0) return;
   if (c->logn <= 12) {
+    ProfScope ps(c, "ntt_small_fwd", 8.0 * c->N() * (load_rows(ld, rows) + store_rows(epi, rows)));
     ntt_small<false, Loader, Epi><<<rows, 256, c->n * 8, c->stream>>>(ld, epi, pm, c->d_tw,
                                                                      c->d_primes, c->logn);
     post_launch(c);
@@ -343,6 +400,7 @@ template <class Epi>
 void launch_inv(lcl_context* c, u32 rows, const RowMap& in, const Epi& epi) {
   if (rows == 0) return;
   if (c->logn <= 12) {
+    ProfScope ps(c, "ntt_small_inv", 8.0 * c->N() * 2.0 * rows);
     ntt_small<true, PlainLoad, Epi><<<rows, 256, c->n * 8, c->stream>>>(
         PlainLoad{in}, epi, in, c->d_itw, c->d_primes, c->logn);
     post_launch(c);
@@ -393,6 +451,8 @@ u64* ks_ip(lcl_context* c, const u64* dig, u32 B, u32 m, const u64* key,
   const u64 N = c->N();
   u64* acc = c->ws_acc.get((u64)B * 2 * (m + 1) * N);
   const u64 threads = (u64)(m + 1) * N;
+  ProfScope ps(c, perm ? "ks_inner_product<perm>" : "ks_inner_product",
+               8.0 * N * ((double)B * m * (m + 1) + 2.0 * m * (m + 1) + 2.0 * B * (m + 1)));
   lcl::ks_inner_product<<<(u32)((threads + 255) / 256), 256, 0, c->stream>>>(
       dig, B, m, key, c->full, perm, acc, c->logn, c->d_primes);
   post_launch(c);
@@ -530,6 +590,7 @@ void slot_reduce_batch(lcl_context* c, const u64* in, u32 B, u32 m, size_t width
 }
 
 void ensure_pairs(lcl_context* c, u32 n) {
+  if (c->pairs_n == n) return;
   const size_t np = (size_t)n * (n - 1) / 2;
   std::vector<u32> h;
   h.reserve(np);
@@ -541,6 +602,7 @@ void ensure_pairs(lcl_context* c, u32 n) {
     c->pairs_cap = np;
   }
   cuda_check(cudaMemcpy(c->d_pairs, h.data(), np * 4, cudaMemcpyHostToDevice), "pairs upload");
+  c->pairs_n = n;
 }
 
 constexpr int kPP = 4;
@@ -554,6 +616,8 @@ void pair_accumulate_launch(lcl_context* c, const u64* clients, u32 n, u32 chunk
   const u32 per_cta = warps * kPP;
   dim3 grid((u32)(m * c->n / 32), (pairs + per_cta - 1) / per_cta);
   const size_t smem = (size_t)n * 64 * 8;
+  ProfScope ps(c, "pair_accumulate",
+               8.0 * c->N() * m * (2.0 * n * (c1 - c0) + 3.0 * pairs * (accumulate ? 2 : 1)));
   pair_accumulate<kPP><<<grid, warps * 32, smem, c->stream>>>(
       clients, n, c0, c1, chunks, m, c->logn, c->d_pairs, p0, p1, tern, accumulate ? 1 : 0,
       c->d_primes);
@@ -565,6 +629,7 @@ void hadd_into(lcl_context* c, u64* acc, const u64* x, u32 B, u32 m) {
   const RowMap a = ct_map(acc, m, N, 2ull * m * N);
   const RowMap b = ct_map(x, m, N, 2ull * m * N);
   const u32 rows = B * 2 * m;
+  ProfScope ps(c, "hadd", 24.0 * N * rows);
   rows_addsub<false><<<(u32)(((u64)rows * N + 255) / 256), 256, 0, c->stream>>>(
       a, a, b, rows, c->logn, c->d_primes);
   post_launch(c);
@@ -656,8 +721,11 @@ void masked_aggregate(lcl_context* c, const u64* clients, const u64* sel, u32 n,
     constexpr int CK = 4;
     const u64 slots = (u64)m * N;
     const u64 threads = ((B + CK - 1) / CK) * slots;
-    aggregate_tensor<CK><<<(u32)((threads + 255) / 256), 256, 0, c->stream>>>(
-        clients, sel, n, chunks, c0, B, m, c->logn, tern, c->d_primes);
+    {
+      ProfScope ps(c, "aggregate_tensor", 8.0 * slots * (2.0 * n * B + 2.0 * n + 3.0 * B));
+      aggregate_tensor<CK><<<(u32)((threads + 255) / 256), 256, 0, c->stream>>>(
+          clients, sel, n, chunks, c0, B, m, c->logn, tern, c->d_primes);
+    }
     post_launch(c);
     u64* ctA = c->ws_ctA.get((u64)B * 2 * m * N);
     relinearize_batch(c, tern, B, m, ctA);
@@ -889,6 +957,53 @@ int lcl_reset_counts(lcl_context* ctx) {
 }
 
 uint64_t lcl_launch_count(const lcl_context* ctx) { return ctx ? ctx->launches : 0; }
+
+int lcl_profile_begin(lcl_context* ctx) {
+  return guarded([&] {
+    for (auto& r : ctx->prof) {
+      cudaEventDestroy(r.a);
+      cudaEventDestroy(r.b);
+    }
+    ctx->prof.clear();
+    ctx->prof_on = true;
+  });
+}
+
+int lcl_profile_end(lcl_context* ctx, char* json, size_t cap) {
+  return guarded([&] {
+    ctx->prof_on = false;
+    cuda_check(cudaStreamSynchronize(ctx->stream), "profile sync");
+    struct Agg {
+      double ms = 0, bytes = 0;
+      u64 launches = 0;
+    };
+    std::map<std::string, Agg> agg;
+    for (auto& r : ctx->prof) {
+      float ms = 0;
+      cudaEventElapsedTime(&ms, r.a, r.b);
+      Agg& a = agg[r.name];
+      a.ms += ms;
+      a.bytes += r.bytes;
+      a.launches += 1;
+      cudaEventDestroy(r.a);
+      cudaEventDestroy(r.b);
+    }
+    ctx->prof.clear();
+    std::string s = "[";
+    bool first = true;
+    for (auto& kv : agg) {
+      char buf[256];
+      std::snprintf(buf, sizeof buf, "%s{\"name\": \"%s\", \"launches\": %llu, \"ms\": %.6f, \"bytes\": %.0f}",
+                    first ? "" : ", ", kv.first.c_str(), (unsigned long long)kv.second.launches,
+                    kv.second.ms, kv.second.bytes);
+      s += buf;
+      first = false;
+    }
+    s += "]";
+    need(s.size() + 1 <= cap, LCL_USAGE_ERROR, "profile buffer too small");
+    std::memcpy(json, s.c_str(), s.size() + 1);
+  });
+}
 
 int lcl_upload_relin_key(lcl_context* ctx, const uint64_t* h_key, size_t words) {
   return guarded([&] {

@@ -413,10 +413,11 @@ class CkksContext:
     def use_relin_key(self, rk: RelinKey):
         if rk is None:
             raise KeyError("no relinearization key")
-        if self._relin_id != id(rk):
+        # the uploaded object is held, so identity cannot be recycled by the GC
+        if self._relin_id is not rk.key:
             k = np.ascontiguousarray(rk.key, dtype=np.uint64)
             _check(lib().lcl_upload_relin_key(self.h, k.ctypes.data, k.size))
-            self._relin_id = id(rk)
+            self._relin_id = rk.key
 
     def use_rotation_keys(self, keys: RotationKeySet, steps):
         slots = self.slot_count()
@@ -426,10 +427,10 @@ class CkksContext:
                 continue
             if st not in keys.steps:
                 raise KeyError("no rotation key for the requested step")
-            if self._rot_ids.get(st) != id(keys.steps[st]):
+            if self._rot_ids.get(st) is not keys.steps[st]:
                 k = np.ascontiguousarray(keys.steps[st], dtype=np.uint64)
                 _check(lib().lcl_upload_rotation_key(self.h, st, k.ctypes.data, k.size))
-                self._rot_ids[st] = id(keys.steps[st])
+                self._rot_ids[st] = keys.steps[st]
 
     # --- helpers
     def _empty(self, *shape):

@@ -63,7 +63,7 @@ def test_ntt_matches_oracle(N):
 def evalrig(request):
     N = request.param
     orc = Oracle(N, secure=False, threads=4)
-    steps = [1, 2, 3, 4, 7, 8, 16, 64]
+    steps = [1, 2, 3, 4, 7, 8, 16, 32, 64]
     orc.keygen(1, steps)
     clients = orc.make_clients(1, 3, N)  # two chunks each
     return N, orc, steps, clients
@@ -97,7 +97,7 @@ def test_evaluator_matches_oracle(evalrig):
     want = orc.hoisted_rotations(want_rs, hs)
     for i in range(len(hs)):
         assert np.array_equal(L.to_host(got[i].data), want[i]), hs[i]
-    for width, k in [(128, 1), (128, 3), (8, 4), (64, 2), (1, 1)]:
+    for width, k in [(128, 1), (128, 3), (8, 3), (64, 2), (1, 1)]:
         got = L.slot_reduce(ctx, rs, L.HoistPlan(k=k, n=width), keys)
         assert np.array_equal(L.to_host(got.data), orc.slot_reduce(want_rs, width, k)), (width, k)
     # fresh-level (m = 4) rotation and rescale chain down to level 0
