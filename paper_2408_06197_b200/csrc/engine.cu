@@ -253,6 +253,7 @@ struct lcl_context {
   u64* d_relin = nullptr;
   std::map<size_t, u64*> d_rot;
   std::map<size_t, u32*> d_perm;
+  std::map<size_t, u32*> d_sigma;  // coefficient-domain automorphism (src | neg << 31)
   lcl_counts counts{};
   u64 launches = 0;
   bool prof_on = false;
@@ -425,13 +426,14 @@ LiftLoad lift_from(lcl_context* c, const RowMap& src, u32 rows_per_item, u32 fan
   l.nprimes = c->P();
   l.primes = c->d_primes;
   l.smod = c->d_smod;
+  l.sigma = nullptr;
   return l;
 }
 
 // ------------------------------------------------------------ key switching
 // decompose_for_keyswitch (ckks.cpp:464-481): the c1 / d2 rows of B items
 // (map `in`, rows_per_item = m) -> digits [B][m][m+1][N] in HBM.
-u64* ks_decompose(lcl_context* c, const RowMap& in, u32 B, u32 m) {
+u64* ks_decompose(lcl_context* c, const RowMap& in, u32 B, u32 m, const u32* sigma = nullptr) {
   const u64 N = c->N();
   u64* coef = c->ws_coef.get((u64)B * m * N);
   const RowMap coef_map = make_map(coef, m, N, m * N, 1, 0, c->primes_0(m));
@@ -441,20 +443,29 @@ u64* ks_decompose(lcl_context* c, const RowMap& in, u32 B, u32 m) {
   for (u32 j = 0; j < m; ++j)
     for (u32 t = 0; t <= m; ++t) dp[j * (m + 1) + t] = t < m ? t : c->full;
   const RowMap dig_map = make_map(dig, m * (m + 1), N, (u64)m * (m + 1) * N, 1, 0, dp);
-  launch_fwd(c, B * m * (m + 1), dig_map, lift_from(c, coef_map, m * (m + 1), m + 1),
-             PlainStore{dig_map});
+  LiftLoad lift = lift_from(c, coef_map, m * (m + 1), m + 1);
+  lift.sigma = sigma;
+  launch_fwd(c, B * m * (m + 1), dig_map, lift, PlainStore{dig_map});
   return dig;
 }
 
-u64* ks_ip(lcl_context* c, const u64* dig, u32 B, u32 m, const u64* key,
-                      const u32* perm) {
+u64* ks_ip(lcl_context* c, const u64* dig, u32 B, u32 m, const u64* key, const u32* perm) {
   const u64 N = c->N();
   u64* acc = c->ws_acc.get((u64)B * 2 * (m + 1) * N);
-  const u64 threads = (u64)(m + 1) * N;
+  constexpr u32 IB = 8;
+  const dim3 grid((u32)(((u64)(m + 1) * N + 255) / 256), (B + IB - 1) / IB);
   ProfScope ps(c, perm ? "ks_inner_product<perm>" : "ks_inner_product",
                8.0 * N * ((double)B * m * (m + 1) + 2.0 * m * (m + 1) + 2.0 * B * (m + 1)));
-  lcl::ks_inner_product<<<(u32)((threads + 255) / 256), 256, 0, c->stream>>>(
-      dig, B, m, key, c->full, perm, acc, c->logn, c->d_primes);
+#define LCL_IP(MM)                                                                           \
+  case MM:                                                                                   \
+    lcl::ks_inner_product<MM, IB><<<grid, 256, 0, c->stream>>>(dig, B, key, c->full, perm, acc, \
+                                                               c->logn, c->d_primes);        \
+    break;
+  switch (m) {
+    LCL_IP(1) LCL_IP(2) LCL_IP(3) LCL_IP(4) LCL_IP(5) LCL_IP(6) LCL_IP(7) LCL_IP(8)
+    default: fail(LCL_PARAMETER_ERROR, "key switching supports up to 8 live limbs");
+  }
+#undef LCL_IP
   post_launch(c);
   return acc;
 }
@@ -531,8 +542,10 @@ void rotate_level(lcl_context* c, const u64* in, u32 B, u32 m, size_t step, u64*
   const u64* key = rot_key(c, step);
   const u32* perm = c->d_perm.at(step);
   const RowMap c1 = make_map(in + (u64)m * N, m, N, 2ull * m * N, 1, 0, c->primes_0(m));
-  u64* dig = ks_decompose(c, c1, B, m);
-  u64* acc = ks_ip(c, dig, B, m, key, perm);
+  // automorphism applied to the coefficient-domain c1 before the lift: the
+  // digits come out already permuted and the inner product reads contiguously
+  u64* dig = ks_decompose(c, c1, B, m, c->d_sigma.at(step));
+  u64* acc = ks_ip(c, dig, B, m, key, nullptr);
   const RowMap inm = ct_map(in, m, N, 2ull * m * N);
   ks_moddown(c, acc, B, m, ct_map(out, m, N, 2ull * m * N), accumulate ? inm : null_map(), inm,
              perm);
@@ -868,6 +881,7 @@ void free_context(lcl_context* c) {
   cudaFree(c->d_relin);
   for (auto& kv : c->d_rot) cudaFree(kv.second);
   for (auto& kv : c->d_perm) cudaFree(kv.second);
+  for (auto& kv : c->d_sigma) cudaFree(kv.second);
   for (DevBuf* b : {&c->ws_coef, &c->ws_digits, &c->ws_acc, &c->ws_coefsp, &c->ws_mid,
                     &c->ws_tern, &c->ws_ctA, &c->ws_ctB, &c->ws_ctC, &c->ws_pt, &c->ws_io_in,
                     &c->ws_io_sel, &c->ws_io_dist, &c->ws_io_agg})
@@ -897,6 +911,24 @@ std::vector<u32> galois_perm(size_t n, int logn, size_t step) {
     p[i] = (u32)h_brv((size_t)((t - 1) / 2), logn);
   }
   return p;
+}
+
+// The same automorphism on coefficients: y(X) = x(X^elt), gathered as
+// y[k] = +-x[src] with src = k * elt^-1 mod 2N folded into [0, N).
+std::vector<u32> galois_sigma(size_t n, size_t step) {
+  const u64 two_n = 2 * (u64)n;
+  u64 elt = 1;
+  for (size_t i = 0; i < step % (n / 2); ++i) elt = (elt * 5) % two_n;
+  // elt is odd, so it is invertible mod 2N (a power of two): Newton iteration
+  u64 inv = elt;
+  for (int i = 0; i < 6; ++i) inv = (inv * (2 - elt * inv)) % two_n;
+  inv %= two_n;
+  std::vector<u32> s(n);
+  for (size_t k = 0; k < n; ++k) {
+    const u64 src = ((u64)k * inv) % two_n;
+    s[k] = src < n ? (u32)src : ((u32)(src - n) | 0x80000000u);
+  }
+  return s;
 }
 
 void check_count(const lcl_context* c, size_t count) {
@@ -1029,6 +1061,11 @@ int lcl_upload_rotation_key(lcl_context* ctx, size_t step, const uint64_t* h_key
       cuda_check(cudaMalloc(&dp, p.size() * 4), "perm alloc");
       cuda_check(cudaMemcpy(dp, p.data(), p.size() * 4, cudaMemcpyHostToDevice), "perm upload");
       ctx->d_perm[step] = dp;
+      const std::vector<u32> sg = galois_sigma(ctx->n, step);
+      u32* ds = nullptr;
+      cuda_check(cudaMalloc(&ds, sg.size() * 4), "sigma alloc");
+      cuda_check(cudaMemcpy(ds, sg.data(), sg.size() * 4, cudaMemcpyHostToDevice), "sigma upload");
+      ctx->d_sigma[step] = ds;
     }
   });
 }

@@ -148,40 +148,45 @@ __global__ void __launch_bounds__(256)
 // ------------------------------------------------------------------------
 // Key inner product (ckks.cpp:490-518 without the ModDown):
 //   acc_x[b][r][a] = sum_j digit_j[b][r][g(a)] * key_x[j][kr][a],  g = perm or identity
-// digits: [B][m][m+1][N]; key: [full][2][full+1][N]; acc: [B][2][m+1][N].
-// A thread owns one slot of one target row and walks the batch, so every key
-// word is read once per launch (all B ciphertexts share the key).
+// digits: [B][M][M+1][N]; key: [full][2][full+1][N]; acc: [B][2][M+1][N].
+// A thread owns one slot of one target row for IB consecutive ciphertexts:
+// the 2M key words stay in registers and are reused IB times; grid.y walks
+// the batch, so every key word is read from HBM once per launch (L2 serves
+// the other item blocks). Products < 2^108 are summed exactly in 128 bits.
+template <int M, int IB>
 __global__ void __launch_bounds__(256)
-    ks_inner_product(const u64* __restrict__ digits, u32 B, u32 m, const u64* __restrict__ key,
+    ks_inner_product(const u64* __restrict__ digits, u32 B, const u64* __restrict__ key,
                      u32 full, const u32* __restrict__ perm, u64* __restrict__ acc, u32 logn,
                      const PrimeConst* __restrict__ primes) {
   const u32 N = 1u << logn;
   const u32 gid = blockIdx.x * blockDim.x + threadIdx.x;
   const u32 r = gid >> logn, a = gid & (N - 1);
-  if (r > m) return;
-  const u32 kr = r < m ? r : full;
+  if (r > (u32)M) return;
+  const u32 b0 = blockIdx.y * IB;
+  const u32 kr = r < (u32)M ? r : full;
   const PrimeConst P = primes[kr];
   const u64 kstride = (u64)(full + 1) * N;
-  u64 k0[LCL_MAXP], k1[LCL_MAXP];
+  u64 k0[M], k1[M];
 #pragma unroll
-  for (u32 j = 0; j < LCL_MAXP; ++j) {
-    if (j < m) {
-      k0[j] = __ldg(key + (2ull * j) * kstride + (u64)kr * N + a);
-      k1[j] = __ldg(key + (2ull * j + 1) * kstride + (u64)kr * N + a);
-    }
+  for (int j = 0; j < M; ++j) {
+    k0[j] = __ldg(key + (2ull * j) * kstride + (u64)kr * N + a);
+    k1[j] = __ldg(key + (2ull * j + 1) * kstride + (u64)kr * N + a);
   }
   const u32 g = perm ? __ldg(perm + a) : a;
-  const u64 dstride = (u64)(m + 1) * N;
-  for (u32 b = 0; b < B; ++b) {
-    const u64* d = digits + (u64)b * m * dstride + (u64)r * N + g;
+  const u64 dstride = (u64)(M + 1) * N;
+#pragma unroll 2
+  for (int i = 0; i < IB; ++i) {
+    const u32 b = b0 + i;
+    if (b >= B) break;
+    const u64* d = digits + (u64)b * M * dstride + (u64)r * N + g;
+    u64 v[M];
+#pragma unroll
+    for (int j = 0; j < M; ++j) v[j] = __ldg(d + j * dstride);
     u64 l0 = 0, h0 = 0, l1 = 0, h1 = 0;
 #pragma unroll
-    for (u32 j = 0; j < LCL_MAXP; ++j) {
-      if (j < m) {
-        const u64 v = __ldg(d + j * dstride);
-        mac128(l0, h0, v, k0[j]);
-        mac128(l1, h1, v, k1[j]);
-      }
+    for (int j = 0; j < M; ++j) {
+      mac128(l0, h0, v[j], k0[j]);
+      mac128(l1, h1, v[j], k1[j]);
     }
     u64* o = acc + (u64)b * 2 * dstride + (u64)r * N + a;
     o[0] = reduce128(l0, h0, P);

@@ -39,12 +39,16 @@ __device__ __forceinline__ Tw ldtw(const ulonglong2* t, u32 idx) {
   return Tw{v.x, v.y};
 }
 
-// Forward CT butterfly: x, y in [0, 4q) -> x', y' in [0, 4q).
+// Forward CT butterfly without intermediate reduction: with t = y*w mod q in
+// [0, 2q), x' = x + t and y' = x + 2q - t both stay below B + 2q when x < B.
+// Starting from inputs < q, after s stages every value is < (1 + 2s) q; for
+// s <= 17 and q < 2^55 that is < 35 * 2^55 < 2^61, so no word overflows and
+// the only reduction is the final one (reduce64). Shoup accepts any y < 2^64.
 __device__ __forceinline__ void ct_bfly(u64& x, u64& y, Tw w, u64 q, u64 two_q) {
-  const u64 a = x >= two_q ? x - two_q : x;
   const u64 t = mul_shoup_lazy(y, w.w, w.ws, q);
+  const u64 a = x;
   x = a + t;
-  y = a - t + two_q;
+  y = a + (two_q - t);
 }
 
 // Inverse GS butterfly: x, y in [0, 2q) -> x', y' in [0, 2q).
@@ -55,49 +59,83 @@ __device__ __forceinline__ void gs_bfly(u64& x, u64& y, Tw w, u64 q, u64 two_q) 
   y = mul_shoup_lazy(a - b + two_q, w.w, w.ws, q);
 }
 
-__device__ __forceinline__ u64 reduce_4q(u64 x, u64 q, u64 two_q) {
-  x = x >= two_q ? x - two_q : x;
-  return x >= q ? x - q : x;
-}
-
 // ------------------------------------------------------------ loaders
-// Loader(r, a, dst_prime_index, dst) -> value in [0, q) (or any < 4q).
+// A loader is bound once per row (all address / constant lookups hoisted):
+//   auto row = ld.bind(r, dst_prime_index, dst);  row(a) -> value < q
 struct PlainLoad {
   RowMap in;
-  __device__ __forceinline__ u64 operator()(u32 r, u32 a, u32, const PrimeConst&) const {
-    return __ldg(row_ptr(in, r) + a);
+  struct Row {
+    const u64* p;
+    __device__ __forceinline__ u64 operator()(u32 a) const { return __ldg(p + a); }
+  };
+  __device__ __forceinline__ Row bind(u32 r, u32, const PrimeConst&) const {
+    return Row{row_ptr(in, r)};
   }
+  __host__ __device__ static constexpr double rows_read(double rows, u32) { return rows; }
 };
 
 // Centred lift of a coefficient-domain source row into the destination prime
 // (single-prime mod_up branch, rns.cpp:367-383; the lift inside
 // divide_and_round_by_last, rns.cpp:484-494). Destination row r of a launch
-// reads source row  (r / rows_per_item) * src_item_stride + ((r % rows_per_item) / fan) * n.
+// reads source row (r / rows_per_item) * (rows_per_item / fan) + (r % rows_per_item) / fan.
+// With `sigma` set, the source is read through the Galois automorphism
+// X -> X^elt in the coefficient domain (entry = src index | negate << 31);
+// lifting commutes with that signed permutation, so the lifted, transformed
+// digit equals apply_galois of the reference's digit (ckks.cpp:497-501).
 struct LiftLoad {
-  RowMap src;                // source rows: rows_per_item / fan per destination item
-  u32 rows_per_item;         // destination rows per item
-  u32 fan;                   // destination rows per source row
+  RowMap src;
+  u32 rows_per_item;
+  u32 fan;
   u32 nprimes;               // full + 1
   const PrimeConst* primes;  // device table
   const u64* smod;           // smod[s * nprimes + d] = q_s mod q_d
-  __device__ __forceinline__ u64 operator()(u32 r, u32 a, u32 dpi, const PrimeConst& dst) const {
+  const u32* sigma;          // nullptr: identity
+  struct Row {
+    const u64* s;
+    const u32* sigma;
+    u64 qs, half, sd, q, one_shoup;
+    __device__ __forceinline__ u64 operator()(u32 a) const {
+      u64 v;
+      if (sigma) {
+        const u32 e = __ldg(sigma + a);
+        v = __ldg(s + (e & 0x7FFFFFFFu));
+        if ((e >> 31) && v) v = qs - v;
+      } else {
+        v = __ldg(s + a);
+      }
+      u64 x = v - __umul64hi(v, one_shoup) * q;
+      x = x >= q ? x - q : x;
+      if (v > half) x = x >= sd ? x - sd : x + q - sd;
+      return x;
+    }
+  };
+  __device__ __forceinline__ Row bind(u32 r, u32 dpi, const PrimeConst& dst) const {
     const u32 item = r / rows_per_item;
     const u32 sub = (r - item * rows_per_item) / fan;
     const u32 srow = item * (rows_per_item / fan) + sub;
     const u32 sp = row_prime(src, srow);
-    const u64 v = __ldg(row_ptr(src, srow) + a);
-    u64 x = reduce64(v, dst);
-    if (v > __ldg(&primes[sp].half)) x = sub_mod(x, __ldg(smod + sp * nprimes + dpi), dst.q);
-    return x;
+    Row w;
+    w.s = row_ptr(src, srow);
+    w.sigma = sigma;
+    w.qs = __ldg(&primes[sp].q);
+    w.half = __ldg(&primes[sp].half);
+    w.sd = __ldg(smod + sp * nprimes + dpi);
+    w.q = dst.q;
+    w.one_shoup = dst.one_shoup;
+    return w;
   }
 };
 
 // ------------------------------------------------------------ epilogues
-// Epilogue(r, a, value in [0, q), dst_prime_index, dst)
+// auto row = epi.bind(r, dst_prime_index, dst);  row(a, value < q)
 struct PlainStore {
   RowMap out;
-  __device__ __forceinline__ void operator()(u32 r, u32 a, u64 v, u32, const PrimeConst&) const {
-    row_ptr(out, r)[a] = v;
+  struct Row {
+    u64* p;
+    __device__ __forceinline__ void operator()(u32 a, u64 v) const { p[a] = v; }
+  };
+  __device__ __forceinline__ Row bind(u32 r, u32, const PrimeConst&) const {
+    return Row{row_ptr(out, r)};
   }
 };
 
@@ -112,17 +150,34 @@ struct DivRoundStore {
   RowMap add2;  // base == nullptr: absent
   const u32* perm;  // gather for add2 (nullptr: identity)
   const ulonglong2* pinv;  // indexed by destination prime: (p^-1 mod q, shoup)
-  __device__ __forceinline__ void operator()(u32 r, u32 a, u64 lift, u32 dpi,
-                                             const PrimeConst& P) const {
-    const ulonglong2 iv = __ldg(pinv + dpi);
-    const u64 xv = row_ptr(x, r)[a];
-    u64 v = mul_shoup(xv - lift + P.q, iv.x, iv.y, P.q);
-    if (add1.base) v = add_mod(v, row_ptr(add1, r)[a], P.q);
-    if (add2.base && ((r / out.rows_per_item) % out.items_per_group) == 0) {
-      const u32 src = perm ? __ldg(perm + a) : a;
-      v = add_mod(v, row_ptr(add2, r)[src], P.q);
+  struct Row {
+    u64* o;
+    const u64* x;
+    const u64* a1;
+    const u64* a2;
+    const u32* perm;
+    u64 iv, ivs, q;
+    __device__ __forceinline__ void operator()(u32 a, u64 lift) const {
+      const u64 xv = x[a];
+      u64 v = mul_shoup(xv - lift + q, iv, ivs, q);
+      if (a1) v = add_mod(v, a1[a], q);
+      if (a2) v = add_mod(v, a2[perm ? __ldg(perm + a) : a], q);
+      o[a] = v;
     }
-    row_ptr(out, r)[a] = v;
+  };
+  __device__ __forceinline__ Row bind(u32 r, u32 dpi, const PrimeConst& P) const {
+    Row w;
+    const ulonglong2 iv = __ldg(pinv + dpi);
+    w.o = row_ptr(out, r);
+    w.x = row_ptr(x, r);
+    w.a1 = add1.base ? row_ptr(add1, r) : nullptr;
+    w.a2 = (add2.base && ((r / out.rows_per_item) % out.items_per_group) == 0) ? row_ptr(add2, r)
+                                                                                : nullptr;
+    w.perm = perm;
+    w.iv = iv.x;
+    w.ivs = iv.y;
+    w.q = P.q;
+    return w;
   }
 };
 
@@ -182,8 +237,11 @@ __global__ void __launch_bounds__(16 * ((1 << LOGN1) / E))
   const PrimeConst P = primes[pi];
   const ulonglong2* tw = tw_all + (u64)pi * n;
   u64 x[E];
+  {
+    const auto row = ld.bind(r, pi, P);
 #pragma unroll
-  for (int e = 0; e < E; ++e) x[e] = ld(r, j + (k + R * e) * n2, pi, P);
+    for (int e = 0; e < E; ++e) x[e] = row(j + (k + R * e) * n2);
+  }
   // phase 1: m = 1 .. E/2; group g of a stage is twiddle root[m + g]
   static_for<0, LOGE, 1>([&](auto LM) {
     constexpr int lm = decltype(LM)::value;
@@ -247,10 +305,11 @@ __global__ void __launch_bounds__(64)
   });
   __syncwarp();
 #pragma unroll
-  for (int e = 0; e < 16; ++e) s[16 * l + e + l] = reduce_4q(x[e], P.q, P.two_q);
+  for (int e = 0; e < 16; ++e) s[16 * l + e + l] = reduce64(x[e], P);
   __syncwarp();
+  const auto row = epi.bind(r, pi, P);
 #pragma unroll
-  for (int e = 0; e < 16; ++e) epi(r, (b << 8) + l + 16 * e, s[l + 16 * e + e], pi, P);
+  for (int e = 0; e < 16; ++e) row((b << 8) + l + 16 * e, s[l + 16 * e + e]);
 }
 
 // Block pass, inverse: GS stages m = N/2 .. N1 (local m' = 128 .. 1).
@@ -340,11 +399,9 @@ __global__ void __launch_bounds__(16 * ((1 << LOGN1) / E))
     constexpr int lm = decltype(LM)::value;
     gs_stage<E, (E >> (lm + 1))>(x, [&](int gi) { return ldtw(tw, (1 << lm) + gi); }, P.q, P.two_q);
   });
+  const auto row = epi.bind(r, pi, P);
 #pragma unroll
-  for (int e = 0; e < E; ++e) {
-    const u64 v = mul_shoup(x[e], P.n_inv, P.n_inv_shoup, P.q);
-    epi(r, j + (k + R * e) * n2, v, pi, P);
-  }
+  for (int e = 0; e < E; ++e) row(j + (k + R * e) * n2, mul_shoup(x[e], P.n_inv, P.n_inv_shoup, P.q));
 }
 
 // Single-CTA transform for small rings (N <= 4096): the whole row in shared
@@ -360,8 +417,12 @@ __global__ void __launch_bounds__(256)
   const u32 pi = row_prime(rows, r);
   const PrimeConst P = primes[pi];
   const ulonglong2* tw = tw_all + (u64)pi * n;
-  for (u32 a = threadIdx.x; a < n; a += blockDim.x) smem[a] = ld(r, a, pi, P);
+  {
+    const auto row = ld.bind(r, pi, P);
+    for (u32 a = threadIdx.x; a < n; a += blockDim.x) smem[a] = row(a);
+  }
   __syncthreads();
+  const auto out = epi.bind(r, pi, P);
   if (!INV) {
     u32 half = n;
     for (u32 m = 1; m < n; m <<= 1) {
@@ -373,7 +434,7 @@ __global__ void __launch_bounds__(256)
       }
       __syncthreads();
     }
-    for (u32 a = threadIdx.x; a < n; a += blockDim.x) epi(r, a, reduce_4q(smem[a], P.q, P.two_q), pi, P);
+    for (u32 a = threadIdx.x; a < n; a += blockDim.x) out(a, reduce64(smem[a], P));
   } else {
     u32 half = 1;
     for (u32 m = n >> 1; m >= 1; m >>= 1) {
@@ -386,7 +447,7 @@ __global__ void __launch_bounds__(256)
       half <<= 1;
     }
     for (u32 a = threadIdx.x; a < n; a += blockDim.x)
-      epi(r, a, mul_shoup(smem[a], P.n_inv, P.n_inv_shoup, P.q), pi, P);
+      out(a, mul_shoup(smem[a], P.n_inv, P.n_inv_shoup, P.q));
   }
 }
 
