@@ -53,6 +53,10 @@ void cuda_check(cudaError_t e, const char* what) {
   if (e != cudaSuccess) fail(LCL_CUDA_ERROR, std::string(what) + ": " + cudaGetErrorString(e));
 }
 
+void need(bool ok, int code, const char* msg) {
+  if (!ok) fail(code, msg);
+}
+
 // ------------------------------------------------------------ host modular math
 // Setup-time only (basis construction); restates modmath.cpp:24-132.
 u64 h_mulmod(u64 a, u64 b, u64 q) { return (u64)((u128)a * b % q); }
@@ -251,7 +255,9 @@ struct lcl_context {
   size_t pairs_cap = 0;
   u32 pairs_n = 0;
   u64* d_relin = nullptr;
+  u64* d_relin_shoup = nullptr;
   std::map<size_t, u64*> d_rot;
+  std::map<size_t, u64*> d_rot_shoup;
   std::map<size_t, u32*> d_perm;
   std::map<size_t, u32*> d_sigma;  // coefficient-domain automorphism (src | neg << 31)
   lcl_counts counts{};
@@ -397,6 +403,72 @@ void launch_fwd(lcl_context* c, u32 rows, const RowMap& pm, const Loader& ld, co
   }
 }
 
+LiftLoad lift_from(lcl_context* c, const RowMap& src, u32 rows_per_item, u32 fan) {
+  LiftLoad l;
+  l.src = src;
+  l.rows_per_item = rows_per_item;
+  l.fan = fan;
+  l.nprimes = c->P();
+  l.primes = c->d_primes;
+  l.smod = c->d_smod;
+  l.sigma = nullptr;
+  return l;
+}
+
+// Column pass only (first log2 N1 forward stages), writing `out` (lazy values).
+template <int LOGN1, int E, class Loader>
+void col_only(lcl_context* c, u32 rows, const RowMap& out, const Loader& ld) {
+  constexpr int N1 = 1 << LOGN1;
+  constexpr size_t smem = (size_t)N1 * 16 * 8;
+  static bool once = (allow_smem(ntt_col_fwd<LOGN1, E, Loader>, smem), true);
+  (void)once;
+  const u32 groups = (u32)(c->n >> LOGN1) >> 4;
+  ProfScope ps(c, "ntt_col_fwd<lift>", 8.0 * c->N() * (load_rows(ld, rows) + rows));
+  ntt_col_fwd<LOGN1, E, Loader><<<rows * groups, 16 * (N1 / E), smem, c->stream>>>(
+      out, ld, c->d_tw, c->d_primes, c->logn);
+}
+
+template <int LOGN1, int M>
+void modup_ip_launch(lcl_context* c, u32 B, const u64* mid, const u64* c1, u64 c1_stride,
+                     const u32* perm, const u64* key, const u64* key_shoup, u64* acc) {
+  constexpr int N1 = 1 << LOGN1;
+  const double rb = 8.0 * c->N();
+  ProfScope ps(c, perm ? "modup_ip_blk<perm>" : "modup_ip_blk",
+               rb * ((double)B * M * M + B * M + 4.0 * M * (M + 1) + 2.0 * B * (M + 1)));
+  modup_ip_blk<LOGN1, M><<<B * (M + 1) * N1 / 4, 64, 0, c->stream>>>(
+      mid, c1, c1_stride, perm, key, key_shoup, c->full, acc, c->d_tw, c->d_primes, c->logn);
+}
+
+template <int LOGN1, int E>
+void modup_ip_n(lcl_context* c, u32 B, u32 m, const RowMap& coef_map, const u32* sigma,
+                const u64* c1, u64 c1_stride, const u32* perm, const u64* key,
+                const u64* key_shoup, u64* acc) {
+  const u64 N = c->N();
+  // column pass over the m*m non-identity digit rows (b, j, t')
+  u64* mid = c->ws_digits.get((u64)B * m * m * N);
+  std::vector<u32> dp(m * m);
+  for (u32 j = 0; j < m; ++j)
+    for (u32 tp = 0; tp < m; ++tp) {
+      const u32 t = tp < j ? tp : tp + 1;
+      dp[j * m + tp] = t < m ? t : c->full;
+    }
+  const RowMap mid_map2 = make_map(mid, m * m, N, (u64)m * m * N, 1, 0, dp);
+  LiftLoad lift = lift_from(c, coef_map, m * m, m);
+  lift.sigma = sigma;
+  col_only<LOGN1, E>(c, B * m * m, mid_map2, lift);
+  post_launch(c);
+  switch (m) {
+    case 1: modup_ip_launch<LOGN1, 1>(c, B, mid, c1, c1_stride, perm, key, key_shoup, acc); break;
+    case 2: modup_ip_launch<LOGN1, 2>(c, B, mid, c1, c1_stride, perm, key, key_shoup, acc); break;
+    case 3: modup_ip_launch<LOGN1, 3>(c, B, mid, c1, c1_stride, perm, key, key_shoup, acc); break;
+    case 4: modup_ip_launch<LOGN1, 4>(c, B, mid, c1, c1_stride, perm, key, key_shoup, acc); break;
+    case 5: modup_ip_launch<LOGN1, 5>(c, B, mid, c1, c1_stride, perm, key, key_shoup, acc); break;
+    case 6: modup_ip_launch<LOGN1, 6>(c, B, mid, c1, c1_stride, perm, key, key_shoup, acc); break;
+    default: fail(LCL_PARAMETER_ERROR, "fused key switching supports up to 6 live limbs");
+  }
+  post_launch(c);
+}
+
 template <class Epi>
 void launch_inv(lcl_context* c, u32 rows, const RowMap& in, const Epi& epi) {
   if (rows == 0) return;
@@ -418,17 +490,6 @@ void launch_inv(lcl_context* c, u32 rows, const RowMap& in, const Epi& epi) {
   }
 }
 
-LiftLoad lift_from(lcl_context* c, const RowMap& src, u32 rows_per_item, u32 fan) {
-  LiftLoad l;
-  l.src = src;
-  l.rows_per_item = rows_per_item;
-  l.fan = fan;
-  l.nprimes = c->P();
-  l.primes = c->d_primes;
-  l.smod = c->d_smod;
-  l.sigma = nullptr;
-  return l;
-}
 
 // ------------------------------------------------------------ key switching
 // decompose_for_keyswitch (ckks.cpp:464-481): the c1 / d2 rows of B items
@@ -470,6 +531,33 @@ u64* ks_ip(lcl_context* c, const u64* dig, u32 B, u32 m, const u64* key, const u
   return acc;
 }
 
+// decompose_for_keyswitch + inner product (ckks.cpp:464-518) for the c1 / d2
+// limbs of B items: `in` maps them (rows_per_item = m); c1 / c1_stride address
+// the same limbs for the identity digits. sigma / perm: the rotation's
+// coefficient- / evaluation-domain automorphism (nullptr for relinearize).
+// Returns acc [B][2][m+1][N].
+u64* ks_switch(lcl_context* c, const RowMap& in, const u64* c1, u64 c1_stride, u32 B, u32 m,
+               const u32* sigma, const u32* perm, const u64* key, const u64* key_shoup) {
+  if (c->logn < 13 || m > 6) {
+    u64* dig = ks_decompose(c, in, B, m, sigma);
+    return ks_ip(c, dig, B, m, key, nullptr);
+  }
+  const u64 N = c->N();
+  u64* coef = c->ws_coef.get((u64)B * m * N);
+  const RowMap coef_map = make_map(coef, m, N, m * N, 1, 0, c->primes_0(m));
+  launch_inv(c, B * m, in, PlainStore{coef_map});
+  u64* acc = c->ws_acc.get((u64)B * 2 * (m + 1) * N);
+  switch (c->logn) {
+    case 13: modup_ip_n<5, 16>(c, B, m, coef_map, sigma, c1, c1_stride, perm, key, key_shoup, acc); break;
+    case 14: modup_ip_n<6, 16>(c, B, m, coef_map, sigma, c1, c1_stride, perm, key, key_shoup, acc); break;
+    case 15: modup_ip_n<7, 16>(c, B, m, coef_map, sigma, c1, c1_stride, perm, key, key_shoup, acc); break;
+    case 16: modup_ip_n<8, 16>(c, B, m, coef_map, sigma, c1, c1_stride, perm, key, key_shoup, acc); break;
+    case 17: modup_ip_n<9, 32>(c, B, m, coef_map, sigma, c1, c1_stride, perm, key, key_shoup, acc); break;
+    default: fail(LCL_PARAMETER_ERROR, "ring degree outside 2^13..2^17");
+  }
+  return acc;
+}
+
 // ModDown of acc [B][2][m+1][N] into `out` (items (b, x), rows_per_item m,
 // 2 items per group) with the fused output additions.
 void ks_moddown(lcl_context* c, const u64* acc, u32 B, u32 m, const RowMap& out,
@@ -500,8 +588,8 @@ void relinearize_batch(lcl_context* c, const u64* tern, u32 B, u32 m, u64* out) 
   if (!c->d_relin) fail(LCL_KEY_ERROR, "no relinearization key uploaded");
   const u64 N = c->N();
   const RowMap d2 = make_map(tern + 2ull * m * N, m, N, 3ull * m * N, 1, 0, c->primes_0(m));
-  u64* dig = ks_decompose(c, d2, B, m);
-  u64* acc = ks_ip(c, dig, B, m, c->d_relin, nullptr);
+  u64* acc = ks_switch(c, d2, tern + 2ull * m * N, 3ull * m * N, B, m, nullptr, nullptr,
+                       c->d_relin, c->d_relin_shoup);
   ks_moddown(c, acc, B, m, ct_map(out, m, N, 2ull * m * N), ct_map(tern, m, N, 3ull * m * N),
              null_map(), nullptr);
   c->counts.relinearizations += B;
@@ -544,8 +632,8 @@ void rotate_level(lcl_context* c, const u64* in, u32 B, u32 m, size_t step, u64*
   const RowMap c1 = make_map(in + (u64)m * N, m, N, 2ull * m * N, 1, 0, c->primes_0(m));
   // automorphism applied to the coefficient-domain c1 before the lift: the
   // digits come out already permuted and the inner product reads contiguously
-  u64* dig = ks_decompose(c, c1, B, m, c->d_sigma.at(step));
-  u64* acc = ks_ip(c, dig, B, m, key, nullptr);
+  u64* acc = ks_switch(c, c1, in + (u64)m * N, 2ull * m * N, B, m, c->d_sigma.at(step), perm,
+                       key, c->d_rot_shoup.at(step));
   const RowMap inm = ct_map(in, m, N, 2ull * m * N);
   ks_moddown(c, acc, B, m, ct_map(out, m, N, 2ull * m * N), accumulate ? inm : null_map(), inm,
              perm);
@@ -619,19 +707,22 @@ void ensure_pairs(lcl_context* c, u32 n) {
 }
 
 constexpr int kPP = 4;
+constexpr int kStages = 3;
 
 // Lazy ternary accumulators for pairs [p0, p1) over chunks [c0, c1).
 void pair_accumulate_launch(lcl_context* c, const u64* clients, u32 n, u32 chunks, u32 c0,
                             u32 c1, u32 p0, u32 p1, u64* tern, bool accumulate) {
   const u32 m = c->full;
-  const u32 warps = 8;
+  const u32 warps = 4;
   const u32 pairs = p1 - p0;
   const u32 per_cta = warps * kPP;
   dim3 grid((u32)(m * c->n / 32), (pairs + per_cta - 1) / per_cta);
-  const size_t smem = (size_t)n * 64 * 8;
+  const size_t smem = (size_t)kStages * n * 64 * 8;
+  need(smem <= 200 * 1024, LCL_SHAPE_ERROR, "too many clients for one tile");
+  allow_smem(pair_accumulate<kPP, kStages>, smem);
   ProfScope ps(c, "pair_accumulate",
                8.0 * c->N() * m * (2.0 * n * (c1 - c0) + 3.0 * pairs * (accumulate ? 2 : 1)));
-  pair_accumulate<kPP><<<grid, warps * 32, smem, c->stream>>>(
+  pair_accumulate<kPP, kStages><<<grid, warps * 32, smem, c->stream>>>(
       clients, n, c0, c1, chunks, m, c->logn, c->d_pairs, p0, p1, tern, accumulate ? 1 : 0,
       c->d_primes);
   post_launch(c);
@@ -782,9 +873,6 @@ int guarded(F&& f) {
   }
 }
 
-void need(bool ok, int code, const char* msg) {
-  if (!ok) fail(code, msg);
-}
 
 void build_context(lcl_context* c, size_t degree, int depth, int secure, int device) {
   need(degree >= 8 && (degree & (degree - 1)) == 0, LCL_PARAMETER_ERROR,
@@ -879,7 +967,9 @@ void free_context(lcl_context* c) {
   cudaFree(c->d_pinv);
   cudaFree(c->d_pairs);
   cudaFree(c->d_relin);
+  cudaFree(c->d_relin_shoup);
   for (auto& kv : c->d_rot) cudaFree(kv.second);
+  for (auto& kv : c->d_rot_shoup) cudaFree(kv.second);
   for (auto& kv : c->d_perm) cudaFree(kv.second);
   for (auto& kv : c->d_sigma) cudaFree(kv.second);
   for (DevBuf* b : {&c->ws_coef, &c->ws_digits, &c->ws_acc, &c->ws_coefsp, &c->ws_mid,
@@ -890,12 +980,26 @@ void free_context(lcl_context* c) {
 
 u64 key_words(const lcl_context* c) { return (u64)c->full * 2 * c->P() * c->N(); }
 
-u64* upload_key(lcl_context* c, const u64* h, size_t words) {
+u64* upload_key(lcl_context* c, const u64* h, size_t words, u64** shoup_out) {
   need(h != nullptr, LCL_KEY_ERROR, "null key");
   need(words == key_words(c), LCL_KEY_ERROR, "switch key has the wrong shape");
+  // Shoup companions floor(k * 2^64 / q_row) for the fused inner product.
+  std::vector<u64> sh(words);
+  const u64 N = c->N();
+  const u32 P = c->P();
+  for (size_t i = 0; i < words; ++i) {
+    const u32 row = (u32)((i / N) % P);
+    const u64 q = c->primes[row];
+    need(h[i] < q, LCL_KEY_ERROR, "key residue outside its modulus");
+    sh[i] = h_shoup(h[i], q);
+  }
   u64* d = nullptr;
+  u64* ds = nullptr;
   cuda_check(cudaMalloc(&d, words * 8), "key alloc");
+  cuda_check(cudaMalloc(&ds, words * 8), "key alloc");
   cuda_check(cudaMemcpy(d, h, words * 8, cudaMemcpyHostToDevice), "key upload");
+  cuda_check(cudaMemcpy(ds, sh.data(), words * 8, cudaMemcpyHostToDevice), "key upload");
+  *shoup_out = ds;
   return d;
 }
 
@@ -1040,9 +1144,12 @@ int lcl_profile_end(lcl_context* ctx, char* json, size_t cap) {
 int lcl_upload_relin_key(lcl_context* ctx, const uint64_t* h_key, size_t words) {
   return guarded([&] {
     cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
-    u64* d = upload_key(ctx, h_key, words);
+    u64* ds = nullptr;
+    u64* d = upload_key(ctx, h_key, words, &ds);
     if (ctx->d_relin) cudaFree(ctx->d_relin);
+    if (ctx->d_relin_shoup) cudaFree(ctx->d_relin_shoup);
     ctx->d_relin = d;
+    ctx->d_relin_shoup = ds;
   });
 }
 
@@ -1051,10 +1158,15 @@ int lcl_upload_rotation_key(lcl_context* ctx, size_t step, const uint64_t* h_key
     cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
     step %= ctx->n / 2;
     need(step != 0, LCL_KEY_ERROR, "rotation step 0 needs no key");
-    u64* d = upload_key(ctx, h_key, words);
+    u64* ds = nullptr;
+    u64* d = upload_key(ctx, h_key, words, &ds);
     auto it = ctx->d_rot.find(step);
-    if (it != ctx->d_rot.end()) cudaFree(it->second);
+    if (it != ctx->d_rot.end()) {
+      cudaFree(it->second);
+      cudaFree(ctx->d_rot_shoup[step]);
+    }
     ctx->d_rot[step] = d;
+    ctx->d_rot_shoup[step] = ds;
     if (!ctx->d_perm.count(step)) {
       const std::vector<u32> p = galois_perm(ctx->n, ctx->logn, step);
       u32* dp = nullptr;

@@ -15,15 +15,27 @@ namespace lcl {
 // and reused by every pair in the CTA).
 //
 // CTA: 32 consecutive slots of one limb row r; warp w, lane e handles PP pairs
-// of that slot. Grid: x = m * N / 32 slot tiles, y = pair groups.
+// of that slot. Grid: x = m * N / 32 slot tiles, y = pair groups. The client
+// tile of chunk c + STAGES - 1 streams into shared memory (cp.async) while
+// chunk c is being accumulated.
 // clients: [n][C][2][m][N]; tern out: [pairs][3][m][N] (pair p at out + (p - p0) * 3mN).
-template <int PP>
-__global__ void __launch_bounds__(256)
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  const u32 s = (u32)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n"); }
+template <int K>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(K));
+}
+
+template <int PP, int STAGES>
+__global__ void __launch_bounds__(128)
     pair_accumulate(const u64* __restrict__ clients, u32 n, u32 c_begin, u32 c_end,
                     u32 chunks_total, u32 m, u32 logn, const u32* __restrict__ pairs,
                     u32 p_begin, u32 p_end, u64* __restrict__ tern, int accumulate,
                     const PrimeConst* __restrict__ primes) {
-  extern __shared__ u64 tile[];  // [n][2][32]
+  extern __shared__ u64 tile[];  // [STAGES][n][2][32]
   const u32 N = 1u << logn;
   const u32 tiles_per_row = N >> 5;
   const u32 r = blockIdx.x / tiles_per_row;
@@ -33,15 +45,27 @@ __global__ void __launch_bounds__(256)
   const PrimeConst P = primes[r];
   const u64 q = P.q;
   const u64 ct_words = 2ull * m * N;
+  const u32 tw = n * 64;
   const u32 pbase = p_begin + (blockIdx.y * nwarps + warp) * PP;
+
+  auto issue = [&](u32 c, u32 stage) {
+    if (c < c_end) {
+      for (u32 v = threadIdx.x; v < tw; v += blockDim.x) {
+        const u32 cl = v >> 6, h = (v >> 5) & 1, e = v & 31;
+        cp_async8(tile + stage * tw + v, clients + ((u64)cl * chunks_total + c) * ct_words +
+                                             (u64)h * m * N + (u64)r * N + a0 + e);
+      }
+    }
+    cp_async_commit();  // empty groups keep the wait count uniform
+  };
 
   u32 pi[PP], pj[PP];
 #pragma unroll
   for (int t = 0; t < PP; ++t) {
     const u32 p = pbase + t;
     const u32 pk = p < p_end ? __ldg(pairs + p) : 0u;
-    pi[t] = pk & 0xFFFFu;
-    pj[t] = pk >> 16;
+    pi[t] = (pk & 0xFFFFu) * 64;
+    pj[t] = (pk >> 16) * 64;
   }
   Acc3 A00[PP], A01[PP], A11[PP];
 #pragma unroll
@@ -50,23 +74,25 @@ __global__ void __launch_bounds__(256)
     A01[t].zero();
     A11[t].zero();
   }
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) issue(c_begin + s, s);
+  u32 stage = 0;
   for (u32 c = c_begin; c < c_end; ++c) {
+    issue(c + STAGES - 1, (stage + STAGES - 1) % STAGES);
+    cp_async_wait<STAGES - 1>();
     __syncthreads();
-    for (u32 v = threadIdx.x; v < n * 64; v += blockDim.x) {
-      const u32 cl = v >> 6, h = (v >> 5) & 1, e = v & 31;
-      tile[v] = __ldg(clients + ((u64)cl * chunks_total + c) * ct_words + (u64)h * m * N +
-                      (u64)r * N + a0 + e);
-    }
-    __syncthreads();
+    const u64* tl = tile + stage * tw;
 #pragma unroll
     for (int t = 0; t < PP; ++t) {
-      const u64 x0 = tile[pi[t] * 64 + lane], x1 = tile[pi[t] * 64 + 32 + lane];
-      const u64 y0 = tile[pj[t] * 64 + lane], y1 = tile[pj[t] * 64 + 32 + lane];
+      const u64 x0 = tl[pi[t] + lane], x1 = tl[pi[t] + 32 + lane];
+      const u64 y0 = tl[pj[t] + lane], y1 = tl[pj[t] + 32 + lane];
       const Split e0 = split23(x0 - y0 + q), e1 = split23(x1 - y1 + q);
       A00[t].sq(e0);
       A01[t].mac(e0, e1);
       A11[t].sq(e1);
     }
+    __syncthreads();
+    stage = (stage + 1) % STAGES;
   }
 #pragma unroll
   for (int t = 0; t < PP; ++t) {

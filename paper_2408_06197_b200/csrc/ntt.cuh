@@ -130,9 +130,12 @@ struct LiftLoad {
 // auto row = epi.bind(r, dst_prime_index, dst);  row(a, value < q)
 struct PlainStore {
   RowMap out;
+  struct Pre {};
   struct Row {
     u64* p;
     __device__ __forceinline__ void operator()(u32 a, u64 v) const { p[a] = v; }
+    __device__ __forceinline__ void prefetch(Pre&, u32) const {}
+    __device__ __forceinline__ void store(const Pre&, u32 a, u64 v) const { p[a] = v; }
   };
   __device__ __forceinline__ Row bind(u32 r, u32, const PrimeConst&) const {
     return Row{row_ptr(out, r)};
@@ -150,6 +153,9 @@ struct DivRoundStore {
   RowMap add2;  // base == nullptr: absent
   const u32* perm;  // gather for add2 (nullptr: identity)
   const ulonglong2* pinv;  // indexed by destination prime: (p^-1 mod q, shoup)
+  struct Pre {
+    u64 x, add;  // x[a] and the sum of the (up to two) addends
+  };
   struct Row {
     u64* o;
     const u64* x;
@@ -158,11 +164,19 @@ struct DivRoundStore {
     const u32* perm;
     u64 iv, ivs, q;
     __device__ __forceinline__ void operator()(u32 a, u64 lift) const {
-      const u64 xv = x[a];
-      u64 v = mul_shoup(xv - lift + q, iv, ivs, q);
-      if (a1) v = add_mod(v, a1[a], q);
-      if (a2) v = add_mod(v, a2[perm ? __ldg(perm + a) : a], q);
-      o[a] = v;
+      Pre p;
+      prefetch(p, a);
+      store(p, a, lift);
+    }
+    __device__ __forceinline__ void prefetch(Pre& p, u32 a) const {
+      p.x = x[a];
+      u64 s = a1 ? a1[a] : 0;
+      if (a2) s = add_mod(s, a2[perm ? __ldg(perm + a) : a], q);
+      p.add = s;
+    }
+    __device__ __forceinline__ void store(const Pre& p, u32 a, u64 lift) const {
+      const u64 v = mul_shoup(p.x - lift + q, iv, ivs, q);
+      o[a] = add_mod(v, p.add, q);
     }
   };
   __device__ __forceinline__ Row bind(u32 r, u32 dpi, const PrimeConst& P) const {
@@ -264,8 +278,43 @@ __global__ void __launch_bounds__(16 * ((1 << LOGN1) / E))
   for (int e = 0; e < E; ++e) o[j + (k * E + e) * n2] = x[e];
 }
 
+// Block pass body, forward: x[e] holds element l + 16 e of one 256-point
+// block (coalesced order) on entry and the fully reduced output in the same
+// order on exit. Phase 1 runs local stages m' = 1..8 on s = l + 16 e, phase 2
+// m' = 16..128 on s = 16 l + e after a warp-local shared transpose.
+template <int LOGN1>
+__device__ __forceinline__ void blk_fwd_body(u64 (&x)[16], u64* s, const ulonglong2* tw, u32 b,
+                                             u32 l, const PrimeConst& P) {
+  constexpr int N1 = 1 << LOGN1;
+  static_for<0, 4, 1>([&](auto LM) {
+    constexpr int lm = decltype(LM)::value;
+    ct_stage<16, (16 >> (lm + 1))>(x, [&](int gi) { return ldtw(tw, (N1 + b) * (1 << lm) + gi); },
+                                   P.q, P.two_q);
+  });
+#pragma unroll
+  for (int e = 0; e < 16; ++e) s[l + 16 * e + e] = x[e];
+  __syncwarp();
+#pragma unroll
+  for (int e = 0; e < 16; ++e) x[e] = s[16 * l + e + l];
+  static_for<4, 8, 1>([&](auto LM) {
+    constexpr int lm = decltype(LM)::value;
+    constexpr int d = 256 >> (lm + 1);
+    ct_stage<16, d>(x,
+                    [&](int gi) { return ldtw(tw, (N1 + b) * (1 << lm) + ((16 * l + gi * 2 * d) >> (8 - lm))); },
+                    P.q, P.two_q);
+  });
+  __syncwarp();
+#pragma unroll
+  for (int e = 0; e < 16; ++e) s[16 * l + e + l] = reduce64(x[e], P);
+  __syncwarp();
+#pragma unroll
+  for (int e = 0; e < 16; ++e) x[e] = s[l + 16 * e + e];
+  __syncwarp();
+}
+
 // Block pass, forward: 256-point blocks, 16 threads per block, 16 elements per
-// thread, 4 blocks per CTA. Phase 1 on s = l + 16 e, phase 2 on s = 16 l + e.
+// thread, 4 blocks per CTA. The epilogue's operands are prefetched before the
+// butterflies so their latency overlaps the arithmetic.
 template <int LOGN1, class Epi>
 __global__ void __launch_bounds__(64)
     ntt_blk_fwd(const __grid_constant__ RowMap in, const __grid_constant__ Epi epi,
@@ -285,31 +334,84 @@ __global__ void __launch_bounds__(64)
   u64 x[16];
 #pragma unroll
   for (int e = 0; e < 16; ++e) x[e] = src[l + 16 * e];
-  static_for<0, 4, 1>([&](auto LM) {
-    constexpr int lm = decltype(LM)::value;
-    ct_stage<16, (16 >> (lm + 1))>(x, [&](int gi) { return ldtw(tw, (N1 + b) * (1 << lm) + gi); },
-                                   P.q, P.two_q);
-  });
-  u64* s = sm[bw];
-#pragma unroll
-  for (int e = 0; e < 16; ++e) s[l + 16 * e + e] = x[e];
-  __syncwarp();
-#pragma unroll
-  for (int e = 0; e < 16; ++e) x[e] = s[16 * l + e + l];
-  static_for<4, 8, 1>([&](auto LM) {
-    constexpr int lm = decltype(LM)::value;
-    constexpr int d = 256 >> (lm + 1);
-    ct_stage<16, d>(x,
-                    [&](int gi) { return ldtw(tw, (N1 + b) * (1 << lm) + ((16 * l + gi * 2 * d) >> (8 - lm))); },
-                    P.q, P.two_q);
-  });
-  __syncwarp();
-#pragma unroll
-  for (int e = 0; e < 16; ++e) s[16 * l + e + l] = reduce64(x[e], P);
-  __syncwarp();
   const auto row = epi.bind(r, pi, P);
+  typename Epi::Pre pre[16];
 #pragma unroll
-  for (int e = 0; e < 16; ++e) row((b << 8) + l + 16 * e, s[l + 16 * e + e]);
+  for (int e = 0; e < 16; ++e) row.prefetch(pre[e], (b << 8) + l + 16 * e);
+  blk_fwd_body<LOGN1>(x, sm[bw], tw, b, l, P);
+#pragma unroll
+  for (int e = 0; e < 16; ++e) row.store(pre[e], (b << 8) + l + 16 * e, x[e]);
+}
+
+// ModUp block pass fused with the key inner product (ckks.cpp:464-518).
+// A 16-thread group owns block blk of target row t of ciphertext b and walks
+// the M digits: digit j is the column-pass output mid[b][j][t'] run through
+// the block stages, except the identity row t == j, whose lifted NTT is the
+// input limb itself (mod_up returns the row unchanged, rns.cpp:371-381), read
+// through the rotation's evaluation-domain permutation when one is given.
+// Each digit is multiplied by the key in Shoup form and accumulated lazily
+// (< 2Mq), so the m(m+1) digit rows never reach HBM.
+//   mid: [B][M][M][N] (t' = t < j ? t : t - 1); c1: limb j of item b at
+//   c1 + b * c1_stride + j * N; key / key_shoup: [full][2][full+1][N];
+//   acc: [B][2][M+1][N].
+template <int LOGN1, int M>
+__global__ void __launch_bounds__(64)
+    modup_ip_blk(const u64* __restrict__ mid, const u64* __restrict__ c1, u64 c1_stride,
+                 const u32* __restrict__ perm, const u64* __restrict__ key,
+                 const u64* __restrict__ key_shoup, u32 full, u64* __restrict__ acc,
+                 const ulonglong2* __restrict__ tw_all, const PrimeConst* __restrict__ primes,
+                 u32 logn) {
+  constexpr int N1 = 1 << LOGN1;
+  __shared__ u64 sm[4][256 + 16];
+  const u32 n = 1u << logn;
+  const u32 l = threadIdx.x & 15, bw = threadIdx.x >> 4;
+  const u32 blk_global = blockIdx.x * 4 + bw;
+  const u32 row = blk_global / N1;  // = b * (M + 1) + t
+  const u32 blk = blk_global - row * N1;
+  const u32 bi = row / (M + 1), t = row - bi * (M + 1);
+  const u32 pi = t < (u32)M ? t : full;
+  const PrimeConst P = primes[pi];
+  const ulonglong2* tw = tw_all + (u64)pi * n;
+  const u64 kstride = (u64)(full + 1) * n;
+  const u32 a0 = (blk << 8) + l;
+  u64 acc0[16], acc1[16];
+#pragma unroll
+  for (int e = 0; e < 16; ++e) acc0[e] = acc1[e] = 0;
+#pragma unroll 1
+  for (int j = 0; j < M; ++j) {
+    u64 x[16];
+    if (t == (u32)j) {
+      const u64* src = c1 + (u64)bi * c1_stride + (u64)j * n;
+#pragma unroll
+      for (int e = 0; e < 16; ++e) {
+        const u32 a = a0 + 16 * e;
+        x[e] = __ldg(src + (perm ? __ldg(perm + a) : a));
+      }
+    } else {
+      const u32 tp = t < (u32)j ? t : t - 1;
+      const u64* src = mid + (((u64)bi * M + j) * M + tp) * n + (blk << 8);
+#pragma unroll
+      for (int e = 0; e < 16; ++e) x[e] = src[l + 16 * e];
+      blk_fwd_body<LOGN1>(x, sm[bw], tw, blk, l, P);
+    }
+    const u64* k0 = key + (2ull * j) * kstride + (u64)pi * n;
+    const u64* k1 = k0 + kstride;
+    const u64* s0 = key_shoup + (2ull * j) * kstride + (u64)pi * n;
+    const u64* s1 = s0 + kstride;
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+      const u32 a = a0 + 16 * e;
+      acc0[e] += mul_shoup_lazy(x[e], __ldg(k0 + a), __ldg(s0 + a), P.q);
+      acc1[e] += mul_shoup_lazy(x[e], __ldg(k1 + a), __ldg(s1 + a), P.q);
+    }
+  }
+  u64* o0 = acc + ((u64)bi * 2 * (M + 1) + t) * n;
+  u64* o1 = o0 + (u64)(M + 1) * n;
+#pragma unroll
+  for (int e = 0; e < 16; ++e) {
+    o0[a0 + 16 * e] = reduce64(acc0[e], P);
+    o1[a0 + 16 * e] = reduce64(acc1[e], P);
+  }
 }
 
 // Block pass, inverse: GS stages m = N/2 .. N1 (local m' = 128 .. 1).

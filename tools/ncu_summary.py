@@ -21,7 +21,7 @@ METRICS = [
     ("warp_insts_M", "smsp__inst_executed.sum"),
     ("l2_hit_pct", "lts__t_sector_hit_rate.pct"),
 ]
-STALLS = "smsp__average_warp_latency_issue_stalled_"
+STALLS = "smsp__average_warps_issue_stalled_"
 
 
 def load(path):
@@ -42,7 +42,7 @@ def main():
     path = sys.argv[1]
     hdr, units, rows = load(path)
     col = {h: i for i, h in enumerate(hdr)}
-    stall_cols = [h for h in hdr if h.startswith(STALLS) and h.endswith(".ratio")]
+    stall_cols = [h for h in hdr if h.startswith(STALLS) and h.endswith("_per_issue_active.ratio")]
     for r in rows:
         name = r[col["Kernel Name"]][:90]
         print(f"== {name}")
@@ -62,7 +62,7 @@ def main():
                     v = v / 1e6
                 parts.append(f"{label}={v:.1f}")
         print("   " + " ".join(parts))
-        st = sorted(((num(r[col[h]]), h[len(STALLS):-6]) for h in stall_cols), reverse=True)[:5]
+        st = sorted(((num(r[col[h]]), h[len(STALLS):-len("_per_issue_active.ratio")]) for h in stall_cols), reverse=True)[:6]
         print("   stalls: " + ", ".join(f"{n}={v:.1f}" for v, n in st if v == v))
 
 
