@@ -24,6 +24,7 @@ struct PrimeConst {
   u64 one_shoup;           // floor(2^64 / q): 64-bit reduction via Shoup with w = 1
   u64 half;                // q >> 1: centred-lift threshold (rns.cpp:370-378)
   u64 n_inv, n_inv_shoup;  // N^-1 mod q
+  u64 w1n, w1n_shoup;      // iroot[1] * N^-1: last inverse stage with the scaling folded in
 };
 
 // Row addressing for batched transforms. Row r of a launch is row

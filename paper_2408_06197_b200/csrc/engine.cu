@@ -435,8 +435,8 @@ void modup_ip_launch(lcl_context* c, u32 B, const u64* mid, const u64* c1, u64 c
   const double rb = 8.0 * c->N();
   ProfScope ps(c, perm ? "modup_ip_blk<perm>" : "modup_ip_blk",
                rb * ((double)B * M * M + B * M + 4.0 * M * (M + 1) + 2.0 * B * (M + 1)));
-  modup_ip_blk<LOGN1, M><<<B * (M + 1) * N1 / 4, 64, 0, c->stream>>>(
-      mid, c1, c1_stride, perm, key, key_shoup, c->full, acc, c->d_tw, c->d_primes, c->logn);
+  modup_ip_blk<LOGN1, M><<<((B + 3) / 4) * (M + 1) * N1, 64, 0, c->stream>>>(
+      B, mid, c1, c1_stride, perm, key, key_shoup, c->full, acc, c->d_tw, c->d_primes, c->logn);
 }
 
 template <int LOGN1, int E>
@@ -930,6 +930,9 @@ void build_context(lcl_context* c, size_t degree, int depth, int secure, int dev
     k.n_inv_shoup = h_shoup(k.n_inv, q);
     // build_tables (rns.cpp:115-138): root[brv(i)] = psi^i, inverse likewise.
     const u64 psi = h_root_2n(n, q), psi_inv = h_invmod(psi, q);
+    // iroot[1] = psi^-brv(1) = psi^-(n/2)
+    k.w1n = h_mulmod(h_powmod(psi_inv, n / 2, q), k.n_inv, q);
+    k.w1n_shoup = h_shoup(k.w1n, q);
     u64 f = 1, g = 1;
     for (size_t t = 0; t < n; ++t) {
       const size_t r = h_brv(t, c->logn);

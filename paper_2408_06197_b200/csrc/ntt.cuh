@@ -334,13 +334,18 @@ __global__ void __launch_bounds__(64)
   u64 x[16];
 #pragma unroll
   for (int e = 0; e < 16; ++e) x[e] = src[l + 16 * e];
-  const auto row = epi.bind(r, pi, P);
-  typename Epi::Pre pre[16];
-#pragma unroll
-  for (int e = 0; e < 16; ++e) row.prefetch(pre[e], (b << 8) + l + 16 * e);
   blk_fwd_body<LOGN1>(x, sm[bw], tw, b, l, P);
+  const auto row = epi.bind(r, pi, P);
+  // operands of 4 elements in flight at a time: latency overlap without the
+  // register cost of prefetching all 16
 #pragma unroll
-  for (int e = 0; e < 16; ++e) row.store(pre[e], (b << 8) + l + 16 * e, x[e]);
+  for (int e0 = 0; e0 < 16; e0 += 4) {
+    typename Epi::Pre pre[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) row.prefetch(pre[e], (b << 8) + l + 16 * (e0 + e));
+#pragma unroll
+    for (int e = 0; e < 4; ++e) row.store(pre[e], (b << 8) + l + 16 * (e0 + e), x[e0 + e]);
+  }
 }
 
 // ModUp block pass fused with the key inner product (ckks.cpp:464-518).
@@ -355,28 +360,33 @@ __global__ void __launch_bounds__(64)
 //   c1 + b * c1_stride + j * N; key / key_shoup: [full][2][full+1][N];
 //   acc: [B][2][M+1][N].
 template <int LOGN1, int M>
-__global__ void __launch_bounds__(64)
-    modup_ip_blk(const u64* __restrict__ mid, const u64* __restrict__ c1, u64 c1_stride,
+__global__ void __launch_bounds__(64, 8)
+    modup_ip_blk(u32 B, const u64* __restrict__ mid, const u64* __restrict__ c1, u64 c1_stride,
                  const u32* __restrict__ perm, const u64* __restrict__ key,
                  const u64* __restrict__ key_shoup, u32 full, u64* __restrict__ acc,
                  const ulonglong2* __restrict__ tw_all, const PrimeConst* __restrict__ primes,
                  u32 logn) {
   constexpr int N1 = 1 << LOGN1;
   __shared__ u64 sm[4][256 + 16];
+  __shared__ u64 sacc[4][2][256];  // lazy accumulators (< 2Mq), coalesced order
   const u32 n = 1u << logn;
   const u32 l = threadIdx.x & 15, bw = threadIdx.x >> 4;
-  const u32 blk_global = blockIdx.x * 4 + bw;
-  const u32 row = blk_global / N1;  // = b * (M + 1) + t
-  const u32 blk = blk_global - row * N1;
-  const u32 bi = row / (M + 1), t = row - bi * (M + 1);
+  // the 4 groups of a CTA take 4 consecutive ciphertexts of the same
+  // (target row, block): the key words they share are served from L1
+  const u32 bq_count = (B + 3) >> 2;
+  const u32 bq = blockIdx.x % bq_count;
+  const u32 tb = blockIdx.x / bq_count;  // = t * N1 + blk
+  const u32 t = tb / N1, blk = tb - t * N1;
+  const u32 bi_raw = bq * 4 + bw;
+  const bool live = bi_raw < B;
+  const u32 bi = live ? bi_raw : B - 1;
   const u32 pi = t < (u32)M ? t : full;
   const PrimeConst P = primes[pi];
   const ulonglong2* tw = tw_all + (u64)pi * n;
   const u64 kstride = (u64)(full + 1) * n;
   const u32 a0 = (blk << 8) + l;
-  u64 acc0[16], acc1[16];
-#pragma unroll
-  for (int e = 0; e < 16; ++e) acc0[e] = acc1[e] = 0;
+  u64* s0acc = sacc[bw][0];
+  u64* s1acc = sacc[bw][1];
 #pragma unroll 1
   for (int j = 0; j < M; ++j) {
     u64 x[16];
@@ -396,21 +406,26 @@ __global__ void __launch_bounds__(64)
     }
     const u64* k0 = key + (2ull * j) * kstride + (u64)pi * n;
     const u64* k1 = k0 + kstride;
-    const u64* s0 = key_shoup + (2ull * j) * kstride + (u64)pi * n;
-    const u64* s1 = s0 + kstride;
+    const u64* ks0 = key_shoup + (2ull * j) * kstride + (u64)pi * n;
+    const u64* ks1 = ks0 + kstride;
 #pragma unroll
     for (int e = 0; e < 16; ++e) {
       const u32 a = a0 + 16 * e;
-      acc0[e] += mul_shoup_lazy(x[e], __ldg(k0 + a), __ldg(s0 + a), P.q);
-      acc1[e] += mul_shoup_lazy(x[e], __ldg(k1 + a), __ldg(s1 + a), P.q);
+      const u64 p0 = mul_shoup_lazy(x[e], __ldg(k0 + a), __ldg(ks0 + a), P.q);
+      const u64 p1 = mul_shoup_lazy(x[e], __ldg(k1 + a), __ldg(ks1 + a), P.q);
+      const u32 si = l + 16 * e;
+      s0acc[si] = j ? s0acc[si] + p0 : p0;
+      s1acc[si] = j ? s1acc[si] + p1 : p1;
     }
   }
+  if (!live) return;
   u64* o0 = acc + ((u64)bi * 2 * (M + 1) + t) * n;
   u64* o1 = o0 + (u64)(M + 1) * n;
 #pragma unroll
   for (int e = 0; e < 16; ++e) {
-    o0[a0 + 16 * e] = reduce64(acc0[e], P);
-    o1[a0 + 16 * e] = reduce64(acc1[e], P);
+    const u32 si = l + 16 * e;
+    o0[a0 + 16 * e] = reduce64(s0acc[si], P);
+    o1[a0 + 16 * e] = reduce64(s1acc[si], P);
   }
 }
 
@@ -497,13 +512,20 @@ __global__ void __launch_bounds__(16 * ((1 << LOGN1) / E))
   __syncthreads();
 #pragma unroll
   for (int e = 0; e < E; ++e) x[e] = sm[(k + R * e) * 16 + c];
-  static_for<LOGE - 1, -1, -1>([&](auto LM) {
+  static_for<LOGE - 1, 0, -1>([&](auto LM) {
     constexpr int lm = decltype(LM)::value;
     gs_stage<E, (E >> (lm + 1))>(x, [&](int gi) { return ldtw(tw, (1 << lm) + gi); }, P.q, P.two_q);
   });
+  // last stage (m = 1) with N^-1 folded in: x' = (x + y) N^-1, y' = (x - y) (w N^-1)
   const auto row = epi.bind(r, pi, P);
 #pragma unroll
-  for (int e = 0; e < E; ++e) row(j + (k + R * e) * n2, mul_shoup(x[e], P.n_inv, P.n_inv_shoup, P.q));
+  for (int e = 0; e < E / 2; ++e) {
+    const u64 a = x[e], bb = x[e + E / 2];
+    x[e] = mul_shoup(a + bb, P.n_inv, P.n_inv_shoup, P.q);
+    x[e + E / 2] = mul_shoup(a - bb + P.two_q, P.w1n, P.w1n_shoup, P.q);
+  }
+#pragma unroll
+  for (int e = 0; e < E; ++e) row(j + (k + R * e) * n2, x[e]);
 }
 
 // Single-CTA transform for small rings (N <= 4096): the whole row in shared
