@@ -333,6 +333,7 @@ def our_arm(args, cfg):
                     "d2h_bytes_per_step": d2h},
             "gpu_launches": int(launches // max(1, args.steps)),
             "roofline": prof.get("roofline"),
+            "roofline_int": prof.get("roofline_int"),
             "kernels": prof.get("kernels"),
             "cpu_baseline": cpu,
         }
@@ -342,38 +343,51 @@ def our_arm(args, cfg):
 
 
 def profile_round(ctx, step, stream, N, m, npairs, Cc, width, n):
-    """Times every launch of one round with CUDA events (lcl profiling hooks)
-    and returns the per-kernel totals plus the roofline of the top kernel."""
+    """Times every launch of one round with CUDA events on the context's
+    stream (lcl_profile_begin/end) and returns the per-kernel totals plus the
+    rooflines of the top kernel: HBM (algorithmic bytes / time vs the measured
+    copy bandwidth) and integer (algorithmic butterflies / time vs the
+    measured butterfly peak of lcl_peak_butterflies)."""
     import ctypes as C
     import json as _json
 
     import paper_2408_06197_b200.lancelot as L
     lib = L.lib()
-    if not hasattr(lib, "lcl_profile_begin"):
-        return {}
-    lib.lcl_profile_begin.argtypes = [C.c_void_p]
-    lib.lcl_profile_end.argtypes = [C.c_void_p, C.c_char_p, C.c_size_t]
-    lib.lcl_profile_end.restype = C.c_int
     step()
     stream.synchronize()
-    lib.lcl_profile_begin(ctx.h)
+    L._check(lib.lcl_profile_begin(ctx.h))
     step()
     buf = C.create_string_buffer(1 << 20)
-    lib.lcl_profile_end(ctx.h, buf, len(buf))
+    L._check(lib.lcl_profile_end(ctx.h, buf, len(buf)))
     rows = _json.loads(buf.value.decode())
+    peak = C.c_double()
+    L._check(lib.lcl_peak_butterflies(ctx.h, C.byref(peak)))
     peaks = load_peaks()
     kernels = sorted(rows, key=lambda r: -r["ms"])
-    top = kernels[0] if kernels else None
-    roof = None
-    if top:
-        achieved = top["bytes"] / (top["ms"] / top["launches"] * 1e-3) / top["launches"] / 1e9
-        roof = {"bound": "hbm", "kernel": top["name"], "achieved": achieved,
-                "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"],
-                "traffic": None, "peak_source": peaks["source"],
-                "bytes_per_launch": top["bytes"] / top["launches"],
-                "avg_launch_ms": top["ms"] / top["launches"],
-                "share_of_round": top["ms"] / sum(k["ms"] for k in kernels)}
-    return {"roofline": roof, "kernels": kernels[:12]}
+    total = sum(k["ms"] for k in kernels)
+    for k in kernels:
+        s = k["ms"] * 1e-3
+        k["hbm_gbs"] = k["bytes"] / s / 1e9
+        k["gbfly_s"] = k["bfly"] / s / 1e9 if k["bfly"] else None
+        k["share"] = k["ms"] / total
+    top = kernels[0]
+    avg_s = top["ms"] / top["launches"] * 1e-3
+    achieved = top["bytes"] / top["launches"] / avg_s / 1e9
+    roof = {"bound": "hbm", "kernel": top["name"], "achieved": achieved,
+            "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"],
+            "traffic": None, "peak_source": peaks["source"],
+            "bytes_per_launch": top["bytes"] / top["launches"],
+            "avg_launch_ms": top["ms"] / top["launches"], "share_of_round": top["share"]}
+    int_roof = None
+    if top["bfly"]:
+        ach = top["bfly"] / top["launches"] / avg_s / 1e9
+        int_roof = {"bound": "int (64-bit Shoup butterflies)", "kernel": top["name"],
+                    "achieved": ach, "peak": peak.value, "unit": "Gbfly/s",
+                    "frac": ach / peak.value,
+                    "peak_source": "measured live: lcl_peak_butterflies (register-resident "
+                                   "independent CT butterflies, all SMs)"}
+    return {"roofline": roof, "roofline_int": int_roof, "kernels": kernels[:12],
+            "peak_gbfly_s": peak.value}
 
 
 def load_peaks():

@@ -88,6 +88,9 @@ uint64_t lcl_launch_count(const lcl_context* ctx);
 /* Per-launch CUDA-event timing between begin and end; end writes a JSON list
  * of {name, launches, ms, bytes (algorithmic)} per kernel into json[cap]. */
 int lcl_profile_begin(lcl_context* ctx);
+/* Integer roofline probe: forward-NTT butterflies/s (Shoup product + lazy
+ * add/sub) on register-resident independent chains over the whole device. */
+int lcl_peak_butterflies(lcl_context* ctx, double* gbfly_per_s);
 int lcl_profile_end(lcl_context* ctx, char* json, size_t cap);
 
 /* ------------------------------------------------------------ keys */

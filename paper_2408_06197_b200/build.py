@@ -32,8 +32,29 @@ def _stale():
     return any(os.path.getmtime(d) > t for d in deps)
 
 
+CPP_DRIVER = os.path.join(OUT_DIR, "server_round")
+CPP_SRC = os.path.join(os.path.dirname(HERE), "tests", "cpp", "server_round.cpp")
+
+
+def build_cpp_driver(verbose: bool = False) -> str:
+    """The C++ mirror (include/lancelot_b200.hpp) exercised as a reference
+    caller would link it; used by tests/test_cpp_mirror.py."""
+    hdrs = [os.path.join(os.path.dirname(HERE), "include", h)
+            for h in ("lancelot_b200.h", "lancelot_b200.hpp")]
+    if os.path.exists(CPP_DRIVER) and all(
+            os.path.getmtime(CPP_DRIVER) > os.path.getmtime(x) for x in hdrs + [CPP_SRC, LIB]):
+        return CPP_DRIVER
+    cmd = ["g++", "-std=c++17", "-O2", "-I", os.path.join(os.path.dirname(HERE), "include"),
+           CPP_SRC, "-o", CPP_DRIVER, "-L", OUT_DIR, "-llancelot_b200", "-Wl,-rpath,$ORIGIN"]
+    if verbose:
+        print(" ".join(cmd))
+    subprocess.run(cmd, check=True)
+    return CPP_DRIVER
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not _stale():
+        build_cpp_driver(verbose)
         return LIB
     os.makedirs(OUT_DIR, exist_ok=True)
     nvcc = os.environ.get("NVCC", "nvcc")
@@ -47,6 +68,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         print(" ".join(cmd))
     subprocess.run(cmd, check=True)
     os.replace(tmp, LIB)
+    build_cpp_driver(verbose)
     return LIB
 
 

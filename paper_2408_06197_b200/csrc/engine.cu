@@ -236,6 +236,7 @@ struct ProfRec {
   const char* name;
   cudaEvent_t a, b;
   double bytes;  // algorithmic bytes moved by the launch
+  double bfly;   // algorithmic radix-2 butterflies of the launch
 };
 
 struct lcl_context {
@@ -292,8 +293,10 @@ struct ProfScope {
   lcl_context* c;
   const char* name;
   double bytes;
+  double bfly;
   cudaEvent_t a = nullptr;
-  ProfScope(lcl_context* c_, const char* n, double b) : c(c_), name(n), bytes(b) {
+  ProfScope(lcl_context* c_, const char* n, double b, double bf = 0)
+      : c(c_), name(n), bytes(b), bfly(bf) {
     if (c->prof_on) {
       cudaEventCreate(&a);
       cudaEventRecord(a, c->stream);
@@ -304,7 +307,7 @@ struct ProfScope {
       cudaEvent_t b2;
       cudaEventCreate(&b2);
       cudaEventRecord(b2, c->stream);
-      c->prof.push_back({name, a, b2, bytes});
+      c->prof.push_back({name, a, b2, bytes, bfly});
     }
   }
 };
@@ -344,15 +347,17 @@ void fwd2(lcl_context* c, u32 rows, const RowMap& mid, const Loader& ld, const E
   (void)once;
   const u32 groups = (u32)(c->n >> LOGN1) >> 4;
   const double rb = 8.0 * c->N();
+  const double bpr = 0.5 * c->N();  // butterflies per row per stage
   {
     ProfScope ps(c, std::is_same<Loader, LiftLoad>::value ? "ntt_col_fwd<lift>" : "ntt_col_fwd",
-                 rb * (load_rows(ld, rows) + rows));
+                 rb * (load_rows(ld, rows) + rows), bpr * rows * LOGN1);
     ntt_col_fwd<LOGN1, E, Loader><<<rows * groups, 16 * (N1 / E), smem, c->stream>>>(
         mid, ld, c->d_tw, c->d_primes, c->logn);
   }
   {
     ProfScope ps(c, std::is_same<Epi, DivRoundStore>::value ? "ntt_blk_fwd<divround>" : "ntt_blk_fwd",
-                 rb * (store_rows(epi, rows) + (std::is_same<Epi, PlainStore>::value ? rows : 0)));
+                 rb * (store_rows(epi, rows) + (std::is_same<Epi, PlainStore>::value ? rows : 0)),
+                 bpr * rows * 8);
     ntt_blk_fwd<LOGN1, Epi><<<rows * N1 / 4, 64, 0, c->stream>>>(mid, epi, c->d_tw, c->d_primes,
                                                                  c->logn);
   }
@@ -367,13 +372,14 @@ void inv2(lcl_context* c, u32 rows, const RowMap& in, const RowMap& mid, const E
   (void)once;
   const u32 groups = (u32)(c->n >> LOGN1) >> 4;
   const double rb = 8.0 * c->N();
+  const double bpr = 0.5 * c->N();
   {
-    ProfScope ps(c, "ntt_blk_inv", rb * 2.0 * rows);
+    ProfScope ps(c, "ntt_blk_inv", rb * 2.0 * rows, bpr * rows * 8);
     ntt_blk_inv<LOGN1><<<rows * N1 / 4, 64, 0, c->stream>>>(in, mid, c->d_itw, c->d_primes,
                                                             c->logn);
   }
   {
-    ProfScope ps(c, "ntt_col_inv", rb * 2.0 * rows);
+    ProfScope ps(c, "ntt_col_inv", rb * 2.0 * rows, bpr * rows * LOGN1);
     ntt_col_inv<LOGN1, E, Epi><<<rows * groups, 16 * (N1 / E), smem, c->stream>>>(
         mid, epi, c->d_itw, c->d_primes, c->logn);
   }
@@ -386,7 +392,8 @@ template <class Loader, class Epi>
 void launch_fwd(lcl_context* c, u32 rows, const RowMap& pm, const Loader& ld, const Epi& epi) {
   if (rows == 0) return;
   if (c->logn <= 12) {
-    ProfScope ps(c, "ntt_small_fwd", 8.0 * c->N() * (load_rows(ld, rows) + store_rows(epi, rows)));
+    ProfScope ps(c, "ntt_small_fwd", 8.0 * c->N() * (load_rows(ld, rows) + store_rows(epi, rows)),
+                 0.5 * c->N() * rows * c->logn);
     ntt_small<false, Loader, Epi><<<rows, 256, c->n * 8, c->stream>>>(ld, epi, pm, c->d_tw,
                                                                      c->d_primes, c->logn);
     post_launch(c);
@@ -423,7 +430,8 @@ void col_only(lcl_context* c, u32 rows, const RowMap& out, const Loader& ld) {
   static bool once = (allow_smem(ntt_col_fwd<LOGN1, E, Loader>, smem), true);
   (void)once;
   const u32 groups = (u32)(c->n >> LOGN1) >> 4;
-  ProfScope ps(c, "ntt_col_fwd<lift>", 8.0 * c->N() * (load_rows(ld, rows) + rows));
+  ProfScope ps(c, "ntt_col_fwd<lift>", 8.0 * c->N() * (load_rows(ld, rows) + rows),
+               0.5 * c->N() * rows * LOGN1);
   ntt_col_fwd<LOGN1, E, Loader><<<rows * groups, 16 * (N1 / E), smem, c->stream>>>(
       out, ld, c->d_tw, c->d_primes, c->logn);
 }
@@ -434,7 +442,8 @@ void modup_ip_launch(lcl_context* c, u32 B, const u64* mid, const u64* c1, u64 c
   constexpr int N1 = 1 << LOGN1;
   const double rb = 8.0 * c->N();
   ProfScope ps(c, perm ? "modup_ip_blk<perm>" : "modup_ip_blk",
-               rb * ((double)B * M * M + B * M + 4.0 * M * (M + 1) + 2.0 * B * (M + 1)));
+               rb * ((double)B * M * M + B * M + 4.0 * M * (M + 1) + 2.0 * B * (M + 1)),
+               0.5 * c->N() * B * M * M * 8);
   modup_ip_blk<LOGN1, M><<<((B + 3) / 4) * (M + 1) * N1, 64, 0, c->stream>>>(
       B, mid, c1, c1_stride, perm, key, key_shoup, c->full, acc, c->d_tw, c->d_primes, c->logn);
 }
@@ -473,7 +482,7 @@ template <class Epi>
 void launch_inv(lcl_context* c, u32 rows, const RowMap& in, const Epi& epi) {
   if (rows == 0) return;
   if (c->logn <= 12) {
-    ProfScope ps(c, "ntt_small_inv", 8.0 * c->N() * 2.0 * rows);
+    ProfScope ps(c, "ntt_small_inv", 8.0 * c->N() * 2.0 * rows, 0.5 * c->N() * rows * c->logn);
     ntt_small<true, PlainLoad, Epi><<<rows, 256, c->n * 8, c->stream>>>(
         PlainLoad{in}, epi, in, c->d_itw, c->d_primes, c->logn);
     post_launch(c);
@@ -1097,6 +1106,28 @@ int lcl_reset_counts(lcl_context* ctx) {
 
 uint64_t lcl_launch_count(const lcl_context* ctx) { return ctx ? ctx->launches : 0; }
 
+int lcl_peak_butterflies(lcl_context* ctx, double* gbfly_per_s) {
+  return guarded([&] {
+    const u32 blocks = 148 * 8, threads = 256, iters = 4096;
+    u64* sink = ctx->ws_pt.get((u64)blocks * threads);
+    const u64 q = ctx->primes[0];
+    const u64 w = q / 3 + 7;
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    lcl::peak_butterfly<<<blocks, threads, 0, ctx->stream>>>(sink, 64, q, w, h_shoup(w, q));
+    cudaEventRecord(a, ctx->stream);
+    lcl::peak_butterfly<<<blocks, threads, 0, ctx->stream>>>(sink, iters, q, w, h_shoup(w, q));
+    cudaEventRecord(b, ctx->stream);
+    cuda_check(cudaEventSynchronize(b), "peak butterfly");
+    float ms = 0;
+    cudaEventElapsedTime(&ms, a, b);
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    *gbfly_per_s = (double)blocks * threads * iters * 16 / (ms * 1e-3) / 1e9;
+  });
+}
+
 int lcl_profile_begin(lcl_context* ctx) {
   return guarded([&] {
     for (auto& r : ctx->prof) {
@@ -1113,7 +1144,7 @@ int lcl_profile_end(lcl_context* ctx, char* json, size_t cap) {
     ctx->prof_on = false;
     cuda_check(cudaStreamSynchronize(ctx->stream), "profile sync");
     struct Agg {
-      double ms = 0, bytes = 0;
+      double ms = 0, bytes = 0, bfly = 0;
       u64 launches = 0;
     };
     std::map<std::string, Agg> agg;
@@ -1123,6 +1154,7 @@ int lcl_profile_end(lcl_context* ctx, char* json, size_t cap) {
       Agg& a = agg[r.name];
       a.ms += ms;
       a.bytes += r.bytes;
+      a.bfly += r.bfly;
       a.launches += 1;
       cudaEventDestroy(r.a);
       cudaEventDestroy(r.b);
@@ -1132,9 +1164,11 @@ int lcl_profile_end(lcl_context* ctx, char* json, size_t cap) {
     bool first = true;
     for (auto& kv : agg) {
       char buf[256];
-      std::snprintf(buf, sizeof buf, "%s{\"name\": \"%s\", \"launches\": %llu, \"ms\": %.6f, \"bytes\": %.0f}",
+      std::snprintf(buf, sizeof buf,
+                    "%s{\"name\": \"%s\", \"launches\": %llu, \"ms\": %.6f, \"bytes\": %.0f, "
+                    "\"bfly\": %.0f}",
                     first ? "" : ", ", kv.first.c_str(), (unsigned long long)kv.second.launches,
-                    kv.second.ms, kv.second.bytes);
+                    kv.second.ms, kv.second.bytes, kv.second.bfly);
       s += buf;
       first = false;
     }

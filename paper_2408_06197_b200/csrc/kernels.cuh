@@ -250,4 +250,32 @@ __global__ void __launch_bounds__(256)
   row_ptr(out, r)[k] = SUB ? sub_mod(x, y, q) : add_mod(x, y, q);
 }
 
+// ------------------------------------------------------------------------
+// Integer roofline probe: independent chains of the forward NTT butterfly
+// (Shoup product + add / offset-sub, the instruction mix of ct_bfly) on
+// register-resident data. 16 independent butterflies per thread per
+// iteration; the result is folded into one store so nothing is dead code.
+__global__ void __launch_bounds__(256) peak_butterfly(u64* __restrict__ sink, u32 iters, u64 q,
+                                                      u64 w, u64 ws) {
+  u64 x[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) x[i] = (threadIdx.x * 131 + i * 977 + blockIdx.x) % q;
+  const u64 two_q = 2 * q;
+  for (u32 it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      // the forward butterfly of ntt.cuh (values wrap here; only the
+      // instruction stream matters for the probe)
+      const u64 t = mul_shoup_lazy(x[2 * i + 1], w, ws, q);
+      const u64 a = x[2 * i];
+      x[2 * i] = a + t;
+      x[2 * i + 1] = a + (two_q - t);
+    }
+  }
+  u64 s = 0;
+#pragma unroll
+  for (int i = 0; i < 32; ++i) s ^= x[i];
+  sink[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
 }  // namespace lcl

@@ -149,6 +149,13 @@ def lib():
                                  C.POINTER(C.c_double)],
         "lcl_server_round_host": [_P, _P, _P, _SZ, _SZ, C.c_double, _SZ, _SZ, _SZ, C.c_int, _P,
                                   _P],
+        "lcl_profile_begin": [_P],
+        "lcl_profile_end": [_P, C.c_char_p, _SZ],
+        "lcl_peak_butterflies": [_P, C.POINTER(C.c_double)],
+        "lcl_device_alloc": [_P, _SZ, C.POINTER(_P)],
+        "lcl_device_free": [_P, _P],
+        "lcl_copy_h2d": [_P, _P, _P, _SZ],
+        "lcl_copy_d2h": [_P, _P, _P, _SZ],
     }
     for name, args in sig.items():
         f = getattr(L, name)
