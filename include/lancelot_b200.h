@@ -19,6 +19,8 @@
  *   lcl_pairwise_distance    encrypted_pairwise_distance               distance.cpp:107-142
  *   lcl_distance_matrix      build_distance_matrix (per_pair)          distance.cpp:242-300
  *   lcl_masked_aggregate     masked_aggregate                          aggregation.cpp:188-229
+ *   lcl_*_pairs / _chunks    the same, one shard of pairs / chunks     distance.cpp:257-272,
+ *                            (the reference's parallel_for ranges)     aggregation.cpp:211
  *   lcl_get_counts           OpCounters::snapshot                      ckks.cpp:134-156
  *
  * Conventions
@@ -151,6 +153,18 @@ int lcl_distance_matrix(lcl_context* ctx, const uint64_t* d_clients, size_t n, s
 int lcl_masked_aggregate(lcl_context* ctx, const uint64_t* d_clients, const uint64_t* d_sel,
                          size_t n, size_t chunks, double w_scale, double sel_scale, size_t l,
                          int average, uint64_t* d_out, double* out_scale);
+/* Shards for multi-GPU runs: pairs [pair_begin, pair_end) of the (i<j) order
+ * (out [pair_end - pair_begin][2][full-1][N]) and chunks [chunk_begin,
+ * chunk_end) of the aggregate. Concatenating the shards in order gives the
+ * unsharded result word for word. */
+int lcl_distance_matrix_pairs(lcl_context* ctx, const uint64_t* d_clients, size_t n,
+                              size_t chunks, double in_scale, size_t width, size_t k, int lazy,
+                              int reduce, size_t pair_begin, size_t pair_end, uint64_t* d_out,
+                              double* out_scale);
+int lcl_masked_aggregate_chunks(lcl_context* ctx, const uint64_t* d_clients,
+                                const uint64_t* d_sel, size_t n, size_t chunks, double w_scale,
+                                double sel_scale, size_t l, int average, size_t chunk_begin,
+                                size_t chunk_end, uint64_t* d_out, double* out_scale);
 /* Host-buffer variant of the server round used by the end-to-end benchmark:
  * H2D of clients + selectors, distance matrix, masked aggregate, D2H of both
  * outputs, synchronised before returning. */

@@ -757,20 +757,28 @@ u32 sub_batch(lcl_context* c, u32 m) {
 }
 
 // build_distance_matrix per_pair (distance.cpp:242-300), pairs in i<j order.
+// Pairs [pair_begin, pair_end) of the (i<j) row-major order; out holds just
+// that range (a shard of the matrix when the pairs are split across GPUs).
 void distance_matrix(lcl_context* c, const u64* clients, u32 n, u32 chunks, size_t width,
-                     size_t k, bool lazy, bool reduce, u64* out) {
+                     size_t k, bool lazy, bool reduce, u64* out, u32 pair_begin = 0,
+                     u32 pair_end = 0xFFFFFFFFu) {
   if (n < 2) fail(LCL_SHAPE_ERROR, "pairwise distances need at least two clients");
   if (n > 65535) fail(LCL_SHAPE_ERROR, "too many clients");
   const u32 m = c->full;
   if (m < 2) fail(LCL_DEPTH_EXHAUSTED, "no prime left to rescale by");
   const u64 N = c->N();
   ensure_pairs(c, n);
-  const u32 P = n * (n - 1) / 2;
+  const u32 P = std::min<u32>(n * (n - 1) / 2, pair_end);
+  need(pair_begin <= P, LCL_SHAPE_ERROR, "pair range outside the matrix");
+  if (reduce) {
+    if (width == 0 || (width & (width - 1))) fail(LCL_WIDTH_ERROR, "reduction width must be a power of two");
+    if (width > c->n / 2) fail(LCL_WIDTH_ERROR, "reduction width exceeds the slot count");
+  }
   const u32 SB = sub_batch(c, m);
   const u64 out_stride = 2ull * (m - 1) * N;
-  for (u32 p0 = 0; p0 < P; p0 += SB) {
+  for (u32 p0 = pair_begin; p0 < P; p0 += SB) {
     const u32 p1 = std::min(P, p0 + SB), B = p1 - p0;
-    u64* o = out + (u64)p0 * out_stride;
+    u64* o = out + (u64)(p0 - pair_begin) * out_stride;
     u64* ctA = c->ws_ctA.get((u64)B * 2 * m * N);
     if (lazy) {
       u64* tern = c->ws_tern.get((u64)B * 3 * m * N);
@@ -797,8 +805,11 @@ void distance_matrix(lcl_context* c, const u64* clients, u32 n, u32 chunks, size
   }
 }
 
+// Chunks [chunk_begin, chunk_end) of the aggregate (a shard when the chunks
+// are split across GPUs); out holds just that range.
 void masked_aggregate(lcl_context* c, const u64* clients, const u64* sel, u32 n, u32 chunks,
-                      size_t l, bool average, u64* out) {
+                      size_t l, bool average, u64* out, u32 chunk_begin = 0,
+                      u32 chunk_end = 0xFFFFFFFFu) {
   if (n == 0) fail(LCL_SHAPE_ERROR, "no client weights to aggregate");
   const u32 m = c->full;
   const u64 N = c->N();
@@ -828,8 +839,10 @@ void masked_aggregate(lcl_context* c, const u64* clients, const u64* sel, u32 n,
     launch_fwd(c, m - 1, ptm, PlainLoad{ptm}, PlainStore{ptm});
     cuda_check(cudaStreamSynchronize(c->stream), "pt encode");  // pt_h must outlive the copy
   }
-  for (u32 c0 = 0; c0 < chunks; c0 += SB) {
-    const u32 c1 = std::min(chunks, c0 + SB), B = c1 - c0;
+  const u32 cend = std::min(chunks, chunk_end);
+  need(chunk_begin <= cend, LCL_SHAPE_ERROR, "chunk range outside the weights");
+  for (u32 c0 = chunk_begin; c0 < cend; c0 += SB) {
+    const u32 c1 = std::min(cend, c0 + SB), B = c1 - c0;
     u64* tern = c->ws_tern.get((u64)B * 3 * m * N);
     constexpr int CK = 4;
     const u64 slots = (u64)m * N;
@@ -842,7 +855,7 @@ void masked_aggregate(lcl_context* c, const u64* clients, const u64* sel, u32 n,
     post_launch(c);
     u64* ctA = c->ws_ctA.get((u64)B * 2 * m * N);
     relinearize_batch(c, tern, B, m, ctA);
-    u64* o = out + (u64)c0 * 2 * mo * N;
+    u64* o = out + (u64)(c0 - chunk_begin) * 2 * mo * N;
     if (!average) {
       rescale_batch(c, ctA, B, m, o);
     } else {
@@ -1416,6 +1429,40 @@ int lcl_distance_matrix(lcl_context* ctx, const uint64_t* d_clients, size_t n, s
     need(chunks >= 1, LCL_SHAPE_ERROR, "empty weight vector");
     distance_matrix(ctx, d_clients, (u32)n, (u32)chunks, width, k, lazy != 0, reduce != 0, d_out);
     if (out_scale) *out_scale = (in_scale * in_scale) / (double)ctx->primes[ctx->full - 1];
+  });
+}
+
+int lcl_distance_matrix_pairs(lcl_context* ctx, const uint64_t* d_clients, size_t n,
+                              size_t chunks, double in_scale, size_t width, size_t k, int lazy,
+                              int reduce, size_t pair_begin, size_t pair_end, uint64_t* d_out,
+                              double* out_scale) {
+  return guarded([&] {
+    need(chunks >= 1, LCL_SHAPE_ERROR, "empty weight vector");
+    need(pair_begin <= pair_end && pair_end <= n * (n - 1) / 2, LCL_SHAPE_ERROR,
+         "pair range outside the matrix");
+    if (pair_end > pair_begin)
+      distance_matrix(ctx, d_clients, (u32)n, (u32)chunks, width, k, lazy != 0, reduce != 0, d_out,
+                      (u32)pair_begin, (u32)pair_end);
+    if (out_scale) *out_scale = (in_scale * in_scale) / (double)ctx->primes[ctx->full - 1];
+  });
+}
+
+int lcl_masked_aggregate_chunks(lcl_context* ctx, const uint64_t* d_clients,
+                                const uint64_t* d_sel, size_t n, size_t chunks, double w_scale,
+                                double sel_scale, size_t l, int average, size_t chunk_begin,
+                                size_t chunk_end, uint64_t* d_out, double* out_scale) {
+  return guarded([&] {
+    need(chunks >= 1, LCL_SHAPE_ERROR, "empty weight vector");
+    need(chunk_begin <= chunk_end && chunk_end <= chunks, LCL_SHAPE_ERROR,
+         "chunk range outside the weights");
+    if (chunk_end > chunk_begin)
+      masked_aggregate(ctx, d_clients, d_sel, (u32)n, (u32)chunks, l, average != 0, d_out,
+                       (u32)chunk_begin, (u32)chunk_end);
+    if (out_scale) {
+      double s = (w_scale * sel_scale) / (double)ctx->primes[ctx->full - 1];
+      if (average) s = (s * ctx->scale) / (double)ctx->primes[ctx->full - 2];
+      *out_scale = s;
+    }
   });
 }
 

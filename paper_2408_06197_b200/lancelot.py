@@ -149,6 +149,10 @@ def lib():
                                  C.POINTER(C.c_double)],
         "lcl_server_round_host": [_P, _P, _P, _SZ, _SZ, C.c_double, _SZ, _SZ, _SZ, C.c_int, _P,
                                   _P],
+        "lcl_distance_matrix_pairs": [_P, _P, _SZ, _SZ, C.c_double, _SZ, _SZ, C.c_int, C.c_int,
+                                      _SZ, _SZ, _P, C.POINTER(C.c_double)],
+        "lcl_masked_aggregate_chunks": [_P, _P, _P, _SZ, _SZ, C.c_double, C.c_double, _SZ, C.c_int,
+                                        _SZ, _SZ, _P, C.POINTER(C.c_double)],
         "lcl_profile_begin": [_P],
         "lcl_profile_end": [_P, C.c_char_p, _SZ],
         "lcl_peak_butterflies": [_P, C.POINTER(C.c_double)],

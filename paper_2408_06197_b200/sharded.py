@@ -1,0 +1,94 @@
+"""Multi-GPU server round: one process per GPU, torch.distributed for the plumbing.
+
+SURVEY.md §8(e). The reference parallelises the server with parallel_for over
+pairs (distance.cpp:266-272) and over chunks (aggregation.cpp:211-227); the
+same two axes shard across GPUs here:
+
+  * build_distance_matrix: rank r owns pairs [P r / G, P (r+1) / G) of the
+    (i<j) row-major order. Every pair's chain (lazy accumulation -> relin ->
+    rescale -> slot_reduce) is independent, so no data-path collective is
+    needed; the per-rank shards are all-gathered (NCCL over NVLink on B200).
+  * masked_aggregate: rank r owns chunks [C r / G, C (r+1) / G); each chunk's
+    n-client tensor + relin + rescale is independent; all-gather again.
+
+Inputs (client ciphertexts, selectors, keys) are replicated on every GPU
+(cfg4's 71.7 GB of client data fits one 180 GB B200). Concatenating the
+shards reproduces the single-GPU result word for word, which the gloo tests
+in tests/test_sharded.py check against the oracle on CPU.
+
+The shard kernels are injected (`compute_pairs`, `compute_chunks`), so the
+same orchestration runs with the CUDA C-ABI on B200 (`cuda_shard_fns`) and
+with CPU stand-ins under gloo in the tests.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+
+def shard_range(total: int, world: int, rank: int):
+    """Contiguous, balanced [begin, end) slice of `total` units for `rank`."""
+    return (total * rank) // world, (total * (rank + 1)) // world
+
+
+def _gather(dist, local, total, unit_shape, world, rank, group):
+    """All-gather uneven contiguous shards (padded to the largest) into one
+    [total, *unit_shape] tensor on every rank."""
+    torch = __import__("torch")
+    per = -(-total // world)
+    pad = torch.zeros((per,) + tuple(unit_shape), dtype=local.dtype, device=local.device)
+    pad[: local.shape[0]] = local
+    bufs = [torch.empty_like(pad) for _ in range(world)]
+    dist.all_gather(bufs, pad, group=group)  # NCCL on B200, gloo in the CPU tests
+    parts = []
+    for r in range(world):
+        b, e = shard_range(total, world, r)
+        parts.append(bufs[r][: e - b])
+    return torch.cat(parts, dim=0)
+
+
+def sharded_server_round(n_pairs, n_chunks, dist_unit_shape, agg_unit_shape, compute_pairs,
+                         compute_chunks, group=None):
+    """Runs this rank's shards and all-gathers the full distance matrix and
+    aggregate. compute_pairs(p0, p1) -> [p1-p0, *dist_unit_shape] tensor;
+    compute_chunks(c0, c1) -> [c1-c0, *agg_unit_shape] tensor."""
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    p0, p1 = shard_range(n_pairs, world, rank)
+    c0, c1 = shard_range(n_chunks, world, rank)
+    d_local = compute_pairs(p0, p1)
+    a_local = compute_chunks(c0, c1)
+    d_full = _gather(dist, d_local, n_pairs, dist_unit_shape, world, rank, group)
+    a_full = _gather(dist, a_local, n_chunks, agg_unit_shape, world, rank, group)
+    return d_full, a_full
+
+
+def cuda_shard_fns(ctx, clients, selectors, n, chunks, scale, sel_scale, width, k, l=1,
+                   average=False, lazy=True, reduce=True):
+    """Shard kernels on the B200 through the C-ABI (lcl_distance_matrix_pairs /
+    lcl_masked_aggregate_chunks)."""
+    import torch
+
+    from . import lancelot as L
+
+    m = ctx.full
+    N = ctx.params().ring_degree
+    mo = m - 2 if average else m - 1
+    osc = C.c_double()
+
+    def pairs(p0, p1):
+        out = torch.empty((p1 - p0, 2, m - 1, N), dtype=torch.int64, device=clients.device)
+        L._check(L.lib().lcl_distance_matrix_pairs(
+            ctx.h, L._ptr(clients), n, chunks, scale, width, k, 1 if lazy else 0,
+            1 if reduce else 0, p0, p1, L._ptr(out), C.byref(osc)))
+        return out
+
+    def chunks_fn(c0, c1):
+        out = torch.empty((c1 - c0, 2, mo, N), dtype=torch.int64, device=clients.device)
+        L._check(L.lib().lcl_masked_aggregate_chunks(
+            ctx.h, L._ptr(clients), L._ptr(selectors), n, chunks, scale, sel_scale, l,
+            1 if average else 0, c0, c1, L._ptr(out), C.byref(osc)))
+        return out
+
+    return pairs, chunks_fn, (2, m - 1, N), (2, mo, N)

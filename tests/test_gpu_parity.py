@@ -221,3 +221,34 @@ def test_shape_and_width_errors():
     with pytest.raises(L.ShapeError):
         L.masked_aggregate(ctx, pw, L.SelectionMask(2, 1, L.to_device(cl[:2, 0]), orc.scale),
                            L.SelectionRule.krum, rk)
+
+
+@pytest.mark.parametrize("name,world", [("cfg1", 3), ("tiny_hoist_multikrum", 4)])
+def test_cuda_shards_concatenate_to_reference(name, world):
+    """The multi-GPU shard entry points (pair / chunk ranges) concatenate to
+    the reference's matrix and aggregate word for word."""
+    import torch
+
+    from paper_2408_06197_b200.sharded import cuda_shard_fns, shard_range
+    L = _L()
+    rig = Rig(name, threads=8)
+    ctx = gpu_ctx(rig.N, secure=bool(rig.meta["options"]["secure"]))
+    ctx.use_relin_key(L.RelinKey(rig.oracle.relin_key()))
+    keys = L.RotationKeySet({s: rig.oracle.rotation_key(s) for s in rig.meta["rot_keys"]})
+    ctx.use_rotation_keys(keys, rig.meta["rot_keys"])
+    clients = L.to_device(rig.clients)
+    sel = L.to_device(rig.selectors)
+    average = rig.average
+    fp, fc, _, _ = cuda_shard_fns(ctx, clients, sel, rig.n, rig.C, rig.oracle.scale,
+                                  rig.oracle.scale, rig.width, rig.k, l=len(rig.selected),
+                                  average=average, lazy=rig.lazy)
+    npairs = rig.n * (rig.n - 1) // 2
+    d = torch.cat([fp(*shard_range(npairs, world, r)) for r in range(world)])
+    a = torch.cat([fc(*shard_range(rig.C, world, r)) for r in range(world)])
+    got = L.to_host(d)
+    p = 0
+    for i in range(rig.n):
+        for j in range(i + 1, rig.n):
+            assert sha(got[p]) == rig.meta["sha256"][f"dist_{i}_{j}"], (i, j)
+            p += 1
+    assert sha(L.to_host(a)) == rig.meta["sha256"]["agg"]
