@@ -69,6 +69,17 @@ __device__ __forceinline__ u64 mul_shoup_lazy(u64 a, u64 w, u64 ws, u64 q) {
   const u64 hi = __umul64hi(a, ws);
   return a * w - hi * q;
 }
+// Shoup product with a truncated quotient: the y0*s0 partial product and the
+// carries out of the two 32x32 cross products are dropped, so the quotient
+// estimate is at most 3 below floor(a*w/q) and the result lies in [0, 4q).
+// Three IMAD.WIDE instead of four plus their carry chain.
+__device__ __forceinline__ u64 mul_shoup_lazy4(u64 a, u64 w, u64 ws, u64 q) {
+  const u32 a0 = (u32)a, a1 = (u32)(a >> 32);
+  const u32 s0 = (u32)ws, s1 = (u32)(ws >> 32);
+  const u64 t1 = (u64)a1 * s0, t2 = (u64)a0 * s1;
+  const u64 hi = (u64)a1 * s1 + (t1 >> 32) + (t2 >> 32);
+  return a * w - hi * q;
+}
 __device__ __forceinline__ u64 mul_shoup(u64 a, u64 w, u64 ws, u64 q) {
   return csub(mul_shoup_lazy(a, w, ws, q), q);
 }

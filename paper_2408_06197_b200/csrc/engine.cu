@@ -639,10 +639,12 @@ void rotate_level(lcl_context* c, const u64* in, u32 B, u32 m, size_t step, u64*
   const u64* key = rot_key(c, step);
   const u32* perm = c->d_perm.at(step);
   const RowMap c1 = make_map(in + (u64)m * N, m, N, 2ull * m * N, 1, 0, c->primes_0(m));
-  // automorphism applied to the coefficient-domain c1 before the lift: the
-  // digits come out already permuted and the inner product reads contiguously
-  u64* acc = ks_switch(c, c1, in + (u64)m * N, 2ull * m * N, B, m, c->d_sigma.at(step), perm,
-                       key, c->d_rot_shoup.at(step));
+  // two-pass rings: the Galois permutation is applied block-locally inside the
+  // fused ModUp + inner-product pass; small rings lift through the
+  // coefficient-domain automorphism instead.
+  const u32* sigma = c->logn < 13 ? c->d_sigma.at(step) : nullptr;
+  u64* acc = ks_switch(c, c1, in + (u64)m * N, 2ull * m * N, B, m, sigma, perm, key,
+                       c->d_rot_shoup.at(step));
   const RowMap inm = ct_map(in, m, N, 2ull * m * N);
   ks_moddown(c, acc, B, m, ct_map(out, m, N, 2ull * m * N), accumulate ? inm : null_map(), inm,
              perm);
@@ -715,26 +717,36 @@ void ensure_pairs(lcl_context* c, u32 n) {
   c->pairs_n = n;
 }
 
-constexpr int kPP = 4;
 constexpr int kStages = 3;
 
-// Lazy ternary accumulators for pairs [p0, p1) over chunks [c0, c1).
-void pair_accumulate_launch(lcl_context* c, const u64* clients, u32 n, u32 chunks, u32 c0,
-                            u32 c1, u32 p0, u32 p1, u64* tern, bool accumulate) {
+template <int PP>
+void pair_accumulate_pp(lcl_context* c, const u64* clients, u32 n, u32 chunks, u32 c0, u32 c1,
+                        u32 p0, u32 p1, u64* tern, bool accumulate, u32 warps) {
   const u32 m = c->full;
-  const u32 warps = 4;
   const u32 pairs = p1 - p0;
-  const u32 per_cta = warps * kPP;
+  const u32 per_cta = warps * PP;
   dim3 grid((u32)(m * c->n / 32), (pairs + per_cta - 1) / per_cta);
   const size_t smem = (size_t)kStages * n * 64 * 8;
   need(smem <= 200 * 1024, LCL_SHAPE_ERROR, "too many clients for one tile");
-  allow_smem(pair_accumulate<kPP, kStages>, smem);
+  allow_smem(pair_accumulate<PP, kStages>, smem);
   ProfScope ps(c, "pair_accumulate",
                8.0 * c->N() * m * (2.0 * n * (c1 - c0) + 3.0 * pairs * (accumulate ? 2 : 1)));
-  pair_accumulate<kPP, kStages><<<grid, warps * 32, smem, c->stream>>>(
+  pair_accumulate<PP, kStages><<<grid, warps * 32, smem, c->stream>>>(
       clients, n, c0, c1, chunks, m, c->logn, c->d_pairs, p0, p1, tern, accumulate ? 1 : 0,
       c->d_primes);
   post_launch(c);
+}
+
+// Lazy ternary accumulators for pairs [p0, p1) over chunks [c0, c1). Up to
+// 48 pairs share one CTA (each client tile read once); larger matrices split
+// into groups of 16 pairs per CTA.
+void pair_accumulate_launch(lcl_context* c, const u64* clients, u32 n, u32 chunks, u32 c0,
+                            u32 c1, u32 p0, u32 p1, u64* tern, bool accumulate) {
+  if (p1 - p0 <= 48)
+    pair_accumulate_pp<6>(c, clients, n, chunks, c0, c1, p0, p1, tern, accumulate,
+                          (p1 - p0 + 5) / 6);
+  else
+    pair_accumulate_pp<4>(c, clients, n, chunks, c0, c1, p0, p1, tern, accumulate, 4);
 }
 
 void hadd_into(lcl_context* c, u64* acc, const u64* x, u32 B, u32 m) {

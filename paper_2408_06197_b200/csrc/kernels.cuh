@@ -30,7 +30,7 @@ __device__ __forceinline__ void cp_async_wait() {
 }
 
 template <int PP, int STAGES>
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(256)
     pair_accumulate(const u64* __restrict__ clients, u32 n, u32 c_begin, u32 c_end,
                     u32 chunks_total, u32 m, u32 logn, const u32* __restrict__ pairs,
                     u32 p_begin, u32 p_end, u64* __restrict__ tern, int accumulate,
@@ -266,10 +266,10 @@ __global__ void __launch_bounds__(256) peak_butterfly(u64* __restrict__ sink, u3
     for (int i = 0; i < 16; ++i) {
       // the forward butterfly of ntt.cuh (values wrap here; only the
       // instruction stream matters for the probe)
-      const u64 t = mul_shoup_lazy(x[2 * i + 1], w, ws, q);
+      const u64 t = mul_shoup_lazy4(x[2 * i + 1], w, ws, q);
       const u64 a = x[2 * i];
       x[2 * i] = a + t;
-      x[2 * i + 1] = a + (two_q - t);
+      x[2 * i + 1] = a + (2 * two_q - t);
     }
   }
   u64 s = 0;

@@ -40,15 +40,16 @@ __device__ __forceinline__ Tw ldtw(const ulonglong2* t, u32 idx) {
 }
 
 // Forward CT butterfly without intermediate reduction: with t = y*w mod q in
-// [0, 2q), x' = x + t and y' = x + 2q - t both stay below B + 2q when x < B.
-// Starting from inputs < q, after s stages every value is < (1 + 2s) q; for
-// s <= 17 and q < 2^55 that is < 35 * 2^55 < 2^61, so no word overflows and
-// the only reduction is the final one (reduce64). Shoup accepts any y < 2^64.
-__device__ __forceinline__ void ct_bfly(u64& x, u64& y, Tw w, u64 q, u64 two_q) {
-  const u64 t = mul_shoup_lazy(y, w.w, w.ws, q);
+// [0, 4q) (truncated Shoup quotient), x' = x + t and y' = x + 4q - t both stay
+// below B + 4q when x < B. Starting from inputs < q, after s stages every
+// value is < (1 + 4s) q; for s <= 17 and q < 2^55 that is < 69 * 2^55 < 2^62,
+// so no word overflows and the only reduction is the final one (reduce64).
+// The Shoup product accepts any y < 2^64. (two_q carries 4q here.)
+__device__ __forceinline__ void ct_bfly(u64& x, u64& y, Tw w, u64 q, u64 four_q) {
+  const u64 t = mul_shoup_lazy4(y, w.w, w.ws, q);
   const u64 a = x;
   x = a + t;
-  y = a + (two_q - t);
+  y = a + (four_q - t);
 }
 
 // Inverse GS butterfly: x, y in [0, 2q) -> x', y' in [0, 2q).
@@ -58,6 +59,10 @@ __device__ __forceinline__ void gs_bfly(u64& x, u64& y, Tw w, u64 q, u64 two_q) 
   x = s >= two_q ? s - two_q : s;
   y = mul_shoup_lazy(a - b + two_q, w.w, w.ws, q);
 }
+
+// Padded shared-memory slot of block element i (bank-conflict-free for both
+// the l + 16 e and the 16 l + e access patterns).
+__device__ __forceinline__ u32 pad16(u32 i) { return i + (i >> 4); }
 
 // ------------------------------------------------------------ loaders
 // A loader is bound once per row (all address / constant lookups hoisted):
@@ -134,7 +139,8 @@ struct PlainStore {
   struct Row {
     u64* p;
     __device__ __forceinline__ void operator()(u32 a, u64 v) const { p[a] = v; }
-    __device__ __forceinline__ void prefetch(Pre&, u32) const {}
+    __device__ __forceinline__ void stage(u64*, u32, u32) const {}
+    __device__ __forceinline__ void prefetch(Pre&, u32, const u64*) const {}
     __device__ __forceinline__ void store(const Pre&, u32 a, u64 v) const { p[a] = v; }
   };
   __device__ __forceinline__ Row bind(u32 r, u32, const PrimeConst&) const {
@@ -165,14 +171,27 @@ struct DivRoundStore {
     u64 iv, ivs, q;
     __device__ __forceinline__ void operator()(u32 a, u64 lift) const {
       Pre p;
-      prefetch(p, a);
+      prefetch(p, a, nullptr);
       store(p, a, lift);
     }
-    __device__ __forceinline__ void prefetch(Pre& p, u32 a) const {
+    // With a permuted add2, the 256-element source block of block b is staged
+    // into shared memory s first (block-local Galois permutation).
+    __device__ __forceinline__ void stage(u64* s, u32 b, u32 l) const {
+      if (a2 && perm) {
+        const u32 src_blk = __ldg(perm + (b << 8)) >> 8;
+#pragma unroll
+        for (int e = 0; e < 16; ++e) s[pad16(l + 16 * e)] = a2[(src_blk << 8) + l + 16 * e];
+        __syncwarp();
+      }
+    }
+    __device__ __forceinline__ void prefetch(Pre& p, u32 a, const u64* s) const {
       p.x = x[a];
-      u64 s = a1 ? a1[a] : 0;
-      if (a2) s = add_mod(s, a2[perm ? __ldg(perm + a) : a], q);
-      p.add = s;
+      u64 v = a1 ? a1[a] : 0;
+      if (a2) {
+        const u64 g = perm ? (s ? s[pad16(__ldg(perm + a) & 255u)] : a2[__ldg(perm + a)]) : a2[a];
+        v = add_mod(v, g, q);
+      }
+      p.add = v;
     }
     __device__ __forceinline__ void store(const Pre& p, u32 a, u64 lift) const {
       const u64 v = mul_shoup(p.x - lift + q, iv, ivs, q);
@@ -210,11 +229,12 @@ __device__ __forceinline__ void static_for(F&& f) {
 // butterflies (g*2D + e, g*2D + e + D); twf(g) gives the group's twiddle.
 template <int E, int D, class TwF>
 __device__ __forceinline__ void ct_stage(u64 (&x)[E], const TwF& twf, u64 q, u64 two_q) {
+  const u64 four_q = 2 * two_q;
 #pragma unroll
   for (int g = 0; g < E / (2 * D); ++g) {
     const Tw w = twf(g);
 #pragma unroll
-    for (int e = 0; e < D; ++e) ct_bfly(x[g * 2 * D + e], x[g * 2 * D + e + D], w, q, two_q);
+    for (int e = 0; e < D; ++e) ct_bfly(x[g * 2 * D + e], x[g * 2 * D + e + D], w, q, four_q);
   }
 }
 template <int E, int D, class TwF>
@@ -312,6 +332,21 @@ __device__ __forceinline__ void blk_fwd_body(u64 (&x)[16], u64* s, const ulonglo
   __syncwarp();
 }
 
+// Galois permutation inside one 256-element block. In bit-reversed evaluation
+// order the permutation maps every aligned output block onto exactly one
+// input block (the low 8 index bits only touch the top 8 exponent bits), so a
+// rotation's gather is a coalesced load of the source block followed by a
+// shuffle through shared memory. src_blk = perm[blk * 256] >> 8.
+__device__ __forceinline__ void block_gather(u64 (&x)[16], u64* s, const u64* src_block,
+                                             const u32* perm, u32 blk, u32 l) {
+#pragma unroll
+  for (int e = 0; e < 16; ++e) s[pad16(l + 16 * e)] = __ldg(src_block + l + 16 * e);
+  __syncwarp();
+#pragma unroll
+  for (int e = 0; e < 16; ++e) x[e] = s[pad16(__ldg(perm + (blk << 8) + l + 16 * e) & 255u)];
+  __syncwarp();
+}
+
 // Block pass, forward: 256-point blocks, 16 threads per block, 16 elements per
 // thread, 4 blocks per CTA. The epilogue's operands are prefetched before the
 // butterflies so their latency overlaps the arithmetic.
@@ -336,13 +371,14 @@ __global__ void __launch_bounds__(64)
   for (int e = 0; e < 16; ++e) x[e] = src[l + 16 * e];
   blk_fwd_body<LOGN1>(x, sm[bw], tw, b, l, P);
   const auto row = epi.bind(r, pi, P);
+  row.stage(sm[bw], b, l);
   // operands of 4 elements in flight at a time: latency overlap without the
   // register cost of prefetching all 16
 #pragma unroll
   for (int e0 = 0; e0 < 16; e0 += 4) {
     typename Epi::Pre pre[4];
 #pragma unroll
-    for (int e = 0; e < 4; ++e) row.prefetch(pre[e], (b << 8) + l + 16 * (e0 + e));
+    for (int e = 0; e < 4; ++e) row.prefetch(pre[e], (b << 8) + l + 16 * (e0 + e), sm[bw]);
 #pragma unroll
     for (int e = 0; e < 4; ++e) row.store(pre[e], (b << 8) + l + 16 * (e0 + e), x[e0 + e]);
   }
@@ -355,7 +391,7 @@ __global__ void __launch_bounds__(64)
 // input limb itself (mod_up returns the row unchanged, rns.cpp:371-381), read
 // through the rotation's evaluation-domain permutation when one is given.
 // Each digit is multiplied by the key in Shoup form and accumulated lazily
-// (< 2Mq), so the m(m+1) digit rows never reach HBM.
+// (< 4Mq), so the m(m+1) digit rows never reach HBM.
 //   mid: [B][M][M][N] (t' = t < j ? t : t - 1); c1: limb j of item b at
 //   c1 + b * c1_stride + j * N; key / key_shoup: [full][2][full+1][N];
 //   acc: [B][2][M+1][N].
@@ -368,7 +404,7 @@ __global__ void __launch_bounds__(64, 8)
                  u32 logn) {
   constexpr int N1 = 1 << LOGN1;
   __shared__ u64 sm[4][256 + 16];
-  __shared__ u64 sacc[4][2][256];  // lazy accumulators (< 2Mq), coalesced order
+  __shared__ u64 sacc[4][2][256];  // lazy accumulators (< 4Mq), coalesced order
   const u32 n = 1u << logn;
   const u32 l = threadIdx.x & 15, bw = threadIdx.x >> 4;
   // the 4 groups of a CTA take 4 consecutive ciphertexts of the same
@@ -387,22 +423,33 @@ __global__ void __launch_bounds__(64, 8)
   const u32 a0 = (blk << 8) + l;
   u64* s0acc = sacc[bw][0];
   u64* s1acc = sacc[bw][1];
+  // rotation: output block blk of every digit comes from block src_blk of the
+  // unpermuted digit (block-local Galois permutation, see block_gather)
+  const u32 src_blk = perm ? (__ldg(perm + (blk << 8)) >> 8) : blk;
 #pragma unroll 1
   for (int j = 0; j < M; ++j) {
     u64 x[16];
     if (t == (u32)j) {
-      const u64* src = c1 + (u64)bi * c1_stride + (u64)j * n;
+      const u64* src = c1 + (u64)bi * c1_stride + (u64)j * n + (src_blk << 8);
+      if (perm) {
+        block_gather(x, sm[bw], src, perm, blk, l);
+      } else {
 #pragma unroll
-      for (int e = 0; e < 16; ++e) {
-        const u32 a = a0 + 16 * e;
-        x[e] = __ldg(src + (perm ? __ldg(perm + a) : a));
+        for (int e = 0; e < 16; ++e) x[e] = __ldg(src + l + 16 * e);
       }
     } else {
       const u32 tp = t < (u32)j ? t : t - 1;
-      const u64* src = mid + (((u64)bi * M + j) * M + tp) * n + (blk << 8);
+      const u64* src = mid + (((u64)bi * M + j) * M + tp) * n + (src_blk << 8);
 #pragma unroll
       for (int e = 0; e < 16; ++e) x[e] = src[l + 16 * e];
-      blk_fwd_body<LOGN1>(x, sm[bw], tw, blk, l, P);
+      blk_fwd_body<LOGN1>(x, sm[bw], tw, src_blk, l, P);
+      if (perm) {
+        // the body left the reduced block in shared memory: permuted read
+#pragma unroll
+        for (int e = 0; e < 16; ++e)
+          x[e] = sm[bw][pad16(__ldg(perm + (blk << 8) + l + 16 * e) & 255u)];
+        __syncwarp();
+      }
     }
     const u64* k0 = key + (2ull * j) * kstride + (u64)pi * n;
     const u64* k1 = k0 + kstride;
@@ -411,8 +458,9 @@ __global__ void __launch_bounds__(64, 8)
 #pragma unroll
     for (int e = 0; e < 16; ++e) {
       const u32 a = a0 + 16 * e;
-      const u64 p0 = mul_shoup_lazy(x[e], __ldg(k0 + a), __ldg(ks0 + a), P.q);
-      const u64 p1 = mul_shoup_lazy(x[e], __ldg(k1 + a), __ldg(ks1 + a), P.q);
+      // each product < 4q: the M-term sums stay < 24q (M <= 6)
+      const u64 p0 = mul_shoup_lazy4(x[e], __ldg(k0 + a), __ldg(ks0 + a), P.q);
+      const u64 p1 = mul_shoup_lazy4(x[e], __ldg(k1 + a), __ldg(ks1 + a), P.q);
       const u32 si = l + 16 * e;
       s0acc[si] = j ? s0acc[si] + p0 : p0;
       s1acc[si] = j ? s1acc[si] + p1 : p1;
@@ -554,7 +602,7 @@ __global__ void __launch_bounds__(256)
       for (u32 bt = threadIdx.x; bt < n / 2; bt += blockDim.x) {
         const u32 i = bt / half, jj = bt - i * half;
         const u32 a0 = 2 * i * half + jj;
-        ct_bfly(smem[a0], smem[a0 + half], ldtw(tw, m + i), P.q, P.two_q);
+        ct_bfly(smem[a0], smem[a0 + half], ldtw(tw, m + i), P.q, 2 * P.two_q);
       }
       __syncthreads();
     }
