@@ -37,6 +37,12 @@ CONFIGS = {
     "cfg1": dict(N=8192, clients=4, dim=8192, k=1, rule="krum", select="0", secure=1, lazy=1),
     "cfg2": dict(N=32768, clients=10, dim=272474, k=1, rule="krum", select="0", secure=1,
                  lazy=1),
+    # cfg3's ring (N = 2^16, ResNet-18 width 32768) with 3 clients x 3 chunks,
+    # Multi-Krum averaging, and the N = 2^17 kernels (BASELINE cfg5 sweep)
+    "n16_multikrum": dict(N=65536, clients=3, dim=70000, k=1, rule="multi_krum", select="0,2",
+                          secure=1, lazy=1),
+    "n17_hoist": dict(N=131072, clients=3, dim=140000, k=2, rule="krum", select="1", secure=1,
+                      lazy=1),
 }
 
 

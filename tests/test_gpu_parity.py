@@ -124,7 +124,8 @@ def test_mult_plain_matches_oracle(evalrig):
         assert np.array_equal(L.to_host(ctx.rescale(got).data), want), l
 
 
-GOLDEN = ["tiny_krum", "tiny_hoist_multikrum", "tiny_eager", "tiny_fullhoist", "cfg1", "cfg2"]
+GOLDEN = ["tiny_krum", "tiny_hoist_multikrum", "tiny_eager", "tiny_fullhoist", "cfg1", "cfg2",
+          "n16_multikrum", "n17_hoist"]
 
 
 @pytest.fixture(scope="module", params=GOLDEN)

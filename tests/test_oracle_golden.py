@@ -2,17 +2,20 @@
 regenerates (keys, client ciphertexts, selector ciphertexts, distance
 ciphertexts, aggregate chunks, op counters) must hash to the digest the
 reference produced (tests/golden/*.json, made by tests/golden/make_golden.py)."""
+import os
+
 import numpy as np
 import pytest
 
 from tests.golden_util import Rig, sha
 
-SMALL = ["tiny_krum", "tiny_hoist_multikrum", "tiny_eager", "tiny_fullhoist", "cfg1"]
+SMALL = ["tiny_krum", "tiny_hoist_multikrum", "tiny_eager", "tiny_fullhoist", "cfg1",
+         "n16_multikrum", "n17_hoist"]
 
 
 @pytest.fixture(scope="module", params=SMALL)
 def rig(request):
-    return Rig(request.param)
+    return Rig(request.param, threads=os.cpu_count())
 
 
 def test_basis_matches_reference(rig):
