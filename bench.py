@@ -291,6 +291,19 @@ def our_arm(args, cfg):
         for _ in range(args.warmup):
             step()
         stream.synchronize()
+        # CUDA graph of the whole round (single GPU): after warm-up every
+        # workspace exists and the Krum round has no host synchronisation,
+        # so the ~140 launches are captured once and replayed.
+        graph = None
+        launches_per_step = None
+        if world == 1 and not args.no_graph:
+            l0 = ctx.launch_count()
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph, stream=stream):
+                step()
+            launches_per_step = ctx.launch_count() - l0
+            graph.replay()
+            stream.synchronize()
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
@@ -302,11 +315,16 @@ def our_arm(args, cfg):
                 a = torch.cuda.Event(enable_timing=True)
                 b = torch.cuda.Event(enable_timing=True)
                 a.record(stream)
-                step()
+                if graph is not None:
+                    graph.replay()
+                else:
+                    step()
                 b.record(stream)
                 b.synchronize()
                 total_ms += a.elapsed_time(b)
         launches = ctx.launch_count() - launches0
+        if graph is not None:
+            launches = launches_per_step * args.steps
         torch.cuda.synchronize()
     ms = total_ms / args.steps
     if world > 1:
@@ -377,6 +395,7 @@ def our_arm(args, cfg):
             "e2e": {"value": e2e_ms, "unit": "ms", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h},
             "gpu_launches": int(launches // max(1, args.steps)),
+            "cuda_graph": graph is not None,
             "roofline": prof.get("roofline"),
             "roofline_int": prof.get("roofline_int"),
             "kernels": prof.get("kernels"),
@@ -453,6 +472,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-graph", action="store_true", help="launch the round eagerly")
     ap.add_argument("--cpu-budget-s", type=float, default=120.0)
     ap.add_argument("--ref-budget-s", type=float, default=240.0)
     args = ap.parse_args()

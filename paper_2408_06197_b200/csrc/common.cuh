@@ -25,6 +25,8 @@ struct PrimeConst {
   u64 half;                // q >> 1: centred-lift threshold (rns.cpp:370-378)
   u64 n_inv, n_inv_shoup;  // N^-1 mod q
   u64 w1n, w1n_shoup;      // iroot[1] * N^-1: last inverse stage with the scaling folded in
+  u32 mu56;                // floor(2^56 / q): 32x32 Barrett quotient for lifts (v < 2^55)
+  u32 pad_;
 };
 
 // Row addressing for batched transforms. Row r of a launch is row

@@ -314,7 +314,8 @@ struct ProfScope {
 
 // Algorithmic traffic of the functors (words per output row).
 inline double load_rows(const PlainLoad&, double rows) { return rows; }
-inline double load_rows(const LiftLoad& l, double rows) { return rows / l.fan; }
+template <bool S>
+inline double load_rows(const LiftLoadT<S>& l, double rows) { return rows / l.fan; }
 inline double store_rows(const PlainStore&, double rows) { return rows; }
 inline double store_rows(const DivRoundStore& s, double rows) {
   return rows * (2.0 + (s.add1.base ? 1.0 : 0.0)) + (s.add2.base ? rows / 2 : 0.0);
@@ -349,7 +350,7 @@ void fwd2(lcl_context* c, u32 rows, const RowMap& mid, const Loader& ld, const E
   const double rb = 8.0 * c->N();
   const double bpr = 0.5 * c->N();  // butterflies per row per stage
   {
-    ProfScope ps(c, std::is_same<Loader, LiftLoad>::value ? "ntt_col_fwd<lift>" : "ntt_col_fwd",
+    ProfScope ps(c, std::is_same<Loader, PlainLoad>::value ? "ntt_col_fwd" : "ntt_col_fwd<lift>",
                  rb * (load_rows(ld, rows) + rows), bpr * rows * LOGN1);
     ntt_col_fwd<LOGN1, E, Loader><<<rows * groups, 16 * (N1 / E), smem, c->stream>>>(
         mid, ld, c->d_tw, c->d_primes, c->logn);
@@ -462,9 +463,8 @@ void modup_ip_n(lcl_context* c, u32 B, u32 m, const RowMap& coef_map, const u32*
       dp[j * m + tp] = t < m ? t : c->full;
     }
   const RowMap mid_map2 = make_map(mid, m * m, N, (u64)m * m * N, 1, 0, dp);
-  LiftLoad lift = lift_from(c, coef_map, m * m, m);
-  lift.sigma = sigma;
-  col_only<LOGN1, E>(c, B * m * m, mid_map2, lift);
+  (void)sigma;  // two-pass rings permute block-locally inside modup_ip_blk
+  col_only<LOGN1, E>(c, B * m * m, mid_map2, lift_from(c, coef_map, m * m, m));
   post_launch(c);
   switch (m) {
     case 1: modup_ip_launch<LOGN1, 1>(c, B, mid, c1, c1_stride, perm, key, key_shoup, acc); break;
@@ -513,9 +513,16 @@ u64* ks_decompose(lcl_context* c, const RowMap& in, u32 B, u32 m, const u32* sig
   for (u32 j = 0; j < m; ++j)
     for (u32 t = 0; t <= m; ++t) dp[j * (m + 1) + t] = t < m ? t : c->full;
   const RowMap dig_map = make_map(dig, m * (m + 1), N, (u64)m * (m + 1) * N, 1, 0, dp);
-  LiftLoad lift = lift_from(c, coef_map, m * (m + 1), m + 1);
-  lift.sigma = sigma;
-  launch_fwd(c, B * m * (m + 1), dig_map, lift, PlainStore{dig_map});
+  if (sigma) {
+    const LiftLoad base = lift_from(c, coef_map, m * (m + 1), m + 1);
+    LiftSigmaLoad lift;
+    std::memcpy(&lift, &base, sizeof base);
+    lift.sigma = sigma;
+    launch_fwd(c, B * m * (m + 1), dig_map, lift, PlainStore{dig_map});
+  } else {
+    launch_fwd(c, B * m * (m + 1), dig_map, lift_from(c, coef_map, m * (m + 1), m + 1),
+               PlainStore{dig_map});
+  }
   return dig;
 }
 
@@ -967,6 +974,8 @@ void build_context(lcl_context* c, size_t degree, int depth, int secure, int dev
     // iroot[1] = psi^-brv(1) = psi^-(n/2)
     k.w1n = h_mulmod(h_powmod(psi_inv, n / 2, q), k.n_inv, q);
     k.w1n_shoup = h_shoup(k.w1n, q);
+    k.mu56 = (u32)(((u128)1 << 56) / q);
+    k.pad_ = 0;
     u64 f = 1, g = 1;
     for (size_t t = 0; t < n; ++t) {
       const size_t r = h_brv(t, c->logn);

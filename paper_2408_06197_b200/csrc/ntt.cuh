@@ -83,34 +83,43 @@ struct PlainLoad {
 // (single-prime mod_up branch, rns.cpp:367-383; the lift inside
 // divide_and_round_by_last, rns.cpp:484-494). Destination row r of a launch
 // reads source row (r / rows_per_item) * (rows_per_item / fan) + (r % rows_per_item) / fan.
-// With `sigma` set, the source is read through the Galois automorphism
-// X -> X^elt in the coefficient domain (entry = src index | negate << 31);
-// lifting commutes with that signed permutation, so the lifted, transformed
-// digit equals apply_galois of the reference's digit (ckks.cpp:497-501).
-struct LiftLoad {
+//
+// v mod q_d uses a 32x32 Barrett quotient: with v < 2^55 and 2^39 < q_d <
+// 2^55, qh = ((v >> 24) * floor(2^56 / q_d)) >> 32 is floor(v / q_d) or one
+// less, so v - qh q_d lies in [0, 2 q_d); the centring correction adds
+// q_d - (q_s mod q_d). The value handed to the forward NTT is therefore
+// congruent to the reference's lift and lies in [0, 3 q_d), which the
+// reduction-free butterflies absorb ((3 + 4 s) q_d < 2^62 for s <= 17).
+// With SIGMA the source is read through the Galois automorphism X -> X^elt in
+// the coefficient domain (entry = src index | negate << 31); lifting commutes
+// with that signed permutation (small rings only; the two-pass rings apply the
+// permutation block-locally in the evaluation domain).
+template <bool SIGMA>
+struct LiftLoadT {
   RowMap src;
   u32 rows_per_item;
   u32 fan;
   u32 nprimes;               // full + 1
   const PrimeConst* primes;  // device table
   const u64* smod;           // smod[s * nprimes + d] = q_s mod q_d
-  const u32* sigma;          // nullptr: identity
+  const u32* sigma;          // SIGMA only
   struct Row {
     const u64* s;
     const u32* sigma;
-    u64 qs, half, sd, q, one_shoup;
+    u64 qs, half, corr, q;
+    u32 mu;
     __device__ __forceinline__ u64 operator()(u32 a) const {
       u64 v;
-      if (sigma) {
+      if (SIGMA) {
         const u32 e = __ldg(sigma + a);
         v = __ldg(s + (e & 0x7FFFFFFFu));
         if ((e >> 31) && v) v = qs - v;
       } else {
         v = __ldg(s + a);
       }
-      u64 x = v - __umul64hi(v, one_shoup) * q;
-      x = x >= q ? x - q : x;
-      if (v > half) x = x >= sd ? x - sd : x + q - sd;
+      const u64 qh = ((u64)(u32)(v >> 24) * mu) >> 32;
+      u64 x = v - qh * q;
+      if (v > half) x += corr;
       return x;
     }
   };
@@ -124,16 +133,19 @@ struct LiftLoad {
     w.sigma = sigma;
     w.qs = __ldg(&primes[sp].q);
     w.half = __ldg(&primes[sp].half);
-    w.sd = __ldg(smod + sp * nprimes + dpi);
+    w.corr = dst.q - __ldg(smod + sp * nprimes + dpi);
     w.q = dst.q;
-    w.one_shoup = dst.one_shoup;
+    w.mu = dst.mu56;
     return w;
   }
 };
+using LiftLoad = LiftLoadT<false>;
+using LiftSigmaLoad = LiftLoadT<true>;
 
 // ------------------------------------------------------------ epilogues
 // auto row = epi.bind(r, dst_prime_index, dst);  row(a, value < q)
 struct PlainStore {
+  static constexpr bool kNeedsReduced = true;
   RowMap out;
   struct Pre {};
   struct Row {
@@ -153,6 +165,7 @@ struct PlainStore {
 // first item of every group, i.e. the c0 half]. add2 must not alias out
 // (gathered reads); add1 may alias out (same thread reads then writes one word).
 struct DivRoundStore {
+  static constexpr bool kNeedsReduced = false;  // the lift may be any lazy word < 80q
   RowMap out;
   RowMap x;
   RowMap add1;  // base == nullptr: absent
@@ -168,7 +181,7 @@ struct DivRoundStore {
     const u64* a1;
     const u64* a2;
     const u32* perm;
-    u64 iv, ivs, q;
+    u64 iv, ivs, q, q80;
     __device__ __forceinline__ void operator()(u32 a, u64 lift) const {
       Pre p;
       prefetch(p, a, nullptr);
@@ -194,7 +207,8 @@ struct DivRoundStore {
       p.add = v;
     }
     __device__ __forceinline__ void store(const Pre& p, u32 a, u64 lift) const {
-      const u64 v = mul_shoup(p.x - lift + q, iv, ivs, q);
+      // lift < 80q (lazy NTT output): x + 80q - lift > 0 and congruent
+      const u64 v = mul_shoup(p.x + (q80 - lift), iv, ivs, q);
       o[a] = add_mod(v, p.add, q);
     }
   };
@@ -210,6 +224,7 @@ struct DivRoundStore {
     w.iv = iv.x;
     w.ivs = iv.y;
     w.q = P.q;
+    w.q80 = 80 * P.q;
     return w;
   }
 };
@@ -302,7 +317,7 @@ __global__ void __launch_bounds__(16 * ((1 << LOGN1) / E))
 // block (coalesced order) on entry and the fully reduced output in the same
 // order on exit. Phase 1 runs local stages m' = 1..8 on s = l + 16 e, phase 2
 // m' = 16..128 on s = 16 l + e after a warp-local shared transpose.
-template <int LOGN1>
+template <int LOGN1, bool REDUCE = true>
 __device__ __forceinline__ void blk_fwd_body(u64 (&x)[16], u64* s, const ulonglong2* tw, u32 b,
                                              u32 l, const PrimeConst& P) {
   constexpr int N1 = 1 << LOGN1;
@@ -323,9 +338,11 @@ __device__ __forceinline__ void blk_fwd_body(u64 (&x)[16], u64* s, const ulonglo
                     [&](int gi) { return ldtw(tw, (N1 + b) * (1 << lm) + ((16 * l + gi * 2 * d) >> (8 - lm))); },
                     P.q, P.two_q);
   });
+  // REDUCE = false leaves the lazy words (< 71q, see ct_bfly) for consumers
+  // that only feed them into a Shoup product, which accepts any 64-bit input.
   __syncwarp();
 #pragma unroll
-  for (int e = 0; e < 16; ++e) s[16 * l + e + l] = reduce64(x[e], P);
+  for (int e = 0; e < 16; ++e) s[16 * l + e + l] = REDUCE ? reduce64(x[e], P) : x[e];
   __syncwarp();
 #pragma unroll
   for (int e = 0; e < 16; ++e) x[e] = s[l + 16 * e + e];
@@ -369,7 +386,7 @@ __global__ void __launch_bounds__(64)
   u64 x[16];
 #pragma unroll
   for (int e = 0; e < 16; ++e) x[e] = src[l + 16 * e];
-  blk_fwd_body<LOGN1>(x, sm[bw], tw, b, l, P);
+  blk_fwd_body<LOGN1, Epi::kNeedsReduced>(x, sm[bw], tw, b, l, P);
   const auto row = epi.bind(r, pi, P);
   row.stage(sm[bw], b, l);
   // operands of 4 elements in flight at a time: latency overlap without the
@@ -442,9 +459,9 @@ __global__ void __launch_bounds__(64, 8)
       const u64* src = mid + (((u64)bi * M + j) * M + tp) * n + (src_blk << 8);
 #pragma unroll
       for (int e = 0; e < 16; ++e) x[e] = src[l + 16 * e];
-      blk_fwd_body<LOGN1>(x, sm[bw], tw, src_blk, l, P);
+      blk_fwd_body<LOGN1, false>(x, sm[bw], tw, src_blk, l, P);
       if (perm) {
-        // the body left the reduced block in shared memory: permuted read
+        // the body left the (lazy) block in shared memory: permuted read
 #pragma unroll
         for (int e = 0; e < 16; ++e)
           x[e] = sm[bw][pad16(__ldg(perm + (blk << 8) + l + 16 * e) & 255u)];
