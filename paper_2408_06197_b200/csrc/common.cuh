@@ -26,7 +26,7 @@ struct PrimeConst {
   u64 n_inv, n_inv_shoup;  // N^-1 mod q
   u64 w1n, w1n_shoup;      // iroot[1] * N^-1: last inverse stage with the scaling folded in
   u32 mu56;                // floor(2^56 / q): 32x32 Barrett quotient for lifts (v < 2^55)
-  u32 pad_;
+  u32 mu62;                // floor(2^62 / q): reduce62 for lazy NTT outputs (x < 2^62)
 };
 
 // Row addressing for batched transforms. Row r of a launch is row
@@ -88,6 +88,18 @@ __device__ __forceinline__ u64 mul_shoup(u64 a, u64 w, u64 ws, u64 q) {
 // a mod q for any 64-bit a.
 __device__ __forceinline__ u64 reduce64(u64 a, const PrimeConst& p) {
   return csub(a - __umul64hi(a, p.one_shoup) * p.q, p.q);
+}
+
+// Exact x mod q for a lazy word x < 2^62 (2^39 < q < 2^55): one 32x32 high
+// product estimates the quotient (qh = floor(x/q) - {0,1,2}), the remainder
+// x - qh q lies in [0, 3q) and two conditional subtractions finish. Costs one
+// IMAD.HI + one IMAD.WIDE instead of reduce64's full 64x64 high product
+// (IMAD.WIDE / IMAD.HI retire at half the rate of IMAD on sm_100).
+__device__ __forceinline__ u64 reduce62(u64 x, u64 q, u32 mu62) {
+  const u32 qh = __umulhi((u32)(x >> 30), mu62);
+  u64 r = x - (u64)qh * q;
+  r = r >= q ? r - q : r;
+  return r >= q ? r - q : r;
 }
 
 // Exact reduction of the 128-bit value (hi, lo) mod q (modmath.hpp:62-73).

@@ -975,7 +975,7 @@ void build_context(lcl_context* c, size_t degree, int depth, int secure, int dev
     k.w1n = h_mulmod(h_powmod(psi_inv, n / 2, q), k.n_inv, q);
     k.w1n_shoup = h_shoup(k.w1n, q);
     k.mu56 = (u32)(((u128)1 << 56) / q);
-    k.pad_ = 0;
+    k.mu62 = (u32)(((u128)1 << 62) / q);
     u64 f = 1, g = 1;
     for (size_t t = 0; t < n; ++t) {
       const size_t r = h_brv(t, c->logn);

@@ -43,7 +43,7 @@ __device__ __forceinline__ Tw ldtw(const ulonglong2* t, u32 idx) {
 // [0, 4q) (truncated Shoup quotient), x' = x + t and y' = x + 4q - t both stay
 // below B + 4q when x < B. Starting from inputs < q, after s stages every
 // value is < (1 + 4s) q; for s <= 17 and q < 2^55 that is < 69 * 2^55 < 2^62,
-// so no word overflows and the only reduction is the final one (reduce64).
+// so no word overflows and the only reduction is the final one (reduce62).
 // The Shoup product accepts any y < 2^64. (two_q carries 4q here.)
 __device__ __forceinline__ void ct_bfly(u64& x, u64& y, Tw w, u64 q, u64 four_q) {
   const u64 t = mul_shoup_lazy4(y, w.w, w.ws, q);
@@ -342,7 +342,7 @@ __device__ __forceinline__ void blk_fwd_body(u64 (&x)[16], u64* s, const ulonglo
   // that only feed them into a Shoup product, which accepts any 64-bit input.
   __syncwarp();
 #pragma unroll
-  for (int e = 0; e < 16; ++e) s[16 * l + e + l] = REDUCE ? reduce64(x[e], P) : x[e];
+  for (int e = 0; e < 16; ++e) s[16 * l + e + l] = REDUCE ? reduce62(x[e], P.q, P.mu62) : x[e];
   __syncwarp();
 #pragma unroll
   for (int e = 0; e < 16; ++e) x[e] = s[l + 16 * e + e];
@@ -489,8 +489,8 @@ __global__ void __launch_bounds__(64, 8)
 #pragma unroll
   for (int e = 0; e < 16; ++e) {
     const u32 si = l + 16 * e;
-    o0[a0 + 16 * e] = reduce64(s0acc[si], P);
-    o1[a0 + 16 * e] = reduce64(s1acc[si], P);
+    o0[a0 + 16 * e] = reduce62(s0acc[si], P.q, P.mu62);
+    o1[a0 + 16 * e] = reduce62(s1acc[si], P.q, P.mu62);
   }
 }
 
@@ -623,7 +623,7 @@ __global__ void __launch_bounds__(256)
       }
       __syncthreads();
     }
-    for (u32 a = threadIdx.x; a < n; a += blockDim.x) out(a, reduce64(smem[a], P));
+    for (u32 a = threadIdx.x; a < n; a += blockDim.x) out(a, reduce62(smem[a], P.q, P.mu62));
   } else {
     u32 half = 1;
     for (u32 m = n >> 1; m >= 1; m >>= 1) {
