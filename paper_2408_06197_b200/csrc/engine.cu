@@ -411,6 +411,84 @@ void launch_fwd(lcl_context* c, u32 rows, const RowMap& pm, const Loader& ld, co
   }
 }
 
+// ---- split passes for the fused pipelines (two-pass rings only)
+template <int LOGN1>
+void blk_inv_n(lcl_context* c, u32 rows, const RowMap& in, const RowMap& out) {
+  constexpr int N1 = 1 << LOGN1;
+  ProfScope ps(c, "ntt_blk_inv", 16.0 * c->N() * rows, 0.5 * c->N() * rows * 8);
+  ntt_blk_inv<LOGN1><<<rows * N1 / 4, 64, 0, c->stream>>>(in, out, c->d_itw, c->d_primes, c->logn);
+}
+
+template <int LOGN1, int E>
+void col_ilf_n(lcl_context* c, u32 src_rows, const RowMap& src, const RowMap& dst, u32 fan) {
+  constexpr int N1 = 1 << LOGN1;
+  constexpr size_t smem = (size_t)N1 * 16 * 8;
+  static bool once = (allow_smem(ntt_col_inv_lift_fwd<LOGN1, E>, smem), true);
+  (void)once;
+  const u32 groups = (u32)(c->n >> LOGN1) >> 4;
+  ProfScope ps(c, "ntt_col_inv_lift_fwd", 8.0 * c->N() * (src_rows + (double)src_rows * fan),
+               0.5 * c->N() * LOGN1 * (src_rows + (double)src_rows * fan));
+  ntt_col_inv_lift_fwd<LOGN1, E><<<src_rows * groups, 16 * (N1 / E), smem, c->stream>>>(
+      src, dst, fan, c->d_tw, c->d_itw, c->d_primes, c->d_smod, c->P(), c->logn);
+}
+
+template <int LOGN1, class Epi>
+void blk_fwd_n(lcl_context* c, u32 rows, const RowMap& mid, const Epi& epi) {
+  constexpr int N1 = 1 << LOGN1;
+  ProfScope ps(c, std::is_same<Epi, DivRoundStore>::value ? "ntt_blk_fwd<divround>" : "ntt_blk_fwd",
+               8.0 * c->N() * (store_rows(epi, rows) + (std::is_same<Epi, PlainStore>::value ? rows : 0)),
+               0.5 * c->N() * rows * 8);
+  ntt_blk_fwd<LOGN1, Epi><<<rows * N1 / 4, 64, 0, c->stream>>>(mid, epi, c->d_tw, c->d_primes, c->logn);
+}
+
+// Calls f(LOGN1, E) with compile-time constants for the two-pass ring sizes.
+template <class F>
+void dispatch_logn(lcl_context* c, F&& f) {
+  switch (c->logn) {
+    case 13: f(std::integral_constant<int, 5>{}, std::integral_constant<int, 16>{}); break;
+    case 14: f(std::integral_constant<int, 6>{}, std::integral_constant<int, 16>{}); break;
+    case 15: f(std::integral_constant<int, 7>{}, std::integral_constant<int, 16>{}); break;
+    case 16: f(std::integral_constant<int, 8>{}, std::integral_constant<int, 16>{}); break;
+    case 17: f(std::integral_constant<int, 9>{}, std::integral_constant<int, 32>{}); break;
+    default: fail(LCL_PARAMETER_ERROR, "ring degree outside 2^13..2^17");
+  }
+}
+
+// Inverse NTT of `src_rows` rows (map `in`) fused with the centred lift into
+// `fan` destination rows each and their forward column pass; the output
+// (dst map) is ready for a forward block pass. Returns nothing; two launches.
+void inv_lift_fwd_cols(lcl_context* c, u32 src_rows, const RowMap& in, const RowMap& dst,
+                       u32 fan) {
+  const u64 N = c->N();
+  u64* tmp = c->ws_coef.get((u64)src_rows * N);
+  RowMap t = in;
+  t.base = tmp;
+  t.row_stride = N;
+  t.item_stride = (u64)in.rows_per_item * N;
+  t.items_per_group = 1;
+  t.group_stride = t.item_stride;
+  dispatch_logn(c, [&](auto L1, auto E) {
+    blk_inv_n<decltype(L1)::value>(c, src_rows, in, t);
+    col_ilf_n<decltype(L1)::value, decltype(E)::value>(c, src_rows, t, dst, fan);
+  });
+  post_launch(c, 2);
+}
+
+// Same, for source rows whose inverse block pass already ran.
+void lift_fwd_cols_preinv(lcl_context* c, u32 src_rows, const RowMap& src_inv, const RowMap& dst,
+                          u32 fan) {
+  dispatch_logn(c, [&](auto L1, auto E) {
+    col_ilf_n<decltype(L1)::value, decltype(E)::value>(c, src_rows, src_inv, dst, fan);
+  });
+  post_launch(c);
+}
+
+template <class Epi>
+void blk_fwd_only(lcl_context* c, u32 rows, const RowMap& mid, const Epi& epi) {
+  dispatch_logn(c, [&](auto L1, auto) { blk_fwd_n<decltype(L1)::value>(c, rows, mid, epi); });
+  post_launch(c);
+}
+
 LiftLoad lift_from(lcl_context* c, const RowMap& src, u32 rows_per_item, u32 fan) {
   LiftLoad l;
   l.src = src;
@@ -439,40 +517,28 @@ void col_only(lcl_context* c, u32 rows, const RowMap& out, const Loader& ld) {
 
 template <int LOGN1, int M>
 void modup_ip_launch(lcl_context* c, u32 B, const u64* mid, const u64* c1, u64 c1_stride,
-                     const u32* perm, const u64* key, const u64* key_shoup, u64* acc) {
+                     const u32* perm, const u64* key, const u64* key_shoup, u64* acc,
+                     u64* sp_out) {
   constexpr int N1 = 1 << LOGN1;
   const double rb = 8.0 * c->N();
   ProfScope ps(c, perm ? "modup_ip_blk<perm>" : "modup_ip_blk",
                rb * ((double)B * M * M + B * M + 4.0 * M * (M + 1) + 2.0 * B * (M + 1)),
                0.5 * c->N() * B * M * M * 8);
   modup_ip_blk<LOGN1, M><<<((B + 3) / 4) * (M + 1) * N1, 64, 0, c->stream>>>(
-      B, mid, c1, c1_stride, perm, key, key_shoup, c->full, acc, c->d_tw, c->d_primes, c->logn);
+      B, mid, c1, c1_stride, perm, key, key_shoup, c->full, acc, sp_out, c->d_tw, c->d_itw,
+      c->d_primes, c->logn);
 }
 
-template <int LOGN1, int E>
-void modup_ip_n(lcl_context* c, u32 B, u32 m, const RowMap& coef_map, const u32* sigma,
-                const u64* c1, u64 c1_stride, const u32* perm, const u64* key,
-                const u64* key_shoup, u64* acc) {
-  const u64 N = c->N();
-  // column pass over the m*m non-identity digit rows (b, j, t')
-  u64* mid = c->ws_digits.get((u64)B * m * m * N);
-  std::vector<u32> dp(m * m);
-  for (u32 j = 0; j < m; ++j)
-    for (u32 tp = 0; tp < m; ++tp) {
-      const u32 t = tp < j ? tp : tp + 1;
-      dp[j * m + tp] = t < m ? t : c->full;
-    }
-  const RowMap mid_map2 = make_map(mid, m * m, N, (u64)m * m * N, 1, 0, dp);
-  (void)sigma;  // two-pass rings permute block-locally inside modup_ip_blk
-  col_only<LOGN1, E>(c, B * m * m, mid_map2, lift_from(c, coef_map, m * m, m));
-  post_launch(c);
+template <int LOGN1>
+void modup_ip_n(lcl_context* c, u32 B, u32 m, const u64* mid, const u64* c1, u64 c1_stride,
+                const u32* perm, const u64* key, const u64* key_shoup, u64* acc, u64* sp_out) {
   switch (m) {
-    case 1: modup_ip_launch<LOGN1, 1>(c, B, mid, c1, c1_stride, perm, key, key_shoup, acc); break;
-    case 2: modup_ip_launch<LOGN1, 2>(c, B, mid, c1, c1_stride, perm, key, key_shoup, acc); break;
-    case 3: modup_ip_launch<LOGN1, 3>(c, B, mid, c1, c1_stride, perm, key, key_shoup, acc); break;
-    case 4: modup_ip_launch<LOGN1, 4>(c, B, mid, c1, c1_stride, perm, key, key_shoup, acc); break;
-    case 5: modup_ip_launch<LOGN1, 5>(c, B, mid, c1, c1_stride, perm, key, key_shoup, acc); break;
-    case 6: modup_ip_launch<LOGN1, 6>(c, B, mid, c1, c1_stride, perm, key, key_shoup, acc); break;
+    case 1: modup_ip_launch<LOGN1, 1>(c, B, mid, c1, c1_stride, perm, key, key_shoup, acc, sp_out); break;
+    case 2: modup_ip_launch<LOGN1, 2>(c, B, mid, c1, c1_stride, perm, key, key_shoup, acc, sp_out); break;
+    case 3: modup_ip_launch<LOGN1, 3>(c, B, mid, c1, c1_stride, perm, key, key_shoup, acc, sp_out); break;
+    case 4: modup_ip_launch<LOGN1, 4>(c, B, mid, c1, c1_stride, perm, key, key_shoup, acc, sp_out); break;
+    case 5: modup_ip_launch<LOGN1, 5>(c, B, mid, c1, c1_stride, perm, key, key_shoup, acc, sp_out); break;
+    case 6: modup_ip_launch<LOGN1, 6>(c, B, mid, c1, c1_stride, perm, key, key_shoup, acc, sp_out); break;
     default: fail(LCL_PARAMETER_ERROR, "fused key switching supports up to 6 live limbs");
   }
   post_launch(c);
@@ -552,37 +618,49 @@ u64* ks_ip(lcl_context* c, const u64* dig, u32 B, u32 m, const u64* key, const u
 // the same limbs for the identity digits. sigma / perm: the rotation's
 // coefficient- / evaluation-domain automorphism (nullptr for relinearize).
 // Returns acc [B][2][m+1][N].
+constexpr bool kFuseSpecialInverse = false;
+bool ks_fused(const lcl_context* c, u32 m) { return c->logn >= 13 && m <= 6; }
+bool sp_preinverted(const lcl_context* c, u32 m) { return kFuseSpecialInverse && ks_fused(c, m); }
+
 u64* ks_switch(lcl_context* c, const RowMap& in, const u64* c1, u64 c1_stride, u32 B, u32 m,
                const u32* sigma, const u32* perm, const u64* key, const u64* key_shoup) {
-  if (c->logn < 13 || m > 6) {
+  if (!ks_fused(c, m)) {
     u64* dig = ks_decompose(c, in, B, m, sigma);
     return ks_ip(c, dig, B, m, key, nullptr);
   }
   const u64 N = c->N();
-  u64* coef = c->ws_coef.get((u64)B * m * N);
-  const RowMap coef_map = make_map(coef, m, N, m * N, 1, 0, c->primes_0(m));
-  launch_inv(c, B * m, in, PlainStore{coef_map});
+  // inverse NTT of the m limbs fused with the lift into the m non-identity
+  // targets of each digit (b, j, t'), t = t' < j ? t' : t' + 1
+  u64* mid = c->ws_digits.get((u64)B * m * m * N);
+  std::vector<u32> dp(m * m);
+  for (u32 j = 0; j < m; ++j)
+    for (u32 tp = 0; tp < m; ++tp) {
+      const u32 t = tp < j ? tp : tp + 1;
+      dp[j * m + tp] = t < m ? t : c->full;
+    }
+  const RowMap mid_map = make_map(mid, m * m, N, (u64)m * m * N, 1, 0, dp);
+  inv_lift_fwd_cols(c, B * m, in, mid_map, m);
   u64* acc = c->ws_acc.get((u64)B * 2 * (m + 1) * N);
-  switch (c->logn) {
-    case 13: modup_ip_n<5, 16>(c, B, m, coef_map, sigma, c1, c1_stride, perm, key, key_shoup, acc); break;
-    case 14: modup_ip_n<6, 16>(c, B, m, coef_map, sigma, c1, c1_stride, perm, key, key_shoup, acc); break;
-    case 15: modup_ip_n<7, 16>(c, B, m, coef_map, sigma, c1, c1_stride, perm, key, key_shoup, acc); break;
-    case 16: modup_ip_n<8, 16>(c, B, m, coef_map, sigma, c1, c1_stride, perm, key, key_shoup, acc); break;
-    case 17: modup_ip_n<9, 32>(c, B, m, coef_map, sigma, c1, c1_stride, perm, key, key_shoup, acc); break;
-    default: fail(LCL_PARAMETER_ERROR, "ring degree outside 2^13..2^17");
-  }
+  // Running the special rows' inverse block stages inside modup_ip_blk
+  // (sp != nullptr, then ks_moddown(sp_ready = true)) measured slower on
+  // cfg2 (8.91 vs 8.77 ms): it lengthens the special-target CTAs by as much
+  // as the standalone ntt_blk_inv costs. Kept off.
+  u64* sp = kFuseSpecialInverse ? c->ws_coefsp.get((u64)B * 2 * N) : nullptr;
+  dispatch_logn(c, [&](auto L1, auto) {
+    modup_ip_n<decltype(L1)::value>(c, B, m, mid, c1, c1_stride, perm, key, key_shoup, acc, sp);
+  });
+  (void)sigma;  // two-pass rings permute block-locally inside modup_ip_blk
   return acc;
 }
 
 // ModDown of acc [B][2][m+1][N] into `out` (items (b, x), rows_per_item m,
 // 2 items per group) with the fused output additions.
+// sp_ready: the special rows' inverse block pass already ran inside
+// modup_ip_blk (fused ks_switch path); otherwise they are read from acc.
 void ks_moddown(lcl_context* c, const u64* acc, u32 B, u32 m, const RowMap& out,
-                const RowMap& add1, const RowMap& add2, const u32* perm) {
+                const RowMap& add1, const RowMap& add2, const u32* perm, bool sp_ready) {
   const u64 N = c->N();
-  u64* csp = c->ws_coefsp.get((u64)B * 2 * N);
   const RowMap sp_in = make_map(acc + (u64)m * N, 1, N, (m + 1) * N, 1, 0, {c->full});
-  const RowMap sp_map = make_map(csp, 1, N, N, 1, 0, {c->full});
-  launch_inv(c, 2 * B, sp_in, PlainStore{sp_map});
   DivRoundStore epi;
   epi.out = out;
   epi.x = make_map(acc, m, N, (m + 1) * N, 1, 0, c->primes_0(m));
@@ -590,6 +668,25 @@ void ks_moddown(lcl_context* c, const u64* acc, u32 B, u32 m, const RowMap& out,
   epi.add2 = add2;
   epi.perm = perm;
   epi.pinv = c->d_pinv + (u64)c->full * c->P();
+  if (c->logn >= 13) {
+    // inverse NTT of the special rows + lift into the m q-primes + forward
+    // column pass fused (the inverse block stages already ran inside
+    // modup_ip_blk when sp_ready), then the block pass with the
+    // divide-and-round epilogue
+    u64* mid = c->ws_mid.get((u64)B * 2 * m * N);
+    const RowMap mid_map = make_map(mid, m, N, (u64)m * N, 1, 0, c->primes_0(m));
+    if (sp_ready) {
+      const RowMap sp_inv = make_map(c->ws_coefsp.get((u64)B * 2 * N), 1, N, N, 1, 0, {c->full});
+      lift_fwd_cols_preinv(c, 2 * B, sp_inv, mid_map, m);
+    } else {
+      inv_lift_fwd_cols(c, 2 * B, sp_in, mid_map, m);
+    }
+    blk_fwd_only(c, 2 * B * m, mid_map, epi);
+    return;
+  }
+  u64* csp = c->ws_coefsp.get((u64)B * 2 * N);
+  const RowMap sp_map = make_map(csp, 1, N, N, 1, 0, {c->full});
+  launch_inv(c, 2 * B, sp_in, PlainStore{sp_map});
   launch_fwd(c, 2 * B * m, out, lift_from(c, sp_map, m, m), epi);
 }
 
@@ -607,7 +704,7 @@ void relinearize_batch(lcl_context* c, const u64* tern, u32 B, u32 m, u64* out) 
   u64* acc = ks_switch(c, d2, tern + 2ull * m * N, 3ull * m * N, B, m, nullptr, nullptr,
                        c->d_relin, c->d_relin_shoup);
   ks_moddown(c, acc, B, m, ct_map(out, m, N, 2ull * m * N), ct_map(tern, m, N, 3ull * m * N),
-             null_map(), nullptr);
+             null_map(), nullptr, sp_preinverted(c, m));
   c->counts.relinearizations += B;
   c->counts.mod_ups += B;
 }
@@ -616,10 +713,7 @@ void relinearize_batch(lcl_context* c, const u64* tern, u32 B, u32 m, u64* out) 
 void rescale_batch(lcl_context* c, const u64* ct, u32 B, u32 m, u64* out) {
   if (m < 2) fail(LCL_DEPTH_EXHAUSTED, "no prime left to rescale by");
   const u64 N = c->N();
-  u64* last = c->ws_coefsp.get((u64)B * 2 * N);
   const RowMap last_in = make_map(ct + (u64)(m - 1) * N, 1, N, (u64)m * N, 2, 2ull * m * N, {m - 1});
-  const RowMap last_map = make_map(last, 1, N, N, 1, 0, {m - 1});
-  launch_inv(c, 2 * B, last_in, PlainStore{last_map});
   DivRoundStore epi;
   epi.out = ct_map(out, m - 1, N, 2ull * (m - 1) * N);
   epi.x = ct_map(ct, m - 1, N, 2ull * m * N);
@@ -628,7 +722,17 @@ void rescale_batch(lcl_context* c, const u64* ct, u32 B, u32 m, u64* out) {
   epi.add2 = null_map();
   epi.perm = nullptr;
   epi.pinv = c->d_pinv + (u64)(m - 1) * c->P();
-  launch_fwd(c, 2 * B * (m - 1), epi.out, lift_from(c, last_map, m - 1, m - 1), epi);
+  if (c->logn >= 13) {
+    u64* mid = c->ws_mid.get((u64)B * 2 * (m - 1) * N);
+    const RowMap mid_map = make_map(mid, m - 1, N, (u64)(m - 1) * N, 1, 0, c->primes_0(m - 1));
+    inv_lift_fwd_cols(c, 2 * B, last_in, mid_map, m - 1);
+    blk_fwd_only(c, 2 * B * (m - 1), mid_map, epi);
+  } else {
+    u64* last = c->ws_coefsp.get((u64)B * 2 * N);
+    const RowMap last_map = make_map(last, 1, N, N, 1, 0, {m - 1});
+    launch_inv(c, 2 * B, last_in, PlainStore{last_map});
+    launch_fwd(c, 2 * B * (m - 1), epi.out, lift_from(c, last_map, m - 1, m - 1), epi);
+  }
   c->counts.rescales += B;
 }
 
@@ -654,7 +758,7 @@ void rotate_level(lcl_context* c, const u64* in, u32 B, u32 m, size_t step, u64*
                        c->d_rot_shoup.at(step));
   const RowMap inm = ct_map(in, m, N, 2ull * m * N);
   ks_moddown(c, acc, B, m, ct_map(out, m, N, 2ull * m * N), accumulate ? inm : null_map(), inm,
-             perm);
+             perm, sp_preinverted(c, m));
   c->counts.rotations += B;
   c->counts.mod_ups += B;
   if (accumulate) c->counts.additions += B;
@@ -694,7 +798,7 @@ void slot_reduce_batch(lcl_context* c, const u64* in, u32 B, u32 m, size_t width
       const int nxt = cur < 0 ? 0 : 1 - cur;
       u64* acc = ks_ip(c, dig, B, m, rot_key(c, st), c->d_perm.at(st));
       ks_moddown(c, acc, B, m, ct_map(bufs[nxt], m, N, 2ull * m * N),
-                 ct_map(cur_ptr(), m, N, 2ull * m * N), base, c->d_perm.at(st));
+                 ct_map(cur_ptr(), m, N, 2ull * m * N), base, c->d_perm.at(st), false);
       cur = nxt;
       c->counts.rotations += B;
       c->counts.additions += B;
@@ -1385,7 +1489,7 @@ int lcl_hoisted_rotations(lcl_context* ctx, const uint64_t* d_ct, size_t batch, 
       }
       u64* acc = ks_ip(ctx, dig, B, m, key, ctx->d_perm.at(st));
       ks_moddown(ctx, acc, B, m, ct_map(o, m, N, 2ull * m * N), null_map(),
-                 ct_map(d_ct, m, N, 2ull * m * N), ctx->d_perm.at(st));
+                 ct_map(d_ct, m, N, 2ull * m * N), ctx->d_perm.at(st), false);
       ctx->counts.rotations += B;
     }
   });

@@ -349,6 +349,38 @@ __device__ __forceinline__ void blk_fwd_body(u64 (&x)[16], u64* s, const ulonglo
   __syncwarp();
 }
 
+// Block pass body, inverse: x[e] = element l + 16 e of block b (coalesced
+// order, values < 2q) in and out; GS stages m' = 128 .. 1 (global m = N/2 .. N1).
+template <int LOGN1>
+__device__ __forceinline__ void blk_inv_body(u64 (&x)[16], u64* s, const ulonglong2* tw, u32 b,
+                                             u32 l, const PrimeConst& P) {
+  constexpr int N1 = 1 << LOGN1;
+#pragma unroll
+  for (int e = 0; e < 16; ++e) s[l + 16 * e + e] = x[e];
+  __syncwarp();
+#pragma unroll
+  for (int e = 0; e < 16; ++e) x[e] = s[16 * l + e + l];
+  static_for<7, 3, -1>([&](auto LM) {
+    constexpr int lm = decltype(LM)::value;
+    constexpr int d = 256 >> (lm + 1);
+    gs_stage<16, d>(x,
+                    [&](int gi) { return ldtw(tw, (N1 + b) * (1 << lm) + ((16 * l + gi * 2 * d) >> (8 - lm))); },
+                    P.q, P.two_q);
+  });
+  __syncwarp();
+#pragma unroll
+  for (int e = 0; e < 16; ++e) s[16 * l + e + l] = x[e];
+  __syncwarp();
+#pragma unroll
+  for (int e = 0; e < 16; ++e) x[e] = s[l + 16 * e + e];
+  __syncwarp();
+  static_for<3, -1, -1>([&](auto LM) {
+    constexpr int lm = decltype(LM)::value;
+    gs_stage<16, (16 >> (lm + 1))>(x, [&](int gi) { return ldtw(tw, (N1 + b) * (1 << lm) + gi); },
+                                   P.q, P.two_q);
+  });
+}
+
 // Galois permutation inside one 256-element block. In bit-reversed evaluation
 // order the permutation maps every aligned output block onto exactly one
 // input block (the low 8 index bits only touch the top 8 exponent bits), so a
@@ -417,7 +449,8 @@ __global__ void __launch_bounds__(64, 8)
     modup_ip_blk(u32 B, const u64* __restrict__ mid, const u64* __restrict__ c1, u64 c1_stride,
                  const u32* __restrict__ perm, const u64* __restrict__ key,
                  const u64* __restrict__ key_shoup, u32 full, u64* __restrict__ acc,
-                 const ulonglong2* __restrict__ tw_all, const PrimeConst* __restrict__ primes,
+                 u64* __restrict__ sp_out, const ulonglong2* __restrict__ tw_all,
+                 const ulonglong2* __restrict__ itw_all, const PrimeConst* __restrict__ primes,
                  u32 logn) {
   constexpr int N1 = 1 << LOGN1;
   __shared__ u64 sm[4][256 + 16];
@@ -428,8 +461,11 @@ __global__ void __launch_bounds__(64, 8)
   // (target row, block): the key words they share are served from L1
   const u32 bq_count = (B + 3) >> 2;
   const u32 bq = blockIdx.x % bq_count;
-  const u32 tb = blockIdx.x / bq_count;  // = t * N1 + blk
-  const u32 t = tb / N1, blk = tb - t * N1;
+  const u32 tb = blockIdx.x / bq_count;  // = t_order * N1 + blk
+  const u32 t_order = tb / N1, blk = tb - t_order * N1;
+  // the special target (t = M) carries the extra inverse block stages: it is
+  // scheduled first so the longer CTAs do not form the tail of the grid
+  const u32 t = t_order == 0 ? (u32)M : t_order - 1;
   const u32 bi_raw = bq * 4 + bw;
   const bool live = bi_raw < B;
   const u32 bi = live ? bi_raw : B - 1;
@@ -483,6 +519,26 @@ __global__ void __launch_bounds__(64, 8)
       s1acc[si] = j ? s1acc[si] + p1 : p1;
     }
   }
+  if (t == (u32)M && sp_out) {
+    // ModDown starts with iNTT of this special row: run its block stages here
+    // (the group holds the whole block) and hand the column pass its input
+    // [B][2][N] directly; the evaluation-domain special row is never stored.
+    const ulonglong2* itw = itw_all + (u64)pi * n;
+#pragma unroll 1
+    for (int xh = 0; xh < 2; ++xh) {
+      u64 y[16];
+#pragma unroll
+      for (int e = 0; e < 16; ++e) y[e] = reduce62(sacc[bw][xh][l + 16 * e], P.q, P.mu62);
+      blk_inv_body<LOGN1>(y, sm[bw], itw, blk, l, P);
+      if (live) {
+        u64* o = sp_out + ((u64)bi * 2 + xh) * n + (blk << 8);
+#pragma unroll
+        for (int e = 0; e < 16; ++e) o[l + 16 * e] = y[e];
+      }
+      __syncwarp();
+    }
+    return;
+  }
   if (!live) return;
   u64* o0 = acc + ((u64)bi * 2 * (M + 1) + t) * n;
   u64* o1 = o0 + (u64)(M + 1) * n;
@@ -511,31 +567,10 @@ __global__ void __launch_bounds__(64)
   const PrimeConst P = primes[pi];
   const ulonglong2* tw = itw_all + (u64)pi * n;
   const u64* src = row_ptr(in, r) + (b << 8);
-  u64* s = sm[bw];
   u64 x[16];
 #pragma unroll
-  for (int e = 0; e < 16; ++e) s[l + 16 * e + e] = src[l + 16 * e];
-  __syncwarp();
-#pragma unroll
-  for (int e = 0; e < 16; ++e) x[e] = s[16 * l + e + l];
-  static_for<7, 3, -1>([&](auto LM) {
-    constexpr int lm = decltype(LM)::value;
-    constexpr int d = 256 >> (lm + 1);
-    gs_stage<16, d>(x,
-                    [&](int gi) { return ldtw(tw, (N1 + b) * (1 << lm) + ((16 * l + gi * 2 * d) >> (8 - lm))); },
-                    P.q, P.two_q);
-  });
-  __syncwarp();
-#pragma unroll
-  for (int e = 0; e < 16; ++e) s[16 * l + e + l] = x[e];
-  __syncwarp();
-#pragma unroll
-  for (int e = 0; e < 16; ++e) x[e] = s[l + 16 * e + e];
-  static_for<3, -1, -1>([&](auto LM) {
-    constexpr int lm = decltype(LM)::value;
-    gs_stage<16, (16 >> (lm + 1))>(x, [&](int gi) { return ldtw(tw, (N1 + b) * (1 << lm) + gi); },
-                                   P.q, P.two_q);
-  });
+  for (int e = 0; e < 16; ++e) x[e] = src[l + 16 * e];
+  blk_inv_body<LOGN1>(x, sm[bw], tw, b, l, P);
   u64* dst = row_ptr(out, r) + (b << 8);
 #pragma unroll
   for (int e = 0; e < 16; ++e) dst[l + 16 * e] = x[e];
@@ -591,6 +626,103 @@ __global__ void __launch_bounds__(16 * ((1 << LOGN1) / E))
   }
 #pragma unroll
   for (int e = 0; e < E; ++e) row(j + (k + R * e) * n2, x[e]);
+}
+
+// ------------------------------------------------------------ fused column pass
+// Inverse column pass of one source row + centred lift + forward column pass
+// of each of its `fan` destination rows (ModUp digits, ModDown / rescale
+// lifts). The inverse pass ends with thread (c, k) holding rows k + R e of
+// its column -- exactly the layout the forward pass starts from -- so the
+// coefficient-domain row never leaves registers: one kernel replaces the
+// inverse column pass, its HBM round trip and the lift's fan-out re-reads.
+//   src: rows after the inverse block pass (ntt_blk_inv), prime = source prime
+//   dst: destination rows, dst row = src_row * fan + f, prime from dst.prime_of
+template <int LOGN1, int E>
+__global__ void __launch_bounds__(16 * ((1 << LOGN1) / E))
+    ntt_col_inv_lift_fwd(const __grid_constant__ RowMap src, const __grid_constant__ RowMap dst,
+                         u32 fan, const ulonglong2* __restrict__ tw_all,
+                         const ulonglong2* __restrict__ itw_all,
+                         const PrimeConst* __restrict__ primes, const u64* __restrict__ smod,
+                         u32 nprimes, u32 logn) {
+  constexpr int N1 = 1 << LOGN1;
+  constexpr int R = N1 / E;
+  constexpr int LOGE = __builtin_ctz(E);
+  extern __shared__ u64 sm[];  // [N1][16]
+  const u32 n = 1u << logn;
+  const u32 n2 = n >> LOGN1;
+  const u32 groups = n2 >> 4;
+  const u32 rs = blockIdx.x / groups;
+  const u32 g = blockIdx.x - rs * groups;
+  const u32 c = threadIdx.x & 15, k = threadIdx.x >> 4;
+  const u32 j = (g << 4) + c;
+  const u32 ps = row_prime(src, rs);
+  u64 v[E];  // coefficient-domain source values, rows k + R e
+  {
+    const PrimeConst S = primes[ps];
+    const ulonglong2* itw = itw_all + (u64)ps * n;
+    const u64* in = row_ptr(src, rs);
+#pragma unroll
+    for (int e = 0; e < E; ++e) v[e] = in[j + (k * E + e) * n2];
+    static_for<LOGN1 - 1, LOGE - 1, -1>([&](auto LM) {
+      constexpr int lm = decltype(LM)::value;
+      constexpr int d = N1 >> (lm + 1);
+      gs_stage<E, d>(v, [&](int gi) { return ldtw(itw, (1 << lm) + ((k * E + gi * 2 * d) >> (LOGN1 - lm))); },
+                     S.q, S.two_q);
+    });
+#pragma unroll
+    for (int e = 0; e < E; ++e) sm[(k * E + e) * 16 + c] = v[e];
+    __syncthreads();
+#pragma unroll
+    for (int e = 0; e < E; ++e) v[e] = sm[(k + R * e) * 16 + c];
+    static_for<LOGE - 1, 0, -1>([&](auto LM) {
+      constexpr int lm = decltype(LM)::value;
+      gs_stage<E, (E >> (lm + 1))>(v, [&](int gi) { return ldtw(itw, (1 << lm) + gi); }, S.q, S.two_q);
+    });
+#pragma unroll
+    for (int e = 0; e < E / 2; ++e) {
+      const u64 a = v[e], bb = v[e + E / 2];
+      v[e] = mul_shoup(a + bb, S.n_inv, S.n_inv_shoup, S.q);
+      v[e + E / 2] = mul_shoup(a - bb + S.two_q, S.w1n, S.w1n_shoup, S.q);
+    }
+  }
+  const u64 qs_half = __ldg(&primes[ps].half);
+#pragma unroll 1
+  for (u32 f = 0; f < fan; ++f) {
+    const u32 rd = rs * fan + f;
+    const u32 pd = row_prime(dst, rd);
+    const PrimeConst P = primes[pd];
+    const ulonglong2* tw = tw_all + (u64)pd * n;
+    const u64 corr = P.q - __ldg(smod + ps * nprimes + pd);
+    u64 x[E];
+    // centred lift (rns.cpp:370-378) with the 32x32 Barrett of LiftLoad
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const u64 s = v[e];
+      const u64 qh = ((u64)(u32)(s >> 24) * P.mu56) >> 32;
+      u64 w = s - qh * P.q;
+      if (s > qs_half) w += corr;
+      x[e] = w;
+    }
+    static_for<0, LOGE, 1>([&](auto LM) {
+      constexpr int lm = decltype(LM)::value;
+      ct_stage<E, (E >> (lm + 1))>(x, [&](int gi) { return ldtw(tw, (1 << lm) + gi); }, P.q, P.two_q);
+    });
+    __syncthreads();  // the previous user of sm[] is done
+#pragma unroll
+    for (int e = 0; e < E; ++e) sm[(k + R * e) * 16 + c] = x[e];
+    __syncthreads();
+#pragma unroll
+    for (int e = 0; e < E; ++e) x[e] = sm[(k * E + e) * 16 + c];
+    static_for<LOGE, LOGN1, 1>([&](auto LM) {
+      constexpr int lm = decltype(LM)::value;
+      constexpr int d = N1 >> (lm + 1);
+      ct_stage<E, d>(x, [&](int gi) { return ldtw(tw, (1 << lm) + ((k * E + gi * 2 * d) >> (LOGN1 - lm))); },
+                     P.q, P.two_q);
+    });
+    u64* o = row_ptr(dst, rd);
+#pragma unroll
+    for (int e = 0; e < E; ++e) o[j + (k * E + e) * n2] = x[e];
+  }
 }
 
 // Single-CTA transform for small rings (N <= 4096): the whole row in shared
