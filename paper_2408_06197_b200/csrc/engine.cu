@@ -525,8 +525,8 @@ void modup_ip_launch(lcl_context* c, u32 B, const u64* mid, const u64* c1, u64 c
                rb * ((double)B * M * M + B * M + 4.0 * M * (M + 1) + 2.0 * B * (M + 1)),
                0.5 * c->N() * B * M * M * 8);
   modup_ip_blk<LOGN1, M><<<((B + 3) / 4) * (M + 1) * N1, 64, 0, c->stream>>>(
-      B, mid, c1, c1_stride, perm, key, key_shoup, c->full, acc, sp_out, c->d_tw, c->d_itw,
-      c->d_primes, c->logn);
+      B, mid, c1, c1_stride, perm, key, key_shoup, c->full, acc, c->d_tw, c->d_primes, c->logn);
+  (void)sp_out;
 }
 
 template <int LOGN1>
@@ -641,11 +641,10 @@ u64* ks_switch(lcl_context* c, const RowMap& in, const u64* c1, u64 c1_stride, u
   const RowMap mid_map = make_map(mid, m * m, N, (u64)m * m * N, 1, 0, dp);
   inv_lift_fwd_cols(c, B * m, in, mid_map, m);
   u64* acc = c->ws_acc.get((u64)B * 2 * (m + 1) * N);
-  // Running the special rows' inverse block stages inside modup_ip_blk
-  // (sp != nullptr, then ks_moddown(sp_ready = true)) measured slower on
-  // cfg2 (8.91 vs 8.77 ms): it lengthens the special-target CTAs by as much
-  // as the standalone ntt_blk_inv costs. Kept off.
-  u64* sp = kFuseSpecialInverse ? c->ws_coefsp.get((u64)B * 2 * N) : nullptr;
+  // Running the special rows' inverse block stages inside modup_ip_blk was
+  // measured slower on cfg2 (8.91 vs 8.77 ms): it lengthens the
+  // special-target CTAs by as much as the standalone ntt_blk_inv costs.
+  u64* sp = nullptr;
   dispatch_logn(c, [&](auto L1, auto) {
     modup_ip_n<decltype(L1)::value>(c, B, m, mid, c1, c1_stride, perm, key, key_shoup, acc, sp);
   });
@@ -830,34 +829,27 @@ void ensure_pairs(lcl_context* c, u32 n) {
 
 constexpr int kStages = 3;
 
-template <int PP>
-void pair_accumulate_pp(lcl_context* c, const u64* clients, u32 n, u32 chunks, u32 c0, u32 c1,
-                        u32 p0, u32 p1, u64* tern, bool accumulate, u32 warps) {
-  const u32 m = c->full;
-  const u32 pairs = p1 - p0;
-  const u32 per_cta = warps * PP;
-  dim3 grid((u32)(m * c->n / 32), (pairs + per_cta - 1) / per_cta);
-  const size_t smem = (size_t)kStages * n * 64 * 8;
-  need(smem <= 200 * 1024, LCL_SHAPE_ERROR, "too many clients for one tile");
-  allow_smem(pair_accumulate<PP, kStages>, smem);
-  ProfScope ps(c, "pair_accumulate",
-               8.0 * c->N() * m * (2.0 * n * (c1 - c0) + 3.0 * pairs * (accumulate ? 2 : 1)));
-  pair_accumulate<PP, kStages><<<grid, warps * 32, smem, c->stream>>>(
-      clients, n, c0, c1, chunks, m, c->logn, c->d_pairs, p0, p1, tern, accumulate ? 1 : 0,
-      c->d_primes);
-  post_launch(c);
-}
-
-// Lazy ternary accumulators for pairs [p0, p1) over chunks [c0, c1). Up to
-// 48 pairs share one CTA (each client tile read once); larger matrices split
-// into groups of 16 pairs per CTA.
+// Lazy ternary accumulators for pairs [p0, p1) over chunks [c0, c1). Tiles of
+// 8 slots, 4 threads per pair (2 slots each), up to 256 pairs per CTA: each
+// client word is read from HBM once per pair group.
 void pair_accumulate_launch(lcl_context* c, const u64* clients, u32 n, u32 chunks, u32 c0,
                             u32 c1, u32 p0, u32 p1, u64* tern, bool accumulate) {
-  if (p1 - p0 <= 48)
-    pair_accumulate_pp<6>(c, clients, n, chunks, c0, c1, p0, p1, tern, accumulate,
-                          (p1 - p0 + 5) / 6);
-  else
-    pair_accumulate_pp<4>(c, clients, n, chunks, c0, c1, p0, p1, tern, accumulate, 4);
+  constexpr int TE = 8, EPT = 2, TPP = TE / EPT;
+  const u32 m = c->full;
+  const u32 pairs = p1 - p0;
+  const u32 groups = (pairs + 255) / 256;
+  const u32 per_cta = (pairs + groups - 1) / groups;
+  const u32 threads = ((per_cta * TPP + 31) / 32) * 32;
+  dim3 grid((u32)(m * c->n / TE), groups);
+  const size_t smem = (size_t)kStages * n * (2 * TE + 1) * 8;
+  need(smem <= 200 * 1024, LCL_SHAPE_ERROR, "too many clients for one tile");
+  allow_smem(pair_accumulate<TE, EPT, kStages>, smem);
+  ProfScope ps(c, "pair_accumulate",
+               8.0 * c->N() * m * (2.0 * n * (c1 - c0) * groups + 3.0 * pairs * (accumulate ? 2 : 1)));
+  pair_accumulate<TE, EPT, kStages><<<grid, threads, smem, c->stream>>>(
+      clients, n, c0, c1, chunks, m, c->logn, c->d_pairs, p0, p1, per_cta, tern,
+      accumulate ? 1 : 0, c->d_primes);
+  post_launch(c);
 }
 
 void hadd_into(lcl_context* c, u64* acc, const u64* x, u32 B, u32 m) {

@@ -29,47 +29,49 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(K));
 }
 
-template <int PP, int STAGES>
-__global__ void __launch_bounds__(256)
+// Tile = TE consecutive slots of one limb row r for a group of up to
+// 1024 / (TE / EPT) pairs; thread (pair, eg) owns EPT slots of one pair. Every
+// client word of the tile is streamed into shared memory once per pair group
+// (3-stage cp.async ring) and read by all pairs in it, so for up to 256 pairs
+// the client data crosses HBM exactly once.
+template <int TE, int EPT, int STAGES>
+__global__ void __launch_bounds__(1024)
     pair_accumulate(const u64* __restrict__ clients, u32 n, u32 c_begin, u32 c_end,
                     u32 chunks_total, u32 m, u32 logn, const u32* __restrict__ pairs,
-                    u32 p_begin, u32 p_end, u64* __restrict__ tern, int accumulate,
-                    const PrimeConst* __restrict__ primes) {
-  extern __shared__ u64 tile[];  // [STAGES][n][2][32]
+                    u32 p_begin, u32 p_end, u32 pairs_per_cta, u64* __restrict__ tern,
+                    int accumulate, const PrimeConst* __restrict__ primes) {
+  constexpr int TPP = TE / EPT;   // threads per pair
+  constexpr int CS = 2 * TE + 1;  // words per client in the tile (+1: bank spread)
+  extern __shared__ u64 tile[];   // [STAGES][n][CS]
   const u32 N = 1u << logn;
-  const u32 tiles_per_row = N >> 5;
+  const u32 tiles_per_row = N / TE;
   const u32 r = blockIdx.x / tiles_per_row;
-  const u32 a0 = (blockIdx.x - r * tiles_per_row) << 5;
-  const u32 lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const u32 nwarps = blockDim.x >> 5;
+  const u32 a0 = (blockIdx.x - r * tiles_per_row) * TE;
   const PrimeConst P = primes[r];
   const u64 q = P.q;
   const u64 ct_words = 2ull * m * N;
-  const u32 tw = n * 64;
-  const u32 pbase = p_begin + (blockIdx.y * nwarps + warp) * PP;
+  const u32 tw = n * CS;
+  const u32 p = p_begin + blockIdx.y * pairs_per_cta + threadIdx.x / TPP;
+  const u32 eg = threadIdx.x % TPP;
+  const bool valid = threadIdx.x / TPP < pairs_per_cta && p < p_end;
+  const u32 pk = valid ? __ldg(pairs + p) : 0u;
+  const u32 oi = (pk & 0xFFFFu) * CS + eg * EPT, oj = (pk >> 16) * CS + eg * EPT;
 
   auto issue = [&](u32 c, u32 stage) {
     if (c < c_end) {
-      for (u32 v = threadIdx.x; v < tw; v += blockDim.x) {
-        const u32 cl = v >> 6, h = (v >> 5) & 1, e = v & 31;
-        cp_async8(tile + stage * tw + v, clients + ((u64)cl * chunks_total + c) * ct_words +
-                                             (u64)h * m * N + (u64)r * N + a0 + e);
+      for (u32 v = threadIdx.x; v < n * 2 * TE; v += blockDim.x) {
+        const u32 cl = v / (2 * TE), w = v - cl * 2 * TE, h = w / TE, e = w - h * TE;
+        cp_async8(tile + stage * tw + cl * CS + w,
+                  clients + ((u64)cl * chunks_total + c) * ct_words + (u64)h * m * N +
+                      (u64)r * N + a0 + e);
       }
     }
     cp_async_commit();  // empty groups keep the wait count uniform
   };
 
-  u32 pi[PP], pj[PP];
+  Acc3 A00[EPT], A01[EPT], A11[EPT];
 #pragma unroll
-  for (int t = 0; t < PP; ++t) {
-    const u32 p = pbase + t;
-    const u32 pk = p < p_end ? __ldg(pairs + p) : 0u;
-    pi[t] = (pk & 0xFFFFu) * 64;
-    pj[t] = (pk >> 16) * 64;
-  }
-  Acc3 A00[PP], A01[PP], A11[PP];
-#pragma unroll
-  for (int t = 0; t < PP; ++t) {
+  for (int t = 0; t < EPT; ++t) {
     A00[t].zero();
     A01[t].zero();
     A11[t].zero();
@@ -83,9 +85,9 @@ __global__ void __launch_bounds__(256)
     __syncthreads();
     const u64* tl = tile + stage * tw;
 #pragma unroll
-    for (int t = 0; t < PP; ++t) {
-      const u64 x0 = tl[pi[t] + lane], x1 = tl[pi[t] + 32 + lane];
-      const u64 y0 = tl[pj[t] + lane], y1 = tl[pj[t] + 32 + lane];
+    for (int t = 0; t < EPT; ++t) {
+      const u64 x0 = tl[oi + t], x1 = tl[oi + TE + t];
+      const u64 y0 = tl[oj + t], y1 = tl[oj + TE + t];
       const Split e0 = split23(x0 - y0 + q), e1 = split23(x1 - y1 + q);
       A00[t].sq(e0);
       A01[t].mac(e0, e1);
@@ -94,11 +96,10 @@ __global__ void __launch_bounds__(256)
     __syncthreads();
     stage = (stage + 1) % STAGES;
   }
+  if (!valid) return;
 #pragma unroll
-  for (int t = 0; t < PP; ++t) {
-    const u32 p = pbase + t;
-    if (p >= p_end) break;
-    u64* o = tern + (u64)(p - p_begin) * 3 * m * N + (u64)r * N + a0 + lane;
+  for (int t = 0; t < EPT; ++t) {
+    u64* o = tern + (u64)(p - p_begin) * 3 * m * N + (u64)r * N + a0 + eg * EPT + t;
     u64 d0 = A00[t].reduce(P);
     u64 d1 = A01[t].reduce(P);
     d1 = add_mod(d1, d1, q);

@@ -449,8 +449,7 @@ __global__ void __launch_bounds__(64, 8)
     modup_ip_blk(u32 B, const u64* __restrict__ mid, const u64* __restrict__ c1, u64 c1_stride,
                  const u32* __restrict__ perm, const u64* __restrict__ key,
                  const u64* __restrict__ key_shoup, u32 full, u64* __restrict__ acc,
-                 u64* __restrict__ sp_out, const ulonglong2* __restrict__ tw_all,
-                 const ulonglong2* __restrict__ itw_all, const PrimeConst* __restrict__ primes,
+                 const ulonglong2* __restrict__ tw_all, const PrimeConst* __restrict__ primes,
                  u32 logn) {
   constexpr int N1 = 1 << LOGN1;
   __shared__ u64 sm[4][256 + 16];
@@ -461,11 +460,8 @@ __global__ void __launch_bounds__(64, 8)
   // (target row, block): the key words they share are served from L1
   const u32 bq_count = (B + 3) >> 2;
   const u32 bq = blockIdx.x % bq_count;
-  const u32 tb = blockIdx.x / bq_count;  // = t_order * N1 + blk
-  const u32 t_order = tb / N1, blk = tb - t_order * N1;
-  // the special target (t = M) carries the extra inverse block stages: it is
-  // scheduled first so the longer CTAs do not form the tail of the grid
-  const u32 t = t_order == 0 ? (u32)M : t_order - 1;
+  const u32 tb = blockIdx.x / bq_count;  // = t * N1 + blk
+  const u32 t = tb / N1, blk = tb - t * N1;
   const u32 bi_raw = bq * 4 + bw;
   const bool live = bi_raw < B;
   const u32 bi = live ? bi_raw : B - 1;
@@ -518,26 +514,6 @@ __global__ void __launch_bounds__(64, 8)
       s0acc[si] = j ? s0acc[si] + p0 : p0;
       s1acc[si] = j ? s1acc[si] + p1 : p1;
     }
-  }
-  if (t == (u32)M && sp_out) {
-    // ModDown starts with iNTT of this special row: run its block stages here
-    // (the group holds the whole block) and hand the column pass its input
-    // [B][2][N] directly; the evaluation-domain special row is never stored.
-    const ulonglong2* itw = itw_all + (u64)pi * n;
-#pragma unroll 1
-    for (int xh = 0; xh < 2; ++xh) {
-      u64 y[16];
-#pragma unroll
-      for (int e = 0; e < 16; ++e) y[e] = reduce62(sacc[bw][xh][l + 16 * e], P.q, P.mu62);
-      blk_inv_body<LOGN1>(y, sm[bw], itw, blk, l, P);
-      if (live) {
-        u64* o = sp_out + ((u64)bi * 2 + xh) * n + (blk << 8);
-#pragma unroll
-        for (int e = 0; e < 16; ++e) o[l + 16 * e] = y[e];
-      }
-      __syncwarp();
-    }
-    return;
   }
   if (!live) return;
   u64* o0 = acc + ((u64)bi * 2 * (M + 1) + t) * n;
