@@ -830,18 +830,19 @@ void ensure_pairs(lcl_context* c, u32 n) {
 constexpr int kStages = 3;
 
 // Lazy ternary accumulators for pairs [p0, p1) over chunks [c0, c1). Tiles of
-// 8 slots, 4 threads per pair (2 slots each), up to 256 pairs per CTA: each
+// 8 slots, 2 threads per pair (4 slots each), up to 256 pairs per CTA: each
 // client word is read from HBM once per pair group.
 void pair_accumulate_launch(lcl_context* c, const u64* clients, u32 n, u32 chunks, u32 c0,
                             u32 c1, u32 p0, u32 p1, u64* tern, bool accumulate) {
-  constexpr int TE = 8, EPT = 2, TPP = TE / EPT;
+  constexpr int TE = 8, EPT = 4, TPP = TE / EPT;
   const u32 m = c->full;
   const u32 pairs = p1 - p0;
   const u32 groups = (pairs + 255) / 256;
   const u32 per_cta = (pairs + groups - 1) / groups;
-  const u32 threads = ((per_cta * TPP + 31) / 32) * 32;
+  const u32 threads = std::max<u32>(64, ((per_cta * TPP + 31) / 32) * 32);
+  need(n * TE <= 4 * threads, LCL_SHAPE_ERROR, "too many clients for one tile");
   dim3 grid((u32)(m * c->n / TE), groups);
-  const size_t smem = (size_t)kStages * n * (2 * TE + 1) * 8;
+  const size_t smem = (size_t)kStages * n * (2 * TE + 2) * 8;
   need(smem <= 200 * 1024, LCL_SHAPE_ERROR, "too many clients for one tile");
   allow_smem(pair_accumulate<TE, EPT, kStages>, smem);
   ProfScope ps(c, "pair_accumulate",

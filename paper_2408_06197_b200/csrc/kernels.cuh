@@ -29,20 +29,27 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(K));
 }
 
-// Tile = TE consecutive slots of one limb row r for a group of up to
-// 1024 / (TE / EPT) pairs; thread (pair, eg) owns EPT slots of one pair. Every
-// client word of the tile is streamed into shared memory once per pair group
-// (3-stage cp.async ring) and read by all pairs in it, so for up to 256 pairs
-// the client data crosses HBM exactly once.
+// Tile = TE consecutive slots of one limb row r for a group of pairs; thread
+// (pair, eg) owns EPT slots of one pair. Every client word of the tile is
+// streamed into shared memory once per pair group (16-byte cp.async, STAGES
+// deep; load addresses computed once) and read by all pairs in it, so for up
+// to 256 pairs the client data crosses HBM exactly once.
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const u32 s = (u32)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+
 template <int TE, int EPT, int STAGES>
-__global__ void __launch_bounds__(1024)
+__global__ void __launch_bounds__(512)
     pair_accumulate(const u64* __restrict__ clients, u32 n, u32 c_begin, u32 c_end,
                     u32 chunks_total, u32 m, u32 logn, const u32* __restrict__ pairs,
                     u32 p_begin, u32 p_end, u32 pairs_per_cta, u64* __restrict__ tern,
                     int accumulate, const PrimeConst* __restrict__ primes) {
-  constexpr int TPP = TE / EPT;   // threads per pair
-  constexpr int CS = 2 * TE + 1;  // words per client in the tile (+1: bank spread)
-  extern __shared__ u64 tile[];   // [STAGES][n][CS]
+  constexpr int TPP = TE / EPT;    // threads per pair
+  constexpr int CS = 2 * TE + 2;   // words per client in the tile (16-B aligned, banks spread)
+  constexpr int V = 2 * TE / 2;    // 16-byte vectors per client per chunk
+  constexpr int MAXV = 4;          // vectors per thread (n * V <= MAXV * blockDim)
+  extern __shared__ u64 tile[];    // [STAGES][n][CS]
   const u32 N = 1u << logn;
   const u32 tiles_per_row = N / TE;
   const u32 r = blockIdx.x / tiles_per_row;
@@ -57,14 +64,27 @@ __global__ void __launch_bounds__(1024)
   const u32 pk = valid ? __ldg(pairs + p) : 0u;
   const u32 oi = (pk & 0xFFFFu) * CS + eg * EPT, oj = (pk >> 16) * CS + eg * EPT;
 
+  // this thread's 16-byte load slots: (global address at chunk 0, smem word)
+  const u64* gsrc[MAXV];
+  u32 soff[MAXV];
+  u32 nv = 0;
+#pragma unroll
+  for (int s = 0; s < MAXV; ++s) {
+    const u32 v = threadIdx.x + s * blockDim.x;
+    gsrc[s] = nullptr;
+    soff[s] = 0;
+    if (v < n * V) {
+      const u32 cl = v / V, w = (v - cl * V) * 2, h = w / TE, e = w - h * TE;
+      gsrc[s] = clients + (u64)cl * chunks_total * ct_words + (u64)h * m * N + (u64)r * N + a0 + e;
+      soff[s] = cl * CS + w;
+      nv = s + 1;
+    }
+  }
   auto issue = [&](u32 c, u32 stage) {
     if (c < c_end) {
-      for (u32 v = threadIdx.x; v < n * 2 * TE; v += blockDim.x) {
-        const u32 cl = v / (2 * TE), w = v - cl * 2 * TE, h = w / TE, e = w - h * TE;
-        cp_async8(tile + stage * tw + cl * CS + w,
-                  clients + ((u64)cl * chunks_total + c) * ct_words + (u64)h * m * N +
-                      (u64)r * N + a0 + e);
-      }
+#pragma unroll
+      for (int s = 0; s < MAXV; ++s)
+        if (s < (int)nv) cp_async16(tile + stage * tw + soff[s], gsrc[s] + (u64)c * ct_words);
     }
     cp_async_commit();  // empty groups keep the wait count uniform
   };
@@ -94,7 +114,7 @@ __global__ void __launch_bounds__(1024)
       A11[t].sq(e1);
     }
     __syncthreads();
-    stage = (stage + 1) % STAGES;
+    stage = stage + 1 == STAGES ? 0 : stage + 1;
   }
   if (!valid) return;
 #pragma unroll
