@@ -149,19 +149,24 @@ __device__ __forceinline__ Split split23(u64 x) {
 }
 __device__ __forceinline__ u64 wmul(u32 a, u32 b) { return (u64)a * (u64)b; }
 
+// acc += a * b with one IMAD.WIDE.U32 (64-bit accumulate form).
+__device__ __forceinline__ void madw(u64& acc, u32 a, u32 b) {
+  asm("mad.wide.u32 %0, %1, %2, %0;" : "+l"(acc) : "r"(a), "r"(b));
+}
+
 struct Acc3 {
   u64 s0, s1, s2;
   __device__ __forceinline__ void zero() { s0 = s1 = s2 = 0; }
   __device__ __forceinline__ void mac(Split x, Split y) {
-    s0 += wmul(x.lo, y.lo);
-    s1 += wmul(x.lo, y.hi);
-    s1 += wmul(x.hi, y.lo);
-    s2 += wmul(x.hi, y.hi);
+    madw(s0, x.lo, y.lo);
+    madw(s1, x.lo, y.hi);
+    madw(s1, x.hi, y.lo);
+    madw(s2, x.hi, y.hi);
   }
-  __device__ __forceinline__ void sq(Split x) {  // x^2 with the cross term halved
-    s0 += wmul(x.lo, x.lo);
-    s1 += wmul(x.lo, x.hi) << 1;
-    s2 += wmul(x.hi, x.hi);
+  __device__ __forceinline__ void sq(Split x) {  // x^2: the cross term as lo * (2 hi)
+    madw(s0, x.lo, x.lo);
+    madw(s1, x.lo, x.hi << 1);  // x.hi < 2^23, so 2 x.hi fits 32 bits
+    madw(s2, x.hi, x.hi);
   }
   // Fully reduced value mod q.
   __device__ __forceinline__ u64 reduce(const PrimeConst& p) const {

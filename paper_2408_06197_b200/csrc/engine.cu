@@ -960,7 +960,7 @@ void masked_aggregate(lcl_context* c, const u64* clients, const u64* sel, u32 n,
   for (u32 c0 = chunk_begin; c0 < cend; c0 += SB) {
     const u32 c1 = std::min(cend, c0 + SB), B = c1 - c0;
     u64* tern = c->ws_tern.get((u64)B * 3 * m * N);
-    constexpr int CK = 4;
+    constexpr int CK = 2;
     const u64 slots = (u64)m * N;
     const u64 threads = ((B + CK - 1) / CK) * slots;
     {

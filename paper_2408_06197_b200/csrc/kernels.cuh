@@ -164,20 +164,44 @@ __global__ void __launch_bounds__(256)
     D1[k].zero();
     D2[k].zero();
   }
+  const u64* sp = sel + (u64)r * N + a;
+  const u64* wp = clients + (u64)(c_begin + c0) * ct_words + (u64)r * N + a;
+  const u64 client_stride = (u64)chunks_total * ct_words;
+  // operands of client i + 1 are loaded while client i is accumulated
+  u64 s0 = __ldg(sp), s1 = __ldg(sp + slots);
+  u64 w0[CK], w1[CK];
+#pragma unroll
+  for (int k = 0; k < CK; ++k) {
+    const bool ok = c0 + k < chunks;
+    w0[k] = ok ? __ldg(wp + k * ct_words) : 0;
+    w1[k] = ok ? __ldg(wp + k * ct_words + slots) : 0;
+  }
   for (u32 i = 0; i < n; ++i) {
-    const u64* s = sel + (u64)i * ct_words + (u64)r * N + a;
-    const u64 s0 = __ldg(s), s1 = __ldg(s + slots);
-    const Split S0 = split23(s0), S1 = split23(s1), SS = split23(s0 + s1);
+    const u64 cs0 = s0, cs1 = s1;
+    u64 cw0[CK], cw1[CK];
 #pragma unroll
     for (int k = 0; k < CK; ++k) {
-      if (c0 + k < chunks) {
-        const u64* w =
-            clients + ((u64)i * chunks_total + c_begin + c0 + k) * ct_words + (u64)r * N + a;
-        const u64 w0 = __ldg(w), w1 = __ldg(w + slots);
-        D0[k].mac(split23(w0), S0);
-        D2[k].mac(split23(w1), S1);
-        D1[k].mac(split23(w0 + w1), SS);
+      cw0[k] = w0[k];
+      cw1[k] = w1[k];
+    }
+    if (i + 1 < n) {
+      sp += ct_words;
+      wp += client_stride;
+      s0 = __ldg(sp);
+      s1 = __ldg(sp + slots);
+#pragma unroll
+      for (int k = 0; k < CK; ++k) {
+        const bool ok = c0 + k < chunks;
+        w0[k] = ok ? __ldg(wp + k * ct_words) : 0;
+        w1[k] = ok ? __ldg(wp + k * ct_words + slots) : 0;
       }
+    }
+    const Split S0 = split23(cs0), S1 = split23(cs1), SS = split23(cs0 + cs1);
+#pragma unroll
+    for (int k = 0; k < CK; ++k) {
+      D0[k].mac(split23(cw0[k]), S0);
+      D2[k].mac(split23(cw1[k]), S1);
+      D1[k].mac(split23(cw0[k] + cw1[k]), SS);
     }
   }
 #pragma unroll
