@@ -27,6 +27,23 @@ struct PrimeConst {
   u64 w1n, w1n_shoup;      // iroot[1] * N^-1: last inverse stage with the scaling folded in
   u32 mu56;                // floor(2^56 / q): 32x32 Barrett quotient for lifts (v < 2^55)
   u32 mu62;                // floor(2^62 / q): reduce62 for lazy NTT outputs (x < 2^62)
+  // FP64-pipe companions (used only for primes below 2^46, see "FP64 residue
+  // arithmetic" below): q, 1/q, and (w, w/q) for the N^-1 scalings.
+  double qf, qinvf;
+  double ninvf, ninvq;
+  double w1nf, w1nq;
+};
+
+// Twiddle / constant tables of a context, passed by value to every NTT kernel.
+// fp_mask bit p set: rows of prime p run their butterflies on the FP64 pipe.
+struct NttTabs {
+  const ulonglong2* tw;   // (psi^brv, Shoup) per prime
+  const ulonglong2* itw;  // inverse table
+  const double2* twf;     // (psi^brv, psi^brv / q) as doubles
+  const double2* itwf;
+  const PrimeConst* primes;
+  u32 fp_mask;
+  u32 logn;
 };
 
 // Row addressing for batched transforms. Row r of a launch is row
@@ -100,6 +117,50 @@ __device__ __forceinline__ u64 reduce62(u64 x, u64 q, u32 mu62) {
   u64 r = x - (u64)qh * q;
   r = r >= q ? r - q : r;
   return r >= q ? r - q : r;
+}
+
+// ------------------------------------------------ FP64 residue arithmetic
+// B200 keeps a full-rate FP64 pipe (64 DFMA/clk/SM, measured) beside the
+// integer pipes, and an FP64 butterfly on integer-valued doubles retires 2.3x
+// faster than the 64-bit integer (Shoup) butterfly
+// (tools/microbench/fp64_pipe.cu). For a prime q < 2^46 a residue is held as
+// an exact integer-valued double in signed lazy form; every operation below
+// is exact (no rounding ever reaches the integer result), so the fully
+// reduced outputs are the reference's words.
+constexpr double kMagic = 6755399441055744.0;  // 1.5 * 2^52: round-to-integer bias
+constexpr double kTwo52 = 4503599627370496.0;
+constexpr long long kMagicBits = 0x4338000000000000ll;
+
+// y * w mod q in signed lazy form, |result| <= 0.75 q, for integers |y| <= 2^51,
+// 0 <= w < q < 2^46 and wq = fl(w / q). ph + pl = y*w exactly (FMA two-product);
+// qt = round(y * wq) is within 0.75 of y*w/q, so ph - qt*q and the final sum
+// are integers below 2^47 and both roundings are exact.
+__device__ __forceinline__ double f_mulmod(double y, double w, double wq, double q) {
+  const double ph = __dmul_rn(y, w);
+  const double pl = __fma_rn(y, w, -ph);
+  const double qt = __dadd_rn(__fma_rn(y, wq, kMagic), -kMagic);
+  return __dadd_rn(__fma_rn(-qt, q, ph), pl);
+}
+// x - q * round(x / q) for an integer |x| <= 2^51: |result| <= 0.75 q. For
+// |x| <= 0.75 q the quotient is exact and the result is the centred residue in
+// [-(q-1)/2, (q-1)/2] (q odd: no ties) -- the reference's centred lift
+// (rns.cpp:370-378, v > q/2 means v - q).
+__device__ __forceinline__ double f_reduce(double x, double q, double qinv) {
+  const double qt = __dadd_rn(__fma_rn(x, qinv, kMagic), -kMagic);
+  return __fma_rn(-qt, q, x);
+}
+// u64 x < 2^52 -> exact double.
+__device__ __forceinline__ double u2d(u64 x) {
+  return __dadd_rn(__longlong_as_double((long long)(x | 0x4330000000000000ull)), -kTwo52);
+}
+// integer-valued |r| < 2^51 -> int64.
+__device__ __forceinline__ long long d2ll(double r) {
+  return __double_as_longlong(__dadd_rn(r, kMagic)) - kMagicBits;
+}
+// lazy |x| <= 2^51 -> fully reduced u64 in [0, q).
+__device__ __forceinline__ u64 d_canon(double x, double q, double qinv, u64 qi) {
+  const long long i = d2ll(f_reduce(x, q, qinv));
+  return (u64)(i + ((i >> 63) & (long long)qi));
 }
 
 // Exact reduction of the 128-bit value (hi, lo) mod q (modmath.hpp:62-73).

@@ -17,6 +17,7 @@
 #include <cmath>
 #include <complex>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -250,6 +251,9 @@ struct lcl_context {
   PrimeConst* d_primes = nullptr;
   ulonglong2* d_tw = nullptr;
   ulonglong2* d_itw = nullptr;
+  double2* d_twf = nullptr;   // (w, w / q) doubles for FP64 rows
+  double2* d_itwf = nullptr;
+  u32 fp_mask = 0;            // primes whose rows run on the FP64 pipe
   u64* d_smod = nullptr;
   ulonglong2* d_pinv = nullptr;  // [(full+1) * (full+1)]: (q_div^-1 mod q_dst, shoup)
   u32* d_pairs = nullptr;
@@ -281,6 +285,18 @@ struct lcl_context {
 namespace {
 
 void count_launch(lcl_context* c, u64 k = 1) { c->launches += k; }
+
+NttTabs tabs(const lcl_context* c) {
+  NttTabs t;
+  t.tw = c->d_tw;
+  t.itw = c->d_itw;
+  t.twf = c->d_twf;
+  t.itwf = c->d_itwf;
+  t.primes = c->d_primes;
+  t.fp_mask = c->fp_mask;
+  t.logn = (u32)c->logn;
+  return t;
+}
 
 void post_launch(lcl_context* c, u64 k = 1) {
   count_launch(c, k);
@@ -352,15 +368,13 @@ void fwd2(lcl_context* c, u32 rows, const RowMap& mid, const Loader& ld, const E
   {
     ProfScope ps(c, std::is_same<Loader, PlainLoad>::value ? "ntt_col_fwd" : "ntt_col_fwd<lift>",
                  rb * (load_rows(ld, rows) + rows), bpr * rows * LOGN1);
-    ntt_col_fwd<LOGN1, E, Loader><<<rows * groups, 16 * (N1 / E), smem, c->stream>>>(
-        mid, ld, c->d_tw, c->d_primes, c->logn);
+    ntt_col_fwd<LOGN1, E, Loader><<<rows * groups, 16 * (N1 / E), smem, c->stream>>>(mid, ld, tabs(c));
   }
   {
     ProfScope ps(c, std::is_same<Epi, DivRoundStore>::value ? "ntt_blk_fwd<divround>" : "ntt_blk_fwd",
                  rb * (store_rows(epi, rows) + (std::is_same<Epi, PlainStore>::value ? rows : 0)),
                  bpr * rows * 8);
-    ntt_blk_fwd<LOGN1, Epi><<<rows * N1 / 4, 64, 0, c->stream>>>(mid, epi, c->d_tw, c->d_primes,
-                                                                 c->logn);
+    ntt_blk_fwd<LOGN1, Epi><<<rows * N1 / 4, 64, 0, c->stream>>>(mid, epi, tabs(c));
   }
   post_launch(c, 2);
 }
@@ -376,13 +390,11 @@ void inv2(lcl_context* c, u32 rows, const RowMap& in, const RowMap& mid, const E
   const double bpr = 0.5 * c->N();
   {
     ProfScope ps(c, "ntt_blk_inv", rb * 2.0 * rows, bpr * rows * 8);
-    ntt_blk_inv<LOGN1><<<rows * N1 / 4, 64, 0, c->stream>>>(in, mid, c->d_itw, c->d_primes,
-                                                            c->logn);
+    ntt_blk_inv<LOGN1><<<rows * N1 / 4, 64, 0, c->stream>>>(in, mid, tabs(c));
   }
   {
     ProfScope ps(c, "ntt_col_inv", rb * 2.0 * rows, bpr * rows * LOGN1);
-    ntt_col_inv<LOGN1, E, Epi><<<rows * groups, 16 * (N1 / E), smem, c->stream>>>(
-        mid, epi, c->d_itw, c->d_primes, c->logn);
+    ntt_col_inv<LOGN1, E, Epi><<<rows * groups, 16 * (N1 / E), smem, c->stream>>>(mid, epi, tabs(c));
   }
   post_launch(c, 2);
 }
@@ -395,8 +407,7 @@ void launch_fwd(lcl_context* c, u32 rows, const RowMap& pm, const Loader& ld, co
   if (c->logn <= 12) {
     ProfScope ps(c, "ntt_small_fwd", 8.0 * c->N() * (load_rows(ld, rows) + store_rows(epi, rows)),
                  0.5 * c->N() * rows * c->logn);
-    ntt_small<false, Loader, Epi><<<rows, 256, c->n * 8, c->stream>>>(ld, epi, pm, c->d_tw,
-                                                                     c->d_primes, c->logn);
+    ntt_small<false, Loader, Epi><<<rows, 256, c->n * 8, c->stream>>>(ld, epi, pm, tabs(c));
     post_launch(c);
     return;
   }
@@ -416,7 +427,7 @@ template <int LOGN1>
 void blk_inv_n(lcl_context* c, u32 rows, const RowMap& in, const RowMap& out) {
   constexpr int N1 = 1 << LOGN1;
   ProfScope ps(c, "ntt_blk_inv", 16.0 * c->N() * rows, 0.5 * c->N() * rows * 8);
-  ntt_blk_inv<LOGN1><<<rows * N1 / 4, 64, 0, c->stream>>>(in, out, c->d_itw, c->d_primes, c->logn);
+  ntt_blk_inv<LOGN1><<<rows * N1 / 4, 64, 0, c->stream>>>(in, out, tabs(c));
 }
 
 template <int LOGN1, int E>
@@ -429,7 +440,7 @@ void col_ilf_n(lcl_context* c, u32 src_rows, const RowMap& src, const RowMap& ds
   ProfScope ps(c, "ntt_col_inv_lift_fwd", 8.0 * c->N() * (src_rows + (double)src_rows * fan),
                0.5 * c->N() * LOGN1 * (src_rows + (double)src_rows * fan));
   ntt_col_inv_lift_fwd<LOGN1, E><<<src_rows * groups, 16 * (N1 / E), smem, c->stream>>>(
-      src, dst, fan, c->d_tw, c->d_itw, c->d_primes, c->d_smod, c->P(), c->logn);
+      src, dst, fan, c->d_smod, c->P(), tabs(c));
 }
 
 template <int LOGN1, class Epi>
@@ -438,7 +449,7 @@ void blk_fwd_n(lcl_context* c, u32 rows, const RowMap& mid, const Epi& epi) {
   ProfScope ps(c, std::is_same<Epi, DivRoundStore>::value ? "ntt_blk_fwd<divround>" : "ntt_blk_fwd",
                8.0 * c->N() * (store_rows(epi, rows) + (std::is_same<Epi, PlainStore>::value ? rows : 0)),
                0.5 * c->N() * rows * 8);
-  ntt_blk_fwd<LOGN1, Epi><<<rows * N1 / 4, 64, 0, c->stream>>>(mid, epi, c->d_tw, c->d_primes, c->logn);
+  ntt_blk_fwd<LOGN1, Epi><<<rows * N1 / 4, 64, 0, c->stream>>>(mid, epi, tabs(c));
 }
 
 // Calls f(LOGN1, E) with compile-time constants for the two-pass ring sizes.
@@ -511,8 +522,7 @@ void col_only(lcl_context* c, u32 rows, const RowMap& out, const Loader& ld) {
   const u32 groups = (u32)(c->n >> LOGN1) >> 4;
   ProfScope ps(c, "ntt_col_fwd<lift>", 8.0 * c->N() * (load_rows(ld, rows) + rows),
                0.5 * c->N() * rows * LOGN1);
-  ntt_col_fwd<LOGN1, E, Loader><<<rows * groups, 16 * (N1 / E), smem, c->stream>>>(
-      out, ld, c->d_tw, c->d_primes, c->logn);
+  ntt_col_fwd<LOGN1, E, Loader><<<rows * groups, 16 * (N1 / E), smem, c->stream>>>(out, ld, tabs(c));
 }
 
 template <int LOGN1, int M>
@@ -525,7 +535,7 @@ void modup_ip_launch(lcl_context* c, u32 B, const u64* mid, const u64* c1, u64 c
                rb * ((double)B * M * M + B * M + 4.0 * M * (M + 1) + 2.0 * B * (M + 1)),
                0.5 * c->N() * B * M * M * 8);
   modup_ip_blk<LOGN1, M><<<((B + 3) / 4) * (M + 1) * N1, 64, 0, c->stream>>>(
-      B, mid, c1, c1_stride, perm, key, key_shoup, c->full, acc, c->d_tw, c->d_primes, c->logn);
+      B, mid, c1, c1_stride, perm, key, key_shoup, c->full, acc, tabs(c));
   (void)sp_out;
 }
 
@@ -549,8 +559,8 @@ void launch_inv(lcl_context* c, u32 rows, const RowMap& in, const Epi& epi) {
   if (rows == 0) return;
   if (c->logn <= 12) {
     ProfScope ps(c, "ntt_small_inv", 8.0 * c->N() * 2.0 * rows, 0.5 * c->N() * rows * c->logn);
-    ntt_small<true, PlainLoad, Epi><<<rows, 256, c->n * 8, c->stream>>>(
-        PlainLoad{in}, epi, in, c->d_itw, c->d_primes, c->logn);
+    ntt_small<true, PlainLoad, Epi><<<rows, 256, c->n * 8, c->stream>>>(PlainLoad{in}, epi, in,
+                                                                       tabs(c));
     post_launch(c);
     return;
   }
@@ -1012,6 +1022,25 @@ int guarded(F&& f) {
 }
 
 
+// Primes whose NTT rows run on the FP64 pipe (ntt.cuh FpF). Exactness needs
+// q < 2^46 and every operand of f_mulmod below 2^51: forward inputs are below
+// max(3q, q_s / 2) for the lift sources q_s of the same field, and 17 stages
+// add at most 0.75q each. LCL_FP64=0 forces the integer field everywhere.
+u32 fp_rows(const std::vector<u64>& primes) {
+  const char* env = std::getenv("LCL_FP64");
+  if (env && env[0] == '0') return 0;
+  const u64 lim = 1ull << 46;
+  u32 mask = 0;
+  for (size_t d = 0; d < primes.size() && d < 32; ++d) {
+    if (primes[d] >= lim) continue;
+    double b0 = 3.0;
+    for (u64 s : primes)
+      if (s < lim) b0 = std::max(b0, std::ceil((double)s / 2.0 / (double)primes[d]));
+    if ((b0 + 14.0) * (double)primes[d] < std::ldexp(1.0, 51)) mask |= 1u << d;
+  }
+  return mask;
+}
+
 void build_context(lcl_context* c, size_t degree, int depth, int secure, int device) {
   need(degree >= 8 && (degree & (degree - 1)) == 0, LCL_PARAMETER_ERROR,
        "ring degree must be a power of two >= 8");
@@ -1054,6 +1083,7 @@ void build_context(lcl_context* c, size_t degree, int depth, int secure, int dev
   const size_t n = degree;
   std::vector<PrimeConst> pc(P);
   std::vector<ulonglong2> tw(P * n), itw(P * n);
+  std::vector<double2> twf(P * n), itwf(P * n);
   for (u32 i = 0; i < P; ++i) {
     const u64 q = c->primes[i];
     const u128 ratio = ~(u128)0 / q;
@@ -1073,11 +1103,22 @@ void build_context(lcl_context* c, size_t degree, int depth, int secure, int dev
     k.w1n_shoup = h_shoup(k.w1n, q);
     k.mu56 = (u32)(((u128)1 << 56) / q);
     k.mu62 = (u32)(((u128)1 << 62) / q);
+    // FP64 companions: every value below 2^53 converts exactly, and w / q is
+    // the correctly rounded quotient f_mulmod's error bound assumes
+    const double qd = (double)q;
+    k.qf = qd;
+    k.qinvf = 1.0 / qd;
+    k.ninvf = (double)k.n_inv;
+    k.ninvq = k.ninvf / qd;
+    k.w1nf = (double)k.w1n;
+    k.w1nq = k.w1nf / qd;
     u64 f = 1, g = 1;
     for (size_t t = 0; t < n; ++t) {
       const size_t r = h_brv(t, c->logn);
       tw[i * n + r] = make_ulonglong2(f, h_shoup(f, q));
       itw[i * n + r] = make_ulonglong2(g, h_shoup(g, q));
+      twf[i * n + r] = make_double2((double)f, (double)f / qd);
+      itwf[i * n + r] = make_double2((double)g, (double)g / qd);
       f = h_mulmod(f, psi, q);
       g = h_mulmod(g, psi_inv, q);
     }
@@ -1093,11 +1134,16 @@ void build_context(lcl_context* c, size_t degree, int depth, int secure, int dev
   cuda_check(cudaMalloc(&c->d_primes, P * sizeof(PrimeConst)), "alloc");
   cuda_check(cudaMalloc(&c->d_tw, P * n * sizeof(ulonglong2)), "alloc");
   cuda_check(cudaMalloc(&c->d_itw, P * n * sizeof(ulonglong2)), "alloc");
+  cuda_check(cudaMalloc(&c->d_twf, P * n * sizeof(double2)), "alloc");
+  cuda_check(cudaMalloc(&c->d_itwf, P * n * sizeof(double2)), "alloc");
   cuda_check(cudaMalloc(&c->d_smod, P * P * 8), "alloc");
   cuda_check(cudaMalloc(&c->d_pinv, P * P * sizeof(ulonglong2)), "alloc");
   cuda_check(cudaMemcpy(c->d_primes, pc.data(), P * sizeof(PrimeConst), cudaMemcpyHostToDevice), "upload");
   cuda_check(cudaMemcpy(c->d_tw, tw.data(), P * n * sizeof(ulonglong2), cudaMemcpyHostToDevice), "upload");
   cuda_check(cudaMemcpy(c->d_itw, itw.data(), P * n * sizeof(ulonglong2), cudaMemcpyHostToDevice), "upload");
+  cuda_check(cudaMemcpy(c->d_twf, twf.data(), P * n * sizeof(double2), cudaMemcpyHostToDevice), "upload");
+  cuda_check(cudaMemcpy(c->d_itwf, itwf.data(), P * n * sizeof(double2), cudaMemcpyHostToDevice), "upload");
+  c->fp_mask = fp_rows(c->primes);
   cuda_check(cudaMemcpy(c->d_smod, smod.data(), P * P * 8, cudaMemcpyHostToDevice), "upload");
   cuda_check(cudaMemcpy(c->d_pinv, pinv.data(), P * P * sizeof(ulonglong2), cudaMemcpyHostToDevice), "upload");
 }
@@ -1106,6 +1152,8 @@ void free_context(lcl_context* c) {
   cudaFree(c->d_primes);
   cudaFree(c->d_tw);
   cudaFree(c->d_itw);
+  cudaFree(c->d_twf);
+  cudaFree(c->d_itwf);
   cudaFree(c->d_smod);
   cudaFree(c->d_pinv);
   cudaFree(c->d_pairs);
@@ -1134,7 +1182,12 @@ u64* upload_key(lcl_context* c, const u64* h, size_t words, u64** shoup_out) {
     const u32 row = (u32)((i / N) % P);
     const u64 q = c->primes[row];
     need(h[i] < q, LCL_KEY_ERROR, "key residue outside its modulus");
-    sh[i] = h_shoup(h[i], q);
+    if ((c->fp_mask >> row) & 1u) {
+      const double kq = (double)h[i] / (double)q;  // FP64 rows: fl(k / q)
+      std::memcpy(&sh[i], &kq, 8);
+    } else {
+      sh[i] = h_shoup(h[i], q);
+    }
   }
   u64* d = nullptr;
   u64* ds = nullptr;

@@ -1,4 +1,4 @@
-// Negacyclic NTT over 64-bit primes for sm_100a.
+// Negacyclic NTT over the RNS primes for sm_100a.
 //
 // Mathematically identical to the reference transforms
 // (proj/core/src/rns.cpp:140-181): forward = Cooley-Tukey with the
@@ -14,14 +14,20 @@
 //   * The last log2(N2) stages stay inside block b = a / N2 and use
 //     root[m'(N1 + b) + i'] at local stage m'              -> block pass
 // The inverse runs the block pass first, then the column pass, fusing the
-// N^-1 scaling into the column pass's store.
+// N^-1 scaling into the column pass's last stage.
 //
-// Arithmetic: Harvey lazy butterflies. Forward values live in [0, 4q),
-// inverse values in [0, 2q); twiddles are (w, floor(w 2^64 / q)) pairs.
-// One HBM round trip per pass; shared memory only carries the transpose
-// inside each pass. Loader / epilogue functors fuse the ModUp lift, the
-// ModDown / rescale divide-and-round and the key-switch output adds into the
-// first / last pass, so no standalone elementwise kernel touches HBM.
+// Two arithmetic fields, chosen per row (per CTA) by the prime:
+//   IntF  64-bit integer Harvey/Shoup butterflies on the IMAD pipe (any prime
+//         < 2^55; the 54-bit special prime always runs here);
+//   FpF   exact integer-valued doubles on the FP64 pipe (primes < 2^46: the
+//         44/40-bit q-chain), see common.cuh "FP64 residue arithmetic".
+// Both produce the same fully reduced words at every observable boundary.
+// Between the two passes of one transform the row is stored in the field's
+// own lazy representation (u64 words or double bits): producer and consumer
+// of an intermediate always agree because both read NttTabs::fp_mask.
+// Loader / epilogue functors fuse the ModUp lift, the ModDown / rescale
+// divide-and-round and the key-switch output adds into the first / last
+// pass, so no standalone elementwise kernel touches HBM.
 #pragma once
 
 #include <type_traits>
@@ -30,35 +36,110 @@
 
 namespace lcl {
 
-struct Tw {
-  u64 w, ws;
+__device__ __forceinline__ bool row_fp(const NttTabs& t, u32 pi) { return (t.fp_mask >> pi) & 1u; }
+
+// ------------------------------------------------------------ fields
+struct IntF {
+  using T = u64;
+  using TwPtr = const ulonglong2*;
+  struct Tw {
+    u64 w, ws;
+  };
+  struct K {
+    u64 q, two_q, four_q;
+    u32 mu62;
+  };
+  __device__ static __forceinline__ K konst(const PrimeConst& P) {
+    return K{P.q, P.two_q, 2 * P.two_q, P.mu62};
+  }
+  __device__ static __forceinline__ TwPtr table(const NttTabs& t, bool inv, u32 pi) {
+    return (inv ? t.itw : t.tw) + ((u64)pi << t.logn);
+  }
+  __device__ static __forceinline__ Tw ld(TwPtr t, u32 idx) {
+    const ulonglong2 v = __ldg(t + idx);
+    return Tw{v.x, v.y};
+  }
+  // Forward CT butterfly without intermediate reduction: with t = y*w mod q
+  // in [0, 4q) (truncated Shoup quotient), x' = x + t and y' = x + 4q - t stay
+  // below B + 4q when x < B; from inputs < 3q, after 17 stages every value is
+  // < 71q < 2^62 for q < 2^55, so the only reduction is the final one.
+  __device__ static __forceinline__ void ct(T& x, T& y, Tw w, const K& k) {
+    const u64 t = mul_shoup_lazy4(y, w.w, w.ws, k.q);
+    const u64 a = x;
+    x = a + t;
+    y = a + (k.four_q - t);
+  }
+  // Inverse GS butterfly: x, y in [0, 2q) -> x', y' in [0, 2q).
+  __device__ static __forceinline__ void gs(T& x, T& y, Tw w, const K& k) {
+    const u64 a = x, b = y;
+    const u64 s = a + b;
+    x = s >= k.two_q ? s - k.two_q : s;
+    y = mul_shoup_lazy(a - b + k.two_q, w.w, w.ws, k.q);
+  }
+  template <int E>
+  __device__ static __forceinline__ void gs_fix(T (&)[E], const K&) {}  // GS stays in [0, 2q)
+  __device__ static __forceinline__ T from_u64(u64 v) { return v; }
+  __device__ static __forceinline__ u64 bits(T v) { return v; }
+  __device__ static __forceinline__ T unbits(u64 v) { return v; }
+  __device__ static __forceinline__ u64 canon(T v, const K& k) { return reduce62(v, k.q, k.mu62); }
+  // Last inverse stage with N^-1 folded in: fully reduced outputs.
+  __device__ static __forceinline__ void inv_last(T& a, T& b, const PrimeConst& P) {
+    const u64 x = a, y = b;
+    a = mul_shoup(x + y, P.n_inv, P.n_inv_shoup, P.q);
+    b = mul_shoup(x - y + P.two_q, P.w1n, P.w1n_shoup, P.q);
+  }
+  __device__ static __forceinline__ u64 canon_last(T v, const K&) { return v; }
 };
 
-__device__ __forceinline__ Tw ldtw(const ulonglong2* t, u32 idx) {
-  const ulonglong2 v = __ldg(t + idx);
-  return Tw{v.x, v.y};
-}
-
-// Forward CT butterfly without intermediate reduction: with t = y*w mod q in
-// [0, 4q) (truncated Shoup quotient), x' = x + t and y' = x + 4q - t both stay
-// below B + 4q when x < B. Starting from inputs < q, after s stages every
-// value is < (1 + 4s) q; for s <= 17 and q < 2^55 that is < 69 * 2^55 < 2^62,
-// so no word overflows and the only reduction is the final one (reduce62).
-// The Shoup product accepts any y < 2^64. (two_q carries 4q here.)
-__device__ __forceinline__ void ct_bfly(u64& x, u64& y, Tw w, u64 q, u64 four_q) {
-  const u64 t = mul_shoup_lazy4(y, w.w, w.ws, q);
-  const u64 a = x;
-  x = a + t;
-  y = a + (four_q - t);
-}
-
-// Inverse GS butterfly: x, y in [0, 2q) -> x', y' in [0, 2q).
-__device__ __forceinline__ void gs_bfly(u64& x, u64& y, Tw w, u64 q, u64 two_q) {
-  const u64 a = x, b = y;
-  const u64 s = a + b;
-  x = s >= two_q ? s - two_q : s;
-  y = mul_shoup_lazy(a - b + two_q, w.w, w.ws, q);
-}
+struct FpF {
+  using T = double;
+  using TwPtr = const double2*;
+  struct Tw {
+    double w, wq;
+  };
+  struct K {
+    double q, qinv;
+    u64 qi;
+  };
+  __device__ static __forceinline__ K konst(const PrimeConst& P) { return K{P.qf, P.qinvf, P.q}; }
+  __device__ static __forceinline__ TwPtr table(const NttTabs& t, bool inv, u32 pi) {
+    return (inv ? t.itwf : t.twf) + ((u64)pi << t.logn);
+  }
+  __device__ static __forceinline__ Tw ld(TwPtr t, u32 idx) {
+    const double2 v = __ldg(t + idx);
+    return Tw{v.x, v.y};
+  }
+  // |t| <= 0.75q, so forward values grow by at most 0.75q per stage: from
+  // inputs below 8q (lifts of a wider q-chain prime), 17 stages stay < 22q.
+  __device__ static __forceinline__ void ct(T& x, T& y, Tw w, const K& k) {
+    const double t = f_mulmod(y, w.w, w.wq, k.q);
+    const double a = x;
+    x = __dadd_rn(a, t);
+    y = __dadd_rn(a, -t);
+  }
+  // Sums double per stage; gs_fix (every <= 4 stages) brings them back to
+  // 0.75q, so every operand stays below 24q.
+  __device__ static __forceinline__ void gs(T& x, T& y, Tw w, const K& k) {
+    const double a = x, b = y;
+    x = __dadd_rn(a, b);
+    y = f_mulmod(__dadd_rn(a, -b), w.w, w.wq, k.q);
+  }
+  template <int E>
+  __device__ static __forceinline__ void gs_fix(T (&x)[E], const K& k) {
+#pragma unroll
+    for (int e = 0; e < E; ++e) x[e] = f_reduce(x[e], k.q, k.qinv);
+  }
+  __device__ static __forceinline__ T from_u64(u64 v) { return u2d(v); }
+  __device__ static __forceinline__ u64 bits(T v) { return (u64)__double_as_longlong(v); }
+  __device__ static __forceinline__ T unbits(u64 v) { return __longlong_as_double((long long)v); }
+  __device__ static __forceinline__ u64 canon(T v, const K& k) { return d_canon(v, k.q, k.qinv, k.qi); }
+  __device__ static __forceinline__ void inv_last(T& a, T& b, const PrimeConst& P) {
+    const double x = a, y = b;
+    a = f_mulmod(__dadd_rn(x, y), P.ninvf, P.ninvq, P.qf);
+    b = f_mulmod(__dadd_rn(x, -y), P.w1nf, P.w1nq, P.qf);
+  }
+  __device__ static __forceinline__ u64 canon_last(T v, const K& k) { return canon(v, k); }
+};
 
 // Padded shared-memory slot of block element i (bank-conflict-free for both
 // the l + 16 e and the 16 l + e access patterns).
@@ -66,7 +147,8 @@ __device__ __forceinline__ u32 pad16(u32 i) { return i + (i >> 4); }
 
 // ------------------------------------------------------------ loaders
 // A loader is bound once per row (all address / constant lookups hoisted):
-//   auto row = ld.bind(r, dst_prime_index, dst);  row(a) -> value < q
+//   auto row = ld.bind(r, dst_prime_index, dst);  row(a) -> u64 congruent
+// to the input, below 3q (below 2^52 for FP64 rows).
 struct PlainLoad {
   RowMap in;
   struct Row {
@@ -76,7 +158,6 @@ struct PlainLoad {
   __device__ __forceinline__ Row bind(u32 r, u32, const PrimeConst&) const {
     return Row{row_ptr(in, r)};
   }
-  __host__ __device__ static constexpr double rows_read(double rows, u32) { return rows; }
 };
 
 // Centred lift of a coefficient-domain source row into the destination prime
@@ -88,12 +169,18 @@ struct PlainLoad {
 // 2^55, qh = ((v >> 24) * floor(2^56 / q_d)) >> 32 is floor(v / q_d) or one
 // less, so v - qh q_d lies in [0, 2 q_d); the centring correction adds
 // q_d - (q_s mod q_d). The value handed to the forward NTT is therefore
-// congruent to the reference's lift and lies in [0, 3 q_d), which the
-// reduction-free butterflies absorb ((3 + 4 s) q_d < 2^62 for s <= 17).
+// congruent to the reference's lift and lies in [0, 3 q_d).
 // With SIGMA the source is read through the Galois automorphism X -> X^elt in
 // the coefficient domain (entry = src index | negate << 31); lifting commutes
 // with that signed permutation (small rings only; the two-pass rings apply the
 // permutation block-locally in the evaluation domain).
+__device__ __forceinline__ u64 int_lift(u64 v, u64 half, u64 corr, u64 q, u32 mu) {
+  const u64 qh = ((u64)(u32)(v >> 24) * mu) >> 32;
+  u64 x = v - qh * q;
+  if (v > half) x += corr;
+  return x;
+}
+
 template <bool SIGMA>
 struct LiftLoadT {
   RowMap src;
@@ -117,10 +204,7 @@ struct LiftLoadT {
       } else {
         v = __ldg(s + a);
       }
-      const u64 qh = ((u64)(u32)(v >> 24) * mu) >> 32;
-      u64 x = v - qh * q;
-      if (v > half) x += corr;
-      return x;
+      return int_lift(v, half, corr, q, mu);
     }
   };
   __device__ __forceinline__ Row bind(u32 r, u32 dpi, const PrimeConst& dst) const {
@@ -143,7 +227,9 @@ using LiftLoad = LiftLoadT<false>;
 using LiftSigmaLoad = LiftLoadT<true>;
 
 // ------------------------------------------------------------ epilogues
-// auto row = epi.bind(r, dst_prime_index, dst);  row(a, value < q)
+// auto row = epi.bind(r, dst_prime_index, dst);  row(a, value)
+// kNeedsReduced: the value is fully reduced in [0, q); otherwise an integer
+// row may hand over its lazy word (< 80q); FP64 rows always hand over [0, q).
 struct PlainStore {
   static constexpr bool kNeedsReduced = true;
   RowMap out;
@@ -242,143 +328,190 @@ __device__ __forceinline__ void static_for(F&& f) {
 
 // One radix-2 stage over a register tile: groups of 2D consecutive elements,
 // butterflies (g*2D + e, g*2D + e + D); twf(g) gives the group's twiddle.
-template <int E, int D, class TwF>
-__device__ __forceinline__ void ct_stage(u64 (&x)[E], const TwF& twf, u64 q, u64 two_q) {
-  const u64 four_q = 2 * two_q;
+template <class F, int E, int D, class TwF>
+__device__ __forceinline__ void ct_stage(typename F::T (&x)[E], const TwF& twf, const typename F::K& k) {
 #pragma unroll
   for (int g = 0; g < E / (2 * D); ++g) {
-    const Tw w = twf(g);
+    const typename F::Tw w = twf(g);
 #pragma unroll
-    for (int e = 0; e < D; ++e) ct_bfly(x[g * 2 * D + e], x[g * 2 * D + e + D], w, q, four_q);
+    for (int e = 0; e < D; ++e) F::ct(x[g * 2 * D + e], x[g * 2 * D + e + D], w, k);
   }
 }
-template <int E, int D, class TwF>
-__device__ __forceinline__ void gs_stage(u64 (&x)[E], const TwF& twf, u64 q, u64 two_q) {
+template <class F, int E, int D, class TwF>
+__device__ __forceinline__ void gs_stage(typename F::T (&x)[E], const TwF& twf, const typename F::K& k) {
 #pragma unroll
   for (int g = 0; g < E / (2 * D); ++g) {
-    const Tw w = twf(g);
+    const typename F::Tw w = twf(g);
 #pragma unroll
-    for (int e = 0; e < D; ++e) gs_bfly(x[g * 2 * D + e], x[g * 2 * D + e + D], w, q, two_q);
+    for (int e = 0; e < D; ++e) F::gs(x[g * 2 * D + e], x[g * 2 * D + e + D], w, k);
   }
+}
+
+// Column-pass stage groups. Thread (c, k) of a column CTA holds rows k + R e
+// (layout A) or rows k E + e (layout B) of its column.
+// Forward, layout A: stages m = 1 .. E/2.
+template <class F, int LOGN1, int E>
+__device__ __forceinline__ void col_fwd_phase1(typename F::T (&x)[E], typename F::TwPtr tw,
+                                               const typename F::K& K) {
+  constexpr int LOGE = __builtin_ctz(E);
+  static_for<0, LOGE, 1>([&](auto LM) {
+    constexpr int lm = decltype(LM)::value;
+    ct_stage<F, E, (E >> (lm + 1))>(x, [&](int gi) { return F::ld(tw, (1 << lm) + gi); }, K);
+  });
+}
+// Forward, layout B: stages m = E .. N1/2 (distance N1/(2m) < R <= E).
+template <class F, int LOGN1, int E>
+__device__ __forceinline__ void col_fwd_phase2(typename F::T (&x)[E], typename F::TwPtr tw, u32 k,
+                                               const typename F::K& K) {
+  constexpr int LOGE = __builtin_ctz(E);
+  static_for<LOGE, LOGN1, 1>([&](auto LM) {
+    constexpr int lm = decltype(LM)::value;
+    constexpr int d = (1 << LOGN1) >> (lm + 1);
+    ct_stage<F, E, d>(x, [&](int gi) { return F::ld(tw, (1 << lm) + ((k * E + gi * 2 * d) >> (LOGN1 - lm))); },
+                      K);
+  });
+}
+// Inverse, layout B: GS stages m = N1/2 .. E.
+template <class F, int LOGN1, int E>
+__device__ __forceinline__ void col_inv_phase1(typename F::T (&x)[E], typename F::TwPtr tw, u32 k,
+                                               const typename F::K& K) {
+  constexpr int LOGE = __builtin_ctz(E);
+  static_for<LOGN1 - 1, LOGE - 1, -1>([&](auto LM) {
+    constexpr int lm = decltype(LM)::value;
+    constexpr int d = (1 << LOGN1) >> (lm + 1);
+    gs_stage<F, E, d>(x, [&](int gi) { return F::ld(tw, (1 << lm) + ((k * E + gi * 2 * d) >> (LOGN1 - lm))); },
+                      K);
+  });
+}
+// Inverse, layout A: GS stages m = E/2 .. 2, then the last stage (m = 1) with
+// N^-1 folded in: x' = (x + y) N^-1, y' = (x - y) (w N^-1).
+template <class F, int E>
+__device__ __forceinline__ void col_inv_phase2(typename F::T (&x)[E], typename F::TwPtr tw,
+                                               const typename F::K& K, const PrimeConst& P) {
+  constexpr int LOGE = __builtin_ctz(E);
+  static_for<LOGE - 1, 0, -1>([&](auto LM) {
+    constexpr int lm = decltype(LM)::value;
+    gs_stage<F, E, (E >> (lm + 1))>(x, [&](int gi) { return F::ld(tw, (1 << lm) + gi); }, K);
+  });
+#pragma unroll
+  for (int e = 0; e < E / 2; ++e) F::inv_last(x[e], x[e + E / 2], P);
 }
 
 // ------------------------------------------------------------ kernels
 // Column pass, forward. CTA = 16 consecutive columns x N1 rows of one row-poly.
 // Thread (c, k): column c, rows k + R e (phase 1, log2 E stages in registers),
 // then rows k E + e (phase 2, log2 R stages) after one shared transpose.
+// Output: the field's lazy words (bits) in out.
+template <class F, int LOGN1, int E, class Loader>
+__device__ __forceinline__ void col_fwd_body(const RowMap& out, const Loader& ld, const NttTabs& tb,
+                                             u64* sm, u32 r, u32 j, u32 c, u32 k, u32 pi) {
+  constexpr int N1 = 1 << LOGN1;
+  constexpr int R = N1 / E;
+  const u32 n2 = (1u << tb.logn) >> LOGN1;
+  const PrimeConst P = tb.primes[pi];
+  const typename F::K K = F::konst(P);
+  const typename F::TwPtr tw = F::table(tb, false, pi);
+  typename F::T x[E];
+  {
+    const auto row = ld.bind(r, pi, P);
+#pragma unroll
+    for (int e = 0; e < E; ++e) x[e] = F::from_u64(row(j + (k + R * e) * n2));
+  }
+  col_fwd_phase1<F, LOGN1, E>(x, tw, K);
+#pragma unroll
+  for (int e = 0; e < E; ++e) sm[(k + R * e) * 16 + c] = F::bits(x[e]);
+  __syncthreads();
+#pragma unroll
+  for (int e = 0; e < E; ++e) x[e] = F::unbits(sm[(k * E + e) * 16 + c]);
+  col_fwd_phase2<F, LOGN1, E>(x, tw, k, K);
+  u64* o = row_ptr(out, r);
+#pragma unroll
+  for (int e = 0; e < E; ++e) o[j + (k * E + e) * n2] = F::bits(x[e]);
+}
+
 template <int LOGN1, int E, class Loader>
 __global__ void __launch_bounds__(16 * ((1 << LOGN1) / E))
     ntt_col_fwd(const __grid_constant__ RowMap out, const __grid_constant__ Loader ld,
-                const ulonglong2* __restrict__ tw_all, const PrimeConst* __restrict__ primes,
-                u32 logn) {
-  constexpr int N1 = 1 << LOGN1;
-  constexpr int R = N1 / E;
-  constexpr int LOGE = __builtin_ctz(E);
+                const __grid_constant__ NttTabs tb) {
   extern __shared__ u64 sm[];  // [N1][16]
-  const u32 n = 1u << logn;
-  const u32 n2 = n >> LOGN1;
-  const u32 groups = n2 >> 4;
+  const u32 groups = ((1u << tb.logn) >> LOGN1) >> 4;
   const u32 r = blockIdx.x / groups;
   const u32 g = blockIdx.x - r * groups;
   const u32 c = threadIdx.x & 15, k = threadIdx.x >> 4;
   const u32 j = (g << 4) + c;
   const u32 pi = row_prime(out, r);
-  const PrimeConst P = primes[pi];
-  const ulonglong2* tw = tw_all + (u64)pi * n;
-  u64 x[E];
-  {
-    const auto row = ld.bind(r, pi, P);
-#pragma unroll
-    for (int e = 0; e < E; ++e) x[e] = row(j + (k + R * e) * n2);
-  }
-  // phase 1: m = 1 .. E/2; group g of a stage is twiddle root[m + g]
-  static_for<0, LOGE, 1>([&](auto LM) {
-    constexpr int lm = decltype(LM)::value;
-    ct_stage<E, (E >> (lm + 1))>(x, [&](int gi) { return ldtw(tw, (1 << lm) + gi); }, P.q, P.two_q);
-  });
-#pragma unroll
-  for (int e = 0; e < E; ++e) sm[(k + R * e) * 16 + c] = x[e];
-  __syncthreads();
-#pragma unroll
-  for (int e = 0; e < E; ++e) x[e] = sm[(k * E + e) * 16 + c];
-  // phase 2: m = E .. N1/2 on rows t = kE + e; distance N1/(2m) < R <= E
-  static_for<LOGE, LOGN1, 1>([&](auto LM) {
-    constexpr int lm = decltype(LM)::value;
-    constexpr int d = N1 >> (lm + 1);
-    ct_stage<E, d>(x, [&](int gi) { return ldtw(tw, (1 << lm) + ((k * E + gi * 2 * d) >> (LOGN1 - lm))); },
-                   P.q, P.two_q);
-  });
-  u64* o = row_ptr(out, r);
-#pragma unroll
-  for (int e = 0; e < E; ++e) o[j + (k * E + e) * n2] = x[e];
+  if (row_fp(tb, pi))
+    col_fwd_body<FpF, LOGN1, E>(out, ld, tb, sm, r, j, c, k, pi);
+  else
+    col_fwd_body<IntF, LOGN1, E>(out, ld, tb, sm, r, j, c, k, pi);
 }
 
 // Block pass body, forward: x[e] holds element l + 16 e of one 256-point
-// block (coalesced order) on entry and the fully reduced output in the same
-// order on exit. Phase 1 runs local stages m' = 1..8 on s = l + 16 e, phase 2
+// block (coalesced order) on entry; on exit o[e] = fin(output element
+// l + 16 e). Phase 1 runs local stages m' = 1..8 on s = l + 16 e, phase 2
 // m' = 16..128 on s = 16 l + e after a warp-local shared transpose.
-template <int LOGN1, bool REDUCE = true>
-__device__ __forceinline__ void blk_fwd_body(u64 (&x)[16], u64* s, const ulonglong2* tw, u32 b,
-                                             u32 l, const PrimeConst& P) {
+template <class F, int LOGN1, class Fin>
+__device__ __forceinline__ void blk_fwd_body(typename F::T (&x)[16], u64 (&o)[16], u64* s,
+                                             typename F::TwPtr tw, u32 b, u32 l,
+                                             const typename F::K& K, const Fin& fin) {
   constexpr int N1 = 1 << LOGN1;
   static_for<0, 4, 1>([&](auto LM) {
     constexpr int lm = decltype(LM)::value;
-    ct_stage<16, (16 >> (lm + 1))>(x, [&](int gi) { return ldtw(tw, (N1 + b) * (1 << lm) + gi); },
-                                   P.q, P.two_q);
+    ct_stage<F, 16, (16 >> (lm + 1))>(x, [&](int gi) { return F::ld(tw, (N1 + b) * (1 << lm) + gi); }, K);
   });
 #pragma unroll
-  for (int e = 0; e < 16; ++e) s[l + 16 * e + e] = x[e];
+  for (int e = 0; e < 16; ++e) s[l + 16 * e + e] = F::bits(x[e]);
   __syncwarp();
 #pragma unroll
-  for (int e = 0; e < 16; ++e) x[e] = s[16 * l + e + l];
+  for (int e = 0; e < 16; ++e) x[e] = F::unbits(s[16 * l + e + l]);
   static_for<4, 8, 1>([&](auto LM) {
     constexpr int lm = decltype(LM)::value;
     constexpr int d = 256 >> (lm + 1);
-    ct_stage<16, d>(x,
-                    [&](int gi) { return ldtw(tw, (N1 + b) * (1 << lm) + ((16 * l + gi * 2 * d) >> (8 - lm))); },
-                    P.q, P.two_q);
+    ct_stage<F, 16, d>(x,
+                       [&](int gi) { return F::ld(tw, (N1 + b) * (1 << lm) + ((16 * l + gi * 2 * d) >> (8 - lm))); },
+                       K);
   });
-  // REDUCE = false leaves the lazy words (< 71q, see ct_bfly) for consumers
-  // that only feed them into a Shoup product, which accepts any 64-bit input.
   __syncwarp();
 #pragma unroll
-  for (int e = 0; e < 16; ++e) s[16 * l + e + l] = REDUCE ? reduce62(x[e], P.q, P.mu62) : x[e];
+  for (int e = 0; e < 16; ++e) s[16 * l + e + l] = fin(x[e]);
   __syncwarp();
 #pragma unroll
-  for (int e = 0; e < 16; ++e) x[e] = s[l + 16 * e + e];
+  for (int e = 0; e < 16; ++e) o[e] = s[l + 16 * e + e];
   __syncwarp();
 }
 
 // Block pass body, inverse: x[e] = element l + 16 e of block b (coalesced
-// order, values < 2q) in and out; GS stages m' = 128 .. 1 (global m = N/2 .. N1).
-template <int LOGN1>
-__device__ __forceinline__ void blk_inv_body(u64 (&x)[16], u64* s, const ulonglong2* tw, u32 b,
-                                             u32 l, const PrimeConst& P) {
+// order) in and out; GS stages m' = 128 .. 1 (global m = N/2 .. N1). FP64
+// rows are brought back to |x| <= 0.75q after each 4-stage phase.
+template <class F, int LOGN1>
+__device__ __forceinline__ void blk_inv_body(typename F::T (&x)[16], u64* s, typename F::TwPtr tw,
+                                             u32 b, u32 l, const typename F::K& K) {
   constexpr int N1 = 1 << LOGN1;
 #pragma unroll
-  for (int e = 0; e < 16; ++e) s[l + 16 * e + e] = x[e];
+  for (int e = 0; e < 16; ++e) s[l + 16 * e + e] = F::bits(x[e]);
   __syncwarp();
 #pragma unroll
-  for (int e = 0; e < 16; ++e) x[e] = s[16 * l + e + l];
+  for (int e = 0; e < 16; ++e) x[e] = F::unbits(s[16 * l + e + l]);
   static_for<7, 3, -1>([&](auto LM) {
     constexpr int lm = decltype(LM)::value;
     constexpr int d = 256 >> (lm + 1);
-    gs_stage<16, d>(x,
-                    [&](int gi) { return ldtw(tw, (N1 + b) * (1 << lm) + ((16 * l + gi * 2 * d) >> (8 - lm))); },
-                    P.q, P.two_q);
+    gs_stage<F, 16, d>(x,
+                       [&](int gi) { return F::ld(tw, (N1 + b) * (1 << lm) + ((16 * l + gi * 2 * d) >> (8 - lm))); },
+                       K);
   });
+  F::gs_fix(x, K);
   __syncwarp();
 #pragma unroll
-  for (int e = 0; e < 16; ++e) s[16 * l + e + l] = x[e];
+  for (int e = 0; e < 16; ++e) s[16 * l + e + l] = F::bits(x[e]);
   __syncwarp();
 #pragma unroll
-  for (int e = 0; e < 16; ++e) x[e] = s[l + 16 * e + e];
+  for (int e = 0; e < 16; ++e) x[e] = F::unbits(s[l + 16 * e + e]);
   __syncwarp();
   static_for<3, -1, -1>([&](auto LM) {
     constexpr int lm = decltype(LM)::value;
-    gs_stage<16, (16 >> (lm + 1))>(x, [&](int gi) { return ldtw(tw, (N1 + b) * (1 << lm) + gi); },
-                                   P.q, P.two_q);
+    gs_stage<F, 16, (16 >> (lm + 1))>(x, [&](int gi) { return F::ld(tw, (N1 + b) * (1 << lm) + gi); }, K);
   });
+  F::gs_fix(x, K);
 }
 
 // Galois permutation inside one 256-element block. In bit-reversed evaluation
@@ -397,40 +530,51 @@ __device__ __forceinline__ void block_gather(u64 (&x)[16], u64* s, const u64* sr
 }
 
 // Block pass, forward: 256-point blocks, 16 threads per block, 16 elements per
-// thread, 4 blocks per CTA. The epilogue's operands are prefetched before the
-// butterflies so their latency overlaps the arithmetic.
-template <int LOGN1, class Epi>
-__global__ void __launch_bounds__(64)
-    ntt_blk_fwd(const __grid_constant__ RowMap in, const __grid_constant__ Epi epi,
-                const ulonglong2* __restrict__ tw_all, const PrimeConst* __restrict__ primes,
-                u32 logn) {
-  constexpr int N1 = 1 << LOGN1;
-  __shared__ u64 sm[4][256 + 16];
-  const u32 n = 1u << logn;
-  const u32 l = threadIdx.x & 15, bw = threadIdx.x >> 4;
-  const u32 blk_global = blockIdx.x * 4 + bw;
-  const u32 r = blk_global / N1;
-  const u32 b = blk_global - r * N1;
-  const u32 pi = row_prime(in, r);
-  const PrimeConst P = primes[pi];
-  const ulonglong2* tw = tw_all + (u64)pi * n;
+// thread, 4 blocks (of one row) per CTA. The epilogue's operands are
+// prefetched before the butterflies so their latency overlaps the arithmetic.
+template <class F, int LOGN1, class Epi>
+__device__ __forceinline__ void blk_fwd_kernel_body(const RowMap& in, const Epi& epi, const NttTabs& tb,
+                                                    u64* s, u32 r, u32 b, u32 l, u32 pi) {
+  const PrimeConst P = tb.primes[pi];
+  const typename F::K K = F::konst(P);
   const u64* src = row_ptr(in, r) + (b << 8);
-  u64 x[16];
+  typename F::T x[16];
 #pragma unroll
-  for (int e = 0; e < 16; ++e) x[e] = src[l + 16 * e];
-  blk_fwd_body<LOGN1, Epi::kNeedsReduced>(x, sm[bw], tw, b, l, P);
+  for (int e = 0; e < 16; ++e) x[e] = F::unbits(src[l + 16 * e]);
+  u64 o[16];
+  blk_fwd_body<F, LOGN1>(x, o, s, F::table(tb, false, pi), b, l, K, [&](typename F::T v) -> u64 {
+    if (std::is_same<F, FpF>::value || Epi::kNeedsReduced) return F::canon(v, K);
+    return F::bits(v);
+  });
   const auto row = epi.bind(r, pi, P);
-  row.stage(sm[bw], b, l);
+  row.stage(s, b, l);
   // operands of 4 elements in flight at a time: latency overlap without the
   // register cost of prefetching all 16
 #pragma unroll
   for (int e0 = 0; e0 < 16; e0 += 4) {
     typename Epi::Pre pre[4];
 #pragma unroll
-    for (int e = 0; e < 4; ++e) row.prefetch(pre[e], (b << 8) + l + 16 * (e0 + e), sm[bw]);
+    for (int e = 0; e < 4; ++e) row.prefetch(pre[e], (b << 8) + l + 16 * (e0 + e), s);
 #pragma unroll
-    for (int e = 0; e < 4; ++e) row.store(pre[e], (b << 8) + l + 16 * (e0 + e), x[e0 + e]);
+    for (int e = 0; e < 4; ++e) row.store(pre[e], (b << 8) + l + 16 * (e0 + e), o[e0 + e]);
   }
+}
+
+template <int LOGN1, class Epi>
+__global__ void __launch_bounds__(64)
+    ntt_blk_fwd(const __grid_constant__ RowMap in, const __grid_constant__ Epi epi,
+                const __grid_constant__ NttTabs tb) {
+  constexpr int N1 = 1 << LOGN1;
+  __shared__ u64 sm[4][256 + 16];
+  const u32 l = threadIdx.x & 15, bw = threadIdx.x >> 4;
+  const u32 blk_global = blockIdx.x * 4 + bw;
+  const u32 r = blk_global / N1;
+  const u32 b = blk_global - r * N1;
+  const u32 pi = row_prime(in, r);
+  if (row_fp(tb, pi))
+    blk_fwd_kernel_body<FpF, LOGN1>(in, epi, tb, sm[bw], r, b, l, pi);
+  else
+    blk_fwd_kernel_body<IntF, LOGN1>(in, epi, tb, sm[bw], r, b, l, pi);
 }
 
 // ModUp block pass fused with the key inner product (ckks.cpp:464-518).
@@ -439,80 +583,92 @@ __global__ void __launch_bounds__(64)
 // the block stages, except the identity row t == j, whose lifted NTT is the
 // input limb itself (mod_up returns the row unchanged, rns.cpp:371-381), read
 // through the rotation's evaluation-domain permutation when one is given.
-// Each digit is multiplied by the key in Shoup form and accumulated lazily
-// (< 4Mq), so the m(m+1) digit rows never reach HBM.
+// Each digit is multiplied by the key and accumulated lazily, so the m(m+1)
+// digit rows never reach HBM. Integer rows use the key in Shoup form
+// (key_aux = floor(k 2^64 / q)); FP64 rows use key_aux = bits of fl(k / q).
 //   mid: [B][M][M][N] (t' = t < j ? t : t - 1); c1: limb j of item b at
-//   c1 + b * c1_stride + j * N; key / key_shoup: [full][2][full+1][N];
+//   c1 + b * c1_stride + j * N; key / key_aux: [full][2][full+1][N];
 //   acc: [B][2][M+1][N].
-template <int LOGN1, int M>
-__global__ void __launch_bounds__(64, 8)
-    modup_ip_blk(u32 B, const u64* __restrict__ mid, const u64* __restrict__ c1, u64 c1_stride,
-                 const u32* __restrict__ perm, const u64* __restrict__ key,
-                 const u64* __restrict__ key_shoup, u32 full, u64* __restrict__ acc,
-                 const ulonglong2* __restrict__ tw_all, const PrimeConst* __restrict__ primes,
-                 u32 logn) {
-  constexpr int N1 = 1 << LOGN1;
-  __shared__ u64 sm[4][256 + 16];
-  __shared__ u64 sacc[4][2][256];  // lazy accumulators (< 4Mq), coalesced order
-  const u32 n = 1u << logn;
-  const u32 l = threadIdx.x & 15, bw = threadIdx.x >> 4;
-  // the 4 groups of a CTA take 4 consecutive ciphertexts of the same
-  // (target row, block): the key words they share are served from L1
-  const u32 bq_count = (B + 3) >> 2;
-  const u32 bq = blockIdx.x % bq_count;
-  const u32 tb = blockIdx.x / bq_count;  // = t * N1 + blk
-  const u32 t = tb / N1, blk = tb - t * N1;
-  const u32 bi_raw = bq * 4 + bw;
-  const bool live = bi_raw < B;
-  const u32 bi = live ? bi_raw : B - 1;
-  const u32 pi = t < (u32)M ? t : full;
-  const PrimeConst P = primes[pi];
-  const ulonglong2* tw = tw_all + (u64)pi * n;
+template <class F>
+struct IpOps;
+template <>
+struct IpOps<IntF> {
+  // each product < 4q: the M-term sums stay < 24q (M <= 6)
+  __device__ static __forceinline__ u64 mul(u64 x, u64 k, u64 ks, const IntF::K& K) {
+    return mul_shoup_lazy4(x, k, ks, K.q);
+  }
+  __device__ static __forceinline__ u64 add(u64 a, u64 b) { return a + b; }
+};
+template <>
+struct IpOps<FpF> {
+  // each product |p| <= 0.75q
+  __device__ static __forceinline__ u64 mul(double x, u64 k, u64 kq, const FpF::K& K) {
+    return (u64)__double_as_longlong(f_mulmod(x, u2d(k), __longlong_as_double((long long)kq), K.q));
+  }
+  __device__ static __forceinline__ u64 add(u64 a, u64 b) {
+    return (u64)__double_as_longlong(__dadd_rn(__longlong_as_double((long long)a),
+                                               __longlong_as_double((long long)b)));
+  }
+};
+
+template <class F, int LOGN1, int M>
+__device__ __forceinline__ void modup_ip_body(u32 bi, bool live, u32 t, u32 blk, u32 pi, u32 l,
+                                              u64* s, u64* s0acc, u64* s1acc, const u64* mid,
+                                              const u64* c1, u64 c1_stride, const u32* perm,
+                                              const u64* key, const u64* key_aux, u32 full,
+                                              u64* acc, const NttTabs& tb) {
+  const u32 n = 1u << tb.logn;
+  const PrimeConst P = tb.primes[pi];
+  const typename F::K K = F::konst(P);
+  const typename F::TwPtr tw = F::table(tb, false, pi);
   const u64 kstride = (u64)(full + 1) * n;
   const u32 a0 = (blk << 8) + l;
-  u64* s0acc = sacc[bw][0];
-  u64* s1acc = sacc[bw][1];
   // rotation: output block blk of every digit comes from block src_blk of the
   // unpermuted digit (block-local Galois permutation, see block_gather)
   const u32 src_blk = perm ? (__ldg(perm + (blk << 8)) >> 8) : blk;
 #pragma unroll 1
   for (int j = 0; j < M; ++j) {
-    u64 x[16];
+    typename F::T x[16];
     if (t == (u32)j) {
       const u64* src = c1 + (u64)bi * c1_stride + (u64)j * n + (src_blk << 8);
+      u64 v[16];
       if (perm) {
-        block_gather(x, sm[bw], src, perm, blk, l);
+        block_gather(v, s, src, perm, blk, l);
       } else {
 #pragma unroll
-        for (int e = 0; e < 16; ++e) x[e] = __ldg(src + l + 16 * e);
+        for (int e = 0; e < 16; ++e) v[e] = __ldg(src + l + 16 * e);
       }
+#pragma unroll
+      for (int e = 0; e < 16; ++e) x[e] = F::from_u64(v[e]);
     } else {
       const u32 tp = t < (u32)j ? t : t - 1;
       const u64* src = mid + (((u64)bi * M + j) * M + tp) * n + (src_blk << 8);
 #pragma unroll
-      for (int e = 0; e < 16; ++e) x[e] = src[l + 16 * e];
-      blk_fwd_body<LOGN1, false>(x, sm[bw], tw, src_blk, l, P);
+      for (int e = 0; e < 16; ++e) x[e] = F::unbits(src[l + 16 * e]);
+      u64 o[16];
+      blk_fwd_body<F, LOGN1>(x, o, s, tw, src_blk, l, K, [](typename F::T v) { return F::bits(v); });
       if (perm) {
         // the body left the (lazy) block in shared memory: permuted read
 #pragma unroll
-        for (int e = 0; e < 16; ++e)
-          x[e] = sm[bw][pad16(__ldg(perm + (blk << 8) + l + 16 * e) & 255u)];
+        for (int e = 0; e < 16; ++e) x[e] = F::unbits(s[pad16(__ldg(perm + (blk << 8) + l + 16 * e) & 255u)]);
         __syncwarp();
+      } else {
+#pragma unroll
+        for (int e = 0; e < 16; ++e) x[e] = F::unbits(o[e]);
       }
     }
     const u64* k0 = key + (2ull * j) * kstride + (u64)pi * n;
     const u64* k1 = k0 + kstride;
-    const u64* ks0 = key_shoup + (2ull * j) * kstride + (u64)pi * n;
+    const u64* ks0 = key_aux + (2ull * j) * kstride + (u64)pi * n;
     const u64* ks1 = ks0 + kstride;
 #pragma unroll
     for (int e = 0; e < 16; ++e) {
       const u32 a = a0 + 16 * e;
-      // each product < 4q: the M-term sums stay < 24q (M <= 6)
-      const u64 p0 = mul_shoup_lazy4(x[e], __ldg(k0 + a), __ldg(ks0 + a), P.q);
-      const u64 p1 = mul_shoup_lazy4(x[e], __ldg(k1 + a), __ldg(ks1 + a), P.q);
+      const u64 p0 = IpOps<F>::mul(x[e], __ldg(k0 + a), __ldg(ks0 + a), K);
+      const u64 p1 = IpOps<F>::mul(x[e], __ldg(k1 + a), __ldg(ks1 + a), K);
       const u32 si = l + 16 * e;
-      s0acc[si] = j ? s0acc[si] + p0 : p0;
-      s1acc[si] = j ? s1acc[si] + p1 : p1;
+      s0acc[si] = j ? IpOps<F>::add(s0acc[si], p0) : p0;
+      s1acc[si] = j ? IpOps<F>::add(s1acc[si], p1) : p1;
     }
   }
   if (!live) return;
@@ -521,87 +677,116 @@ __global__ void __launch_bounds__(64, 8)
 #pragma unroll
   for (int e = 0; e < 16; ++e) {
     const u32 si = l + 16 * e;
-    o0[a0 + 16 * e] = reduce62(s0acc[si], P.q, P.mu62);
-    o1[a0 + 16 * e] = reduce62(s1acc[si], P.q, P.mu62);
+    o0[a0 + 16 * e] = F::canon(F::unbits(s0acc[si]), K);
+    o1[a0 + 16 * e] = F::canon(F::unbits(s1acc[si]), K);
   }
 }
 
-// Block pass, inverse: GS stages m = N/2 .. N1 (local m' = 128 .. 1).
+template <int LOGN1, int M>
+__global__ void __launch_bounds__(64, 8)
+    modup_ip_blk(u32 B, const u64* __restrict__ mid, const u64* __restrict__ c1, u64 c1_stride,
+                 const u32* __restrict__ perm, const u64* __restrict__ key,
+                 const u64* __restrict__ key_aux, u32 full, u64* __restrict__ acc,
+                 const __grid_constant__ NttTabs tb) {
+  constexpr int N1 = 1 << LOGN1;
+  __shared__ u64 sm[4][256 + 16];
+  __shared__ u64 sacc[4][2][256];  // lazy accumulators, coalesced order
+  const u32 l = threadIdx.x & 15, bw = threadIdx.x >> 4;
+  // the 4 groups of a CTA take 4 consecutive ciphertexts of the same
+  // (target row, block): the key words they share are served from L1
+  const u32 bq_count = (B + 3) >> 2;
+  const u32 bq = blockIdx.x % bq_count;
+  const u32 tb_ = blockIdx.x / bq_count;  // = t * N1 + blk
+  const u32 t = tb_ / N1, blk = tb_ - t * N1;
+  const u32 bi_raw = bq * 4 + bw;
+  const bool live = bi_raw < B;
+  const u32 bi = live ? bi_raw : B - 1;
+  const u32 pi = t < (u32)M ? t : full;
+  if (row_fp(tb, pi))
+    modup_ip_body<FpF, LOGN1, M>(bi, live, t, blk, pi, l, sm[bw], sacc[bw][0], sacc[bw][1], mid, c1,
+                                 c1_stride, perm, key, key_aux, full, acc, tb);
+  else
+    modup_ip_body<IntF, LOGN1, M>(bi, live, t, blk, pi, l, sm[bw], sacc[bw][0], sacc[bw][1], mid, c1,
+                                  c1_stride, perm, key, key_aux, full, acc, tb);
+}
+
+// Block pass, inverse: GS stages m = N/2 .. N1 (local m' = 128 .. 1). Input:
+// fully reduced words; output: the field's lazy words for the column pass.
+template <class F, int LOGN1>
+__device__ __forceinline__ void blk_inv_kernel_body(const RowMap& in, const RowMap& out,
+                                                    const NttTabs& tb, u64* s, u32 r, u32 b, u32 l,
+                                                    u32 pi) {
+  const typename F::K K = F::konst(tb.primes[pi]);
+  const u64* src = row_ptr(in, r) + (b << 8);
+  typename F::T x[16];
+#pragma unroll
+  for (int e = 0; e < 16; ++e) x[e] = F::from_u64(src[l + 16 * e]);
+  blk_inv_body<F, LOGN1>(x, s, F::table(tb, true, pi), b, l, K);
+  u64* dst = row_ptr(out, r) + (b << 8);
+#pragma unroll
+  for (int e = 0; e < 16; ++e) dst[l + 16 * e] = F::bits(x[e]);
+}
+
 template <int LOGN1>
 __global__ void __launch_bounds__(64)
     ntt_blk_inv(const __grid_constant__ RowMap in, const __grid_constant__ RowMap out,
-                const ulonglong2* __restrict__ itw_all, const PrimeConst* __restrict__ primes,
-                u32 logn) {
+                const __grid_constant__ NttTabs tb) {
   constexpr int N1 = 1 << LOGN1;
   __shared__ u64 sm[4][256 + 16];
-  const u32 n = 1u << logn;
   const u32 l = threadIdx.x & 15, bw = threadIdx.x >> 4;
   const u32 blk_global = blockIdx.x * 4 + bw;
   const u32 r = blk_global / N1;
   const u32 b = blk_global - r * N1;
   const u32 pi = row_prime(in, r);
-  const PrimeConst P = primes[pi];
-  const ulonglong2* tw = itw_all + (u64)pi * n;
-  const u64* src = row_ptr(in, r) + (b << 8);
-  u64 x[16];
-#pragma unroll
-  for (int e = 0; e < 16; ++e) x[e] = src[l + 16 * e];
-  blk_inv_body<LOGN1>(x, sm[bw], tw, b, l, P);
-  u64* dst = row_ptr(out, r) + (b << 8);
-#pragma unroll
-  for (int e = 0; e < 16; ++e) dst[l + 16 * e] = x[e];
+  if (row_fp(tb, pi))
+    blk_inv_kernel_body<FpF, LOGN1>(in, out, tb, sm[bw], r, b, l, pi);
+  else
+    blk_inv_kernel_body<IntF, LOGN1>(in, out, tb, sm[bw], r, b, l, pi);
 }
 
-// Column pass, inverse: GS stages m = N1/2 .. 1, then x N^-1 and a full
-// reduction; the result goes through the epilogue.
+// Column pass, inverse: GS stages m = N1/2 .. 1 with x N^-1 folded into the
+// last one; the fully reduced result goes through the epilogue.
+template <class F, int LOGN1, int E, class Epi>
+__device__ __forceinline__ void col_inv_body(const RowMap& in, const Epi& epi, const NttTabs& tb,
+                                             u64* sm, u32 r, u32 j, u32 c, u32 k, u32 pi) {
+  constexpr int N1 = 1 << LOGN1;
+  constexpr int R = N1 / E;
+  const u32 n2 = (1u << tb.logn) >> LOGN1;
+  const PrimeConst P = tb.primes[pi];
+  const typename F::K K = F::konst(P);
+  const typename F::TwPtr tw = F::table(tb, true, pi);
+  const u64* src = row_ptr(in, r);
+  typename F::T x[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) x[e] = F::unbits(src[j + (k * E + e) * n2]);
+  col_inv_phase1<F, LOGN1, E>(x, tw, k, K);
+  F::gs_fix(x, K);
+#pragma unroll
+  for (int e = 0; e < E; ++e) sm[(k * E + e) * 16 + c] = F::bits(x[e]);
+  __syncthreads();
+#pragma unroll
+  for (int e = 0; e < E; ++e) x[e] = F::unbits(sm[(k + R * e) * 16 + c]);
+  col_inv_phase2<F, E>(x, tw, K, P);
+  const auto row = epi.bind(r, pi, P);
+#pragma unroll
+  for (int e = 0; e < E; ++e) row(j + (k + R * e) * n2, F::canon_last(x[e], K));
+}
+
 template <int LOGN1, int E, class Epi>
 __global__ void __launch_bounds__(16 * ((1 << LOGN1) / E))
     ntt_col_inv(const __grid_constant__ RowMap in, const __grid_constant__ Epi epi,
-                const ulonglong2* __restrict__ itw_all, const PrimeConst* __restrict__ primes,
-                u32 logn) {
-  constexpr int N1 = 1 << LOGN1;
-  constexpr int R = N1 / E;
-  constexpr int LOGE = __builtin_ctz(E);
+                const __grid_constant__ NttTabs tb) {
   extern __shared__ u64 sm[];  // [N1][16]
-  const u32 n = 1u << logn;
-  const u32 n2 = n >> LOGN1;
-  const u32 groups = n2 >> 4;
+  const u32 groups = ((1u << tb.logn) >> LOGN1) >> 4;
   const u32 r = blockIdx.x / groups;
   const u32 g = blockIdx.x - r * groups;
   const u32 c = threadIdx.x & 15, k = threadIdx.x >> 4;
   const u32 j = (g << 4) + c;
   const u32 pi = row_prime(in, r);
-  const PrimeConst P = primes[pi];
-  const ulonglong2* tw = itw_all + (u64)pi * n;
-  const u64* src = row_ptr(in, r);
-  u64 x[E];
-#pragma unroll
-  for (int e = 0; e < E; ++e) x[e] = src[j + (k * E + e) * n2];
-  static_for<LOGN1 - 1, LOGE - 1, -1>([&](auto LM) {
-    constexpr int lm = decltype(LM)::value;
-    constexpr int d = N1 >> (lm + 1);
-    gs_stage<E, d>(x, [&](int gi) { return ldtw(tw, (1 << lm) + ((k * E + gi * 2 * d) >> (LOGN1 - lm))); },
-                   P.q, P.two_q);
-  });
-#pragma unroll
-  for (int e = 0; e < E; ++e) sm[(k * E + e) * 16 + c] = x[e];
-  __syncthreads();
-#pragma unroll
-  for (int e = 0; e < E; ++e) x[e] = sm[(k + R * e) * 16 + c];
-  static_for<LOGE - 1, 0, -1>([&](auto LM) {
-    constexpr int lm = decltype(LM)::value;
-    gs_stage<E, (E >> (lm + 1))>(x, [&](int gi) { return ldtw(tw, (1 << lm) + gi); }, P.q, P.two_q);
-  });
-  // last stage (m = 1) with N^-1 folded in: x' = (x + y) N^-1, y' = (x - y) (w N^-1)
-  const auto row = epi.bind(r, pi, P);
-#pragma unroll
-  for (int e = 0; e < E / 2; ++e) {
-    const u64 a = x[e], bb = x[e + E / 2];
-    x[e] = mul_shoup(a + bb, P.n_inv, P.n_inv_shoup, P.q);
-    x[e + E / 2] = mul_shoup(a - bb + P.two_q, P.w1n, P.w1n_shoup, P.q);
-  }
-#pragma unroll
-  for (int e = 0; e < E; ++e) row(j + (k + R * e) * n2, x[e]);
+  if (row_fp(tb, pi))
+    col_inv_body<FpF, LOGN1, E>(in, epi, tb, sm, r, j, c, k, pi);
+  else
+    col_inv_body<IntF, LOGN1, E>(in, epi, tb, sm, r, j, c, k, pi);
 }
 
 // ------------------------------------------------------------ fused column pass
@@ -613,107 +798,129 @@ __global__ void __launch_bounds__(16 * ((1 << LOGN1) / E))
 // inverse column pass, its HBM round trip and the lift's fan-out re-reads.
 //   src: rows after the inverse block pass (ntt_blk_inv), prime = source prime
 //   dst: destination rows, dst row = src_row * fan + f, prime from dst.prime_of
+// The coefficient v of the source prime q_s is lifted by the reference's rule
+// (centred: v > q_s / 2 means v - q_s) into each destination prime:
+//   integer source: v in [0, q_s) -> int_lift (integer dest) or its double;
+//   FP64 source: the exact centred double c -> c itself (FP64 dest) or
+//   c mod q_d as a word (integer dest).
+template <class Fs, class Fd>
+__device__ __forceinline__ typename Fd::T lift_to(typename Fs::T v, u64 qs_half, u64 corr,
+                                                  const PrimeConst& D) {
+  if constexpr (std::is_same<Fs, IntF>::value) {
+    const u64 x = int_lift(v, qs_half, corr, D.q, D.mu56);
+    if constexpr (std::is_same<Fd, IntF>::value)
+      return x;
+    else
+      return u2d(x);
+  } else {
+    if constexpr (std::is_same<Fd, FpF>::value) {
+      return v;
+    } else {
+      const long long i = d2ll(v);
+      return (u64)(i + ((i >> 63) & (long long)D.q));
+    }
+  }
+}
+
+template <class Fs, class Fd, int LOGN1, int E>
+__device__ __forceinline__ void col_lift_fwd(const typename Fs::T (&v)[E], const RowMap& dst, u32 rd,
+                                             u32 pd, u64 qs_half, u64 corr, const NttTabs& tb,
+                                             u64* sm, u32 j, u32 c, u32 k) {
+  constexpr int N1 = 1 << LOGN1;
+  constexpr int R = N1 / E;
+  const u32 n2 = (1u << tb.logn) >> LOGN1;
+  const PrimeConst D = tb.primes[pd];
+  const typename Fd::K K = Fd::konst(D);
+  const typename Fd::TwPtr tw = Fd::table(tb, false, pd);
+  typename Fd::T x[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) x[e] = lift_to<Fs, Fd>(v[e], qs_half, corr, D);
+  col_fwd_phase1<Fd, LOGN1, E>(x, tw, K);
+  __syncthreads();  // the previous user of sm[] is done
+#pragma unroll
+  for (int e = 0; e < E; ++e) sm[(k + R * e) * 16 + c] = Fd::bits(x[e]);
+  __syncthreads();
+#pragma unroll
+  for (int e = 0; e < E; ++e) x[e] = Fd::unbits(sm[(k * E + e) * 16 + c]);
+  col_fwd_phase2<Fd, LOGN1, E>(x, tw, k, K);
+  u64* o = row_ptr(dst, rd);
+#pragma unroll
+  for (int e = 0; e < E; ++e) o[j + (k * E + e) * n2] = Fd::bits(x[e]);
+}
+
+template <class Fs, int LOGN1, int E>
+__device__ __forceinline__ void col_ilf_body(const RowMap& src, const RowMap& dst, u32 fan,
+                                             const u64* smod, u32 nprimes, const NttTabs& tb,
+                                             u64* sm, u32 rs, u32 j, u32 c, u32 k, u32 ps) {
+  constexpr int N1 = 1 << LOGN1;
+  constexpr int R = N1 / E;
+  const u32 n2 = (1u << tb.logn) >> LOGN1;
+  typename Fs::T v[E];  // coefficient-domain source values, rows k + R e
+  {
+    const PrimeConst S = tb.primes[ps];
+    const typename Fs::K K = Fs::konst(S);
+    const typename Fs::TwPtr itw = Fs::table(tb, true, ps);
+    const u64* in = row_ptr(src, rs);
+#pragma unroll
+    for (int e = 0; e < E; ++e) v[e] = Fs::unbits(in[j + (k * E + e) * n2]);
+    col_inv_phase1<Fs, LOGN1, E>(v, itw, k, K);
+    Fs::gs_fix(v, K);
+#pragma unroll
+    for (int e = 0; e < E; ++e) sm[(k * E + e) * 16 + c] = Fs::bits(v[e]);
+    __syncthreads();
+#pragma unroll
+    for (int e = 0; e < E; ++e) v[e] = Fs::unbits(sm[(k + R * e) * 16 + c]);
+    col_inv_phase2<Fs, E>(v, itw, K, S);
+    if constexpr (std::is_same<Fs, FpF>::value) {
+      // exact centred coefficient (|v| <= 0.75 q_s on entry)
+#pragma unroll
+      for (int e = 0; e < E; ++e) v[e] = f_reduce(v[e], K.q, K.qinv);
+    }
+  }
+  const u64 qs_half = __ldg(&tb.primes[ps].half);
+#pragma unroll 1
+  for (u32 f = 0; f < fan; ++f) {
+    const u32 rd = rs * fan + f;
+    const u32 pd = row_prime(dst, rd);
+    const u64 corr = __ldg(&tb.primes[pd].q) - __ldg(smod + ps * nprimes + pd);
+    if (row_fp(tb, pd))
+      col_lift_fwd<Fs, FpF, LOGN1, E>(v, dst, rd, pd, qs_half, corr, tb, sm, j, c, k);
+    else
+      col_lift_fwd<Fs, IntF, LOGN1, E>(v, dst, rd, pd, qs_half, corr, tb, sm, j, c, k);
+  }
+}
+
 template <int LOGN1, int E>
 __global__ void __launch_bounds__(16 * ((1 << LOGN1) / E))
     ntt_col_inv_lift_fwd(const __grid_constant__ RowMap src, const __grid_constant__ RowMap dst,
-                         u32 fan, const ulonglong2* __restrict__ tw_all,
-                         const ulonglong2* __restrict__ itw_all,
-                         const PrimeConst* __restrict__ primes, const u64* __restrict__ smod,
-                         u32 nprimes, u32 logn) {
-  constexpr int N1 = 1 << LOGN1;
-  constexpr int R = N1 / E;
-  constexpr int LOGE = __builtin_ctz(E);
+                         u32 fan, const u64* __restrict__ smod, u32 nprimes,
+                         const __grid_constant__ NttTabs tb) {
   extern __shared__ u64 sm[];  // [N1][16]
-  const u32 n = 1u << logn;
-  const u32 n2 = n >> LOGN1;
-  const u32 groups = n2 >> 4;
+  const u32 groups = ((1u << tb.logn) >> LOGN1) >> 4;
   const u32 rs = blockIdx.x / groups;
   const u32 g = blockIdx.x - rs * groups;
   const u32 c = threadIdx.x & 15, k = threadIdx.x >> 4;
   const u32 j = (g << 4) + c;
   const u32 ps = row_prime(src, rs);
-  u64 v[E];  // coefficient-domain source values, rows k + R e
-  {
-    const PrimeConst S = primes[ps];
-    const ulonglong2* itw = itw_all + (u64)ps * n;
-    const u64* in = row_ptr(src, rs);
-#pragma unroll
-    for (int e = 0; e < E; ++e) v[e] = in[j + (k * E + e) * n2];
-    static_for<LOGN1 - 1, LOGE - 1, -1>([&](auto LM) {
-      constexpr int lm = decltype(LM)::value;
-      constexpr int d = N1 >> (lm + 1);
-      gs_stage<E, d>(v, [&](int gi) { return ldtw(itw, (1 << lm) + ((k * E + gi * 2 * d) >> (LOGN1 - lm))); },
-                     S.q, S.two_q);
-    });
-#pragma unroll
-    for (int e = 0; e < E; ++e) sm[(k * E + e) * 16 + c] = v[e];
-    __syncthreads();
-#pragma unroll
-    for (int e = 0; e < E; ++e) v[e] = sm[(k + R * e) * 16 + c];
-    static_for<LOGE - 1, 0, -1>([&](auto LM) {
-      constexpr int lm = decltype(LM)::value;
-      gs_stage<E, (E >> (lm + 1))>(v, [&](int gi) { return ldtw(itw, (1 << lm) + gi); }, S.q, S.two_q);
-    });
-#pragma unroll
-    for (int e = 0; e < E / 2; ++e) {
-      const u64 a = v[e], bb = v[e + E / 2];
-      v[e] = mul_shoup(a + bb, S.n_inv, S.n_inv_shoup, S.q);
-      v[e + E / 2] = mul_shoup(a - bb + S.two_q, S.w1n, S.w1n_shoup, S.q);
-    }
-  }
-  const u64 qs_half = __ldg(&primes[ps].half);
-#pragma unroll 1
-  for (u32 f = 0; f < fan; ++f) {
-    const u32 rd = rs * fan + f;
-    const u32 pd = row_prime(dst, rd);
-    const PrimeConst P = primes[pd];
-    const ulonglong2* tw = tw_all + (u64)pd * n;
-    const u64 corr = P.q - __ldg(smod + ps * nprimes + pd);
-    u64 x[E];
-    // centred lift (rns.cpp:370-378) with the 32x32 Barrett of LiftLoad
-#pragma unroll
-    for (int e = 0; e < E; ++e) {
-      const u64 s = v[e];
-      const u64 qh = ((u64)(u32)(s >> 24) * P.mu56) >> 32;
-      u64 w = s - qh * P.q;
-      if (s > qs_half) w += corr;
-      x[e] = w;
-    }
-    static_for<0, LOGE, 1>([&](auto LM) {
-      constexpr int lm = decltype(LM)::value;
-      ct_stage<E, (E >> (lm + 1))>(x, [&](int gi) { return ldtw(tw, (1 << lm) + gi); }, P.q, P.two_q);
-    });
-    __syncthreads();  // the previous user of sm[] is done
-#pragma unroll
-    for (int e = 0; e < E; ++e) sm[(k + R * e) * 16 + c] = x[e];
-    __syncthreads();
-#pragma unroll
-    for (int e = 0; e < E; ++e) x[e] = sm[(k * E + e) * 16 + c];
-    static_for<LOGE, LOGN1, 1>([&](auto LM) {
-      constexpr int lm = decltype(LM)::value;
-      constexpr int d = N1 >> (lm + 1);
-      ct_stage<E, d>(x, [&](int gi) { return ldtw(tw, (1 << lm) + ((k * E + gi * 2 * d) >> (LOGN1 - lm))); },
-                     P.q, P.two_q);
-    });
-    u64* o = row_ptr(dst, rd);
-#pragma unroll
-    for (int e = 0; e < E; ++e) o[j + (k * E + e) * n2] = x[e];
-  }
+  if (row_fp(tb, ps))
+    col_ilf_body<FpF, LOGN1, E>(src, dst, fan, smod, nprimes, tb, sm, rs, j, c, k, ps);
+  else
+    col_ilf_body<IntF, LOGN1, E>(src, dst, fan, smod, nprimes, tb, sm, rs, j, c, k, ps);
 }
 
 // Single-CTA transform for small rings (N <= 4096): the whole row in shared
-// memory, reference stage order.
+// memory, reference stage order, integer field only.
 template <bool INV, class Loader, class Epi>
 __global__ void __launch_bounds__(256)
     ntt_small(const __grid_constant__ Loader ld, const __grid_constant__ Epi epi,
-              const __grid_constant__ RowMap rows, const ulonglong2* __restrict__ tw_all,
-              const PrimeConst* __restrict__ primes, u32 logn) {
+              const __grid_constant__ RowMap rows, const __grid_constant__ NttTabs tb) {
   extern __shared__ u64 smem[];
-  const u32 n = 1u << logn;
+  const u32 n = 1u << tb.logn;
   const u32 r = blockIdx.x;
   const u32 pi = row_prime(rows, r);
-  const PrimeConst P = primes[pi];
-  const ulonglong2* tw = tw_all + (u64)pi * n;
+  const PrimeConst P = tb.primes[pi];
+  const IntF::K K = IntF::konst(P);
+  const IntF::TwPtr tw = IntF::table(tb, INV, pi);
   {
     const auto row = ld.bind(r, pi, P);
     for (u32 a = threadIdx.x; a < n; a += blockDim.x) smem[a] = row(a);
@@ -727,7 +934,7 @@ __global__ void __launch_bounds__(256)
       for (u32 bt = threadIdx.x; bt < n / 2; bt += blockDim.x) {
         const u32 i = bt / half, jj = bt - i * half;
         const u32 a0 = 2 * i * half + jj;
-        ct_bfly(smem[a0], smem[a0 + half], ldtw(tw, m + i), P.q, 2 * P.two_q);
+        IntF::ct(smem[a0], smem[a0 + half], IntF::ld(tw, m + i), K);
       }
       __syncthreads();
     }
@@ -738,7 +945,7 @@ __global__ void __launch_bounds__(256)
       for (u32 bt = threadIdx.x; bt < n / 2; bt += blockDim.x) {
         const u32 i = bt / half, jj = bt - i * half;
         const u32 a0 = 2 * i * half + jj;
-        gs_bfly(smem[a0], smem[a0 + half], ldtw(tw, m + i), P.q, P.two_q);
+        IntF::gs(smem[a0], smem[a0 + half], IntF::ld(tw, m + i), K);
       }
       __syncthreads();
       half <<= 1;
