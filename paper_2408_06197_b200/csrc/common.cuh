@@ -229,11 +229,21 @@ struct Acc3 {
     madw(s1, x.lo, x.hi << 1);  // x.hi < 2^23, so 2 x.hi fits 32 bits
     madw(s2, x.hi, x.hi);
   }
+  // x^2 with the cross term halved: s1 += lo * hi (value = s0 + s1*2^24 + s2*2^46,
+  // see reduce_sq); one IMAD.WIDE and no shift per square.
+  __device__ __forceinline__ void sqh(Split x) {
+    madw(s0, x.lo, x.lo);
+    madw(s1, x.lo, x.hi);
+    madw(s2, x.hi, x.hi);
+  }
   // Fully reduced value mod q.
-  __device__ __forceinline__ u64 reduce(const PrimeConst& p) const {
-    // v = s0 + s1*2^23 + s2*2^46 as a 128-bit (lo, hi).
+  __device__ __forceinline__ u64 reduce(const PrimeConst& p) const { return reduce_sh<23>(p); }
+  __device__ __forceinline__ u64 reduce_sq(const PrimeConst& p) const { return reduce_sh<24>(p); }
+  template <int SH>
+  __device__ __forceinline__ u64 reduce_sh(const PrimeConst& p) const {
+    // v = s0 + s1*2^SH + s2*2^46 as a 128-bit (lo, hi).
     u64 lo = s0, hi = 0;
-    const u64 a = s1 << 23, ah = s1 >> 41;
+    const u64 a = s1 << SH, ah = s1 >> (64 - SH);
     lo += a;
     hi += ah + (lo < a ? 1ull : 0ull);
     const u64 b = s2 << 46, bh = s2 >> 18;

@@ -20,6 +20,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <tuple>
 #include <memory>
 #include <string>
 #include <vector>
@@ -254,11 +255,13 @@ struct lcl_context {
   double2* d_twf = nullptr;   // (w, w / q) doubles for FP64 rows
   double2* d_itwf = nullptr;
   u32 fp_mask = 0;            // primes whose rows run on the FP64 pipe
+  bool pair_f64 = false;      // q-chain below 2^44: pair accumulation on the FP64 pipe
   u64* d_smod = nullptr;
   ulonglong2* d_pinv = nullptr;  // [(full+1) * (full+1)]: (q_div^-1 mod q_dst, shoup)
   u32* d_pairs = nullptr;
   size_t pairs_cap = 0;
   u32 pairs_n = 0;
+  std::map<std::tuple<u32, u32, u32, u32>, uint2*> sched;  // pair_schedule cache
   u64* d_relin = nullptr;
   u64* d_relin_shoup = nullptr;
   std::map<size_t, u64*> d_rot;
@@ -837,14 +840,15 @@ void ensure_pairs(lcl_context* c, u32 n) {
   c->pairs_n = n;
 }
 
-constexpr int kStages = 3;
-
 // Lazy ternary accumulators for pairs [p0, p1) over chunks [c0, c1). Tiles of
-// 8 slots, 2 threads per pair (4 slots each), up to 256 pairs per CTA: each
-// client word is read from HBM once per pair group.
-void pair_accumulate_launch(lcl_context* c, const u64* clients, u32 n, u32 chunks, u32 c0,
-                            u32 c1, u32 p0, u32 p1, u64* tern, bool accumulate) {
-  constexpr int TE = 8, EPT = 4, TPP = TE / EPT;
+// TE slots, TE / EPT threads per pair, up to 256 pairs per CTA: each client
+// word is read from HBM once per pair group. STAGES chunks are in flight per
+// CTA (one CTA per SM: the accumulators of 190 pairs x 8 slots fill the
+// register file, so the copy pipeline, not occupancy, hides HBM latency).
+template <int TE, int EPT, int STAGES>
+void pair_accumulate_cfg(lcl_context* c, const u64* clients, u32 n, u32 chunks, u32 c0,
+                         u32 c1, u32 p0, u32 p1, u64* tern, bool accumulate) {
+  constexpr int TPP = TE / EPT;
   const u32 m = c->full;
   const u32 pairs = p1 - p0;
   const u32 groups = (pairs + 255) / 256;
@@ -852,15 +856,116 @@ void pair_accumulate_launch(lcl_context* c, const u64* clients, u32 n, u32 chunk
   const u32 threads = std::max<u32>(64, ((per_cta * TPP + 31) / 32) * 32);
   need(n * TE <= 4 * threads, LCL_SHAPE_ERROR, "too many clients for one tile");
   dim3 grid((u32)(m * c->n / TE), groups);
-  const size_t smem = (size_t)kStages * n * (2 * TE + 2) * 8;
+  const size_t smem = (size_t)STAGES * n * (2 * TE + 2) * 8;
   need(smem <= 200 * 1024, LCL_SHAPE_ERROR, "too many clients for one tile");
-  allow_smem(pair_accumulate<TE, EPT, kStages>, smem);
+  allow_smem(pair_accumulate<TE, EPT, STAGES>, smem);
   ProfScope ps(c, "pair_accumulate",
                8.0 * c->N() * m * (2.0 * n * (c1 - c0) * groups + 3.0 * pairs * (accumulate ? 2 : 1)));
-  pair_accumulate<TE, EPT, kStages><<<grid, threads, smem, c->stream>>>(
+  pair_accumulate<TE, EPT, STAGES><<<grid, threads, smem, c->stream>>>(
       clients, n, c0, c1, chunks, m, c->logn, c->d_pairs, p0, p1, per_cta, tern,
       accumulate ? 1 : 0, c->d_primes);
   post_launch(c);
+}
+
+// Bank-aware pair schedule for pair_accumulate_f64 (TPP = 1): pairs
+// [p0, p1) of the i<j order cut into CTA groups of per_cta; inside a group,
+// every quarter warp (8 threads, one 16-byte shared-memory wavefront) gets
+// pairs whose i's and j's fall in distinct bank groups (client k's tile row
+// starts at 16-byte unit k * CS / 2, CS / 2 odd), greedily.
+const uint2* pair_schedule(lcl_context* c, u32 n, u32 p0, u32 p1, u32 per_cta, u32 cs_half) {
+  const auto key = std::make_tuple(n, p0, p1, per_cta * 64 + cs_half);
+  auto it = c->sched.find(key);
+  if (it != c->sched.end()) return it->second;
+  std::vector<uint2> all;
+  {
+    u32 p = 0;
+    for (u32 i = 0; i < n; ++i)
+      for (u32 j = i + 1; j < n; ++j, ++p)
+        if (p >= p0 && p < p1) all.push_back(make_uint2(i | (j << 16), p - p0));
+  }
+  std::vector<uint2> out;
+  out.reserve(all.size());
+  for (size_t g0 = 0; g0 < all.size(); g0 += per_cta) {
+    std::vector<uint2> rem(all.begin() + g0, all.begin() + std::min(all.size(), (size_t)g0 + per_cta));
+    while (!rem.empty()) {
+      int ib[8], jb[8];
+      for (int b = 0; b < 8; ++b) ib[b] = jb[b] = -1;
+      std::vector<uint2> grp, rest;
+      for (const uint2& e : rem) {
+        const int i = e.x & 0xFFFF, j = e.x >> 16;
+        const int bi = (int)((i * cs_half) % 8), bj = (int)((j * cs_half) % 8);
+        if (grp.size() < 8 && (ib[bi] < 0 || ib[bi] == i) && (jb[bj] < 0 || jb[bj] == j)) {
+          ib[bi] = i;
+          jb[bj] = j;
+          grp.push_back(e);
+        } else {
+          rest.push_back(e);
+        }
+      }
+      while (grp.size() < 8 && !rest.empty()) {  // no conflict-free pair left: accept one
+        grp.push_back(rest.front());
+        rest.erase(rest.begin());
+      }
+      out.insert(out.end(), grp.begin(), grp.end());
+      rem.swap(rest);
+    }
+  }
+  uint2* d = nullptr;
+  cuda_check(cudaMalloc(&d, out.size() * sizeof(uint2)), "schedule alloc");
+  cuda_check(cudaMemcpy(d, out.data(), out.size() * sizeof(uint2), cudaMemcpyHostToDevice),
+             "schedule upload");
+  c->sched[key] = d;
+  return d;
+}
+
+template <int TE, int STAGES>
+bool pair_accumulate_f64_cfg(lcl_context* c, const u64* clients, u32 n, u32 chunks, u32 c0,
+                             u32 c1, u32 p0, u32 p1, u64* tern, bool accumulate) {
+  constexpr int MAXT = 192;
+  const u32 m = c->full;
+  const u32 pairs = p1 - p0;
+  const u32 groups = (pairs + MAXT - 1) / MAXT;
+  const u32 per_cta = (pairs + groups - 1) / groups;
+  const u32 threads = std::max<u32>(64, ((per_cta + 31) / 32) * 32);
+  if (n * TE > threads) return false;  // one copy per thread per chunk
+  const size_t smem = (size_t)STAGES * n * (2 * TE + 2) * 8;
+  if (smem > 100 * 1024) return false;
+  const uint2* sched = pair_schedule(c, n, p0, p1, per_cta, TE + 1);
+  const u64 tiles = (u64)m * c->n / TE;
+  allow_smem(pair_accumulate_f64<TE, STAGES, MAXT>, smem);
+  for (u32 cb = c0; cb < c1; cb += 256) {  // exact for 256 chunks per pass
+    const u32 ce = std::min(c1, cb + 256);
+    const bool acc = accumulate || cb > c0;
+    ProfScope ps(c, "pair_accumulate",
+                 8.0 * c->N() * m * (2.0 * n * (ce - cb) * groups + 3.0 * pairs * (acc ? 2 : 1)));
+    pair_accumulate_f64<TE, STAGES, MAXT><<<(u32)(tiles * groups), threads, smem, c->stream>>>(
+        clients, n, cb, ce, chunks, m, c->logn, sched, pairs, groups, per_cta, tern, acc ? 1 : 0,
+        c->d_primes);
+    post_launch(c);
+  }
+  return true;
+}
+
+void pair_accumulate_launch(lcl_context* c, const u64* clients, u32 n, u32 chunks, u32 c0,
+                            u32 c1, u32 p0, u32 p1, u64* tern, bool accumulate) {
+  static const int variant = [] {
+    const char* e = getenv("LCL_PA_VARIANT");
+    return e ? atoi(e) : 0;
+  }();
+  if (c->pair_f64) {
+    if (variant == 0 && pair_accumulate_f64_cfg<4, 8>(c, clients, n, chunks, c0, c1, p0, p1, tern, accumulate)) return;
+    if (variant == 10 && pair_accumulate_f64_cfg<4, 5>(c, clients, n, chunks, c0, c1, p0, p1, tern, accumulate)) return;
+    if (variant == 11 && pair_accumulate_f64_cfg<2, 8>(c, clients, n, chunks, c0, c1, p0, p1, tern, accumulate)) return;
+    if (variant == 12 && pair_accumulate_f64_cfg<4, 12>(c, clients, n, chunks, c0, c1, p0, p1, tern, accumulate)) return;
+  }
+  switch (variant) {
+    case 1: return pair_accumulate_cfg<8, 4, 4>(c, clients, n, chunks, c0, c1, p0, p1, tern, accumulate);
+    case 2: return pair_accumulate_cfg<8, 4, 12>(c, clients, n, chunks, c0, c1, p0, p1, tern, accumulate);
+    case 3: return pair_accumulate_cfg<4, 2, 8>(c, clients, n, chunks, c0, c1, p0, p1, tern, accumulate);
+    case 4: return pair_accumulate_cfg<4, 4, 8>(c, clients, n, chunks, c0, c1, p0, p1, tern, accumulate);
+    case 5: return pair_accumulate_cfg<8, 2, 8>(c, clients, n, chunks, c0, c1, p0, p1, tern, accumulate);
+    default: return pair_accumulate_cfg<8, 4, 8>(c, clients, n, chunks, c0, c1, p0, p1, tern, accumulate);
+  }
 }
 
 void hadd_into(lcl_context* c, u64* acc, const u64* x, u32 B, u32 m) {
@@ -975,8 +1080,21 @@ void masked_aggregate(lcl_context* c, const u64* clients, const u64* sel, u32 n,
     const u64 threads = ((B + CK - 1) / CK) * slots;
     {
       ProfScope ps(c, "aggregate_tensor", 8.0 * slots * (2.0 * n * B + 2.0 * n + 3.0 * B));
-      aggregate_tensor<CK><<<(u32)((threads + 255) / 256), 256, 0, c->stream>>>(
-          clients, sel, n, chunks, c0, B, m, c->logn, tern, c->d_primes);
+      static const bool stream_form = [] {
+        const char* e = getenv("LCL_AGG_VARIANT");
+        return !(e && atoi(e) == 1);
+      }();
+      if (stream_form) {
+        constexpr int ST = 6;
+        const size_t smem = (size_t)ST * 4 * 256 * 16;
+        allow_smem(aggregate_stream<ST>, smem);
+        const u64 th = (u64)B * slots / 2;
+        aggregate_stream<ST><<<(u32)((th + 255) / 256), 256, smem, c->stream>>>(
+            clients, sel, n, chunks, c0, B, m, c->logn, tern, c->d_primes);
+      } else {
+        aggregate_tensor<CK><<<(u32)((threads + 255) / 256), 256, 0, c->stream>>>(
+            clients, sel, n, chunks, c0, B, m, c->logn, tern, c->d_primes);
+      }
     }
     post_launch(c);
     u64* ctA = c->ws_ctA.get((u64)B * 2 * m * N);
@@ -1144,6 +1262,13 @@ void build_context(lcl_context* c, size_t degree, int depth, int secure, int dev
   cuda_check(cudaMemcpy(c->d_twf, twf.data(), P * n * sizeof(double2), cudaMemcpyHostToDevice), "upload");
   cuda_check(cudaMemcpy(c->d_itwf, itwf.data(), P * n * sizeof(double2), cudaMemcpyHostToDevice), "upload");
   c->fp_mask = fp_rows(c->primes);
+  {
+    // pair_accumulate_f64 needs |x - y| < 2^44 for every q-chain residue
+    const char* env = std::getenv("LCL_PAIR_F64");
+    bool ok = !(env && env[0] == '0');
+    for (u32 d = 0; d < c->full; ++d) ok = ok && c->primes[d] < (1ull << 44);
+    c->pair_f64 = ok;
+  }
   cuda_check(cudaMemcpy(c->d_smod, smod.data(), P * P * 8, cudaMemcpyHostToDevice), "upload");
   cuda_check(cudaMemcpy(c->d_pinv, pinv.data(), P * P * sizeof(ulonglong2), cudaMemcpyHostToDevice), "upload");
 }
@@ -1157,6 +1282,7 @@ void free_context(lcl_context* c) {
   cudaFree(c->d_smod);
   cudaFree(c->d_pinv);
   cudaFree(c->d_pairs);
+  for (auto& kv : c->sched) cudaFree(kv.second);
   cudaFree(c->d_relin);
   cudaFree(c->d_relin_shoup);
   for (auto& kv : c->d_rot) cudaFree(kv.second);

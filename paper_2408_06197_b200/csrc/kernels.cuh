@@ -45,6 +45,7 @@ __global__ void __launch_bounds__(512)
                     u32 chunks_total, u32 m, u32 logn, const u32* __restrict__ pairs,
                     u32 p_begin, u32 p_end, u32 pairs_per_cta, u64* __restrict__ tern,
                     int accumulate, const PrimeConst* __restrict__ primes) {
+  static_assert(EPT % 2 == 0, "slots are read from shared memory in 16-byte pairs");
   constexpr int TPP = TE / EPT;    // threads per pair
   constexpr int CS = 2 * TE + 2;   // words per client in the tile (16-B aligned, banks spread)
   constexpr int V = 2 * TE / 2;    // 16-byte vectors per client per chunk
@@ -89,6 +90,8 @@ __global__ void __launch_bounds__(512)
     cp_async_commit();  // empty groups keep the wait count uniform
   };
 
+  // A00 / A11 hold e^2 with the cross term accumulated once (lo * hi) and
+  // doubled in the final reduction; A01 holds e0 * e1.
   Acc3 A00[EPT], A01[EPT], A11[EPT];
 #pragma unroll
   for (int t = 0; t < EPT; ++t) {
@@ -98,32 +101,182 @@ __global__ void __launch_bounds__(512)
   }
 #pragma unroll
   for (int s = 0; s < STAGES - 1; ++s) issue(c_begin + s, s);
+  // One barrier per chunk: after it every thread has finished chunk c - 1, so
+  // its stage can be refilled with chunk c + STAGES - 1 while c is consumed.
   u32 stage = 0;
   for (u32 c = c_begin; c < c_end; ++c) {
-    issue(c + STAGES - 1, (stage + STAGES - 1) % STAGES);
-    cp_async_wait<STAGES - 1>();
+    cp_async_wait<STAGES - 2>();
     __syncthreads();
+    issue(c + STAGES - 1, stage == 0 ? STAGES - 1 : stage - 1);
     const u64* tl = tile + stage * tw;
 #pragma unroll
-    for (int t = 0; t < EPT; ++t) {
-      const u64 x0 = tl[oi + t], x1 = tl[oi + TE + t];
-      const u64 y0 = tl[oj + t], y1 = tl[oj + TE + t];
-      const Split e0 = split23(x0 - y0 + q), e1 = split23(x1 - y1 + q);
-      A00[t].sq(e0);
-      A01[t].mac(e0, e1);
-      A11[t].sq(e1);
+    for (int t = 0; t < EPT; t += 2) {
+      const ulonglong2 x0 = *reinterpret_cast<const ulonglong2*>(tl + oi + t);
+      const ulonglong2 x1 = *reinterpret_cast<const ulonglong2*>(tl + oi + TE + t);
+      const ulonglong2 y0 = *reinterpret_cast<const ulonglong2*>(tl + oj + t);
+      const ulonglong2 y1 = *reinterpret_cast<const ulonglong2*>(tl + oj + TE + t);
+      {
+        const Split e0 = split23(x0.x - y0.x + q), e1 = split23(x1.x - y1.x + q);
+        A00[t].sqh(e0);
+        A01[t].mac(e0, e1);
+        A11[t].sqh(e1);
+      }
+      {
+        const Split e0 = split23(x0.y - y0.y + q), e1 = split23(x1.y - y1.y + q);
+        A00[t + 1].sqh(e0);
+        A01[t + 1].mac(e0, e1);
+        A11[t + 1].sqh(e1);
+      }
     }
-    __syncthreads();
     stage = stage + 1 == STAGES ? 0 : stage + 1;
   }
   if (!valid) return;
 #pragma unroll
   for (int t = 0; t < EPT; ++t) {
     u64* o = tern + (u64)(p - p_begin) * 3 * m * N + (u64)r * N + a0 + eg * EPT + t;
-    u64 d0 = A00[t].reduce(P);
+    u64 d0 = A00[t].reduce_sq(P);
     u64 d1 = A01[t].reduce(P);
     d1 = add_mod(d1, d1, q);
-    u64 d2 = A11[t].reduce(P);
+    u64 d2 = A11[t].reduce_sq(P);
+    if (accumulate) {
+      d0 = add_mod(d0, o[0], q);
+      d1 = add_mod(d1, o[(u64)m * N], q);
+      d2 = add_mod(d2, o[2ull * m * N], q);
+    }
+    o[0] = d0;
+    o[(u64)m * N] = d1;
+    o[2ull * m * N] = d2;
+  }
+}
+
+// FP64-pipe form of the same accumulation, for q-chains below 2^44. B200
+// retires 64 DFMA/clk/SM but only 32 IMAD.WIDE/clk/SM, so the products run
+// on the FP64 pipe (tools/microbench/pair_forms.cu: 4.3 vs 1.7 pair-slots per
+// clock per SM). Per slot: e = x - y + 2^45 on the integer ALU, split into
+// e = eh * 2^22 + el with |eh| <= 2^22, 0 <= el < 2^22 (shift / mask), each
+// half turned into an exact double by one DADD on the exponent-biased word;
+// then ten exact DFMA products (each |p| <= 2^45) feed ten double
+// accumulators that stay exact (< 2^53) for up to 256 chunks -- the launcher
+// splits longer chunk ranges and re-enters with accumulate = 1. Results are
+// the same integers as the split-23 kernel, reduced mod q once at the end.
+__device__ __forceinline__ u64 dmodq(double v, u64 q, const PrimeConst& P) {
+  const long long i = __double2ll_rn(v);  // exact: |v| < 2^53 is an integer
+  if (i >= 0) return reduce64((u64)i, P);
+  const u64 r = reduce64((u64)(-i), P);
+  return r ? q - r : 0;
+}
+
+// A thread owns one pair for the TE slots of its tile. Pairs are assigned to
+// threads by a host schedule (sched[k] = (i | j << 16, output index)) that
+// puts clients of distinct shared-memory bank groups in every quarter warp,
+// so the 16-byte tile reads are conflict-free. Each thread issues at most one
+// 16-byte cp.async per chunk (n * TE <= blockDim, checked by the launcher).
+template <int TE, int STAGES, int MAXT>
+__global__ void __launch_bounds__(MAXT, 2)
+    pair_accumulate_f64(const u64* __restrict__ clients, u32 n, u32 c_begin, u32 c_end,
+                        u32 chunks_total, u32 m, u32 logn, const uint2* __restrict__ sched,
+                        u32 pairs, u32 groups, u32 pairs_per_cta, u64* __restrict__ tern,
+                        int accumulate, const PrimeConst* __restrict__ primes) {
+  static_assert(TE % 2 == 0, "slots are read from shared memory in 16-byte pairs");
+  constexpr int CS = 2 * TE + 2;  // words per client: CS / 2 odd spreads clients over bank groups
+  extern __shared__ u64 tile[];   // [STAGES][n][CS]
+  const u32 N = 1u << logn;
+  const u32 tiles_per_row = N / TE;
+  const u32 g = blockIdx.x % groups;
+  const u32 tix = blockIdx.x / groups;
+  const u32 r = tix / tiles_per_row;
+  const u32 a0 = (tix - r * tiles_per_row) * TE;
+  const u64 ct_words = 2ull * m * N;
+  const u32 tw = n * CS;
+  const u32 k = g * pairs_per_cta + threadIdx.x;
+  const bool valid = threadIdx.x < pairs_per_cta && k < pairs;
+  const uint2 sk = valid ? __ldg(sched + k) : make_uint2(0u, 0u);
+  const u32 oi = (sk.x & 0xFFFFu) * CS, oj = (sk.x >> 16) * CS;
+
+  // this thread's copy: vector v = threadIdx.x of the n * TE per chunk
+  const bool copier = threadIdx.x < n * TE;
+  const u64* gsrc = clients;
+  u32 soff = 0;
+  if (copier) {
+    const u32 cl = threadIdx.x / TE, w = (threadIdx.x - cl * TE) * 2, h = w / TE, e = w - h * TE;
+    gsrc = clients + (u64)cl * chunks_total * ct_words + (u64)h * m * N + (u64)r * N + a0 + e +
+           (u64)c_begin * ct_words;
+    soff = cl * CS + w;
+  }
+  auto issue = [&](u32 c, u32 stage) {
+    if (copier && c < c_end) cp_async16(tile + stage * tw + soff, gsrc + (u64)(c - c_begin) * ct_words);
+    cp_async_commit();
+  };
+
+  // per slot: e0^2 -> A = (sum el0^2, sum eh0 el0, sum eh0^2), e1^2 -> B,
+  // e0 e1 -> X = (sum el0 el1, sum el0 eh1 + eh0 el1, sum eh0 eh1)
+  double A[TE][3], Bv[TE][3], X[TE][3];
+#pragma unroll
+  for (int t = 0; t < TE; ++t)
+#pragma unroll
+    for (int q = 0; q < 3; ++q) A[t][q] = Bv[t][q] = X[t][q] = 0.0;
+  constexpr double kB52 = 4503599627370496.0;              // 2^52
+  constexpr double kB52h = 4503599627370496.0 + 8388608.0;  // 2^52 + 2^23
+  auto halves = [&](u64 x, u64 y, double& eh, double& el) {
+    const u64 e = x - y + (1ull << 45);  // in (2^44, 3 * 2^44): e - 2^45 = x - y
+    eh = __hiloint2double(0x43300000, (int)(u32)(e >> 22)) - kB52h;
+    el = __hiloint2double(0x43300000, (int)((u32)e & 0x3FFFFFu)) - kB52;
+  };
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) issue(c_begin + s, s);
+  u32 stage = 0;
+  for (u32 c = c_begin; c < c_end; ++c) {
+    cp_async_wait<STAGES - 2>();
+    __syncthreads();
+    issue(c + STAGES - 1, stage == 0 ? STAGES - 1 : stage - 1);
+    const u64* tl = tile + stage * tw;
+#pragma unroll
+    for (int t = 0; t < TE; t += 2) {
+      const ulonglong2 x0 = *reinterpret_cast<const ulonglong2*>(tl + oi + t);
+      const ulonglong2 x1 = *reinterpret_cast<const ulonglong2*>(tl + oi + TE + t);
+      const ulonglong2 y0 = *reinterpret_cast<const ulonglong2*>(tl + oj + t);
+      const ulonglong2 y1 = *reinterpret_cast<const ulonglong2*>(tl + oj + TE + t);
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        double h0, l0, h1, l1;
+        halves(u ? x0.y : x0.x, u ? y0.y : y0.x, h0, l0);
+        halves(u ? x1.y : x1.x, u ? y1.y : y1.x, h1, l1);
+        double* a = A[t + u];
+        double* b = Bv[t + u];
+        double* x = X[t + u];
+        a[0] = __fma_rn(l0, l0, a[0]);
+        a[1] = __fma_rn(h0, l0, a[1]);
+        a[2] = __fma_rn(h0, h0, a[2]);
+        b[0] = __fma_rn(l1, l1, b[0]);
+        b[1] = __fma_rn(h1, l1, b[1]);
+        b[2] = __fma_rn(h1, h1, b[2]);
+        x[0] = __fma_rn(l0, l1, x[0]);
+        x[1] = __fma_rn(l0, h1, x[1]);
+        x[1] = __fma_rn(h0, l1, x[1]);
+        x[2] = __fma_rn(h0, h1, x[2]);
+      }
+    }
+    stage = stage + 1 == STAGES ? 0 : stage + 1;
+  }
+  if (!valid) return;
+  const PrimeConst P = primes[r];
+  const u64 q = P.q;
+  const u64 w22 = reduce64(1ull << 22, P), w23 = reduce64(1ull << 23, P),
+            w44 = reduce64(1ull << 44, P);
+  auto combine = [&](const double* v, u64 wmid) {
+    // v[2] * 2^44 + v[1] * wmid + v[0]  (mod q)
+    u64 s = mul_mod(dmodq(v[2], q, P), w44, P);
+    s = add_mod(s, mul_mod(dmodq(v[1], q, P), wmid, P), q);
+    return add_mod(s, dmodq(v[0], q, P), q);
+  };
+  u64* ob = tern + (u64)sk.y * 3 * m * N + (u64)r * N + a0;
+#pragma unroll
+  for (int t = 0; t < TE; ++t) {
+    u64* o = ob + t;
+    u64 d0 = combine(A[t], w23);  // e0^2 = eh^2 2^44 + 2 eh el 2^22 + el^2
+    u64 d1 = combine(X[t], w22);
+    d1 = add_mod(d1, d1, q);      // hsquare's 2 c0 c1
+    u64 d2 = combine(Bv[t], w23);
     if (accumulate) {
       d0 = add_mod(d0, o[0], q);
       d1 = add_mod(d1, o[(u64)m * N], q);
@@ -214,6 +367,82 @@ __global__ void __launch_bounds__(256)
     o[slots] = d1;
     o[2 * slots] = d2;
   }
+}
+
+// Streaming form of the same tensor: a thread owns 2 consecutive slots of one
+// limb of one chunk (16-byte loads) and walks the n clients; the (w0, w1, s0,
+// s1) vectors of client i + STAGES - 1 are copied into a private shared-memory
+// ring (cp.async, no barrier: a thread only reads what it copied) while
+// client i is accumulated, so HBM latency is hidden by the copy ring rather
+// than by registers. Selectors are re-read per chunk from L2 (n * ct, small).
+template <int STAGES>
+__global__ void __launch_bounds__(256)
+    aggregate_stream(const u64* __restrict__ clients, const u64* __restrict__ sel, u32 n,
+                     u32 chunks_total, u32 c_begin, u32 chunks, u32 m, u32 logn,
+                     u64* __restrict__ tern, const PrimeConst* __restrict__ primes) {
+  extern __shared__ ulonglong2 ring[];  // [STAGES][4][blockDim]
+  const u32 N = 1u << logn;
+  const u64 half_slots = (u64)m * N / 2;
+  const u64 gid = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  const u32 ch = (u32)(gid / half_slots);
+  if (ch >= chunks) return;  // whole warps: m * N / 2 is a multiple of 32
+  const u32 rem = (u32)(gid - (u64)ch * half_slots) * 2;
+  const u32 r = rem >> logn, a = rem & (N - 1);
+  const PrimeConst P = primes[r];
+  const u64 q = P.q;
+  const u64 slots = (u64)m * N;
+  const u64 ct_words = 2ull * m * N;
+  const u64 client_stride = (u64)chunks_total * ct_words;
+  const u64* wp = clients + (u64)(c_begin + ch) * ct_words + (u64)r * N + a;
+  const u64* sp = sel + (u64)r * N + a;
+  const u32 bd = blockDim.x;
+  ulonglong2* my = ring + threadIdx.x;
+  auto issue = [&](u32 i, u32 st) {
+    if (i < n) {
+      ulonglong2* d = my + st * 4 * bd;
+      const u64* w = wp + (u64)i * client_stride;
+      const u64* s = sp + (u64)i * ct_words;
+      cp_async16(d, w);
+      cp_async16(d + bd, w + slots);
+      cp_async16(d + 2 * bd, s);
+      cp_async16(d + 3 * bd, s + slots);
+    }
+    cp_async_commit();
+  };
+  Acc3 D0[2], D1[2], D2[2];
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    D0[k].zero();
+    D1[k].zero();
+    D2[k].zero();
+  }
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) issue(s, s);
+  u32 st = 0;
+  for (u32 i = 0; i < n; ++i) {
+    cp_async_wait<STAGES - 2>();
+    const ulonglong2* d = my + st * 4 * bd;
+    const ulonglong2 w0 = d[0], w1 = d[bd], s0 = d[2 * bd], s1 = d[3 * bd];
+    issue(i + STAGES - 1, st == 0 ? STAGES - 1 : st - 1);
+    D0[0].mac(split23(w0.x), split23(s0.x));
+    D2[0].mac(split23(w1.x), split23(s1.x));
+    D1[0].mac(split23(w0.x + w1.x), split23(s0.x + s1.x));
+    D0[1].mac(split23(w0.y), split23(s0.y));
+    D2[1].mac(split23(w1.y), split23(s1.y));
+    D1[1].mac(split23(w0.y + w1.y), split23(s0.y + s1.y));
+    st = st + 1 == STAGES ? 0 : st + 1;
+  }
+  u64* o = tern + (u64)ch * 3 * slots + (u64)r * N + a;
+  ulonglong2 o0, o1, o2;
+  o0.x = D0[0].reduce(P);
+  o2.x = D2[0].reduce(P);
+  o1.x = sub_mod(sub_mod(D1[0].reduce(P), o0.x, q), o2.x, q);
+  o0.y = D0[1].reduce(P);
+  o2.y = D2[1].reduce(P);
+  o1.y = sub_mod(sub_mod(D1[1].reduce(P), o0.y, q), o2.y, q);
+  *reinterpret_cast<ulonglong2*>(o) = o0;
+  *reinterpret_cast<ulonglong2*>(o + slots) = o1;
+  *reinterpret_cast<ulonglong2*>(o + 2 * slots) = o2;
 }
 
 // ------------------------------------------------------------------------

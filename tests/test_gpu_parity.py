@@ -253,3 +253,35 @@ def test_cuda_shards_concatenate_to_reference(name, world):
             assert sha(got[p]) == rig.meta["sha256"][f"dist_{i}_{j}"], (i, j)
             p += 1
     assert sha(L.to_host(a)) == rig.meta["sha256"]["agg"]
+
+
+@pytest.mark.parametrize("pair_f64", ["1", "0"])
+def test_pair_accumulation_long_ranges_and_extremes(pair_f64, monkeypatch):
+    """Lazy pair accumulation over 600 chunks (three 256-chunk passes of the
+    FP64-pipe kernel) with boundary residues (all 0 against all q-1), for
+    both arithmetic forms (LCL_PAIR_F64=1: FP64 pipe, 0: split-23 integer),
+    word for word against the oracle's distance matrix."""
+    L = _L()
+    monkeypatch.setenv("LCL_PAIR_F64", pair_f64)
+    N, n, C = 256, 4, 600
+    orc = Oracle(N, secure=False, threads=8)
+    width = 128
+    steps = slot_reduce_steps(width, 1)
+    orc.keygen(3, steps)
+    rng = np.random.default_rng(7)
+    m = orc.full
+    clients = np.zeros((n, C, 2, m, N), np.uint64)
+    for r in range(m):
+        q = orc.primes[r]
+        clients[1, :, :, r] = np.uint64(q - 1)
+        clients[2, :, :, r] = rng.integers(0, q, size=(C, 2, N), dtype=np.uint64)
+        clients[3, :, :, r] = rng.integers(q - 4096, q, size=(C, 2, N), dtype=np.uint64)
+    ctx = L.CkksContext(L.CkksParams(ring_degree=N, security=L.SecurityLevel.none))
+    rk = L.RelinKey(orc.relin_key())
+    keys = L.RotationKeySet({s: orc.rotation_key(s) for s in steps})
+    dev = L.to_device(clients)
+    pw = [L.PackedWeights(dev[i], C * (N // 2), 1.0, orc.scale) for i in range(n)]
+    dm = L.build_distance_matrix(ctx, pw, rk, L.HoistPlan(k=1, n=width),
+                                 L.DistanceMode.per_pair, keys, L.DistanceOptions())
+    want = orc.distance_matrix(clients, width, 1)
+    assert np.array_equal(L.to_host(dm.batch), want)
