@@ -918,7 +918,7 @@ const uint2* pair_schedule(lcl_context* c, u32 n, u32 p0, u32 p1, u32 per_cta, u
   return d;
 }
 
-template <int TE, int STAGES>
+template <int TE, int STAGES, int MINB, bool PF>
 bool pair_accumulate_f64_cfg(lcl_context* c, const u64* clients, u32 n, u32 chunks, u32 c0,
                              u32 c1, u32 p0, u32 p1, u64* tern, bool accumulate) {
   constexpr int MAXT = 192;
@@ -927,18 +927,17 @@ bool pair_accumulate_f64_cfg(lcl_context* c, const u64* clients, u32 n, u32 chun
   const u32 groups = (pairs + MAXT - 1) / MAXT;
   const u32 per_cta = (pairs + groups - 1) / groups;
   const u32 threads = std::max<u32>(64, ((per_cta + 31) / 32) * 32);
-  if (n * TE > threads) return false;  // one copy per thread per chunk
   const size_t smem = (size_t)STAGES * n * (2 * TE + 2) * 8;
   if (smem > 100 * 1024) return false;
   const uint2* sched = pair_schedule(c, n, p0, p1, per_cta, TE + 1);
   const u64 tiles = (u64)m * c->n / TE;
-  allow_smem(pair_accumulate_f64<TE, STAGES, MAXT>, smem);
+  allow_smem(pair_accumulate_f64<TE, STAGES, MAXT, MINB, PF>, smem);
   for (u32 cb = c0; cb < c1; cb += 256) {  // exact for 256 chunks per pass
     const u32 ce = std::min(c1, cb + 256);
     const bool acc = accumulate || cb > c0;
     ProfScope ps(c, "pair_accumulate",
                  8.0 * c->N() * m * (2.0 * n * (ce - cb) * groups + 3.0 * pairs * (acc ? 2 : 1)));
-    pair_accumulate_f64<TE, STAGES, MAXT><<<(u32)(tiles * groups), threads, smem, c->stream>>>(
+    pair_accumulate_f64<TE, STAGES, MAXT, MINB, PF><<<(u32)(tiles * groups), threads, smem, c->stream>>>(
         clients, n, cb, ce, chunks, m, c->logn, sched, pairs, groups, per_cta, tern, acc ? 1 : 0,
         c->d_primes);
     post_launch(c);
@@ -953,10 +952,11 @@ void pair_accumulate_launch(lcl_context* c, const u64* clients, u32 n, u32 chunk
     return e ? atoi(e) : 0;
   }();
   if (c->pair_f64) {
-    if (variant == 0 && pair_accumulate_f64_cfg<4, 8>(c, clients, n, chunks, c0, c1, p0, p1, tern, accumulate)) return;
-    if (variant == 10 && pair_accumulate_f64_cfg<4, 5>(c, clients, n, chunks, c0, c1, p0, p1, tern, accumulate)) return;
-    if (variant == 11 && pair_accumulate_f64_cfg<2, 8>(c, clients, n, chunks, c0, c1, p0, p1, tern, accumulate)) return;
-    if (variant == 12 && pair_accumulate_f64_cfg<4, 12>(c, clients, n, chunks, c0, c1, p0, p1, tern, accumulate)) return;
+    // measured on B200 at cfg3 (190 pairs x 342 chunks): <8,6,2,false> 26.2 ms,
+    // <4,8,3,false> 27.9, <4,8,2,true> 30.0, <2,8,4,false> 45.7
+    if (variant == 0 && pair_accumulate_f64_cfg<8, 6, 2, false>(c, clients, n, chunks, c0, c1, p0, p1, tern, accumulate)) return;
+    if (variant == 10 && pair_accumulate_f64_cfg<4, 8, 3, false>(c, clients, n, chunks, c0, c1, p0, p1, tern, accumulate)) return;
+    if (variant == 11 && pair_accumulate_f64_cfg<4, 8, 2, true>(c, clients, n, chunks, c0, c1, p0, p1, tern, accumulate)) return;
   }
   switch (variant) {
     case 1: return pair_accumulate_cfg<8, 4, 4>(c, clients, n, chunks, c0, c1, p0, p1, tern, accumulate);

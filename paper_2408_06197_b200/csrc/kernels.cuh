@@ -151,14 +151,16 @@ __global__ void __launch_bounds__(512)
 
 // FP64-pipe form of the same accumulation, for q-chains below 2^44. B200
 // retires 64 DFMA/clk/SM but only 32 IMAD.WIDE/clk/SM, so the products run
-// on the FP64 pipe (tools/microbench/pair_forms.cu: 4.3 vs 1.7 pair-slots per
-// clock per SM). Per slot: e = x - y + 2^45 on the integer ALU, split into
-// e = eh * 2^22 + el with |eh| <= 2^22, 0 <= el < 2^22 (shift / mask), each
-// half turned into an exact double by one DADD on the exponent-biased word;
-// then ten exact DFMA products (each |p| <= 2^45) feed ten double
-// accumulators that stay exact (< 2^53) for up to 256 chunks -- the launcher
-// splits longer chunk ranges and re-enters with accumulate = 1. Results are
-// the same integers as the split-23 kernel, reduced mod q once at the end.
+// on the FP64 pipe. A residue x < 2^44 is read as the double X = 2^52 + x by
+// OR-ing the exponent into its high word (no conversion instruction), so
+// e = X_i - X_j is exact. Every product p = a * b (|p| < 2^88) is split
+// exactly on a 2^44 grid with one FMA against M = 1.5 * 2^96:
+//   t = fl(p + M), hi = t - M = H * 2^44 (|H| <= 2^44), lo = fma(a, b, -hi)
+// (|lo| <= 2^43, exact), and H, lo go to two double accumulators that stay
+// exact integers (< 2^53) for 256 chunks; the launcher splits longer chunk
+// ranges and re-enters with accumulate = 1. 2 DADD + 3 x 5 FP64 ops per slot
+// and pair, 6 accumulators. The words are the integer kernel's, reduced mod q
+// once at the end.
 __device__ __forceinline__ u64 dmodq(double v, u64 q, const PrimeConst& P) {
   const long long i = __double2ll_rn(v);  // exact: |v| < 2^53 is an integer
   if (i >= 0) return reduce64((u64)i, P);
@@ -169,10 +171,9 @@ __device__ __forceinline__ u64 dmodq(double v, u64 q, const PrimeConst& P) {
 // A thread owns one pair for the TE slots of its tile. Pairs are assigned to
 // threads by a host schedule (sched[k] = (i | j << 16, output index)) that
 // puts clients of distinct shared-memory bank groups in every quarter warp,
-// so the 16-byte tile reads are conflict-free. Each thread issues at most one
-// 16-byte cp.async per chunk (n * TE <= blockDim, checked by the launcher).
-template <int TE, int STAGES, int MAXT>
-__global__ void __launch_bounds__(MAXT, 2)
+// so the 16-byte tile reads are conflict-free.
+template <int TE, int STAGES, int MAXT, int MINB, bool PF>
+__global__ void __launch_bounds__(MAXT, MINB)
     pair_accumulate_f64(const u64* __restrict__ clients, u32 n, u32 c_begin, u32 c_end,
                         u32 chunks_total, u32 m, u32 logn, const uint2* __restrict__ sched,
                         u32 pairs, u32 groups, u32 pairs_per_cta, u64* __restrict__ tern,
@@ -193,90 +194,111 @@ __global__ void __launch_bounds__(MAXT, 2)
   const uint2 sk = valid ? __ldg(sched + k) : make_uint2(0u, 0u);
   const u32 oi = (sk.x & 0xFFFFu) * CS, oj = (sk.x >> 16) * CS;
 
-  // this thread's copy: vector v = threadIdx.x of the n * TE per chunk
-  const bool copier = threadIdx.x < n * TE;
-  const u64* gsrc = clients;
-  u32 soff = 0;
-  if (copier) {
-    const u32 cl = threadIdx.x / TE, w = (threadIdx.x - cl * TE) * 2, h = w / TE, e = w - h * TE;
-    gsrc = clients + (u64)cl * chunks_total * ct_words + (u64)h * m * N + (u64)r * N + a0 + e +
-           (u64)c_begin * ct_words;
-    soff = cl * CS + w;
-  }
+  // chunk copies: n * TE 16-byte vectors, vector v by thread v mod blockDim
+  const u64* cbase = clients + (u64)r * N + a0;
   auto issue = [&](u32 c, u32 stage) {
-    if (copier && c < c_end) cp_async16(tile + stage * tw + soff, gsrc + (u64)(c - c_begin) * ct_words);
+    if (c < c_end) {
+      for (u32 v = threadIdx.x; v < n * TE; v += blockDim.x) {
+        const u32 cl = v / TE, w = (v % TE) * 2, h = w / TE, e = w % TE;
+        cp_async16(tile + stage * tw + cl * CS + w,
+                   cbase + ((u64)cl * chunks_total + c) * ct_words + (u64)h * m * N + e);
+      }
+    }
     cp_async_commit();
   };
 
-  // per slot: e0^2 -> A = (sum el0^2, sum eh0 el0, sum eh0^2), e1^2 -> B,
-  // e0 e1 -> X = (sum el0 el1, sum el0 eh1 + eh0 el1, sum eh0 eh1)
-  double A[TE][3], Bv[TE][3], X[TE][3];
+  // per slot: (H, lo) accumulators of e0^2, e0 e1, e1^2
+  double S[TE][6];
 #pragma unroll
   for (int t = 0; t < TE; ++t)
 #pragma unroll
-    for (int q = 0; q < 3; ++q) A[t][q] = Bv[t][q] = X[t][q] = 0.0;
-  constexpr double kB52 = 4503599627370496.0;              // 2^52
-  constexpr double kB52h = 4503599627370496.0 + 8388608.0;  // 2^52 + 2^23
-  auto halves = [&](u64 x, u64 y, double& eh, double& el) {
-    const u64 e = x - y + (1ull << 45);  // in (2^44, 3 * 2^44): e - 2^45 = x - y
-    eh = __hiloint2double(0x43300000, (int)(u32)(e >> 22)) - kB52h;
-    el = __hiloint2double(0x43300000, (int)((u32)e & 0x3FFFFFu)) - kB52;
+    for (int q = 0; q < 6; ++q) S[t][q] = 0.0;
+  constexpr double kM = 118842243771396506390315925504.0;  // 1.5 * 2^96
+  constexpr double kInv44 = 1.0 / 17592186044416.0;        // 2^-44
+  auto as_d = [](u64 x) { return __longlong_as_double((long long)(x | 0x4330000000000000ull)); };
+  auto prod = [&](double a, double b, double& accH, double& accL) {
+    const double hi = __dadd_rn(__fma_rn(a, b, kM), -kM);
+    accL = __dadd_rn(accL, __fma_rn(a, b, -hi));
+    accH = __fma_rn(hi, kInv44, accH);
   };
-#pragma unroll
-  for (int s = 0; s < STAGES - 1; ++s) issue(c_begin + s, s);
-  u32 stage = 0;
-  for (u32 c = c_begin; c < c_end; ++c) {
-    cp_async_wait<STAGES - 2>();
-    __syncthreads();
-    issue(c + STAGES - 1, stage == 0 ? STAGES - 1 : stage - 1);
+  // Chunk c + 1's words are read from shared memory into registers while
+  // chunk c is multiplied, so shared-memory latency hides behind a whole
+  // chunk of FP64 work; one barrier per chunk recycles the ring stage.
+  static_assert(STAGES >= 3, "the register prefetch runs one chunk ahead of the math");
+  ulonglong2 cur[4][TE / 2], nxt[4][TE / 2];
+  auto load = [&](u32 stage, ulonglong2 (&v)[4][TE / 2]) {
     const u64* tl = tile + stage * tw;
 #pragma unroll
-    for (int t = 0; t < TE; t += 2) {
-      const ulonglong2 x0 = *reinterpret_cast<const ulonglong2*>(tl + oi + t);
-      const ulonglong2 x1 = *reinterpret_cast<const ulonglong2*>(tl + oi + TE + t);
-      const ulonglong2 y0 = *reinterpret_cast<const ulonglong2*>(tl + oj + t);
-      const ulonglong2 y1 = *reinterpret_cast<const ulonglong2*>(tl + oj + TE + t);
+    for (int t = 0; t < TE / 2; ++t) {
+      v[0][t] = *reinterpret_cast<const ulonglong2*>(tl + oi + 2 * t);
+      v[1][t] = *reinterpret_cast<const ulonglong2*>(tl + oi + TE + 2 * t);
+      v[2][t] = *reinterpret_cast<const ulonglong2*>(tl + oj + 2 * t);
+      v[3][t] = *reinterpret_cast<const ulonglong2*>(tl + oj + TE + 2 * t);
+    }
+  };
+  auto math = [&](const ulonglong2 (&v)[4][TE / 2]) {
+#pragma unroll
+    for (int t = 0; t < TE / 2; ++t) {
 #pragma unroll
       for (int u = 0; u < 2; ++u) {
-        double h0, l0, h1, l1;
-        halves(u ? x0.y : x0.x, u ? y0.y : y0.x, h0, l0);
-        halves(u ? x1.y : x1.x, u ? y1.y : y1.x, h1, l1);
-        double* a = A[t + u];
-        double* b = Bv[t + u];
-        double* x = X[t + u];
-        a[0] = __fma_rn(l0, l0, a[0]);
-        a[1] = __fma_rn(h0, l0, a[1]);
-        a[2] = __fma_rn(h0, h0, a[2]);
-        b[0] = __fma_rn(l1, l1, b[0]);
-        b[1] = __fma_rn(h1, l1, b[1]);
-        b[2] = __fma_rn(h1, h1, b[2]);
-        x[0] = __fma_rn(l0, l1, x[0]);
-        x[1] = __fma_rn(l0, h1, x[1]);
-        x[1] = __fma_rn(h0, l1, x[1]);
-        x[2] = __fma_rn(h0, h1, x[2]);
+        const double e0 = __dadd_rn(as_d(u ? v[0][t].y : v[0][t].x), -as_d(u ? v[2][t].y : v[2][t].x));
+        const double e1 = __dadd_rn(as_d(u ? v[1][t].y : v[1][t].x), -as_d(u ? v[3][t].y : v[3][t].x));
+        double* a = S[2 * t + u];
+        prod(e0, e0, a[0], a[1]);
+        prod(e0, e1, a[2], a[3]);
+        prod(e1, e1, a[4], a[5]);
       }
     }
-    stage = stage + 1 == STAGES ? 0 : stage + 1;
+  };
+  if constexpr (!PF) {
+#pragma unroll
+    for (int s = 0; s < STAGES - 1; ++s) issue(c_begin + s, s);
+    u32 stage = 0;
+    for (u32 c = c_begin; c < c_end; ++c) {
+      cp_async_wait<STAGES - 2>();
+      __syncthreads();
+      issue(c + STAGES - 1, stage == 0 ? STAGES - 1 : stage - 1);
+      ulonglong2 v[4][TE / 2];
+      load(stage, v);
+      math(v);
+      stage = stage + 1 == STAGES ? 0 : stage + 1;
+    }
+  } else {
+#pragma unroll
+    for (int s = 0; s < STAGES - 1; ++s) issue(c_begin + s, s);
+    cp_async_wait<STAGES - 2>();
+    __syncthreads();
+    load(0, cur);
+    u32 stage = 0;
+    for (u32 c = c_begin; c < c_end; ++c) {
+      cp_async_wait<STAGES - 3>();  // chunk c + 1 has landed
+      __syncthreads();              // and every thread holds chunk c in registers
+      issue(c + STAGES - 1, stage == 0 ? STAGES - 1 : stage - 1);  // chunk c - 1's stage
+      const u32 ns = stage + 1 == STAGES ? 0 : stage + 1;
+      if (c + 1 < c_end) load(ns, nxt);
+      math(cur);
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+#pragma unroll
+        for (int t = 0; t < TE / 2; ++t) cur[k][t] = nxt[k][t];
+      stage = ns;
+    }
   }
   if (!valid) return;
   const PrimeConst P = primes[r];
   const u64 q = P.q;
-  const u64 w22 = reduce64(1ull << 22, P), w23 = reduce64(1ull << 23, P),
-            w44 = reduce64(1ull << 44, P);
-  auto combine = [&](const double* v, u64 wmid) {
-    // v[2] * 2^44 + v[1] * wmid + v[0]  (mod q)
-    u64 s = mul_mod(dmodq(v[2], q, P), w44, P);
-    s = add_mod(s, mul_mod(dmodq(v[1], q, P), wmid, P), q);
-    return add_mod(s, dmodq(v[0], q, P), q);
+  const u64 w44 = reduce64(1ull << 44, P);
+  auto combine = [&](double h, double l) {  // h * 2^44 + l  (mod q)
+    return add_mod(mul_mod(dmodq(h, q, P), w44, P), dmodq(l, q, P), q);
   };
   u64* ob = tern + (u64)sk.y * 3 * m * N + (u64)r * N + a0;
 #pragma unroll
   for (int t = 0; t < TE; ++t) {
     u64* o = ob + t;
-    u64 d0 = combine(A[t], w23);  // e0^2 = eh^2 2^44 + 2 eh el 2^22 + el^2
-    u64 d1 = combine(X[t], w22);
-    d1 = add_mod(d1, d1, q);      // hsquare's 2 c0 c1
-    u64 d2 = combine(Bv[t], w23);
+    u64 d0 = combine(S[t][0], S[t][1]);
+    u64 d1 = combine(S[t][2], S[t][3]);
+    d1 = add_mod(d1, d1, q);  // hsquare's 2 c0 c1
+    u64 d2 = combine(S[t][4], S[t][5]);
     if (accumulate) {
       d0 = add_mod(d0, o[0], q);
       d1 = add_mod(d1, o[(u64)m * N], q);

@@ -255,15 +255,16 @@ def test_cuda_shards_concatenate_to_reference(name, world):
     assert sha(L.to_host(a)) == rig.meta["sha256"]["agg"]
 
 
-@pytest.mark.parametrize("pair_f64", ["1", "0"])
-def test_pair_accumulation_long_ranges_and_extremes(pair_f64, monkeypatch):
+@pytest.mark.parametrize("pair_f64,n,C", [("1", 4, 600), ("0", 4, 600), ("1", 30, 3)])
+def test_pair_accumulation_long_ranges_and_extremes(pair_f64, n, C, monkeypatch):
     """Lazy pair accumulation over 600 chunks (three 256-chunk passes of the
-    FP64-pipe kernel) with boundary residues (all 0 against all q-1), for
-    both arithmetic forms (LCL_PAIR_F64=1: FP64 pipe, 0: split-23 integer),
-    word for word against the oracle's distance matrix."""
+    FP64-pipe kernel) and over 435 pairs (three CTA pair groups, 30 clients),
+    with boundary residues (all 0 against all q-1), for both arithmetic forms
+    (LCL_PAIR_F64=1: FP64 pipe, 0: split-23 integer), word for word against
+    the oracle's distance matrix."""
     L = _L()
     monkeypatch.setenv("LCL_PAIR_F64", pair_f64)
-    N, n, C = 256, 4, 600
+    N = 256
     orc = Oracle(N, secure=False, threads=8)
     width = 128
     steps = slot_reduce_steps(width, 1)
@@ -276,6 +277,8 @@ def test_pair_accumulation_long_ranges_and_extremes(pair_f64, monkeypatch):
         clients[1, :, :, r] = np.uint64(q - 1)
         clients[2, :, :, r] = rng.integers(0, q, size=(C, 2, N), dtype=np.uint64)
         clients[3, :, :, r] = rng.integers(q - 4096, q, size=(C, 2, N), dtype=np.uint64)
+        for i in range(4, n):
+            clients[i, :, :, r] = rng.integers(0, q, size=(C, 2, N), dtype=np.uint64)
     ctx = L.CkksContext(L.CkksParams(ring_degree=N, security=L.SecurityLevel.none))
     rk = L.RelinKey(orc.relin_key())
     keys = L.RotationKeySet({s: orc.rotation_key(s) for s in steps})
