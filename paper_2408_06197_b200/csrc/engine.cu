@@ -274,7 +274,24 @@ struct lcl_context {
   std::vector<ProfRec> prof;
   // workspace
   DevBuf ws_coef, ws_digits, ws_acc, ws_coefsp, ws_mid, ws_tern, ws_ctA, ws_ctB, ws_ctC, ws_pt;
-  DevBuf ws_io_in, ws_io_sel, ws_io_dist, ws_io_agg;
+  // Concurrent lanes: independent ciphertext groups of a batched key-switch
+  // chain run on their own streams with their own workspaces, so the small,
+  // latency-bound per-level kernels of one group fill the SMs the other
+  // group's kernels leave idle (ramp-up, tails, memory stalls).
+  struct Lane {
+    cudaStream_t stream = nullptr;
+    cudaEvent_t done = nullptr;
+    DevBuf ws_coef, ws_digits, ws_acc, ws_coefsp, ws_mid, ws_ctB, ws_ctC;
+  };
+  std::vector<Lane> lanes;
+  cudaEvent_t fork_ev = nullptr;
+  DevBuf ws_io_in, ws_io_sel, ws_io_dist, ws_io_agg, ws_dtern, ws_ptl;
+  // masked_aggregate's encode(1/l) plaintext, NTT'd on the device once per l
+  size_t pt_l = 0;
+  std::vector<u64> pt_host;
+  // overlapped host round: H2D / D2H copy streams and per-slice events
+  cudaStream_t h2d = nullptr, d2h = nullptr;
+  std::vector<cudaEvent_t> io_ev;
 
   u32 P() const { return full + 1; }
   u64 N() const { return (u64)n; }
@@ -778,9 +795,81 @@ void rotate_level(lcl_context* c, const u64* in, u32 B, u32 m, size_t step, u64*
 
 size_t norm_step(lcl_context* c, size_t step) { return step % (c->n / 2); }
 
+// Swaps the context's stream and key-switch workspaces with lane g's.
+void swap_lane(lcl_context* c, u32 g) {
+  auto& ln = c->lanes[g];
+  std::swap(c->stream, ln.stream);
+  std::swap(c->ws_coef, ln.ws_coef);
+  std::swap(c->ws_digits, ln.ws_digits);
+  std::swap(c->ws_acc, ln.ws_acc);
+  std::swap(c->ws_coefsp, ln.ws_coefsp);
+  std::swap(c->ws_mid, ln.ws_mid);
+  std::swap(c->ws_ctB, ln.ws_ctB);
+  std::swap(c->ws_ctC, ln.ws_ctC);
+}
+
+// Two lanes pay off when a level's working set is L2-sized (cfg2: 45 x 3
+// limbs x 2^15, 7.27 -> 7.07 ms); at cfg3 (190 x 3 x 2^16) the kernels
+// already fill the SMs and a second lane only adds contention (92.8 -> 95.9).
+u32 lane_count(lcl_context* c, u32 B, u32 m) {
+  static const int env = [] {
+    const char* e = std::getenv("LCL_LANES");
+    return e ? std::max(1, atoi(e)) : 0;
+  }();
+  if (c->prof_on) return 1;  // per-kernel attribution needs a serial stream
+  const u32 want = env ? (u32)env : ((u64)B * m * c->N() <= (8ull << 20) ? 2u : 1u);
+  return std::min<u32>(want, std::max<u32>(1, B / 8));
+}
+
+// Runs f(first, count) for G contiguous groups of [0, B) concurrently, group g
+// on lane g (fork / join through events on the context stream, so the lanes
+// are captured into the same CUDA graph as the rest of the round).
+template <class F>
+void run_lanes(lcl_context* c, u32 B, u32 G, F&& f) {
+  if (G <= 1) {
+    f(0u, B);
+    return;
+  }
+  while (c->lanes.size() < G) {
+    c->lanes.emplace_back();
+    auto& ln = c->lanes.back();
+    cuda_check(cudaStreamCreateWithFlags(&ln.stream, cudaStreamNonBlocking), "lane stream");
+    cuda_check(cudaEventCreateWithFlags(&ln.done, cudaEventDisableTiming), "lane event");
+  }
+  if (!c->fork_ev) cuda_check(cudaEventCreateWithFlags(&c->fork_ev, cudaEventDisableTiming), "fork event");
+  cuda_check(cudaEventRecord(c->fork_ev, c->stream), "fork");
+  for (u32 g = 0; g < G; ++g) {
+    const u32 b0 = (u32)((u64)B * g / G), b1 = (u32)((u64)B * (g + 1) / G);
+    cuda_check(cudaStreamWaitEvent(c->lanes[g].stream, c->fork_ev, 0), "lane wait");
+    swap_lane(c, g);
+    try {
+      f(b0, b1 - b0);
+    } catch (...) {
+      swap_lane(c, g);
+      throw;
+    }
+    swap_lane(c, g);
+    cuda_check(cudaEventRecord(c->lanes[g].done, c->lanes[g].stream), "lane done");
+  }
+  for (u32 g = 0; g < G; ++g)
+    cuda_check(cudaStreamWaitEvent(c->stream, c->lanes[g].done, 0), "join");
+}
+
+void slot_reduce_serial(lcl_context* c, const u64* in, u32 B, u32 m, size_t width, size_t k,
+                        u64* out);
+
 // slot_reduce (distance.cpp:214-240) over B ciphertexts; in and out may alias.
+// The B chains are independent: they run as concurrent lanes.
 void slot_reduce_batch(lcl_context* c, const u64* in, u32 B, u32 m, size_t width, size_t k,
                        u64* out) {
+  const u64 words = 2ull * m * c->N();
+  run_lanes(c, B, lane_count(c, B, m), [&](u32 b0, u32 nb) {
+    slot_reduce_serial(c, in + b0 * words, nb, m, width, k, out + b0 * words);
+  });
+}
+
+void slot_reduce_serial(lcl_context* c, const u64* in, u32 B, u32 m, size_t width, size_t k,
+                        u64* out) {
   if (width == 0 || (width & (width - 1))) fail(LCL_WIDTH_ERROR, "reduction width must be a power of two");
   if (width > c->n / 2) fail(LCL_WIDTH_ERROR, "reduction width exceeds the slot count");
   if (k == 0) fail(LCL_PARAMETER_ERROR, "unfold factor starts at 1");
@@ -867,22 +956,33 @@ void pair_accumulate_cfg(lcl_context* c, const u64* clients, u32 n, u32 chunks, 
   post_launch(c);
 }
 
-// Bank-aware pair schedule for pair_accumulate_f64 (TPP = 1): pairs
-// [p0, p1) of the i<j order cut into CTA groups of per_cta; inside a group,
-// every quarter warp (8 threads, one 16-byte shared-memory wavefront) gets
-// pairs whose i's and j's fall in distinct bank groups (client k's tile row
-// starts at 16-byte unit k * CS / 2, CS / 2 odd), greedily.
-const uint2* pair_schedule(lcl_context* c, u32 n, u32 p0, u32 p1, u32 per_cta, u32 cs_half) {
-  const auto key = std::make_tuple(n, p0, p1, per_cta * 64 + cs_half);
+// Pairs one accumulation launch covers: the i<j row-major range [a, b) of
+// the matrix; output index = position in the range.
+struct PairSet {
+  u32 a, b;
+};
+PairSet row_range(u32 p0, u32 p1) { return PairSet{p0, p1}; }
+
+std::vector<uint2> pair_list(u32 n, const PairSet& ps) {
+  std::vector<uint2> all;
+  u32 p = 0;
+  for (u32 i = 0; i < n; ++i)
+    for (u32 j = i + 1; j < n; ++j, ++p)
+      if (p >= ps.a && p < ps.b) all.push_back(make_uint2(i | (j << 16), p - ps.a));
+  return all;
+}
+u32 pair_count(u32, const PairSet& ps) { return ps.b - ps.a; }
+
+// Bank-aware pair schedule for pair_accumulate_f64 (TPP = 1): the set cut
+// into CTA groups of per_cta; inside a group, every quarter warp (8 threads,
+// one 16-byte shared-memory wavefront) gets pairs whose i's and j's fall in
+// distinct bank groups (client k's tile row starts at 16-byte unit
+// k * CS / 2, CS / 2 odd), greedily.
+const uint2* pair_schedule(lcl_context* c, u32 n, const PairSet& ps, u32 per_cta, u32 cs_half) {
+  const auto key = std::make_tuple(n, ps.a, ps.b, per_cta * 64 + cs_half);
   auto it = c->sched.find(key);
   if (it != c->sched.end()) return it->second;
-  std::vector<uint2> all;
-  {
-    u32 p = 0;
-    for (u32 i = 0; i < n; ++i)
-      for (u32 j = i + 1; j < n; ++j, ++p)
-        if (p >= p0 && p < p1) all.push_back(make_uint2(i | (j << 16), p - p0));
-  }
+  const std::vector<uint2> all = pair_list(n, ps);
   std::vector<uint2> out;
   out.reserve(all.size());
   for (size_t g0 = 0; g0 < all.size(); g0 += per_cta) {
@@ -920,16 +1020,16 @@ const uint2* pair_schedule(lcl_context* c, u32 n, u32 p0, u32 p1, u32 per_cta, u
 
 template <int TE, int STAGES, int MINB, bool PF>
 bool pair_accumulate_f64_cfg(lcl_context* c, const u64* clients, u32 n, u32 chunks, u32 c0,
-                             u32 c1, u32 p0, u32 p1, u64* tern, bool accumulate) {
+                             u32 c1, const PairSet& ps, u64* tern, bool accumulate) {
   constexpr int MAXT = 192;
   const u32 m = c->full;
-  const u32 pairs = p1 - p0;
+  const u32 pairs = pair_count(n, ps);
   const u32 groups = (pairs + MAXT - 1) / MAXT;
   const u32 per_cta = (pairs + groups - 1) / groups;
   const u32 threads = std::max<u32>(64, ((per_cta + 31) / 32) * 32);
   const size_t smem = (size_t)STAGES * n * (2 * TE + 2) * 8;
   if (smem > 100 * 1024) return false;
-  const uint2* sched = pair_schedule(c, n, p0, p1, per_cta, TE + 1);
+  const uint2* sched = pair_schedule(c, n, ps, per_cta, TE + 1);
   const u64 tiles = (u64)m * c->n / TE;
   allow_smem(pair_accumulate_f64<TE, STAGES, MAXT, MINB, PF>, smem);
   for (u32 cb = c0; cb < c1; cb += 256) {  // exact for 256 chunks per pass
@@ -945,27 +1045,16 @@ bool pair_accumulate_f64_cfg(lcl_context* c, const u64* clients, u32 n, u32 chun
   return true;
 }
 
+// pair_accumulate on the FP64 pipe when the q-chain allows it (measured at
+// cfg3, 190 pairs x 342 chunks: <8,6,2,false> 26.2 ms, <4,8,3,false> 27.9,
+// <4,8,2,true> 30.0, <2,8,4,false> 45.7; split-23 integer kernel 50.3),
+// else the split-23 integer kernel.
 void pair_accumulate_launch(lcl_context* c, const u64* clients, u32 n, u32 chunks, u32 c0,
-                            u32 c1, u32 p0, u32 p1, u64* tern, bool accumulate) {
-  static const int variant = [] {
-    const char* e = getenv("LCL_PA_VARIANT");
-    return e ? atoi(e) : 0;
-  }();
-  if (c->pair_f64) {
-    // measured on B200 at cfg3 (190 pairs x 342 chunks): <8,6,2,false> 26.2 ms,
-    // <4,8,3,false> 27.9, <4,8,2,true> 30.0, <2,8,4,false> 45.7
-    if (variant == 0 && pair_accumulate_f64_cfg<8, 6, 2, false>(c, clients, n, chunks, c0, c1, p0, p1, tern, accumulate)) return;
-    if (variant == 10 && pair_accumulate_f64_cfg<4, 8, 3, false>(c, clients, n, chunks, c0, c1, p0, p1, tern, accumulate)) return;
-    if (variant == 11 && pair_accumulate_f64_cfg<4, 8, 2, true>(c, clients, n, chunks, c0, c1, p0, p1, tern, accumulate)) return;
-  }
-  switch (variant) {
-    case 1: return pair_accumulate_cfg<8, 4, 4>(c, clients, n, chunks, c0, c1, p0, p1, tern, accumulate);
-    case 2: return pair_accumulate_cfg<8, 4, 12>(c, clients, n, chunks, c0, c1, p0, p1, tern, accumulate);
-    case 3: return pair_accumulate_cfg<4, 2, 8>(c, clients, n, chunks, c0, c1, p0, p1, tern, accumulate);
-    case 4: return pair_accumulate_cfg<4, 4, 8>(c, clients, n, chunks, c0, c1, p0, p1, tern, accumulate);
-    case 5: return pair_accumulate_cfg<8, 2, 8>(c, clients, n, chunks, c0, c1, p0, p1, tern, accumulate);
-    default: return pair_accumulate_cfg<8, 4, 8>(c, clients, n, chunks, c0, c1, p0, p1, tern, accumulate);
-  }
+                            u32 c1, const PairSet& ps, u64* tern, bool accumulate) {
+  if (c->pair_f64 &&
+      pair_accumulate_f64_cfg<8, 6, 2, false>(c, clients, n, chunks, c0, c1, ps, tern, accumulate))
+    return;
+  pair_accumulate_cfg<8, 4, 8>(c, clients, n, chunks, c0, c1, ps.a, ps.b, tern, accumulate);
 }
 
 void hadd_into(lcl_context* c, u64* acc, const u64* x, u32 B, u32 m) {
@@ -1014,7 +1103,7 @@ void distance_matrix(lcl_context* c, const u64* clients, u32 n, u32 chunks, size
     if (lazy) {
       u64* tern = c->ws_tern.get((u64)B * 3 * m * N);
       for (u32 cb = 0; cb < chunks; cb += 32768) {
-        pair_accumulate_launch(c, clients, n, chunks, cb, std::min(chunks, cb + 32768), p0, p1,
+        pair_accumulate_launch(c, clients, n, chunks, cb, std::min(chunks, cb + 32768), row_range(p0, p1),
                                tern, cb > 0);
       }
       relinearize_batch(c, tern, B, m, ctA);
@@ -1023,7 +1112,7 @@ void distance_matrix(lcl_context* c, const u64* clients, u32 n, u32 chunks, size
       u64* tern = c->ws_tern.get((u64)B * 3 * m * N);
       u64* part = c->ws_ctB.get((u64)B * 2 * (m - 1) * N);
       for (u32 ch = 0; ch < chunks; ++ch) {
-        pair_accumulate_launch(c, clients, n, chunks, ch, ch + 1, p0, p1, tern, false);
+        pair_accumulate_launch(c, clients, n, chunks, ch, ch + 1, row_range(p0, p1), tern, false);
         relinearize_batch(c, tern, B, m, ctA);
         rescale_batch(c, ctA, B, m, ch == 0 ? o : part);
         if (ch) hadd_into(c, o, part, B, m - 1);
@@ -1038,6 +1127,75 @@ void distance_matrix(lcl_context* c, const u64* clients, u32 n, u32 chunks, size
 
 // Chunks [chunk_begin, chunk_end) of the aggregate (a shard when the chunks
 // are split across GPUs); out holds just that range.
+// encode(1/l at scale, level of the rescaled chunk) on the host
+// (aggregation.cpp:221-223), NTT'd on the device and kept there per l, so
+// repeated or sliced calls neither re-encode nor synchronise.
+const u64* agg_plaintext(lcl_context* c, size_t l) {
+  const u32 m = c->full;
+  const u64 N = c->N();
+  u64* d_pt = c->ws_ptl.get((u64)(m - 1) * N);
+  if (c->pt_l != l) {
+    std::vector<double> v(c->n / 2, 1.0 / (double)l);
+    const std::vector<long long> rounded = h_encode_rounded(v, c->n, c->scale);
+    c->pt_host.assign((u64)(m - 1) * N, 0);
+    for (u32 r = 0; r < m - 1; ++r) {
+      const u64 q = c->primes[r];
+      for (u64 i = 0; i < N; ++i) {
+        const long long x = rounded[i];
+        const u64 mag = (u64)(x < 0 ? -x : x) % q;
+        c->pt_host[r * N + i] = x < 0 ? (mag == 0 ? 0 : q - mag) : mag;
+      }
+    }
+    // pt_host lives in the context, so the copy may stay asynchronous
+    cuda_check(cudaMemcpyAsync(d_pt, c->pt_host.data(), c->pt_host.size() * 8,
+                               cudaMemcpyHostToDevice, c->stream),
+               "pt upload");
+    const RowMap ptm = make_map(d_pt, m - 1, N, (u64)(m - 1) * N, 1, 0, c->primes_0(m - 1));
+    launch_fwd(c, m - 1, ptm, PlainLoad{ptm}, PlainStore{ptm});
+    c->pt_l = l;
+  }
+  return d_pt;
+}
+
+// Aggregate tensor of chunks [c0, c0 + B) over clients [i0, i1) into tern
+// [B][3][m][N] (added mod q to its contents when accumulate).
+void agg_tensor(lcl_context* c, const u64* clients, const u64* sel, u32 n, u32 chunks, u32 c0,
+                u32 B, u32 i0, u32 i1, u64* tern, bool accumulate) {
+  const u32 m = c->full;
+  const u64 slots = (u64)m * c->N();
+  constexpr int ST = 6;
+  const size_t smem = (size_t)ST * 4 * 256 * 16;
+  allow_smem(aggregate_stream<ST>, smem);
+  const u64 th = (u64)B * slots / 2;
+  ProfScope ps(c, "aggregate_tensor",
+               8.0 * slots * (2.0 * (i1 - i0) * B + 2.0 * (i1 - i0) + 3.0 * B * (accumulate ? 2 : 1)));
+  aggregate_stream<ST><<<(u32)((th + 255) / 256), 256, smem, c->stream>>>(
+      clients, sel, i0, i1, chunks, c0, B, m, c->logn, tern, accumulate ? 1 : 0, c->d_primes);
+  post_launch(c);
+  (void)n;
+}
+
+// relinearize + rescale (+ x encode(1/l) + rescale when averaging) of B
+// aggregate ternaries into out [B][2][mo][N] (aggregation.cpp:218-224).
+void agg_finish(lcl_context* c, const u64* tern, u32 B, bool average, const u64* d_pt, u64* out) {
+  const u32 m = c->full;
+  const u64 N = c->N();
+  u64* ctA = c->ws_ctA.get((u64)B * 2 * m * N);
+  relinearize_batch(c, tern, B, m, ctA);
+  if (!average) {
+    rescale_batch(c, ctA, B, m, out);
+    return;
+  }
+  u64* ctB = c->ws_ctB.get((u64)B * 2 * (m - 1) * N);
+  rescale_batch(c, ctA, B, m, ctB);
+  const u64 total = (u64)B * 2 * (m - 1) * N;
+  mult_plain<<<(u32)((total + 255) / 256), 256, 0, c->stream>>>(ctB, d_pt, B, m - 1, c->logn, ctB,
+                                                                c->d_primes);
+  post_launch(c);
+  rescale_batch(c, ctB, B, m - 1, out);
+  c->counts.multiplications += B;
+}
+
 void masked_aggregate(lcl_context* c, const u64* clients, const u64* sel, u32 n, u32 chunks,
                       size_t l, bool average, u64* out, u32 chunk_begin = 0,
                       u32 chunk_end = 0xFFFFFFFFu) {
@@ -1047,71 +1205,14 @@ void masked_aggregate(lcl_context* c, const u64* clients, const u64* sel, u32 n,
   const u32 SB = sub_batch(c, m);
   const u32 mo = average ? m - 2 : m - 1;
   if (m < 2 || (average && m < 3)) fail(LCL_DEPTH_EXHAUSTED, "no prime left to rescale by");
-  std::vector<u64> pt_h;
-  u64* d_pt = nullptr;
-  if (average) {
-    // encode(1/l at scale, level of the rescaled chunk) on the host (aggregation.cpp:221-223)
-    std::vector<double> v(c->n / 2, 1.0 / (double)l);
-    const std::vector<long long> rounded = h_encode_rounded(v, c->n, c->scale);
-    pt_h.resize((u64)(m - 1) * N);
-    for (u32 r = 0; r < m - 1; ++r) {
-      const u64 q = c->primes[r];
-      for (u64 i = 0; i < N; ++i) {
-        const long long x = rounded[i];
-        const u64 mag = (u64)(x < 0 ? -x : x) % q;
-        pt_h[r * N + i] = x < 0 ? (mag == 0 ? 0 : q - mag) : mag;
-      }
-    }
-    d_pt = c->ws_pt.get(pt_h.size());
-    cuda_check(cudaMemcpyAsync(d_pt, pt_h.data(), pt_h.size() * 8, cudaMemcpyHostToDevice,
-                               c->stream),
-               "pt upload");
-    const RowMap ptm = make_map(d_pt, m - 1, N, (u64)(m - 1) * N, 1, 0, c->primes_0(m - 1));
-    launch_fwd(c, m - 1, ptm, PlainLoad{ptm}, PlainStore{ptm});
-    cuda_check(cudaStreamSynchronize(c->stream), "pt encode");  // pt_h must outlive the copy
-  }
+  const u64* d_pt = average ? agg_plaintext(c, l) : nullptr;
   const u32 cend = std::min(chunks, chunk_end);
   need(chunk_begin <= cend, LCL_SHAPE_ERROR, "chunk range outside the weights");
   for (u32 c0 = chunk_begin; c0 < cend; c0 += SB) {
     const u32 c1 = std::min(cend, c0 + SB), B = c1 - c0;
     u64* tern = c->ws_tern.get((u64)B * 3 * m * N);
-    constexpr int CK = 2;
-    const u64 slots = (u64)m * N;
-    const u64 threads = ((B + CK - 1) / CK) * slots;
-    {
-      ProfScope ps(c, "aggregate_tensor", 8.0 * slots * (2.0 * n * B + 2.0 * n + 3.0 * B));
-      static const bool stream_form = [] {
-        const char* e = getenv("LCL_AGG_VARIANT");
-        return !(e && atoi(e) == 1);
-      }();
-      if (stream_form) {
-        constexpr int ST = 6;
-        const size_t smem = (size_t)ST * 4 * 256 * 16;
-        allow_smem(aggregate_stream<ST>, smem);
-        const u64 th = (u64)B * slots / 2;
-        aggregate_stream<ST><<<(u32)((th + 255) / 256), 256, smem, c->stream>>>(
-            clients, sel, n, chunks, c0, B, m, c->logn, tern, c->d_primes);
-      } else {
-        aggregate_tensor<CK><<<(u32)((threads + 255) / 256), 256, 0, c->stream>>>(
-            clients, sel, n, chunks, c0, B, m, c->logn, tern, c->d_primes);
-      }
-    }
-    post_launch(c);
-    u64* ctA = c->ws_ctA.get((u64)B * 2 * m * N);
-    relinearize_batch(c, tern, B, m, ctA);
-    u64* o = out + (u64)(c0 - chunk_begin) * 2 * mo * N;
-    if (!average) {
-      rescale_batch(c, ctA, B, m, o);
-    } else {
-      u64* ctB = c->ws_ctB.get((u64)B * 2 * (m - 1) * N);
-      rescale_batch(c, ctA, B, m, ctB);
-      const u64 total = (u64)B * 2 * (m - 1) * N;
-      mult_plain<<<(u32)((total + 255) / 256), 256, 0, c->stream>>>(ctB, d_pt, B, m - 1, c->logn,
-                                                                    ctB, c->d_primes);
-      post_launch(c);
-      rescale_batch(c, ctB, B, m - 1, o);
-      c->counts.multiplications += B;
-    }
+    agg_tensor(c, clients, sel, n, chunks, c0, B, 0, n, tern, false);
+    agg_finish(c, tern, B, average, d_pt, out + (u64)(c0 - chunk_begin) * 2 * mo * N);
     c->counts.multiplications += (u64)n * B;
     c->counts.additions += (u64)(n - 1) * B;
   }
@@ -1274,6 +1375,16 @@ void build_context(lcl_context* c, size_t degree, int depth, int secure, int dev
 }
 
 void free_context(lcl_context* c) {
+  for (auto& ln : c->lanes) {
+    for (DevBuf* b : {&ln.ws_coef, &ln.ws_digits, &ln.ws_acc, &ln.ws_coefsp, &ln.ws_mid,
+                      &ln.ws_ctB, &ln.ws_ctC})
+      b->release();
+    if (ln.done) cudaEventDestroy(ln.done);
+    if (ln.stream) cudaStreamDestroy(ln.stream);
+  }
+  c->lanes.clear();
+  if (c->fork_ev) cudaEventDestroy(c->fork_ev);
+  c->fork_ev = nullptr;
   cudaFree(c->d_primes);
   cudaFree(c->d_tw);
   cudaFree(c->d_itw);
@@ -1291,8 +1402,13 @@ void free_context(lcl_context* c) {
   for (auto& kv : c->d_sigma) cudaFree(kv.second);
   for (DevBuf* b : {&c->ws_coef, &c->ws_digits, &c->ws_acc, &c->ws_coefsp, &c->ws_mid,
                     &c->ws_tern, &c->ws_ctA, &c->ws_ctB, &c->ws_ctC, &c->ws_pt, &c->ws_io_in,
-                    &c->ws_io_sel, &c->ws_io_dist, &c->ws_io_agg})
+                    &c->ws_io_sel, &c->ws_io_dist, &c->ws_io_agg, &c->ws_dtern, &c->ws_ptl})
     b->release();
+  for (cudaEvent_t e : c->io_ev) cudaEventDestroy(e);
+  c->io_ev.clear();
+  if (c->h2d) cudaStreamDestroy(c->h2d);
+  if (c->d2h) cudaStreamDestroy(c->d2h);
+  c->h2d = c->d2h = nullptr;
 }
 
 u64 key_words(const lcl_context* c) { return (u64)c->full * 2 * c->P() * c->N(); }
@@ -1300,7 +1416,8 @@ u64 key_words(const lcl_context* c) { return (u64)c->full * 2 * c->P() * c->N();
 u64* upload_key(lcl_context* c, const u64* h, size_t words, u64** shoup_out) {
   need(h != nullptr, LCL_KEY_ERROR, "null key");
   need(words == key_words(c), LCL_KEY_ERROR, "switch key has the wrong shape");
-  // Shoup companions floor(k * 2^64 / q_row) for the fused inner product.
+  // Companions for the fused inner product: Shoup floor(k * 2^64 / q_row) on
+  // integer rows, the key word as a double on FP64 rows.
   std::vector<u64> sh(words);
   const u64 N = c->N();
   const u32 P = c->P();
@@ -1309,8 +1426,8 @@ u64* upload_key(lcl_context* c, const u64* h, size_t words, u64** shoup_out) {
     const u64 q = c->primes[row];
     need(h[i] < q, LCL_KEY_ERROR, "key residue outside its modulus");
     if ((c->fp_mask >> row) & 1u) {
-      const double kq = (double)h[i] / (double)q;  // FP64 rows: fl(k / q)
-      std::memcpy(&sh[i], &kq, 8);
+      const double kd = (double)h[i];  // FP64 rows: the key word as a double
+      std::memcpy(&sh[i], &kd, 8);
     } else {
       sh[i] = h_shoup(h[i], q);
     }
@@ -1783,19 +1900,88 @@ int lcl_server_round_host(lcl_context* ctx, const uint64_t* h_clients, const uin
   return guarded([&] {
     const u32 m = ctx->full;
     const u64 N = ctx->N();
-    const u64 cw = (u64)n * chunks * 2 * m * N, sw = (u64)n * 2 * m * N;
-    const u64 dw = (u64)n * (n - 1) / 2 * 2 * (m - 1) * N;
-    const u64 aw = (u64)chunks * 2 * (average ? m - 2 : m - 1) * N;
+    const u64 ctw = 2ull * m * N;  // words per ciphertext
+    const u64 cw = (u64)n * chunks * ctw, sw = (u64)n * ctw;
+    const u32 P = (u32)(n * (n - 1) / 2);
+    const u64 dstride = 2ull * (m - 1) * N;
+    const u64 astride = 2ull * (average ? m - 2 : m - 1) * N;
+    const u64 dw = (u64)P * dstride, aw = (u64)chunks * astride;
     u64* dc = ctx->ws_io_in.get(cw);
     u64* ds = ctx->ws_io_sel.get(sw);
     u64* dd = ctx->ws_io_dist.get(dw);
     u64* da = ctx->ws_io_agg.get(aw);
-    cuda_check(cudaMemcpyAsync(dc, h_clients, cw * 8, cudaMemcpyHostToDevice, ctx->stream), "h2d");
-    cuda_check(cudaMemcpyAsync(ds, h_sel, sw * 8, cudaMemcpyHostToDevice, ctx->stream), "h2d");
-    distance_matrix(ctx, dc, (u32)n, (u32)chunks, width, k, true, true, dd);
-    masked_aggregate(ctx, dc, ds, (u32)n, (u32)chunks, l, average != 0, da);
-    cuda_check(cudaMemcpyAsync(h_dist, dd, dw * 8, cudaMemcpyDeviceToHost, ctx->stream), "d2h");
-    cuda_check(cudaMemcpyAsync(h_agg, da, aw * 8, cudaMemcpyDeviceToHost, ctx->stream), "d2h");
+    const bool overlap = n >= 2 && n <= 65535 && m >= 2 && chunks >= 2 && P <= sub_batch(ctx, m);
+    if (!overlap) {
+      cuda_check(cudaMemcpyAsync(dc, h_clients, cw * 8, cudaMemcpyHostToDevice, ctx->stream), "h2d");
+      cuda_check(cudaMemcpyAsync(ds, h_sel, sw * 8, cudaMemcpyHostToDevice, ctx->stream), "h2d");
+      distance_matrix(ctx, dc, (u32)n, (u32)chunks, width, k, true, true, dd);
+      masked_aggregate(ctx, dc, ds, (u32)n, (u32)chunks, l, average != 0, da);
+      cuda_check(cudaMemcpyAsync(h_dist, dd, dw * 8, cudaMemcpyDeviceToHost, ctx->stream), "d2h");
+      cuda_check(cudaMemcpyAsync(h_agg, da, aw * 8, cudaMemcpyDeviceToHost, ctx->stream), "d2h");
+      cuda_check(cudaStreamSynchronize(ctx->stream), "round sync");
+      return;
+    }
+    // Overlapped round (LCLT ingest): the clients arrive in chunk
+    // slices on an H2D stream; slice s is accumulated into every pair's
+    // ternary and aggregated (tensor, relinearize, rescale of its chunks)
+    // while slice s + 1 is in flight, and its aggregate chunks leave on a D2H
+    // stream. The pair chains (relinearize, rescale, slot_reduce) follow the
+    // last slice. Same kernels and op counters as distance_matrix +
+    // masked_aggregate, so the words are identical. (A client-major order --
+    // start the chains of the pairs a client group completes -- was measured
+    // too: 17.1 ms at cfg2, where a 10-pair chain costs nearly as much as the
+    // 45-pair one, and 575 vs 584 ms at cfg3, where the H2D dominates.)
+    if (width == 0 || (width & (width - 1))) fail(LCL_WIDTH_ERROR, "reduction width must be a power of two");
+    if (width > ctx->n / 2) fail(LCL_WIDTH_ERROR, "reduction width exceeds the slot count");
+    if (average && m < 3) fail(LCL_DEPTH_EXHAUSTED, "no prime left to rescale by");
+    if (!ctx->d_relin) fail(LCL_KEY_ERROR, "no relinearization key uploaded");
+    ensure_pairs(ctx, (u32)n);
+    if (!ctx->h2d) cuda_check(cudaStreamCreateWithFlags(&ctx->h2d, cudaStreamNonBlocking), "stream");
+    if (!ctx->d2h) cuda_check(cudaStreamCreateWithFlags(&ctx->d2h, cudaStreamNonBlocking), "stream");
+    const u32 C = (u32)chunks;
+    const u32 slices = std::min<u32>(C, 16);
+    const u32 per = (C + slices - 1) / slices;
+    while (ctx->io_ev.size() < 2 * (size_t)slices + 2) {
+      cudaEvent_t e;
+      cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+      ctx->io_ev.push_back(e);
+    }
+    cudaEvent_t* ev = ctx->io_ev.data();
+    cudaEvent_t start = ev[2 * slices], dist_done = ev[2 * slices + 1];
+    // copies start after whatever the compute stream already holds
+    cuda_check(cudaEventRecord(start, ctx->stream), "event");
+    cuda_check(cudaStreamWaitEvent(ctx->h2d, start, 0), "wait");
+    cuda_check(cudaStreamWaitEvent(ctx->d2h, start, 0), "wait");
+    cuda_check(cudaMemcpyAsync(ds, h_sel, sw * 8, cudaMemcpyHostToDevice, ctx->h2d), "h2d");
+    u64* tern = ctx->ws_dtern.get((u64)P * 3 * m * N);
+    u32 s = 0;
+    for (u32 c0 = 0; c0 < C; c0 += per, ++s) {
+      const u32 c1 = std::min(C, c0 + per);
+      // clients' chunks [c0, c1): n rows of (c1 - c0) ciphertexts, pitch C
+      cuda_check(cudaMemcpy2DAsync(dc + (u64)c0 * ctw, (u64)C * ctw * 8, h_clients + (u64)c0 * ctw,
+                                   (u64)C * ctw * 8, (u64)(c1 - c0) * ctw * 8, n,
+                                   cudaMemcpyHostToDevice, ctx->h2d),
+                 "h2d slice");
+      cuda_check(cudaEventRecord(ev[2 * s], ctx->h2d), "event");
+      cuda_check(cudaStreamWaitEvent(ctx->stream, ev[2 * s], 0), "wait");
+      pair_accumulate_launch(ctx, dc, (u32)n, C, c0, c1, row_range(0, P), tern, c0 > 0);
+      masked_aggregate(ctx, dc, ds, (u32)n, C, l, average != 0, da + (u64)c0 * astride, c0, c1);
+      cuda_check(cudaEventRecord(ev[2 * s + 1], ctx->stream), "event");
+      cuda_check(cudaStreamWaitEvent(ctx->d2h, ev[2 * s + 1], 0), "wait");
+      cuda_check(cudaMemcpyAsync(h_agg + (u64)c0 * astride, da + (u64)c0 * astride,
+                                 (u64)(c1 - c0) * astride * 8, cudaMemcpyDeviceToHost, ctx->d2h),
+                 "d2h slice");
+    }
+    ctx->counts.multiplications += (u64)P * C;
+    ctx->counts.additions += (u64)P * (2ull * C - 1);
+    u64* ctA = ctx->ws_ctA.get((u64)P * 2 * m * N);
+    relinearize_batch(ctx, tern, P, m, ctA);
+    rescale_batch(ctx, ctA, P, m, dd);
+    slot_reduce_batch(ctx, dd, P, m - 1, width, k, dd);
+    cuda_check(cudaEventRecord(dist_done, ctx->stream), "event");
+    cuda_check(cudaStreamWaitEvent(ctx->d2h, dist_done, 0), "wait");
+    cuda_check(cudaMemcpyAsync(h_dist, dd, dw * 8, cudaMemcpyDeviceToHost, ctx->d2h), "d2h");
+    cuda_check(cudaStreamSynchronize(ctx->d2h), "round sync");
     cuda_check(cudaStreamSynchronize(ctx->stream), "round sync");
     (void)in_scale;
   });

@@ -313,95 +313,20 @@ __global__ void __launch_bounds__(MAXT, MINB)
 // ------------------------------------------------------------------------
 // Masked aggregation tensor (aggregation.cpp:205-219): per chunk ch,
 //   sum_i hmult_triple(w_i[ch], sel_i) with Karatsuba d1 = (w0+w1)(s0+s1) - d0 - d2,
-// lazily accumulated over the n clients, reduced once. A thread owns one slot
-// of one limb for CK consecutive chunks and reuses the selector words.
-// clients: [n][C][2][m][N]; sel: [n][2][m][N]; tern: [C][3][m][N].
-template <int CK>
-__global__ void __launch_bounds__(256)
-    aggregate_tensor(const u64* __restrict__ clients, const u64* __restrict__ sel, u32 n,
-                     u32 chunks_total, u32 c_begin, u32 chunks, u32 m, u32 logn,
-                     u64* __restrict__ tern, const PrimeConst* __restrict__ primes) {
-  const u32 N = 1u << logn;
-  const u64 gid = (u64)blockIdx.x * blockDim.x + threadIdx.x;
-  const u64 slots = (u64)m * N;
-  const u32 cgroup = (u32)(gid / slots);
-  const u32 rem = (u32)(gid - (u64)cgroup * slots);
-  const u32 r = rem >> logn, a = rem & (N - 1);
-  const u32 c0 = cgroup * CK;
-  if (c0 >= chunks) return;
-  const PrimeConst P = primes[r];
-  const u64 q = P.q;
-  const u64 ct_words = 2ull * m * N;
-  Acc3 D0[CK], D1[CK], D2[CK];
-#pragma unroll
-  for (int k = 0; k < CK; ++k) {
-    D0[k].zero();
-    D1[k].zero();
-    D2[k].zero();
-  }
-  const u64* sp = sel + (u64)r * N + a;
-  const u64* wp = clients + (u64)(c_begin + c0) * ct_words + (u64)r * N + a;
-  const u64 client_stride = (u64)chunks_total * ct_words;
-  // operands of client i + 1 are loaded while client i is accumulated
-  u64 s0 = __ldg(sp), s1 = __ldg(sp + slots);
-  u64 w0[CK], w1[CK];
-#pragma unroll
-  for (int k = 0; k < CK; ++k) {
-    const bool ok = c0 + k < chunks;
-    w0[k] = ok ? __ldg(wp + k * ct_words) : 0;
-    w1[k] = ok ? __ldg(wp + k * ct_words + slots) : 0;
-  }
-  for (u32 i = 0; i < n; ++i) {
-    const u64 cs0 = s0, cs1 = s1;
-    u64 cw0[CK], cw1[CK];
-#pragma unroll
-    for (int k = 0; k < CK; ++k) {
-      cw0[k] = w0[k];
-      cw1[k] = w1[k];
-    }
-    if (i + 1 < n) {
-      sp += ct_words;
-      wp += client_stride;
-      s0 = __ldg(sp);
-      s1 = __ldg(sp + slots);
-#pragma unroll
-      for (int k = 0; k < CK; ++k) {
-        const bool ok = c0 + k < chunks;
-        w0[k] = ok ? __ldg(wp + k * ct_words) : 0;
-        w1[k] = ok ? __ldg(wp + k * ct_words + slots) : 0;
-      }
-    }
-    const Split S0 = split23(cs0), S1 = split23(cs1), SS = split23(cs0 + cs1);
-#pragma unroll
-    for (int k = 0; k < CK; ++k) {
-      D0[k].mac(split23(cw0[k]), S0);
-      D2[k].mac(split23(cw1[k]), S1);
-      D1[k].mac(split23(cw0[k] + cw1[k]), SS);
-    }
-  }
-#pragma unroll
-  for (int k = 0; k < CK; ++k) {
-    if (c0 + k >= chunks) break;
-    u64* o = tern + (u64)(c0 + k) * 3 * slots + (u64)r * N + a;
-    const u64 d0 = D0[k].reduce(P), d2 = D2[k].reduce(P);
-    const u64 d1 = sub_mod(sub_mod(D1[k].reduce(P), d0, q), d2, q);
-    o[0] = d0;
-    o[slots] = d1;
-    o[2 * slots] = d2;
-  }
-}
-
-// Streaming form of the same tensor: a thread owns 2 consecutive slots of one
-// limb of one chunk (16-byte loads) and walks the n clients; the (w0, w1, s0,
-// s1) vectors of client i + STAGES - 1 are copied into a private shared-memory
-// ring (cp.async, no barrier: a thread only reads what it copied) while
-// client i is accumulated, so HBM latency is hidden by the copy ring rather
-// than by registers. Selectors are re-read per chunk from L2 (n * ct, small).
+// lazily accumulated over the clients in split-23 sums, reduced once.
+// A thread owns 2 consecutive slots of one limb of one chunk (16-byte loads)
+// and walks clients [i0, i1); the (w0, w1, s0, s1) vectors of client
+// i + STAGES - 1 are copied into a private shared-memory ring (cp.async, no
+// barrier: a thread only reads what it copied) while client i is
+// accumulated, so HBM latency is hidden by the copy ring rather than by
+// registers. Selectors are re-read per chunk from L2 (n * ct, small). The sum
+// is linear, so client ranges accumulate (accumulate = 1 adds mod q to tern).
+// clients: [n][C][2][m][N]; sel: [n][2][m][N]; tern: [chunks][3][m][N].
 template <int STAGES>
 __global__ void __launch_bounds__(256)
-    aggregate_stream(const u64* __restrict__ clients, const u64* __restrict__ sel, u32 n,
+    aggregate_stream(const u64* __restrict__ clients, const u64* __restrict__ sel, u32 i0, u32 i1,
                      u32 chunks_total, u32 c_begin, u32 chunks, u32 m, u32 logn,
-                     u64* __restrict__ tern, const PrimeConst* __restrict__ primes) {
+                     u64* __restrict__ tern, int accumulate, const PrimeConst* __restrict__ primes) {
   extern __shared__ ulonglong2 ring[];  // [STAGES][4][blockDim]
   const u32 N = 1u << logn;
   const u64 half_slots = (u64)m * N / 2;
@@ -420,7 +345,7 @@ __global__ void __launch_bounds__(256)
   const u32 bd = blockDim.x;
   ulonglong2* my = ring + threadIdx.x;
   auto issue = [&](u32 i, u32 st) {
-    if (i < n) {
+    if (i < i1) {
       ulonglong2* d = my + st * 4 * bd;
       const u64* w = wp + (u64)i * client_stride;
       const u64* s = sp + (u64)i * ct_words;
@@ -439,9 +364,9 @@ __global__ void __launch_bounds__(256)
     D2[k].zero();
   }
 #pragma unroll
-  for (int s = 0; s < STAGES - 1; ++s) issue(s, s);
+  for (int s = 0; s < STAGES - 1; ++s) issue(i0 + s, s);
   u32 st = 0;
-  for (u32 i = 0; i < n; ++i) {
+  for (u32 i = i0; i < i1; ++i) {
     cp_async_wait<STAGES - 2>();
     const ulonglong2* d = my + st * 4 * bd;
     const ulonglong2 w0 = d[0], w1 = d[bd], s0 = d[2 * bd], s1 = d[3 * bd];
@@ -462,6 +387,17 @@ __global__ void __launch_bounds__(256)
   o0.y = D0[1].reduce(P);
   o2.y = D2[1].reduce(P);
   o1.y = sub_mod(sub_mod(D1[1].reduce(P), o0.y, q), o2.y, q);
+  if (accumulate) {
+    const ulonglong2 p0 = *reinterpret_cast<const ulonglong2*>(o);
+    const ulonglong2 p1 = *reinterpret_cast<const ulonglong2*>(o + slots);
+    const ulonglong2 p2 = *reinterpret_cast<const ulonglong2*>(o + 2 * slots);
+    o0.x = add_mod(o0.x, p0.x, q);
+    o0.y = add_mod(o0.y, p0.y, q);
+    o1.x = add_mod(o1.x, p1.x, q);
+    o1.y = add_mod(o1.y, p1.y, q);
+    o2.x = add_mod(o2.x, p2.x, q);
+    o2.y = add_mod(o2.y, p2.y, q);
+  }
   *reinterpret_cast<ulonglong2*>(o) = o0;
   *reinterpret_cast<ulonglong2*>(o + slots) = o1;
   *reinterpret_cast<ulonglong2*>(o + 2 * slots) = o2;

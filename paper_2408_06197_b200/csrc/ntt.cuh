@@ -585,7 +585,8 @@ __global__ void __launch_bounds__(64)
 // through the rotation's evaluation-domain permutation when one is given.
 // Each digit is multiplied by the key and accumulated lazily, so the m(m+1)
 // digit rows never reach HBM. Integer rows use the key in Shoup form
-// (key_aux = floor(k 2^64 / q)); FP64 rows use key_aux = bits of fl(k / q).
+// (key_aux = floor(k 2^64 / q)); FP64 rows read only key_aux = the key word
+// as a double (one load per key word).
 //   mid: [B][M][M][N] (t' = t < j ? t : t - 1); c1: limb j of item b at
 //   c1 + b * c1_stride + j * N; key / key_aux: [full][2][full+1][N];
 //   acc: [B][2][M+1][N].
@@ -593,6 +594,7 @@ template <class F>
 struct IpOps;
 template <>
 struct IpOps<IntF> {
+  static constexpr bool kRawKey = true;
   // each product < 4q: the M-term sums stay < 24q (M <= 6)
   __device__ static __forceinline__ u64 mul(u64 x, u64 k, u64 ks, const IntF::K& K) {
     return mul_shoup_lazy4(x, k, ks, K.q);
@@ -601,9 +603,14 @@ struct IpOps<IntF> {
 };
 template <>
 struct IpOps<FpF> {
-  // each product |p| <= 0.75q
-  __device__ static __forceinline__ u64 mul(double x, u64 k, u64 kq, const FpF::K& K) {
-    return (u64)__double_as_longlong(f_mulmod(x, u2d(k), __longlong_as_double((long long)kq), K.q));
+  // kd = the key word as a double; w / q is formed as kd * fl(1 / q), within
+  // 2^-52 relative of k / q, so for |x| < 2^49 (lazy forward outputs < 22q)
+  // round(x * wq) stays within 0.625 of x k / q -- f_mulmod's 0.75 bound --
+  // and each product is exact with |p| <= 0.75q. The raw key word is unused.
+  static constexpr bool kRawKey = false;
+  __device__ static __forceinline__ u64 mul(double x, u64, u64 kd_bits, const FpF::K& K) {
+    const double kd = __longlong_as_double((long long)kd_bits);
+    return (u64)__double_as_longlong(f_mulmod(x, kd, __dmul_rn(kd, K.qinv), K.q));
   }
   __device__ static __forceinline__ u64 add(u64 a, u64 b) {
     return (u64)__double_as_longlong(__dadd_rn(__longlong_as_double((long long)a),
@@ -664,8 +671,10 @@ __device__ __forceinline__ void modup_ip_body(u32 bi, bool live, u32 t, u32 blk,
 #pragma unroll
     for (int e = 0; e < 16; ++e) {
       const u32 a = a0 + 16 * e;
-      const u64 p0 = IpOps<F>::mul(x[e], __ldg(k0 + a), __ldg(ks0 + a), K);
-      const u64 p1 = IpOps<F>::mul(x[e], __ldg(k1 + a), __ldg(ks1 + a), K);
+      const u64 kw0 = IpOps<F>::kRawKey ? __ldg(k0 + a) : 0;
+      const u64 kw1 = IpOps<F>::kRawKey ? __ldg(k1 + a) : 0;
+      const u64 p0 = IpOps<F>::mul(x[e], kw0, __ldg(ks0 + a), K);
+      const u64 p1 = IpOps<F>::mul(x[e], kw1, __ldg(ks1 + a), K);
       const u32 si = l + 16 * e;
       s0acc[si] = j ? IpOps<F>::add(s0acc[si], p0) : p0;
       s1acc[si] = j ? IpOps<F>::add(s1acc[si], p1) : p1;

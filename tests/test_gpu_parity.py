@@ -175,6 +175,39 @@ def test_masked_aggregate_bit_exact_vs_reference(golden):
     assert agg.scale == rig.meta["agg_scale"]
 
 
+def test_host_round_overlapped_bit_exact_vs_reference(golden):
+    """lcl_server_round_host (host buffers in and out; chunk-sliced H2D
+    overlapped with the accumulation and the aggregate) against the
+    reference digests and op counters."""
+    L = _L()
+    import ctypes as C
+    rig = golden
+    if not rig.lazy:
+        pytest.skip("the host round entry is the lazy, reduced per-pair round")
+    ctx = gpu_ctx(rig.N, secure=bool(rig.meta["options"]["secure"]))
+    ctx.use_relin_key(L.RelinKey(rig.oracle.relin_key()))
+    keys = L.RotationKeySet({s: rig.oracle.rotation_key(s) for s in rig.meta["rot_keys"]})
+    ctx.use_rotation_keys(keys, rig.steps)
+    m, N, n = rig.oracle.full, rig.N, rig.n
+    h_clients = np.ascontiguousarray(rig.clients)
+    h_sel = np.ascontiguousarray(rig.selectors)
+    npairs = n * (n - 1) // 2
+    h_dist = np.zeros((npairs, 2, m - 1, N), np.uint64)
+    mo = m - 2 if rig.average else m - 1
+    h_agg = np.zeros((rig.C, 2, mo, N), np.uint64)
+    ctx.reset_counters()
+    L._check(L.lib().lcl_server_round_host(
+        ctx.h, C.c_void_p(h_clients.ctypes.data), C.c_void_p(h_sel.ctypes.data), n, rig.C,
+        rig.oracle.scale, rig.width, rig.k, len(rig.selected), 1 if rig.average else 0,
+        C.c_void_p(h_dist.ctypes.data), C.c_void_p(h_agg.ctypes.data)))
+    pairs = [(i, j) for i in range(n) for j in range(i + 1, n)]
+    for p, (i, j) in enumerate(pairs):
+        assert sha(h_dist[p]) == rig.meta["sha256"][f"dist_{i}_{j}"], (i, j)
+    assert sha(h_agg) == rig.meta["sha256"]["agg"]
+    want = {k: rig.meta["dist_ops"][k] + rig.meta["agg_ops"][k] for k in rig.meta["dist_ops"]}
+    assert ctx.counters() == want
+
+
 def test_decrypted_results_within_ckks_tolerance(golden):
     """Decrypt the GPU outputs with the oracle: distances within rel 1e-5 of
     the reference's decryption (same words => identical), and within the
