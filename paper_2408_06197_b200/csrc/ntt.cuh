@@ -446,18 +446,57 @@ __global__ void __launch_bounds__(16 * ((1 << LOGN1) / E))
     col_fwd_body<IntF, LOGN1, E>(out, ld, tb, sm, r, j, c, k, pi);
 }
 
+// Block-pass twiddles in shared memory. Block b's 8 local stages use
+// root[(N1 + b) 2^lm + i], i < 2^lm, lm = 0..7: 255 entries, staged once per
+// CTA at slot 2^lm - 1 + i by all its threads (every group of the CTA works
+// on block b of a row of the same prime), so the stages read them with
+// shared-memory latency instead of an L1/L2 round trip per stage.
+constexpr int kBlkTw = 256;  // staged entries per CTA (255 used)
+template <class F>
+__device__ __forceinline__ void stage_blk_tw(ulonglong2* stw, typename F::TwPtr tw, u32 n1, u32 b,
+                                             u32 tid, u32 nthr) {
+  const ulonglong2* t = reinterpret_cast<const ulonglong2*>(tw);
+  for (u32 k = tid; k < 255; k += nthr) {
+    const u32 lm = 31 - __clz(k + 1);
+    stw[k] = __ldg(t + (n1 + b) * (1u << lm) + (k + 1 - (1u << lm)));
+  }
+}
+template <class F>
+struct GlobalTw {  // root[(N1 + b) 2^lm + i] straight from the table (L1 / L2)
+  typename F::TwPtr tw;
+  u32 base;  // N1 + b
+  __device__ __forceinline__ typename F::Tw operator()(int lm, u32 i) const {
+    return F::ld(tw, base * (1u << lm) + i);
+  }
+};
+template <class F>
+struct SmemTw {
+  const ulonglong2* stw;
+  __device__ __forceinline__ typename F::Tw operator()(int lm, u32 i) const {
+    const ulonglong2 v = stw[(1u << lm) - 1 + i];
+    typename F::Tw w;
+    if constexpr (std::is_same<F, FpF>::value) {
+      w.w = __longlong_as_double((long long)v.x);
+      w.wq = __longlong_as_double((long long)v.y);
+    } else {
+      w.w = v.x;
+      w.ws = v.y;
+    }
+    return w;
+  }
+};
+
 // Block pass body, forward: x[e] holds element l + 16 e of one 256-point
 // block (coalesced order) on entry; on exit o[e] = fin(output element
 // l + 16 e). Phase 1 runs local stages m' = 1..8 on s = l + 16 e, phase 2
 // m' = 16..128 on s = 16 l + e after a warp-local shared transpose.
-template <class F, int LOGN1, class Fin>
+template <class F, class TwA, class Fin>
 __device__ __forceinline__ void blk_fwd_body(typename F::T (&x)[16], u64 (&o)[16], u64* s,
-                                             typename F::TwPtr tw, u32 b, u32 l,
-                                             const typename F::K& K, const Fin& fin) {
-  constexpr int N1 = 1 << LOGN1;
+                                             const TwA& twa, u32 l, const typename F::K& K,
+                                             const Fin& fin) {
   static_for<0, 4, 1>([&](auto LM) {
     constexpr int lm = decltype(LM)::value;
-    ct_stage<F, 16, (16 >> (lm + 1))>(x, [&](int gi) { return F::ld(tw, (N1 + b) * (1 << lm) + gi); }, K);
+    ct_stage<F, 16, (16 >> (lm + 1))>(x, [&](int gi) { return twa(lm, (u32)gi); }, K);
   });
 #pragma unroll
   for (int e = 0; e < 16; ++e) s[l + 16 * e + e] = F::bits(x[e]);
@@ -467,9 +506,7 @@ __device__ __forceinline__ void blk_fwd_body(typename F::T (&x)[16], u64 (&o)[16
   static_for<4, 8, 1>([&](auto LM) {
     constexpr int lm = decltype(LM)::value;
     constexpr int d = 256 >> (lm + 1);
-    ct_stage<F, 16, d>(x,
-                       [&](int gi) { return F::ld(tw, (N1 + b) * (1 << lm) + ((16 * l + gi * 2 * d) >> (8 - lm))); },
-                       K);
+    ct_stage<F, 16, d>(x, [&](int gi) { return twa(lm, (16 * l + gi * 2 * d) >> (8 - lm)); }, K);
   });
   __syncwarp();
 #pragma unroll
@@ -483,10 +520,9 @@ __device__ __forceinline__ void blk_fwd_body(typename F::T (&x)[16], u64 (&o)[16
 // Block pass body, inverse: x[e] = element l + 16 e of block b (coalesced
 // order) in and out; GS stages m' = 128 .. 1 (global m = N/2 .. N1). FP64
 // rows are brought back to |x| <= 0.75q after each 4-stage phase.
-template <class F, int LOGN1>
-__device__ __forceinline__ void blk_inv_body(typename F::T (&x)[16], u64* s, typename F::TwPtr tw,
-                                             u32 b, u32 l, const typename F::K& K) {
-  constexpr int N1 = 1 << LOGN1;
+template <class F, class TwA>
+__device__ __forceinline__ void blk_inv_body(typename F::T (&x)[16], u64* s, const TwA& twa, u32 l,
+                                             const typename F::K& K) {
 #pragma unroll
   for (int e = 0; e < 16; ++e) s[l + 16 * e + e] = F::bits(x[e]);
   __syncwarp();
@@ -495,9 +531,7 @@ __device__ __forceinline__ void blk_inv_body(typename F::T (&x)[16], u64* s, typ
   static_for<7, 3, -1>([&](auto LM) {
     constexpr int lm = decltype(LM)::value;
     constexpr int d = 256 >> (lm + 1);
-    gs_stage<F, 16, d>(x,
-                       [&](int gi) { return F::ld(tw, (N1 + b) * (1 << lm) + ((16 * l + gi * 2 * d) >> (8 - lm))); },
-                       K);
+    gs_stage<F, 16, d>(x, [&](int gi) { return twa(lm, (16 * l + gi * 2 * d) >> (8 - lm)); }, K);
   });
   F::gs_fix(x, K);
   __syncwarp();
@@ -509,7 +543,7 @@ __device__ __forceinline__ void blk_inv_body(typename F::T (&x)[16], u64* s, typ
   __syncwarp();
   static_for<3, -1, -1>([&](auto LM) {
     constexpr int lm = decltype(LM)::value;
-    gs_stage<F, 16, (16 >> (lm + 1))>(x, [&](int gi) { return F::ld(tw, (N1 + b) * (1 << lm) + gi); }, K);
+    gs_stage<F, 16, (16 >> (lm + 1))>(x, [&](int gi) { return twa(lm, (u32)gi); }, K);
   });
   F::gs_fix(x, K);
 }
@@ -542,7 +576,8 @@ __device__ __forceinline__ void blk_fwd_kernel_body(const RowMap& in, const Epi&
 #pragma unroll
   for (int e = 0; e < 16; ++e) x[e] = F::unbits(src[l + 16 * e]);
   u64 o[16];
-  blk_fwd_body<F, LOGN1>(x, o, s, F::table(tb, false, pi), b, l, K, [&](typename F::T v) -> u64 {
+  const GlobalTw<F> twa{F::table(tb, false, pi), (1u << LOGN1) + b};
+  blk_fwd_body<F>(x, o, s, twa, l, K, [&](typename F::T v) -> u64 {
     if (std::is_same<F, FpF>::value || Epi::kNeedsReduced) return F::canon(v, K);
     return F::bits(v);
   });
@@ -560,6 +595,10 @@ __device__ __forceinline__ void blk_fwd_kernel_body(const RowMap& in, const Epi&
   }
 }
 
+// Block pass, forward: 256-point blocks, 16 threads per block, 16 elements per
+// thread, 4 consecutive blocks of one row per CTA. (Staging the twiddles in
+// shared memory with 4 same-prime rows per CTA was measured slower here:
+// cfg2 ntt_blk_fwd<divround> 1.55 -> 1.88 ms.)
 template <int LOGN1, class Epi>
 __global__ void __launch_bounds__(64)
     ntt_blk_fwd(const __grid_constant__ RowMap in, const __grid_constant__ Epi epi,
@@ -620,19 +659,23 @@ struct IpOps<FpF> {
 
 template <class F, int LOGN1, int M>
 __device__ __forceinline__ void modup_ip_body(u32 bi, bool live, u32 t, u32 blk, u32 pi, u32 l,
-                                              u64* s, u64* s0acc, u64* s1acc, const u64* mid,
+                                              u64* s, u64* s0acc, u64* s1acc, ulonglong2* stw,
+                                              const u64* mid,
                                               const u64* c1, u64 c1_stride, const u32* perm,
                                               const u64* key, const u64* key_aux, u32 full,
                                               u64* acc, const NttTabs& tb) {
   const u32 n = 1u << tb.logn;
   const PrimeConst P = tb.primes[pi];
   const typename F::K K = F::konst(P);
-  const typename F::TwPtr tw = F::table(tb, false, pi);
   const u64 kstride = (u64)(full + 1) * n;
   const u32 a0 = (blk << 8) + l;
   // rotation: output block blk of every digit comes from block src_blk of the
   // unpermuted digit (block-local Galois permutation, see block_gather)
   const u32 src_blk = perm ? (__ldg(perm + (blk << 8)) >> 8) : blk;
+  // the CTA's 4 groups share (target row, block): its twiddles are staged once
+  stage_blk_tw<F>(stw, F::table(tb, false, pi), 1u << LOGN1, src_blk, threadIdx.x, 64);
+  __syncthreads();
+  const SmemTw<F> twa{stw};
 #pragma unroll 1
   for (int j = 0; j < M; ++j) {
     typename F::T x[16];
@@ -653,7 +696,7 @@ __device__ __forceinline__ void modup_ip_body(u32 bi, bool live, u32 t, u32 blk,
 #pragma unroll
       for (int e = 0; e < 16; ++e) x[e] = F::unbits(src[l + 16 * e]);
       u64 o[16];
-      blk_fwd_body<F, LOGN1>(x, o, s, tw, src_blk, l, K, [](typename F::T v) { return F::bits(v); });
+      blk_fwd_body<F>(x, o, s, twa, l, K, [](typename F::T v) { return F::bits(v); });
       if (perm) {
         // the body left the (lazy) block in shared memory: permuted read
 #pragma unroll
@@ -700,6 +743,7 @@ __global__ void __launch_bounds__(64, 8)
   constexpr int N1 = 1 << LOGN1;
   __shared__ u64 sm[4][256 + 16];
   __shared__ u64 sacc[4][2][256];  // lazy accumulators, coalesced order
+  __shared__ ulonglong2 stw[kBlkTw];
   const u32 l = threadIdx.x & 15, bw = threadIdx.x >> 4;
   // the 4 groups of a CTA take 4 consecutive ciphertexts of the same
   // (target row, block): the key words they share are served from L1
@@ -712,10 +756,10 @@ __global__ void __launch_bounds__(64, 8)
   const u32 bi = live ? bi_raw : B - 1;
   const u32 pi = t < (u32)M ? t : full;
   if (row_fp(tb, pi))
-    modup_ip_body<FpF, LOGN1, M>(bi, live, t, blk, pi, l, sm[bw], sacc[bw][0], sacc[bw][1], mid, c1,
+    modup_ip_body<FpF, LOGN1, M>(bi, live, t, blk, pi, l, sm[bw], sacc[bw][0], sacc[bw][1], stw, mid, c1,
                                  c1_stride, perm, key, key_aux, full, acc, tb);
   else
-    modup_ip_body<IntF, LOGN1, M>(bi, live, t, blk, pi, l, sm[bw], sacc[bw][0], sacc[bw][1], mid, c1,
+    modup_ip_body<IntF, LOGN1, M>(bi, live, t, blk, pi, l, sm[bw], sacc[bw][0], sacc[bw][1], stw, mid, c1,
                                   c1_stride, perm, key, key_aux, full, acc, tb);
 }
 
@@ -730,7 +774,7 @@ __device__ __forceinline__ void blk_inv_kernel_body(const RowMap& in, const RowM
   typename F::T x[16];
 #pragma unroll
   for (int e = 0; e < 16; ++e) x[e] = F::from_u64(src[l + 16 * e]);
-  blk_inv_body<F, LOGN1>(x, s, F::table(tb, true, pi), b, l, K);
+  blk_inv_body<F>(x, s, GlobalTw<F>{F::table(tb, true, pi), (1u << LOGN1) + b}, l, K);
   u64* dst = row_ptr(out, r) + (b << 8);
 #pragma unroll
   for (int e = 0; e < 16; ++e) dst[l + 16 * e] = F::bits(x[e]);
