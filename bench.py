@@ -217,6 +217,8 @@ def cpu_baseline(cfg, name, budget_s):
 
 # ------------------------------------------------------------------ our arm
 def our_arm(args, cfg):
+    global TRAFFIC_CONFIG
+    TRAFFIC_CONFIG = args.config
     import ctypes as C
 
     import torch
@@ -442,6 +444,11 @@ def profile_round(ctx, step, stream, N, m, npairs, Cc, width, n):
             "traffic": None, "peak_source": peaks["source"],
             "bytes_per_launch": top["bytes"] / top["launches"],
             "avg_launch_ms": top["ms"] / top["launches"], "share_of_round": top["share"]}
+    tr = traffic_for(top["name"], roof["bytes_per_launch"])
+    if tr:
+        roof["traffic"] = tr["dram_bytes_per_launch"]
+        roof["traffic_over_algorithmic"] = tr["ratio"]
+        roof["traffic_source"] = tr["source"]
     int_roof = None
     if top["bfly"]:
         ach = top["bfly"] / top["launches"] / avg_s / 1e9
@@ -452,6 +459,25 @@ def profile_round(ctx, step, stream, N, m, npairs, Cc, width, n):
                                    "independent CT butterflies, all SMs)"}
     return {"roofline": roof, "roofline_int": int_roof, "kernels": kernels[:12],
             "peak_gbfly_s": peak.value}
+
+
+TRAFFIC_CONFIG = None  # set by our_arm: the config whose ncu traffic file applies
+
+
+def traffic_for(kernel, algorithmic_bytes):
+    """DRAM bytes per launch of `kernel` from the committed ncu capture of one
+    round of this config (profiles/r01_traffic_<cfg>.json, tools/ncu_traffic.py),
+    or None when no capture exists."""
+    p = os.path.join(ROOT, "profiles", f"r01_traffic_{TRAFFIC_CONFIG}.json")
+    try:
+        with open(p) as f:
+            k = json.load(f)["kernels"][kernel]
+        return {"dram_bytes_per_launch": k["dram_bytes_per_launch"],
+                "algorithmic_bytes_per_launch": algorithmic_bytes,
+                "ratio": k["dram_bytes_per_launch"] / algorithmic_bytes,
+                "source": os.path.relpath(p, ROOT)}
+    except Exception:
+        return None
 
 
 def load_peaks():

@@ -1166,10 +1166,11 @@ void agg_tensor(lcl_context* c, const u64* clients, const u64* sel, u32 n, u32 c
   constexpr int ST = 6;
   const size_t smem = (size_t)ST * 4 * 256 * 16;
   allow_smem(aggregate_stream<ST>, smem);
-  const u64 th = (u64)B * slots / 2;
+  // 2 slots per thread; min(256, N / 2) threads divide m * N / 2 for any m
+  const u32 threads = (u32)std::min<u64>(256, c->N() / 2);
   ProfScope ps(c, "aggregate_tensor",
                8.0 * slots * (2.0 * (i1 - i0) * B + 2.0 * (i1 - i0) + 3.0 * B * (accumulate ? 2 : 1)));
-  aggregate_stream<ST><<<(u32)((th + 255) / 256), 256, smem, c->stream>>>(
+  aggregate_stream<ST><<<(u32)(slots / 2 / threads * B), threads, smem, c->stream>>>(
       clients, sel, i0, i1, chunks, c0, B, m, c->logn, tern, accumulate ? 1 : 0, c->d_primes);
   post_launch(c);
   (void)n;

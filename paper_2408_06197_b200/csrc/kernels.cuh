@@ -329,11 +329,11 @@ __global__ void __launch_bounds__(256)
                      u64* __restrict__ tern, int accumulate, const PrimeConst* __restrict__ primes) {
   extern __shared__ ulonglong2 ring[];  // [STAGES][4][blockDim]
   const u32 N = 1u << logn;
-  const u64 half_slots = (u64)m * N / 2;
-  const u64 gid = (u64)blockIdx.x * blockDim.x + threadIdx.x;
-  const u32 ch = (u32)(gid / half_slots);
-  if (ch >= chunks) return;  // whole warps: m * N / 2 is a multiple of 32
-  const u32 rem = (u32)(gid - (u64)ch * half_slots) * 2;
+  // chunk-fastest CTA order: the `chunks` CTAs of one slot block run back to
+  // back, so its selector words come from L2 instead of being re-read from
+  // HBM once per chunk (the client stream would evict them)
+  const u32 ch = blockIdx.x % chunks;
+  const u32 rem = ((blockIdx.x / chunks) * blockDim.x + threadIdx.x) * 2;
   const u32 r = rem >> logn, a = rem & (N - 1);
   const PrimeConst P = primes[r];
   const u64 q = P.q;
