@@ -400,6 +400,7 @@ def our_arm(args, cfg):
             "cuda_graph": graph is not None,
             "roofline": prof.get("roofline"),
             "roofline_int": prof.get("roofline_int"),
+            "roofline_fp64": prof.get("roofline_fp64"),
             "kernels": prof.get("kernels"),
             "cpu_baseline": cpu,
         }
@@ -457,8 +458,23 @@ def profile_round(ctx, step, stream, N, m, npairs, Cc, width, n):
                     "frac": ach / peak.value,
                     "peak_source": "measured live: lcl_peak_butterflies (register-resident "
                                    "independent CT butterflies, all SMs)"}
-    return {"roofline": roof, "roofline_int": int_roof, "kernels": kernels[:12],
-            "peak_gbfly_s": peak.value}
+    # the pair accumulation runs on the FP64 pipe (q-chain < 2^44): 17 FP64
+    # ops per pair-slot-chunk (2 DADD + 3 x (2 DFMA + 2 DADD + 1 DFMA)) against
+    # 64 ops/clk/SM at the SM clock the round ran at
+    fp64_roof = None
+    pk = next((k for k in kernels if k["name"] == "pair_accumulate"), None)
+    if pk is not None:
+        import torch
+        sms = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+        ops = 17.0 * npairs * Cc * m * N
+        ach = ops / (pk["ms"] * 1e-3) / 1e12
+        pk_peak = 64.0 * sms * 1.965e9 / 1e12
+        fp64_roof = {"bound": "fp64 pipe", "kernel": "pair_accumulate", "achieved": ach,
+                     "peak": pk_peak, "unit": "Tops/s", "frac": ach / pk_peak,
+                     "ops": ops, "peak_source": f"64 FP64 ops/clk/SM x {sms} SMs x 1965 MHz "
+                     "(4.27 pair-slots/clk/SM = 93% of it reached by tools/microbench/pair_forms.cu)"}
+    return {"roofline": roof, "roofline_int": int_roof, "roofline_fp64": fp64_roof,
+            "kernels": kernels[:12], "peak_gbfly_s": peak.value}
 
 
 TRAFFIC_CONFIG = None  # set by our_arm: the config whose ncu traffic file applies
