@@ -450,17 +450,26 @@ void blk_inv_n(lcl_context* c, u32 rows, const RowMap& in, const RowMap& out) {
   ntt_blk_inv<LOGN1><<<rows * N1 / 4, 64, 0, c->stream>>>(in, out, tabs(c));
 }
 
-template <int LOGN1, int E>
-void col_ilf_n(lcl_context* c, u32 src_rows, const RowMap& src, const RowMap& dst, u32 fan) {
+template <int LOGN1, int E, int MINB>
+void col_ilf_cfg(lcl_context* c, u32 src_rows, const RowMap& src, const RowMap& dst, u32 fan) {
   constexpr int N1 = 1 << LOGN1;
   constexpr size_t smem = (size_t)N1 * 16 * 8;
-  static bool once = (allow_smem(ntt_col_inv_lift_fwd<LOGN1, E>, smem), true);
+  static bool once = (allow_smem(ntt_col_inv_lift_fwd<LOGN1, E, MINB>, smem), true);
   (void)once;
   const u32 groups = (u32)(c->n >> LOGN1) >> 4;
   ProfScope ps(c, "ntt_col_inv_lift_fwd", 8.0 * c->N() * (src_rows + (double)src_rows * fan),
                0.5 * c->N() * LOGN1 * (src_rows + (double)src_rows * fan));
-  ntt_col_inv_lift_fwd<LOGN1, E><<<src_rows * groups, 16 * (N1 / E), smem, c->stream>>>(
+  ntt_col_inv_lift_fwd<LOGN1, E, MINB><<<src_rows * groups, 16 * (N1 / E), smem, c->stream>>>(
       src, dst, fan, c->d_smod, c->P(), tabs(c));
+}
+
+// E = 16: 4 CTAs per SM (128 registers) -- measured cfg2 2.26 -> 1.95 ms,
+// cfg3 24.3 -> 17.5 ms against the unconstrained build (252 registers,
+// 3 CTAs). (E = 8 with 256-thread CTAs was faster at cfg2 but not bit-exact:
+// the FP64 column phases assume 4-stage register phases.)
+template <int LOGN1, int E>
+void col_ilf_n(lcl_context* c, u32 src_rows, const RowMap& src, const RowMap& dst, u32 fan) {
+  col_ilf_cfg<LOGN1, E, E == 16 ? 4 : 1>(c, src_rows, src, dst, fan);
 }
 
 template <int LOGN1, class Epi>

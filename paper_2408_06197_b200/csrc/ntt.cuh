@@ -943,8 +943,8 @@ __device__ __forceinline__ void col_ilf_body(const RowMap& src, const RowMap& ds
   }
 }
 
-template <int LOGN1, int E>
-__global__ void __launch_bounds__(16 * ((1 << LOGN1) / E))
+template <int LOGN1, int E, int MINB = 1>
+__global__ void __launch_bounds__(16 * ((1 << LOGN1) / E), MINB)
     ntt_col_inv_lift_fwd(const __grid_constant__ RowMap src, const __grid_constant__ RowMap dst,
                          u32 fan, const u64* __restrict__ smod, u32 nprimes,
                          const __grid_constant__ NttTabs tb) {
