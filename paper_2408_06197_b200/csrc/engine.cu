@@ -394,7 +394,7 @@ void fwd2(lcl_context* c, u32 rows, const RowMap& mid, const Loader& ld, const E
     ProfScope ps(c, std::is_same<Epi, DivRoundStore>::value ? "ntt_blk_fwd<divround>" : "ntt_blk_fwd",
                  rb * (store_rows(epi, rows) + (std::is_same<Epi, PlainStore>::value ? rows : 0)),
                  bpr * rows * 8);
-    ntt_blk_fwd<LOGN1, Epi><<<rows * N1 / 4, 64, 0, c->stream>>>(mid, epi, tabs(c));
+    ntt_blk_fwd<LOGN1, Epi, 16><<<rows * N1 / 4, 64, 0, c->stream>>>(mid, epi, tabs(c));
   }
   post_launch(c, 2);
 }
@@ -465,8 +465,8 @@ void col_ilf_cfg(lcl_context* c, u32 src_rows, const RowMap& src, const RowMap& 
 
 // E = 16: 4 CTAs per SM (128 registers) -- measured cfg2 2.26 -> 1.95 ms,
 // cfg3 24.3 -> 17.5 ms against the unconstrained build (252 registers,
-// 3 CTAs). (E = 8 with 256-thread CTAs was faster at cfg2 but not bit-exact:
-// the FP64 column phases assume 4-stage register phases.)
+// 3 CTAs). (E = 8 with 256-thread CTAs was faster at cfg2 but produced
+// wrong words in the cfg2 distance test; not pursued.)
 template <int LOGN1, int E>
 void col_ilf_n(lcl_context* c, u32 src_rows, const RowMap& src, const RowMap& dst, u32 fan) {
   col_ilf_cfg<LOGN1, E, E == 16 ? 4 : 1>(c, src_rows, src, dst, fan);
@@ -478,7 +478,10 @@ void blk_fwd_n(lcl_context* c, u32 rows, const RowMap& mid, const Epi& epi) {
   ProfScope ps(c, std::is_same<Epi, DivRoundStore>::value ? "ntt_blk_fwd<divround>" : "ntt_blk_fwd",
                8.0 * c->N() * (store_rows(epi, rows) + (std::is_same<Epi, PlainStore>::value ? rows : 0)),
                0.5 * c->N() * rows * 8);
-  ntt_blk_fwd<LOGN1, Epi><<<rows * N1 / 4, 64, 0, c->stream>>>(mid, epi, tabs(c));
+  // 16 CTAs per SM (64-register cap): measured cfg2 1.87 -> 1.49 ms, cfg3
+  // 15.65 -> 11.44 ms against the unconstrained build (128 registers); the
+  // same cap on ntt_blk_inv and a 10-CTA cap on modup_ip_blk were slower
+  ntt_blk_fwd<LOGN1, Epi, 16><<<rows * N1 / 4, 64, 0, c->stream>>>(mid, epi, tabs(c));
 }
 
 // Calls f(LOGN1, E) with compile-time constants for the two-pass ring sizes.

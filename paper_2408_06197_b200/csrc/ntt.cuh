@@ -599,8 +599,8 @@ __device__ __forceinline__ void blk_fwd_kernel_body(const RowMap& in, const Epi&
 // thread, 4 consecutive blocks of one row per CTA. (Staging the twiddles in
 // shared memory with 4 same-prime rows per CTA was measured slower here:
 // cfg2 ntt_blk_fwd<divround> 1.55 -> 1.88 ms.)
-template <int LOGN1, class Epi>
-__global__ void __launch_bounds__(64)
+template <int LOGN1, class Epi, int MINB = 1>
+__global__ void __launch_bounds__(64, MINB)
     ntt_blk_fwd(const __grid_constant__ RowMap in, const __grid_constant__ Epi epi,
                 const __grid_constant__ NttTabs tb) {
   constexpr int N1 = 1 << LOGN1;
@@ -734,8 +734,8 @@ __device__ __forceinline__ void modup_ip_body(u32 bi, bool live, u32 t, u32 blk,
   }
 }
 
-template <int LOGN1, int M>
-__global__ void __launch_bounds__(64, 8)
+template <int LOGN1, int M, int MINB = 8>
+__global__ void __launch_bounds__(64, MINB)
     modup_ip_blk(u32 B, const u64* __restrict__ mid, const u64* __restrict__ c1, u64 c1_stride,
                  const u32* __restrict__ perm, const u64* __restrict__ key,
                  const u64* __restrict__ key_aux, u32 full, u64* __restrict__ acc,
@@ -780,8 +780,8 @@ __device__ __forceinline__ void blk_inv_kernel_body(const RowMap& in, const RowM
   for (int e = 0; e < 16; ++e) dst[l + 16 * e] = F::bits(x[e]);
 }
 
-template <int LOGN1>
-__global__ void __launch_bounds__(64)
+template <int LOGN1, int MINB = 1>
+__global__ void __launch_bounds__(64, MINB)
     ntt_blk_inv(const __grid_constant__ RowMap in, const __grid_constant__ RowMap out,
                 const __grid_constant__ NttTabs tb) {
   constexpr int N1 = 1 << LOGN1;
