@@ -273,7 +273,8 @@ struct lcl_context {
   bool prof_on = false;
   std::vector<ProfRec> prof;
   // workspace
-  DevBuf ws_coef, ws_digits, ws_acc, ws_coefsp, ws_mid, ws_tern, ws_ctA, ws_ctB, ws_ctC, ws_pt;
+  DevBuf ws_coef, ws_digits, ws_acc, ws_coefsp, ws_mid, ws_tern, ws_ctA, ws_ctB, ws_ctC, ws_pt,
+      ws_c1inv;
   // Concurrent lanes: independent ciphertext groups of a batched key-switch
   // chain run on their own streams with their own workspaces, so the small,
   // latency-bound per-level kernels of one group fill the SMs the other
@@ -281,7 +282,7 @@ struct lcl_context {
   struct Lane {
     cudaStream_t stream = nullptr;
     cudaEvent_t done = nullptr;
-    DevBuf ws_coef, ws_digits, ws_acc, ws_coefsp, ws_mid, ws_ctB, ws_ctC;
+    DevBuf ws_coef, ws_digits, ws_acc, ws_coefsp, ws_mid, ws_ctB, ws_ctC, ws_c1inv;
   };
   std::vector<Lane> lanes;
   cudaEvent_t fork_ev = nullptr;
@@ -355,6 +356,9 @@ inline double load_rows(const LiftLoadT<S>& l, double rows) { return rows / l.fa
 inline double store_rows(const PlainStore&, double rows) { return rows; }
 inline double store_rows(const DivRoundStore& s, double rows) {
   return rows * (2.0 + (s.add1.base ? 1.0 : 0.0)) + (s.add2.base ? rows / 2 : 0.0);
+}
+inline double store_rows(const DivRoundInvStore& s, double rows) {
+  return store_rows(static_cast<const DivRoundStore&>(s), rows) + rows / 2;  // + the c1 inverse rows
 }
 
 // ------------------------------------------------------------ NTT launchers
@@ -475,9 +479,12 @@ void col_ilf_n(lcl_context* c, u32 src_rows, const RowMap& src, const RowMap& ds
 template <int LOGN1, class Epi>
 void blk_fwd_n(lcl_context* c, u32 rows, const RowMap& mid, const Epi& epi) {
   constexpr int N1 = 1 << LOGN1;
-  ProfScope ps(c, std::is_same<Epi, DivRoundStore>::value ? "ntt_blk_fwd<divround>" : "ntt_blk_fwd",
+  ProfScope ps(c,
+               std::is_same<Epi, DivRoundStore>::value      ? "ntt_blk_fwd<divround>"
+               : std::is_same<Epi, DivRoundInvStore>::value ? "ntt_blk_fwd<divround+inv>"
+                                                            : "ntt_blk_fwd",
                8.0 * c->N() * (store_rows(epi, rows) + (std::is_same<Epi, PlainStore>::value ? rows : 0)),
-               0.5 * c->N() * rows * 8);
+               0.5 * c->N() * rows * (std::is_same<Epi, DivRoundInvStore>::value ? 12 : 8));
   // 16 CTAs per SM (64-register cap): measured cfg2 1.87 -> 1.49 ms, cfg3
   // 15.65 -> 11.44 ms against the unconstrained build (128 registers); the
   // same cap on ntt_blk_inv and a 10-CTA cap on modup_ip_blk were slower
@@ -664,8 +671,11 @@ constexpr bool kFuseSpecialInverse = false;
 bool ks_fused(const lcl_context* c, u32 m) { return c->logn >= 13 && m <= 6; }
 bool sp_preinverted(const lcl_context* c, u32 m) { return kFuseSpecialInverse && ks_fused(c, m); }
 
+// preinv: the c1 limbs' inverse block pass already ran (fused into the
+// previous level's divide-and-round, rows [B][m][N]); fused path only.
 u64* ks_switch(lcl_context* c, const RowMap& in, const u64* c1, u64 c1_stride, u32 B, u32 m,
-               const u32* sigma, const u32* perm, const u64* key, const u64* key_shoup) {
+               const u32* sigma, const u32* perm, const u64* key, const u64* key_shoup,
+               const u64* preinv = nullptr) {
   if (!ks_fused(c, m)) {
     u64* dig = ks_decompose(c, in, B, m, sigma);
     return ks_ip(c, dig, B, m, key, nullptr);
@@ -681,7 +691,11 @@ u64* ks_switch(lcl_context* c, const RowMap& in, const u64* c1, u64 c1_stride, u
       dp[j * m + tp] = t < m ? t : c->full;
     }
   const RowMap mid_map = make_map(mid, m * m, N, (u64)m * m * N, 1, 0, dp);
-  inv_lift_fwd_cols(c, B * m, in, mid_map, m);
+  if (preinv)
+    lift_fwd_cols_preinv(c, B * m, make_map(preinv, m, N, (u64)m * N, 1, 0, c->primes_0(m)),
+                         mid_map, m);
+  else
+    inv_lift_fwd_cols(c, B * m, in, mid_map, m);
   u64* acc = c->ws_acc.get((u64)B * 2 * (m + 1) * N);
   // Running the special rows' inverse block stages inside modup_ip_blk was
   // measured slower on cfg2 (8.91 vs 8.77 ms): it lengthens the
@@ -699,7 +713,8 @@ u64* ks_switch(lcl_context* c, const RowMap& in, const u64* c1, u64 c1_stride, u
 // sp_ready: the special rows' inverse block pass already ran inside
 // modup_ip_blk (fused ks_switch path); otherwise they are read from acc.
 void ks_moddown(lcl_context* c, const u64* acc, u32 B, u32 m, const RowMap& out,
-                const RowMap& add1, const RowMap& add2, const u32* perm, bool sp_ready) {
+                const RowMap& add1, const RowMap& add2, const u32* perm, bool sp_ready,
+                u64* c1inv = nullptr) {
   const u64 N = c->N();
   const RowMap sp_in = make_map(acc + (u64)m * N, 1, N, (m + 1) * N, 1, 0, {c->full});
   DivRoundStore epi;
@@ -722,9 +737,18 @@ void ks_moddown(lcl_context* c, const u64* acc, u32 B, u32 m, const RowMap& out,
     } else {
       inv_lift_fwd_cols(c, 2 * B, sp_in, mid_map, m);
     }
-    blk_fwd_only(c, 2 * B * m, mid_map, epi);
+    if (c1inv) {
+      // also the next key switch's inverse block pass over the c1 limbs
+      DivRoundInvStore ie;
+      static_cast<DivRoundStore&>(ie) = epi;
+      ie.inv_out = make_map(c1inv, m, N, 0, 2, (u64)m * N, c->primes_0(m));
+      blk_fwd_only(c, 2 * B * m, mid_map, ie);
+    } else {
+      blk_fwd_only(c, 2 * B * m, mid_map, epi);
+    }
     return;
   }
+  need(!c1inv, LCL_USAGE_ERROR, "fused next-level inverse needs a two-pass ring");
   u64* csp = c->ws_coefsp.get((u64)B * 2 * N);
   const RowMap sp_map = make_map(csp, 1, N, N, 1, 0, {c->full});
   launch_inv(c, 2 * B, sp_in, PlainStore{sp_map});
@@ -785,8 +809,10 @@ const u64* rot_key(lcl_context* c, size_t step) {
 
 // out = in + rotate(in, step) over B ciphertexts (one slot_reduce level,
 // distance.cpp:235-237), or plain rotate when accumulate == false.
+// preinv_in: in's c1 inverse block pass (from the previous level), or null;
+// preinv_out: where to leave out's (fused into this level's divide-and-round).
 void rotate_level(lcl_context* c, const u64* in, u32 B, u32 m, size_t step, u64* out,
-                  bool accumulate) {
+                  bool accumulate, const u64* preinv_in = nullptr, u64* preinv_out = nullptr) {
   const u64 N = c->N();
   const u64* key = rot_key(c, step);
   const u32* perm = c->d_perm.at(step);
@@ -796,10 +822,10 @@ void rotate_level(lcl_context* c, const u64* in, u32 B, u32 m, size_t step, u64*
   // coefficient-domain automorphism instead.
   const u32* sigma = c->logn < 13 ? c->d_sigma.at(step) : nullptr;
   u64* acc = ks_switch(c, c1, in + (u64)m * N, 2ull * m * N, B, m, sigma, perm, key,
-                       c->d_rot_shoup.at(step));
+                       c->d_rot_shoup.at(step), preinv_in);
   const RowMap inm = ct_map(in, m, N, 2ull * m * N);
   ks_moddown(c, acc, B, m, ct_map(out, m, N, 2ull * m * N), accumulate ? inm : null_map(), inm,
-             perm, sp_preinverted(c, m));
+             perm, sp_preinverted(c, m), preinv_out);
   c->counts.rotations += B;
   c->counts.mod_ups += B;
   if (accumulate) c->counts.additions += B;
@@ -818,6 +844,7 @@ void swap_lane(lcl_context* c, u32 g) {
   std::swap(c->ws_mid, ln.ws_mid);
   std::swap(c->ws_ctB, ln.ws_ctB);
   std::swap(c->ws_ctC, ln.ws_ctC);
+  std::swap(c->ws_c1inv, ln.ws_c1inv);
 }
 
 // Two lanes pay off when a level's working set is L2-sized (cfg2: 45 x 3
@@ -917,9 +944,15 @@ void slot_reduce_serial(lcl_context* c, const u64* in, u32 B, u32 m, size_t widt
       c->counts.additions += B;
     }
   }
+  // each level leaves its output's c1 inverse block pass for the next one
+  // (two-pass rings); one buffer suffices: a level's column pass has read it
+  // before the same level's divide-and-round rewrites it
+  const bool chain = ks_fused(c, m);
+  u64* pre = chain ? c->ws_c1inv.get((u64)B * m * N) : nullptr;
   for (size_t j = unf; j < levels; ++j) {
     const int nxt = cur < 0 ? 0 : 1 - cur;
-    rotate_level(c, cur_ptr(), B, m, norm_step(c, size_t{1} << j), bufs[nxt], true);
+    rotate_level(c, cur_ptr(), B, m, norm_step(c, size_t{1} << j), bufs[nxt], true,
+                 chain && j > unf ? pre : nullptr, chain && j + 1 < levels ? pre : nullptr);
     cur = nxt;
   }
   cudaMemcpyAsync(out, cur_ptr(), words * 8, cudaMemcpyDeviceToDevice, c->stream);
@@ -1390,7 +1423,7 @@ void build_context(lcl_context* c, size_t degree, int depth, int secure, int dev
 void free_context(lcl_context* c) {
   for (auto& ln : c->lanes) {
     for (DevBuf* b : {&ln.ws_coef, &ln.ws_digits, &ln.ws_acc, &ln.ws_coefsp, &ln.ws_mid,
-                      &ln.ws_ctB, &ln.ws_ctC})
+                      &ln.ws_ctB, &ln.ws_ctC, &ln.ws_c1inv})
       b->release();
     if (ln.done) cudaEventDestroy(ln.done);
     if (ln.stream) cudaStreamDestroy(ln.stream);
@@ -1414,7 +1447,7 @@ void free_context(lcl_context* c) {
   for (auto& kv : c->d_perm) cudaFree(kv.second);
   for (auto& kv : c->d_sigma) cudaFree(kv.second);
   for (DevBuf* b : {&c->ws_coef, &c->ws_digits, &c->ws_acc, &c->ws_coefsp, &c->ws_mid,
-                    &c->ws_tern, &c->ws_ctA, &c->ws_ctB, &c->ws_ctC, &c->ws_pt, &c->ws_io_in,
+                    &c->ws_tern, &c->ws_ctA, &c->ws_ctB, &c->ws_ctC, &c->ws_pt, &c->ws_c1inv, &c->ws_io_in,
                     &c->ws_io_sel, &c->ws_io_dist, &c->ws_io_agg, &c->ws_dtern, &c->ws_ptl})
     b->release();
   for (cudaEvent_t e : c->io_ev) cudaEventDestroy(e);

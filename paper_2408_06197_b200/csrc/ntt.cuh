@@ -232,6 +232,7 @@ using LiftSigmaLoad = LiftLoadT<true>;
 // row may hand over its lazy word (< 80q); FP64 rows always hand over [0, q).
 struct PlainStore {
   static constexpr bool kNeedsReduced = true;
+  static constexpr bool kInvNext = false;
   RowMap out;
   struct Pre {};
   struct Row {
@@ -252,6 +253,7 @@ struct PlainStore {
 // (gathered reads); add1 may alias out (same thread reads then writes one word).
 struct DivRoundStore {
   static constexpr bool kNeedsReduced = false;  // the lift may be any lazy word < 80q
+  static constexpr bool kInvNext = false;
   RowMap out;
   RowMap x;
   RowMap add1;  // base == nullptr: absent
@@ -292,10 +294,11 @@ struct DivRoundStore {
       }
       p.add = v;
     }
-    __device__ __forceinline__ void store(const Pre& p, u32 a, u64 lift) const {
+    __device__ __forceinline__ u64 store(const Pre& p, u32 a, u64 lift) const {
       // lift < 80q (lazy NTT output): x + 80q - lift > 0 and congruent
-      const u64 v = mul_shoup(p.x + (q80 - lift), iv, ivs, q);
-      o[a] = add_mod(v, p.add, q);
+      const u64 v = add_mod(mul_shoup(p.x + (q80 - lift), iv, ivs, q), p.add, q);
+      o[a] = v;
+      return v;
     }
   };
   __device__ __forceinline__ Row bind(u32 r, u32 dpi, const PrimeConst& P) const {
@@ -313,6 +316,17 @@ struct DivRoundStore {
     w.q80 = 80 * P.q;
     return w;
   }
+};
+
+// DivRoundStore that also runs the NEXT key switch's inverse block pass on the
+// c1 half of every output ciphertext (items with x = 1): the final words of a
+// rotation level are already in registers, so the next level's ntt_blk_inv
+// over its c1 limbs (and that HBM / L2 round trip) disappears. inv_out: the
+// coefficient-bound rows [B][m][N] the next ks_switch hands to its fused
+// column pass (ks_switch's preinv).
+struct DivRoundInvStore : DivRoundStore {
+  static constexpr bool kInvNext = true;
+  RowMap inv_out;  // same row structure as out; group_stride m N, item_stride 0
 };
 
 // ------------------------------------------------------------ stage helpers
@@ -591,7 +605,24 @@ __device__ __forceinline__ void blk_fwd_kernel_body(const RowMap& in, const Epi&
 #pragma unroll
     for (int e = 0; e < 4; ++e) row.prefetch(pre[e], (b << 8) + l + 16 * (e0 + e), s);
 #pragma unroll
-    for (int e = 0; e < 4; ++e) row.store(pre[e], (b << 8) + l + 16 * (e0 + e), o[e0 + e]);
+    for (int e = 0; e < 4; ++e) {
+      if constexpr (Epi::kInvNext)
+        o[e0 + e] = row.store(pre[e], (b << 8) + l + 16 * (e0 + e), o[e0 + e]);
+      else
+        row.store(pre[e], (b << 8) + l + 16 * (e0 + e), o[e0 + e]);
+    }
+  }
+  if constexpr (Epi::kInvNext) {
+    const RowMap& om = epi.out;
+    if (((r / om.rows_per_item) % om.items_per_group) == 1) {
+      __syncwarp();  // s[] (permuted add2 staging) is reused by the inverse body
+#pragma unroll
+      for (int e = 0; e < 16; ++e) x[e] = F::from_u64(o[e]);
+      blk_inv_body<F>(x, s, GlobalTw<F>{F::table(tb, true, pi), (1u << LOGN1) + b}, l, K);
+      u64* dst = row_ptr(epi.inv_out, r) + (b << 8);
+#pragma unroll
+      for (int e = 0; e < 16; ++e) dst[l + 16 * e] = F::bits(x[e]);
+    }
   }
 }
 
