@@ -11,6 +11,7 @@
  *   lcl_upload_*_key         KeyBundle relin / rotation keys           ckks.hpp:73-97
  *   lcl_ntt_forward/inverse  PolyRns::ntt_forward / ntt_inverse        rns.cpp:282-302
  *   lcl_hadd / lcl_hsub      CkksContext::hadd / hsub                  ckks.cpp:395-415
+ *   lcl_hmult / lcl_hsquare  CkksContext::hmult_triple / hsquare       ckks.cpp:417-451
  *   lcl_relinearize          CkksContext::relinearize                  ckks.cpp:522-534
  *   lcl_rescale              CkksContext::rescale                      ckks.cpp:536-547
  *   lcl_rotate               CkksContext::rotate                       ckks.cpp:560-580
@@ -121,6 +122,14 @@ int lcl_hadd(lcl_context* ctx, const uint64_t* d_a, const uint64_t* d_b, size_t 
 int lcl_hsub(lcl_context* ctx, const uint64_t* d_a, const uint64_t* d_b, size_t batch,
              size_t count, uint64_t* d_out);
 /* batch ternaries [batch][3][count][N] -> ciphertexts [batch][2][count][N]. */
+/* CkksContext::hmult_triple (ckks.cpp:417-439, Karatsuba) over `batch` pairs
+ * of ciphertexts at `count` limbs: d_tern [batch][3][count][N]. Scales are
+ * the caller's (product). multiplications += batch. */
+int lcl_hmult(lcl_context* ctx, const uint64_t* d_a, const uint64_t* d_b, size_t batch,
+              size_t count, uint64_t* d_tern);
+/* CkksContext::hsquare (ckks.cpp:441-451): d0 = c0^2, d1 = 2 c0 c1, d2 = c1^2. */
+int lcl_hsquare(lcl_context* ctx, const uint64_t* d_a, size_t batch, size_t count,
+                uint64_t* d_tern);
 int lcl_relinearize(lcl_context* ctx, const uint64_t* d_tern, size_t batch, size_t count,
                     uint64_t* d_out);
 /* [batch][2][count][N] -> [batch][2][count-1][N]; DEPTH_EXHAUSTED at count 1. */

@@ -7,6 +7,8 @@
 //
 //   ref_driver gen   <options> --out DIR   dump keys, inputs, outputs, counters
 //   ref_driver bench <options> --reps R    time build_distance_matrix + masked_aggregate
+//   ref_driver ops   --N N --reps S        per-op latency (NTT, mult+relin+rescale,
+//                                          hoisted rotations, rotate), S s per op
 //
 // Options: --N --depth --clients --dim --k --seed --rule krum|multi_krum|median
 //          --select i,j,... --secure 0|1 --lazy 0|1 --inter 0|1
@@ -334,6 +336,61 @@ int cmd_bench(const Opts& o) {
   return 0;
 }
 
+// Per-op latency of the reference evaluator at ring degree N, on the shapes
+// of its own google-benchmark harness (proj/benchmarks/bench_ring.cpp:28-165,
+// BM_NttRoundtrip / BM_MultRelinRescale / BM_RotationsHoisted(7) /
+// BM_Rotate): a fresh ciphertext at full level, keys for steps 1..7 and the
+// powers of two. Each op repeats until ~budget seconds have elapsed (>= 2 reps).
+int cmd_ops(const Opts& o) {
+  CkksParams p;
+  p.ring_degree = o.N;
+  p.depth = o.depth;
+  p.security = o.secure ? SecurityLevel::bits128 : SecurityLevel::none;
+  const CkksContext ctx(p);
+  std::vector<std::size_t> steps = {1, 2, 3, 4, 5, 6, 7};
+  for (std::size_t st = 8; st < ctx.slot_count(); st *= 2) steps.push_back(st);
+  Sampler key_rng(101);
+  const KeyBundle keys = ctx.generate_keys(key_rng, steps);
+  Sampler rng(202);
+  std::vector<double> v(ctx.slot_count());
+  for (double& x : v) x = rng.uniform_real() - 0.5;
+  const Ciphertext ct = ctx.encrypt(ctx.encode(v), keys.pk, rng);
+  const double budget = (double)o.reps;  // seconds per op
+  auto time_op = [&](auto&& f) {
+    std::size_t n = 0;
+    const auto a = std::chrono::steady_clock::now();
+    double el = 0;
+    do {
+      f();
+      ++n;
+      el = std::chrono::duration<double>(std::chrono::steady_clock::now() - a).count();
+    } while (el < budget || n < 2);
+    return el / (double)n;
+  };
+  PolyRns poly = ct.c0;
+  const double ntt = time_op([&] {
+    poly.ntt_inverse();
+    poly.ntt_forward();
+  });
+  const double mrr = time_op([&] {
+    const Ciphertext out = ctx.rescale(ctx.relinearize(ctx.hsquare(ct), keys.relin));
+    (void)out;
+  });
+  const std::vector<std::size_t> h7 = {1, 2, 3, 4, 5, 6, 7};
+  const double hoist = time_op([&] {
+    const std::vector<Ciphertext> out = ctx.hoisted_rotations(ct, h7, keys.rotations);
+    (void)out;
+  });
+  const double rot = time_op([&] {
+    const Ciphertext out = ctx.rotate(ct, 1, keys.rotations);
+    (void)out;
+  });
+  std::printf("{\"N\": %zu, \"limbs\": %zu, \"threads\": %zu, \"ntt_roundtrip_s\": %.9f, "
+              "\"mult_relin_rescale_s\": %.9f, \"hoisted7_s\": %.9f, \"rotate_s\": %.9f}\n",
+              o.N, ct.c0.row_count(), worker_count(), ntt, mrr, hoist, rot);
+  return 0;
+}
+
 }  // namespace
 
 int main(int argc, char** argv) {
@@ -341,6 +398,7 @@ int main(int argc, char** argv) {
     const Opts o = parse(argc, argv);
     if (o.cmd == "gen") return cmd_gen(o);
     if (o.cmd == "bench") return cmd_bench(o);
+    if (o.cmd == "ops") return cmd_ops(o);
     std::fprintf(stderr, "unknown command %s\n", o.cmd.c_str());
     return 2;
   } catch (const std::exception& e) {

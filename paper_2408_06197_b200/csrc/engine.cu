@@ -1771,6 +1771,25 @@ int lcl_hsub(lcl_context* ctx, const uint64_t* a, const uint64_t* b, size_t batc
   return addsub(ctx, a, b, batch, count, out, true);
 }
 
+int lcl_hmult(lcl_context* ctx, const uint64_t* d_a, const uint64_t* d_b, size_t batch,
+              size_t count, uint64_t* d_tern) {
+  return guarded([&] {
+    check_count(ctx, count);
+    const u64 total = (u64)batch * count * ctx->N();
+    if (total == 0) return;
+    ProfScope ps(ctx, "ct_tensor", 8.0 * (double)total * (d_a == d_b ? 5 : 7));
+    ct_tensor<<<(u32)((total + 255) / 256), 256, 0, ctx->stream>>>(
+        d_a, d_b, (u32)batch, (u32)count, ctx->logn, d_tern, ctx->d_primes);
+    post_launch(ctx);
+    ctx->counts.multiplications += batch;
+  });
+}
+
+int lcl_hsquare(lcl_context* ctx, const uint64_t* d_a, size_t batch, size_t count,
+                uint64_t* d_tern) {
+  return lcl_hmult(ctx, d_a, d_a, batch, count, d_tern);
+}
+
 int lcl_relinearize(lcl_context* ctx, const uint64_t* d_tern, size_t batch, size_t count,
                     uint64_t* d_out) {
   return guarded([&] {

@@ -453,6 +453,39 @@ __global__ void __launch_bounds__(256)
 }
 
 // ------------------------------------------------------------------------
+// ct x ct tensor (ckks.cpp:417-451) over B pairs of ciphertexts [B][2][m][N]:
+// hmult_triple (Karatsuba: d1 = (a0 + a1)(b0 + b1) - d0 - d2) or, when
+// b == a, hsquare (d1 = 2 a0 a1); both are the same residues as the
+// schoolbook product. out: [B][3][m][N].
+__global__ void __launch_bounds__(256)
+    ct_tensor(const u64* __restrict__ a, const u64* __restrict__ b, u32 B, u32 m, u32 logn,
+              u64* __restrict__ out, const PrimeConst* __restrict__ primes) {
+  const u32 N = 1u << logn;
+  const u64 slots = (u64)m * N;
+  const u64 gid = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gid >= (u64)B * slots) return;
+  const u64 item = gid / slots, s = gid - item * slots;
+  const PrimeConst P = primes[(u32)(s >> logn)];
+  const u64 q = P.q;
+  const u64 a0 = a[item * 2 * slots + s], a1 = a[item * 2 * slots + slots + s];
+  u64* o = out + item * 3 * slots + s;
+  if (a == b) {
+    const u64 d0 = mul_mod(a0, a0, P), d2 = mul_mod(a1, a1, P);
+    const u64 x = mul_mod(a0, a1, P);
+    o[0] = d0;
+    o[slots] = add_mod(x, x, q);
+    o[2 * slots] = d2;
+    return;
+  }
+  const u64 b0 = b[item * 2 * slots + s], b1 = b[item * 2 * slots + slots + s];
+  const u64 d0 = mul_mod(a0, b0, P), d2 = mul_mod(a1, b1, P);
+  const u64 k = mul_mod(add_mod(a0, a1, q), add_mod(b0, b1, q), P);
+  o[0] = d0;
+  o[slots] = sub_mod(sub_mod(k, d0, q), d2, q);
+  o[2 * slots] = d2;
+}
+
+// ------------------------------------------------------------------------
 // ct x pt (ckks.cpp:549-558): out[b][x][i][a] = ct[b][x][i][a] * pt[i][a].
 __global__ void __launch_bounds__(256)
     mult_plain(const u64* __restrict__ ct, const u64* __restrict__ pt, u32 B, u32 m, u32 logn,

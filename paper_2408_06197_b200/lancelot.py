@@ -136,6 +136,8 @@ def lib():
         "lcl_ntt_inverse": [_P, _P, _SZ, _SZ, C.c_int],
         "lcl_hadd": [_P, _P, _P, _SZ, _SZ, _P],
         "lcl_hsub": [_P, _P, _P, _SZ, _SZ, _P],
+        "lcl_hmult": [_P, _P, _P, _SZ, _SZ, _P],
+        "lcl_hsquare": [_P, _P, _SZ, _SZ, _P],
         "lcl_relinearize": [_P, _P, _SZ, _SZ, _P],
         "lcl_rescale": [_P, _P, _SZ, _SZ, _P],
         "lcl_rotate": [_P, _P, _SZ, _SZ, _SZ, _P],
@@ -469,6 +471,23 @@ class CkksContext:
         out = self._empty(*a.data.shape)
         _check(lib().lcl_hsub(self.h, _ptr(a.data), _ptr(b.data), 1, a.level() + 1, _ptr(out)))
         return Ciphertext(out, a.scale)
+
+    def hmult_triple(self, a: Ciphertext, b: Ciphertext) -> TernaryCiphertext:
+        """ckks.cpp:417-439 (Karatsuba; scale = product)."""
+        if a.level() != b.level():
+            raise AlignmentError("operands at different levels")
+        m = a.level() + 1
+        out = self._empty(3, m, self._params.ring_degree)
+        _check(lib().lcl_hmult(self.h, _ptr(a.data.contiguous()), _ptr(b.data.contiguous()), 1, m,
+                               _ptr(out)))
+        return TernaryCiphertext(out, a.scale * b.scale)
+
+    def hsquare(self, a: Ciphertext) -> TernaryCiphertext:
+        """ckks.cpp:441-451 (scale = square)."""
+        m = a.level() + 1
+        out = self._empty(3, m, self._params.ring_degree)
+        _check(lib().lcl_hsquare(self.h, _ptr(a.data.contiguous()), 1, m, _ptr(out)))
+        return TernaryCiphertext(out, a.scale * a.scale)
 
     def relinearize(self, t: TernaryCiphertext, rk: RelinKey) -> Ciphertext:
         self.use_relin_key(rk)

@@ -81,6 +81,10 @@ def test_evaluator_matches_oracle(evalrig):
     assert np.array_equal(L.to_host(ctx.hsub(a, b).data), orc.hsub(clients[0, 0], clients[1, 0]))
     assert np.array_equal(L.to_host(ctx.hadd(a, b).data), orc.hadd(clients[0, 0], clients[1, 0]))
     t = orc.hsquare(orc.hsub(clients[0, 0], clients[1, 0]))
+    sq = ctx.hsquare(ctx.hsub(a, b))
+    assert np.array_equal(L.to_host(sq.data), t) and sq.scale == s * s
+    hm = ctx.hmult_triple(a, b)
+    assert np.array_equal(L.to_host(hm.data), orc.hmult_triple(clients[0, 0], clients[1, 0]))
     tern = L.TernaryCiphertext(L.to_device(t), s * s)
     rl = ctx.relinearize(tern, rk)
     want_rl = orc.relinearize(t)
