@@ -1092,7 +1092,10 @@ bool pair_accumulate_f64_cfg(lcl_context* c, const u64* clients, u32 n, u32 chun
 
 // pair_accumulate on the FP64 pipe when the q-chain allows it (measured at
 // cfg3, 190 pairs x 342 chunks: <8,6,2,false> 26.2 ms, <4,8,3,false> 27.9,
-// <4,8,2,true> 30.0, <2,8,4,false> 45.7; split-23 integer kernel 50.3),
+// <4,8,2,true> 30.0, <2,8,4,false> 45.7; split-23 integer kernel 50.3; a
+// warp-specialised variant -- producer warp, full/empty mbarriers, no CTA
+// barrier -- ran 29.6 ms with cp.async and 55 ms with 64-byte TMA bulk
+// copies, which are issue-bound at this row size),
 // else the split-23 integer kernel.
 void pair_accumulate_launch(lcl_context* c, const u64* clients, u32 n, u32 chunks, u32 c0,
                             u32 c1, const PairSet& ps, u64* tern, bool accumulate) {
