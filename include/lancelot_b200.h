@@ -23,6 +23,8 @@
  *   lcl_*_pairs / _chunks    the same, one shard of pairs / chunks     distance.cpp:257-272,
  *                            (the reference's parallel_for ranges)     aggregation.cpp:211
  *   lcl_get_counts           OpCounters::snapshot                      ckks.cpp:134-156
+ *   lcl_decrypt / _decode    CkksContext::decrypt / decode (KGC side)  ckks.cpp:313-393,
+ *   lcl_decrypt_values       + Embedding::coeffs_to_slots              encoding.cpp:118-134
  *
  * Conventions
  *   - Plain pointers and sizes only. Buffers named d_* are DEVICE pointers on
@@ -146,6 +148,21 @@ int lcl_slot_reduce(lcl_context* ctx, const uint64_t* d_ct, size_t batch, size_t
 /* ct x pt with a plaintext encoded on the host at (value, scale, level). */
 int lcl_mult_plain_const(lcl_context* ctx, const uint64_t* d_ct, size_t batch, size_t count,
                          double value, double pt_scale, uint64_t* d_out);
+
+/* KGC side, bit-identical to the reference:
+ * lcl_decrypt         CkksContext::decrypt (ckks.cpp:381-388): d_pt [batch][count][N] =
+ *                     c1 * s + c0 (evaluation domain); d_sk = the first `count` rows of
+ *                     SecretKey::s [count][N] (evaluation domain).
+ * lcl_decode          CkksContext::decode (ckks.cpp:313-348) + Embedding::coeffs_to_slots
+ *                     (encoding.cpp:118-134): d_pt is inverse-transformed in place,
+ *                     d_slots [batch][N/2] doubles.
+ * lcl_decrypt_values  decrypt_values (ckks.cpp:390-393) = decode(decrypt(ct, sk)). */
+int lcl_decrypt(lcl_context* ctx, const uint64_t* d_ct, size_t batch, size_t count,
+                const uint64_t* d_sk, uint64_t* d_pt);
+int lcl_decode(lcl_context* ctx, uint64_t* d_pt, size_t batch, size_t count, double scale,
+               double* d_slots);
+int lcl_decrypt_values(lcl_context* ctx, const uint64_t* d_ct, size_t batch, size_t count,
+                       double scale, const uint64_t* d_sk, double* d_slots);
 
 /* ------------------------------------------------------------ hot path */
 /* a, b: [chunks][2][full][N]; out: [2][full-1][N]. lazy != 0 -> one relin. */

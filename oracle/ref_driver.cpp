@@ -8,7 +8,7 @@
 //   ref_driver gen   <options> --out DIR   dump keys, inputs, outputs, counters
 //   ref_driver bench <options> --reps R    time build_distance_matrix + masked_aggregate
 //   ref_driver ops   --N N --reps S        per-op latency (NTT, mult+relin+rescale,
-//                                          hoisted rotations, rotate), S s per op
+//                                          hoisted rotations, rotate, decrypt_values), S s per op
 //
 // Options: --N --depth --clients --dim --k --seed --rule krum|multi_krum|median
 //          --select i,j,... --secure 0|1 --lazy 0|1 --inter 0|1
@@ -385,9 +385,14 @@ int cmd_ops(const Opts& o) {
     const Ciphertext out = ctx.rotate(ct, 1, keys.rotations);
     (void)out;
   });
+  const double dec = time_op([&] {  // BM_Decrypt
+    const std::vector<double> vals = ctx.decrypt_values(ct, keys.sk);
+    (void)vals;
+  });
   std::printf("{\"N\": %zu, \"limbs\": %zu, \"threads\": %zu, \"ntt_roundtrip_s\": %.9f, "
-              "\"mult_relin_rescale_s\": %.9f, \"hoisted7_s\": %.9f, \"rotate_s\": %.9f}\n",
-              o.N, ct.c0.row_count(), worker_count(), ntt, mrr, hoist, rot);
+              "\"mult_relin_rescale_s\": %.9f, \"hoisted7_s\": %.9f, \"rotate_s\": %.9f, "
+              "\"decrypt_values_s\": %.9f}\n",
+              o.N, ct.c0.row_count(), worker_count(), ntt, mrr, hoist, rot, dec);
   return 0;
 }
 

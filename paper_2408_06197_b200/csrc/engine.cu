@@ -28,6 +28,7 @@
 #include "../../include/lancelot_b200.h"
 #include "common.cuh"
 #include "kernels.cuh"
+#include "decode.cuh"
 #include "ntt.cuh"
 
 using namespace lcl;
@@ -290,6 +291,12 @@ struct lcl_context {
   // masked_aggregate's encode(1/l) plaintext, NTT'd on the device once per l
   size_t pt_l = 0;
   std::vector<u64> pt_host;
+  // decode tables (Embedding, encoding.cpp:40-80), built on first decode
+  double2* d_twist = nullptr;
+  double2* d_roots = nullptr;
+  u32* d_brv = nullptr;
+  u32* d_slot = nullptr;
+  DevBuf ws_dec;
   // overlapped host round: H2D / D2H copy streams and per-slice events
   cudaStream_t h2d = nullptr, d2h = nullptr;
   std::vector<cudaEvent_t> io_ev;
@@ -1105,6 +1112,96 @@ void pair_accumulate_launch(lcl_context* c, const u64* clients, u32 n, u32 chunk
   pair_accumulate_cfg<8, 4, 8>(c, clients, n, chunks, c0, c1, ps.a, ps.b, tern, accumulate);
 }
 
+// ------------------------------------------------------------ KGC decode
+// Embedding tables of the reference (encoding.cpp:40-80): twist[i] =
+// polar(1, pi i / N), roots[k] = polar(1, 2 pi k / h), the bit reversal of
+// log2 h bits and slot_index[j] = (5^j mod 2N - 1) / 4, computed with the same
+// host libm expressions, so the device FFT sees the reference's doubles.
+void ensure_decode_tables(lcl_context* c) {
+  if (c->d_twist) return;
+  const size_t n = c->n, h = n / 2;
+  const int logh = __builtin_ctzll(h);
+  const double pi = 3.141592653589793238462643383279502884;  // std::numbers::pi
+  std::vector<double2> tw(h), rt(h / 2 > 0 ? h / 2 : 1);
+  for (size_t i = 0; i < h; ++i) {
+    const double ang = pi * static_cast<double>(i) / static_cast<double>(n);
+    tw[i] = make_double2(std::cos(ang), std::sin(ang));
+  }
+  for (size_t k = 0; k < h / 2; ++k) {
+    const double ang = 2.0 * pi * static_cast<double>(k) / static_cast<double>(h);
+    rt[k] = make_double2(std::cos(ang), std::sin(ang));
+  }
+  std::vector<u32> brv(h), slot(h);
+  for (size_t i = 0; i < h; ++i) brv[i] = (u32)h_brv(i, logh);
+  u64 g = 1;
+  for (size_t j = 0; j < h; ++j) {
+    slot[j] = (u32)((g - 1) / 4);
+    g = (g * 5) % (2 * n);
+  }
+  cuda_check(cudaMalloc(&c->d_twist, h * sizeof(double2)), "alloc");
+  cuda_check(cudaMalloc(&c->d_roots, rt.size() * sizeof(double2)), "alloc");
+  cuda_check(cudaMalloc(&c->d_brv, h * 4), "alloc");
+  cuda_check(cudaMalloc(&c->d_slot, h * 4), "alloc");
+  cuda_check(cudaMemcpy(c->d_twist, tw.data(), h * sizeof(double2), cudaMemcpyHostToDevice), "upload");
+  cuda_check(cudaMemcpy(c->d_roots, rt.data(), rt.size() * sizeof(double2), cudaMemcpyHostToDevice), "upload");
+  cuda_check(cudaMemcpy(c->d_brv, brv.data(), h * 4, cudaMemcpyHostToDevice), "upload");
+  cuda_check(cudaMemcpy(c->d_slot, slot.data(), h * 4, cudaMemcpyHostToDevice), "upload");
+}
+
+// decrypt (ckks.cpp:381-388): pt [B][m][N] = c1 * s + c0, evaluation domain.
+void decrypt_batch(lcl_context* c, const u64* ct, u32 B, u32 m, const u64* sk, u64* pt) {
+  const u64 total = (u64)B * m * c->N();
+  if (!total) return;
+  ProfScope ps(c, "decrypt_rows", 8.0 * (double)total * 4);
+  decrypt_rows<<<(u32)((total + 255) / 256), 256, 0, c->stream>>>(ct, sk, B, m, c->logn, pt,
+                                                                  c->d_primes);
+  post_launch(c);
+}
+
+// decode (ckks.cpp:313-348 + encoding.cpp:118-134) of B plaintexts [B][m][N]
+// in the evaluation domain (transformed in place to coefficients) into
+// slots [B][N/2] doubles.
+void decode_batch(lcl_context* c, u64* pt, u32 B, u32 m, double scale, double* slots) {
+  if (B == 0) return;
+  need(m >= 1 && m <= c->full, LCL_SHAPE_ERROR, "plaintext level outside the chain");
+  ensure_decode_tables(c);
+  const u64 N = c->N();
+  const u32 h = (u32)(N / 2), logh = (u32)c->logn - 1;
+  const RowMap rows = make_map(pt, m, N, (u64)m * N, 1, 0, c->primes_0(m));
+  launch_inv(c, B * m, rows, PlainStore{rows});
+  CrtConst k;
+  k.q0 = c->primes[0];
+  k.q1 = m >= 2 ? c->primes[1] : 1;
+  k.inv01 = m >= 2 ? h_invmod(k.q0 % k.q1, k.q1) : 0;
+  k.inv01s = m >= 2 ? h_shoup(k.inv01, k.q1) : 0;
+  double2* bk = reinterpret_cast<double2*>(c->ws_dec.get((u64)B * h * 2));
+  const u64 tot = (u64)B * h;
+  {
+    ProfScope ps(c, "decode_twist", 8.0 * (double)tot * (2.0 * std::min<u32>(m, 2) + 2));
+    decode_twist<<<(u32)((tot + 255) / 256), 256, 0, c->stream>>>(pt, B, m, (u32)c->logn, k, scale,
+                                                                  c->d_twist, c->d_brv, bk);
+    post_launch(c);
+  }
+  {
+    const u32 bs = std::min<u32>(h, 256);
+    ProfScope ps(c, "fft_blocks", 32.0 * (double)tot);
+    fft_blocks<<<(u32)(tot / bs), 128, 0, c->stream>>>(bk, logh, c->d_roots);
+    post_launch(c);
+  }
+  if (h > 256) {
+    const size_t smem = (size_t)(h / 256) * 16 * sizeof(double2);
+    allow_smem(fft_columns, smem);
+    ProfScope ps(c, "fft_columns", 32.0 * (double)tot);
+    fft_columns<<<B * 16, 256, smem, c->stream>>>(bk, logh, c->d_roots);
+    post_launch(c);
+  }
+  {
+    ProfScope ps(c, "decode_slots", 24.0 * (double)tot);
+    decode_slots<<<(u32)((tot + 255) / 256), 256, 0, c->stream>>>(bk, B, logh, c->d_slot, slots);
+    post_launch(c);
+  }
+}
+
 void hadd_into(lcl_context* c, u64* acc, const u64* x, u32 B, u32 m) {
   const u64 N = c->N();
   const RowMap a = ct_map(acc, m, N, 2ull * m * N);
@@ -1453,6 +1550,11 @@ void free_context(lcl_context* c) {
                     &c->ws_tern, &c->ws_ctA, &c->ws_ctB, &c->ws_ctC, &c->ws_pt, &c->ws_c1inv, &c->ws_io_in,
                     &c->ws_io_sel, &c->ws_io_dist, &c->ws_io_agg, &c->ws_dtern, &c->ws_ptl})
     b->release();
+  for (void* p : {(void*)c->d_twist, (void*)c->d_roots, (void*)c->d_brv, (void*)c->d_slot})
+    if (p) cudaFree(p);
+  c->d_twist = c->d_roots = nullptr;
+  c->d_brv = c->d_slot = nullptr;
+  c->ws_dec.release();
   for (cudaEvent_t e : c->io_ev) cudaEventDestroy(e);
   c->io_ev.clear();
   if (c->h2d) cudaStreamDestroy(c->h2d);
@@ -1887,6 +1989,34 @@ int lcl_mult_plain_const(lcl_context* ctx, const uint64_t* d_ct, size_t batch, s
     post_launch(ctx);
     cuda_check(cudaStreamSynchronize(ctx->stream), "mult_plain");
     ctx->counts.multiplications += batch;
+  });
+}
+
+int lcl_decrypt(lcl_context* ctx, const uint64_t* d_ct, size_t batch, size_t count,
+                const uint64_t* d_sk, uint64_t* d_pt) {
+  return guarded([&] {
+    check_count(ctx, count);
+    need(d_sk != nullptr, LCL_KEY_ERROR, "null secret key");
+    decrypt_batch(ctx, d_ct, (u32)batch, (u32)count, d_sk, d_pt);
+  });
+}
+
+int lcl_decode(lcl_context* ctx, uint64_t* d_pt, size_t batch, size_t count, double scale,
+               double* d_slots) {
+  return guarded([&] {
+    check_count(ctx, count);
+    decode_batch(ctx, d_pt, (u32)batch, (u32)count, scale, d_slots);
+  });
+}
+
+int lcl_decrypt_values(lcl_context* ctx, const uint64_t* d_ct, size_t batch, size_t count,
+                       double scale, const uint64_t* d_sk, double* d_slots) {
+  return guarded([&] {
+    check_count(ctx, count);
+    need(d_sk != nullptr, LCL_KEY_ERROR, "null secret key");
+    u64* pt = ctx->ws_pt.get((u64)batch * count * ctx->N());
+    decrypt_batch(ctx, d_ct, (u32)batch, (u32)count, d_sk, pt);
+    decode_batch(ctx, pt, (u32)batch, (u32)count, scale, d_slots);
   });
 }
 

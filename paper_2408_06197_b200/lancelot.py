@@ -136,6 +136,9 @@ def lib():
         "lcl_ntt_inverse": [_P, _P, _SZ, _SZ, C.c_int],
         "lcl_hadd": [_P, _P, _P, _SZ, _SZ, _P],
         "lcl_hsub": [_P, _P, _P, _SZ, _SZ, _P],
+        "lcl_decrypt": [_P, _P, _SZ, _SZ, _P, _P],
+        "lcl_decode": [_P, _P, _SZ, _SZ, C.c_double, _P],
+        "lcl_decrypt_values": [_P, _P, _SZ, _SZ, C.c_double, _P, _P],
         "lcl_hmult": [_P, _P, _P, _SZ, _SZ, _P],
         "lcl_hsquare": [_P, _P, _SZ, _SZ, _P],
         "lcl_relinearize": [_P, _P, _SZ, _SZ, _P],
@@ -291,6 +294,20 @@ class PackedWeights:
 
     def chunk_count(self):
         return int(self.chunks.shape[0])
+
+
+class SecretKey:
+    """SecretKey (ckks.hpp:57-60): the evaluation-domain rows of s over the
+    full chain (+ special row); the KGC's key, used by decrypt_values."""
+
+    def __init__(self, rows):
+        self.rows = np.ascontiguousarray(rows, dtype=np.uint64)
+        self._dev = {}
+
+    def device_rows(self, count):
+        if count not in self._dev:
+            self._dev[count] = to_device(self.rows[:count])
+        return self._dev[count]
 
 
 class SelectionRule(Enum):
@@ -471,6 +488,23 @@ class CkksContext:
         out = self._empty(*a.data.shape)
         _check(lib().lcl_hsub(self.h, _ptr(a.data), _ptr(b.data), 1, a.level() + 1, _ptr(out)))
         return Ciphertext(out, a.scale)
+
+    def decrypt_values(self, ct: Ciphertext, sk: "SecretKey"):
+        """decrypt_values (ckks.cpp:390-393) on the device: float64 slots [N/2]."""
+        return self.decrypt_values_batch(ct.data.reshape(1, *ct.data.shape), ct.scale, sk)[0]
+
+    def decrypt_values_batch(self, cts, scale: float, sk: "SecretKey"):
+        """KGC decode of a batch [B][2][m][N] at one scale -> float64 [B][N/2]
+        (the distance matrix or the aggregate chunks in one call)."""
+        import torch
+        B, _, m, N = (int(x) for x in cts.shape)
+        if m > sk.rows.shape[0]:
+            raise KeyError("secret key narrower than the ciphertext")
+        dsk = sk.device_rows(m)
+        out = torch.empty((B, N // 2), dtype=torch.float64, device=dsk.device)
+        _check(lib().lcl_decrypt_values(self.h, _ptr(cts.contiguous()), B, m, scale, _ptr(dsk),
+                                        _ptr(out)))
+        return out
 
     def hmult_triple(self, a: Ciphertext, b: Ciphertext) -> TernaryCiphertext:
         """ckks.cpp:417-439 (Karatsuba; scale = product)."""

@@ -234,6 +234,36 @@ def test_decrypted_results_within_ckks_tolerance(golden):
         assert abs(v - plain) <= 1e-3 * max(1.0, abs(plain))
 
 
+def test_kgc_decrypt_decode_bit_exact(golden):
+    """Batched decrypt_values on the device (KGC side): every
+    slot of every distance ciphertext and aggregate chunk equals the oracle's
+    decode of the same words bit for bit, and slot 0 of each distance equals
+    the reference's own decrypted value from the golden run."""
+    L = _L()
+    rig = golden
+    ctx = gpu_ctx(rig.N, secure=bool(rig.meta["options"]["secure"]))
+    rk = L.RelinKey(rig.oracle.relin_key())
+    keys = L.RotationKeySet({s: rig.oracle.rotation_key(s) for s in rig.meta["rot_keys"]})
+    sk = L.SecretKey(rig.oracle.secret_key())
+    dm = L.build_distance_matrix(ctx, _packed(L, rig), rk, L.HoistPlan(k=rig.k, n=rig.width),
+                                 L.DistanceMode.per_pair, keys,
+                                 L.DistanceOptions(lazy_relin=rig.lazy))
+    got = ctx.decrypt_values_batch(dm.batch, dm.scale, sk).cpu().numpy()
+    words = L.to_host(dm.batch)
+    for p, e in enumerate(rig.meta["dist"]):
+        if p < 6:
+            assert np.array_equal(got[p], rig.oracle.decrypt_values(words[p], dm.scale)), p
+        assert got[p][0] == e["slot0"], p
+    mask = L.SelectionMask(rig.n, len(rig.selected), L.to_device(rig.selectors), rig.oracle.scale)
+    rule = {"krum": L.SelectionRule.krum, "multi_krum": L.SelectionRule.multi_krum,
+            "median": L.SelectionRule.median}[rig.rule]
+    agg = L.masked_aggregate(ctx, _packed(L, rig), mask, rule, rk)
+    got = ctx.decrypt_values_batch(agg.chunks, agg.scale, sk).cpu().numpy()
+    aw = L.to_host(agg.chunks)
+    for c in range(min(3, aw.shape[0])):
+        assert np.array_equal(got[c], rig.oracle.decrypt_values(aw[c], agg.scale)), c
+
+
 def test_shape_and_width_errors():
     L = _L()
     orc = Oracle(256, secure=False, threads=1)

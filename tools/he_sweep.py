@@ -1,5 +1,6 @@
 """HE microbenchmark sweep (BASELINE.json configs[4]): NTT, ct x ct + relin
-(+ rescale) and hoisted-rotation key switching at N = 2^13 .. 2^17 on one
+(+ rescale), hoisted-rotation key switching and the KGC's decrypt_values at
+N = 2^13 .. 2^17 on one
 B200, beside the reference evaluator on the host (oracle/_ref/ref_driver ops,
 the shapes of the reference's own proj/benchmarks/bench_ring.cpp).
 
@@ -87,9 +88,13 @@ def gpu_ops(logn, batch):
             t_h7 = timed(stream, lambda: L._check(
                 lib.lcl_hoisted_rotations(ctx.h, p(ct), B, m, steps, 7, p(rot))))
             t_rot = timed(stream, lambda: L._check(lib.lcl_rotate(ctx.h, p(ct), B, m, 1, p(rl))))
+            sk = residues(ctx, (m, N), 0, qs)
+            slots = torch.empty((B, N // 2), dtype=torch.float64, device="cuda")
+            t_dec = timed(stream, lambda: L._check(lib.lcl_decrypt_values(
+                ctx.h, p(ct), B, m, 2.0 ** 40, p(sk), p(slots))))
             tag = "batch" if B == batch else "single"
             out[tag] = {"B": B, "ntt_roundtrip_s": t_ntt / B, "mult_relin_rescale_s": t_mrr / B,
-                        "hoisted7_s": t_h7 / B, "rotate_s": t_rot / B,
+                        "hoisted7_s": t_h7 / B, "rotate_s": t_rot / B, "decrypt_values_s": t_dec / B,
                         "limb_ntt_per_s": 2 * B * m / t_ntt, "keyswitch_per_s": B / t_rot,
                         "hoisted_keyswitch_per_s": 7 * B / t_h7}
     return out
@@ -120,7 +125,7 @@ def main():
         if r and "ntt_roundtrip_s" in r:
             row["speedup_batched"] = {k: r[k] / g["batch"][k] for k in
                                       ("ntt_roundtrip_s", "mult_relin_rescale_s", "hoisted7_s",
-                                       "rotate_s")}
+                                       "rotate_s", "decrypt_values_s")}
         rows.append(row)
         print(json.dumps(row), file=sys.stderr)
     json.dump({"sweep": rows, "device": torch.cuda.get_device_name(0),
