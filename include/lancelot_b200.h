@@ -187,6 +187,20 @@ int lcl_distance_matrix_pairs(lcl_context* ctx, const uint64_t* d_clients, size_
                               size_t chunks, double in_scale, size_t width, size_t k, int lazy,
                               int reduce, size_t pair_begin, size_t pair_end, uint64_t* d_out,
                               double* out_scale);
+/* Chunk-sharded distance matrix (phase A): a rank holding chunks
+ * [c0, c1) of every client computes the lazy ternary of EVERY pair over its
+ * chunks (lcl_pair_partials, distance.cpp:113-127 restricted to the shard;
+ * d_clients [n][c1-c0][2][full][N], d_tern [n(n-1)/2][3][full][N]); the
+ * shards' partials are summed as plain integers (NCCL SUM, exact below 2^64)
+ * and each rank reduces its pair range mod q (lcl_pair_combine, counting the
+ * shards - 1 modular adds that join them) and finishes it: relinearize,
+ * rescale, slot_reduce (lcl_pair_finish, distance.cpp:128-141, 296). Summed
+ * over ranks, words and counters equal build_distance_matrix's. */
+int lcl_pair_partials(lcl_context* ctx, const uint64_t* d_clients, size_t n, size_t chunks,
+                      uint64_t* d_tern);
+int lcl_pair_combine(lcl_context* ctx, uint64_t* d_tern, size_t pairs, size_t shards);
+int lcl_pair_finish(lcl_context* ctx, const uint64_t* d_tern, size_t pairs, size_t width,
+                    size_t k, int reduce, uint64_t* d_out);
 int lcl_masked_aggregate_chunks(lcl_context* ctx, const uint64_t* d_clients,
                                 const uint64_t* d_sel, size_t n, size_t chunks, double w_scale,
                                 double sel_scale, size_t l, int average, size_t chunk_begin,

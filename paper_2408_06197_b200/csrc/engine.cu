@@ -2059,6 +2059,53 @@ int lcl_distance_matrix_pairs(lcl_context* ctx, const uint64_t* d_clients, size_
   });
 }
 
+int lcl_pair_partials(lcl_context* ctx, const uint64_t* d_clients, size_t n, size_t chunks,
+                      uint64_t* d_tern) {
+  return guarded([&] {
+    need(n >= 2 && n <= 65535, LCL_SHAPE_ERROR, "pairwise distances need 2..65535 clients");
+    need(chunks >= 1, LCL_SHAPE_ERROR, "empty weight vector");
+    const u32 P = (u32)(n * (n - 1) / 2);
+    ensure_pairs(ctx, (u32)n);
+    pair_accumulate_launch(ctx, d_clients, (u32)n, (u32)chunks, 0, (u32)chunks, row_range(0, P),
+                           d_tern, false);
+    ctx->counts.multiplications += (u64)P * chunks;
+    ctx->counts.additions += (u64)P * (2ull * chunks - 1);
+  });
+}
+
+int lcl_pair_combine(lcl_context* ctx, uint64_t* d_tern, size_t pairs, size_t shards) {
+  return guarded([&] {
+    need(shards >= 1 && shards <= 4096, LCL_PARAMETER_ERROR, "shard count outside 1..4096");
+    const u32 m = ctx->full;
+    const u64 words = (u64)pairs * 3 * m * ctx->N();
+    if (words) {
+      ProfScope ps(ctx, "reduce_partials", 16.0 * (double)words);
+      reduce_partials<<<(u32)((words + 255) / 256), 256, 0, ctx->stream>>>(d_tern, words, m,
+                                                                          ctx->logn, ctx->d_primes);
+      post_launch(ctx);
+    }
+    ctx->counts.additions += (u64)pairs * (shards - 1);
+  });
+}
+
+int lcl_pair_finish(lcl_context* ctx, const uint64_t* d_tern, size_t pairs, size_t width,
+                    size_t k, int reduce, uint64_t* d_out) {
+  return guarded([&] {
+    const u32 m = ctx->full;
+    need(m >= 2, LCL_DEPTH_EXHAUSTED, "no prime left to rescale by");
+    if (reduce) {
+      need(width > 0 && (width & (width - 1)) == 0, LCL_WIDTH_ERROR,
+           "reduction width must be a power of two");
+      need(width <= ctx->n / 2, LCL_WIDTH_ERROR, "reduction width exceeds the slot count");
+    }
+    if (!pairs) return;
+    u64* ctA = ctx->ws_ctA.get((u64)pairs * 2 * m * ctx->N());
+    relinearize_batch(ctx, d_tern, (u32)pairs, m, ctA);
+    rescale_batch(ctx, ctA, (u32)pairs, m, d_out);
+    if (reduce) slot_reduce_batch(ctx, d_out, (u32)pairs, m - 1, width, k, d_out);
+  });
+}
+
 int lcl_masked_aggregate_chunks(lcl_context* ctx, const uint64_t* d_clients,
                                 const uint64_t* d_sel, size_t n, size_t chunks, double w_scale,
                                 double sel_scale, size_t l, int average, size_t chunk_begin,

@@ -485,6 +485,18 @@ __global__ void __launch_bounds__(256)
   o[2 * slots] = d2;
 }
 
+// Sum of `shards` partial ternaries (u64 words, each < q, added as plain
+// integers by an NCCL SUM: < shards * q < 2^64) reduced mod q in place;
+// tern [P][3][m][N], row prime = limb index.
+__global__ void __launch_bounds__(256)
+    reduce_partials(u64* __restrict__ tern, u64 words, u32 m, u32 logn,
+                    const PrimeConst* __restrict__ primes) {
+  const u64 gid = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gid >= words) return;
+  const u32 limb = (u32)((gid >> logn) % m);
+  tern[gid] = reduce64(tern[gid], primes[limb]);
+}
+
 // ------------------------------------------------------------------------
 // ct x pt (ckks.cpp:549-558): out[b][x][i][a] = ct[b][x][i][a] * pt[i][a].
 __global__ void __launch_bounds__(256)

@@ -136,6 +136,9 @@ def lib():
         "lcl_ntt_inverse": [_P, _P, _SZ, _SZ, C.c_int],
         "lcl_hadd": [_P, _P, _P, _SZ, _SZ, _P],
         "lcl_hsub": [_P, _P, _P, _SZ, _SZ, _P],
+        "lcl_pair_partials": [_P, _P, _SZ, _SZ, _P],
+        "lcl_pair_combine": [_P, _P, _SZ, _SZ],
+        "lcl_pair_finish": [_P, _P, _SZ, _SZ, _SZ, C.c_int, _P],
         "lcl_decrypt": [_P, _P, _SZ, _SZ, _P, _P],
         "lcl_decode": [_P, _P, _SZ, _SZ, C.c_double, _P],
         "lcl_decrypt_values": [_P, _P, _SZ, _SZ, C.c_double, _P, _P],

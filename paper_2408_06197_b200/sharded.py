@@ -16,6 +16,11 @@ Inputs (client ciphertexts, selectors, keys) are replicated on every GPU
 shards reproduces the single-GPU result word for word, which the gloo tests
 in tests/test_sharded.py check against the oracle on CPU.
 
+chunk_sharded_server_round is the scalable form: each GPU holds
+only its chunk slice of every client (1/G of the client bytes to transfer
+and store), accumulates partial ternaries of all pairs, and one integer
+reduce_scatter joins them before the pair-sharded key-switch chains.
+
 The shard kernels are injected (`compute_pairs`, `compute_chunks`), so the
 same orchestration runs with the CUDA C-ABI on B200 (`cuda_shard_fns`) and
 with CPU stand-ins under gloo in the tests.
@@ -62,6 +67,106 @@ def sharded_server_round(n_pairs, n_chunks, dist_unit_shape, agg_unit_shape, com
     d_full = _gather(dist, d_local, n_pairs, dist_unit_shape, world, rank, group)
     a_full = _gather(dist, a_local, n_chunks, agg_unit_shape, world, rank, group)
     return d_full, a_full
+
+
+def aligned_range(total: int, world: int, rank: int):
+    """[begin, end) of the `rank`-th of `world` equal blocks of ceil(total /
+    world) units (the split reduce_scatter imposes)."""
+    per = -(-total // world)
+    return min(total, per * rank), min(total, per * (rank + 1))
+
+
+def _reduce_scatter_sum(dist, t, total, world, rank, group):
+    """Integer SUM of every rank's [total, ...] tensor, rank r keeping block r
+    (aligned_range). NCCL reduce_scatter on B200; all_reduce + slice under
+    gloo, which has no reduce_scatter."""
+    torch = __import__("torch")
+    per = -(-total // world)
+    pad = torch.zeros((per * world,) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
+    pad[:total] = t
+    b, e = aligned_range(total, world, rank)
+    if dist.get_backend(group) == "nccl":
+        out = torch.empty((per,) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
+        dist.reduce_scatter_tensor(out, pad, op=dist.ReduceOp.SUM, group=group)
+        return out[: e - b]
+    dist.all_reduce(pad, op=dist.ReduceOp.SUM, group=group)
+    return pad[b:e]
+
+
+def _gather_aligned(dist, local, total, unit_shape, world, group):
+    torch = __import__("torch")
+    per = -(-total // world)
+    pad = torch.zeros((per,) + tuple(unit_shape), dtype=local.dtype, device=local.device)
+    pad[: local.shape[0]] = local
+    bufs = [torch.empty_like(pad) for _ in range(world)]
+    dist.all_gather(bufs, pad, group=group)
+    return torch.cat(bufs, dim=0)[:total]
+
+
+def chunk_sharded_server_round(n_pairs, n_chunks, dist_unit_shape, agg_unit_shape,
+                               compute_partials, finish_pairs, compute_chunks, group=None):
+    """SURVEY 8e phase A/B/C: this rank holds chunks shard_range(n_chunks) of
+    every client (1/G of the client data and of the H2D). It accumulates the
+    partial ternaries of ALL pairs over its chunks (compute_partials() ->
+    [n_pairs, 3, m, N] u64 words), the partials are summed across ranks as
+    integers (NCCL reduce_scatter: the only data-path collective; sums stay
+    below 2^64), rank r finishes pair block aligned_range(n_pairs) -- modular
+    reduction of the sum, relinearize, rescale, slot_reduce:
+    finish_pairs(p0, p1, summed, world) -> [p1-p0, *dist_unit_shape] -- and
+    aggregates its own chunks (compute_chunks() -> [c1-c0, *agg_unit_shape]).
+    Both results are all-gathered."""
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    t = compute_partials()
+    summed = _reduce_scatter_sum(dist, t, n_pairs, world, rank, group)
+    p0, p1 = aligned_range(n_pairs, world, rank)
+    d_local = finish_pairs(p0, p1, summed, world)
+    a_local = compute_chunks()
+    d_full = _gather_aligned(dist, d_local, n_pairs, dist_unit_shape, world, group)
+    a_full = _gather(dist, a_local, n_chunks, agg_unit_shape, world, rank, group)
+    return d_full, a_full
+
+
+def cuda_chunk_shard_fns(ctx, local_clients, selectors, n, local_chunks, scale, sel_scale, width,
+                         k, l=1, average=False):
+    """CUDA shard kernels of chunk_sharded_server_round through the C-ABI:
+    lcl_pair_partials on this rank's clients slice [n][local_chunks][2][m][N],
+    lcl_pair_combine + lcl_pair_finish on the summed block, and
+    lcl_masked_aggregate_chunks over the local chunks."""
+    import torch
+
+    from . import lancelot as L
+
+    m = ctx.full
+    N = ctx.params().ring_degree
+    mo = m - 2 if average else m - 1
+    P = n * (n - 1) // 2
+    lib = L.lib()
+    dev = local_clients.device
+
+    def partials():
+        t = torch.empty((P, 3, m, N), dtype=torch.int64, device=dev)
+        L._check(lib.lcl_pair_partials(ctx.h, L._ptr(local_clients), n, local_chunks, L._ptr(t)))
+        return t
+
+    def finish(p0, p1, summed, world):
+        summed = summed.contiguous()
+        out = torch.empty((p1 - p0, 2, m - 1, N), dtype=torch.int64, device=dev)
+        L._check(lib.lcl_pair_combine(ctx.h, L._ptr(summed), p1 - p0, world))
+        L._check(lib.lcl_pair_finish(ctx.h, L._ptr(summed), p1 - p0, width, k, 1, L._ptr(out)))
+        return out
+
+    def chunks_fn():
+        out = torch.empty((local_chunks, 2, mo, N), dtype=torch.int64, device=dev)
+        osc = C.c_double()
+        L._check(lib.lcl_masked_aggregate_chunks(
+            ctx.h, L._ptr(local_clients), L._ptr(selectors), n, local_chunks, scale, sel_scale, l,
+            1 if average else 0, 0, local_chunks, L._ptr(out), C.byref(osc)))
+        return out
+
+    return partials, finish, chunks_fn, (2, m - 1, N), (2, mo, N)
 
 
 def cuda_shard_fns(ctx, clients, selectors, n, chunks, scale, sel_scale, width, k, l=1,

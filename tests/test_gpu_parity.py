@@ -264,6 +264,43 @@ def test_kgc_decrypt_decode_bit_exact(golden):
         assert np.array_equal(got[c], rig.oracle.decrypt_values(aw[c], agg.scale)), c
 
 
+@pytest.mark.parametrize("name,shards", [("cfg2", 3), ("tiny_hoist_multikrum", 2)])
+def test_chunk_sharded_partials_bit_exact(name, shards):
+    """The chunk-sharded distance path (lcl_pair_partials per chunk slice,
+    integer sum of the partial ternaries, lcl_pair_combine, lcl_pair_finish)
+    run shard by shard on one GPU reproduces the reference digests and op
+    counters; the multi-rank orchestration is tests/test_sharded.py."""
+    L = _L()
+    import torch
+    from paper_2408_06197_b200.sharded import shard_range
+    rig = Rig(name, threads=8)
+    if not rig.lazy:
+        pytest.skip("lazy accumulation only")
+    ctx = gpu_ctx(rig.N, secure=bool(rig.meta["options"]["secure"]))
+    ctx.use_relin_key(L.RelinKey(rig.oracle.relin_key()))
+    keys = L.RotationKeySet({s: rig.oracle.rotation_key(s) for s in rig.meta["rot_keys"]})
+    ctx.use_rotation_keys(keys, rig.steps)
+    lib = L.lib()
+    m, N, n = rig.oracle.full, rig.N, rig.n
+    P = n * (n - 1) // 2
+    ctx.reset_counters()
+    total = None
+    for g in range(shards):
+        c0, c1 = shard_range(rig.C, shards, g)
+        local = L.to_device(np.ascontiguousarray(rig.clients[:, c0:c1]))
+        t = torch.empty((P, 3, m, N), dtype=torch.int64, device="cuda")
+        L._check(lib.lcl_pair_partials(ctx.h, L._ptr(local), n, c1 - c0, L._ptr(t)))
+        total = t if total is None else total + t
+    L._check(lib.lcl_pair_combine(ctx.h, L._ptr(total), P, shards))
+    out = torch.empty((P, 2, m - 1, N), dtype=torch.int64, device="cuda")
+    L._check(lib.lcl_pair_finish(ctx.h, L._ptr(total), P, rig.width, rig.k, 1, L._ptr(out)))
+    got = L.to_host(out)
+    pairs = [(i, j) for i in range(n) for j in range(i + 1, n)]
+    for p, (i, j) in enumerate(pairs):
+        assert sha(got[p]) == rig.meta["sha256"][f"dist_{i}_{j}"], (i, j)
+    assert ctx.counters() == rig.meta["dist_ops"]
+
+
 def test_shape_and_width_errors():
     L = _L()
     orc = Oracle(256, secure=False, threads=1)
