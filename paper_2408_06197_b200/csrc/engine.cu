@@ -558,23 +558,9 @@ LiftLoad lift_from(lcl_context* c, const RowMap& src, u32 rows_per_item, u32 fan
   return l;
 }
 
-// Column pass only (first log2 N1 forward stages), writing `out` (lazy values).
-template <int LOGN1, int E, class Loader>
-void col_only(lcl_context* c, u32 rows, const RowMap& out, const Loader& ld) {
-  constexpr int N1 = 1 << LOGN1;
-  constexpr size_t smem = (size_t)N1 * 16 * 8;
-  static bool once = (allow_smem(ntt_col_fwd<LOGN1, E, Loader>, smem), true);
-  (void)once;
-  const u32 groups = (u32)(c->n >> LOGN1) >> 4;
-  ProfScope ps(c, "ntt_col_fwd<lift>", 8.0 * c->N() * (load_rows(ld, rows) + rows),
-               0.5 * c->N() * rows * LOGN1);
-  ntt_col_fwd<LOGN1, E, Loader><<<rows * groups, 16 * (N1 / E), smem, c->stream>>>(out, ld, tabs(c));
-}
-
 template <int LOGN1, int M>
 void modup_ip_launch(lcl_context* c, u32 B, const u64* mid, const u64* c1, u64 c1_stride,
-                     const u32* perm, const u64* key, const u64* key_shoup, u64* acc,
-                     u64* sp_out) {
+                     const u32* perm, const u64* key, const u64* key_shoup, u64* acc) {
   constexpr int N1 = 1 << LOGN1;
   const double rb = 8.0 * c->N();
   ProfScope ps(c, perm ? "modup_ip_blk<perm>" : "modup_ip_blk",
@@ -582,19 +568,18 @@ void modup_ip_launch(lcl_context* c, u32 B, const u64* mid, const u64* c1, u64 c
                0.5 * c->N() * B * M * M * 8);
   modup_ip_blk<LOGN1, M><<<((B + 3) / 4) * (M + 1) * N1, 64, 0, c->stream>>>(
       B, mid, c1, c1_stride, perm, key, key_shoup, c->full, acc, tabs(c));
-  (void)sp_out;
 }
 
 template <int LOGN1>
 void modup_ip_n(lcl_context* c, u32 B, u32 m, const u64* mid, const u64* c1, u64 c1_stride,
-                const u32* perm, const u64* key, const u64* key_shoup, u64* acc, u64* sp_out) {
+                const u32* perm, const u64* key, const u64* key_shoup, u64* acc) {
   switch (m) {
-    case 1: modup_ip_launch<LOGN1, 1>(c, B, mid, c1, c1_stride, perm, key, key_shoup, acc, sp_out); break;
-    case 2: modup_ip_launch<LOGN1, 2>(c, B, mid, c1, c1_stride, perm, key, key_shoup, acc, sp_out); break;
-    case 3: modup_ip_launch<LOGN1, 3>(c, B, mid, c1, c1_stride, perm, key, key_shoup, acc, sp_out); break;
-    case 4: modup_ip_launch<LOGN1, 4>(c, B, mid, c1, c1_stride, perm, key, key_shoup, acc, sp_out); break;
-    case 5: modup_ip_launch<LOGN1, 5>(c, B, mid, c1, c1_stride, perm, key, key_shoup, acc, sp_out); break;
-    case 6: modup_ip_launch<LOGN1, 6>(c, B, mid, c1, c1_stride, perm, key, key_shoup, acc, sp_out); break;
+    case 1: modup_ip_launch<LOGN1, 1>(c, B, mid, c1, c1_stride, perm, key, key_shoup, acc); break;
+    case 2: modup_ip_launch<LOGN1, 2>(c, B, mid, c1, c1_stride, perm, key, key_shoup, acc); break;
+    case 3: modup_ip_launch<LOGN1, 3>(c, B, mid, c1, c1_stride, perm, key, key_shoup, acc); break;
+    case 4: modup_ip_launch<LOGN1, 4>(c, B, mid, c1, c1_stride, perm, key, key_shoup, acc); break;
+    case 5: modup_ip_launch<LOGN1, 5>(c, B, mid, c1, c1_stride, perm, key, key_shoup, acc); break;
+    case 6: modup_ip_launch<LOGN1, 6>(c, B, mid, c1, c1_stride, perm, key, key_shoup, acc); break;
     default: fail(LCL_PARAMETER_ERROR, "fused key switching supports up to 6 live limbs");
   }
   post_launch(c);
@@ -674,9 +659,7 @@ u64* ks_ip(lcl_context* c, const u64* dig, u32 B, u32 m, const u64* key, const u
 // the same limbs for the identity digits. sigma / perm: the rotation's
 // coefficient- / evaluation-domain automorphism (nullptr for relinearize).
 // Returns acc [B][2][m+1][N].
-constexpr bool kFuseSpecialInverse = false;
 bool ks_fused(const lcl_context* c, u32 m) { return c->logn >= 13 && m <= 6; }
-bool sp_preinverted(const lcl_context* c, u32 m) { return kFuseSpecialInverse && ks_fused(c, m); }
 
 // preinv: the c1 limbs' inverse block pass already ran (fused into the
 // previous level's divide-and-round, rows [B][m][N]); fused path only.
@@ -704,23 +687,21 @@ u64* ks_switch(lcl_context* c, const RowMap& in, const u64* c1, u64 c1_stride, u
   else
     inv_lift_fwd_cols(c, B * m, in, mid_map, m);
   u64* acc = c->ws_acc.get((u64)B * 2 * (m + 1) * N);
-  // Running the special rows' inverse block stages inside modup_ip_blk was
-  // measured slower on cfg2 (8.91 vs 8.77 ms): it lengthens the
-  // special-target CTAs by as much as the standalone ntt_blk_inv costs.
-  u64* sp = nullptr;
+  // (Running the special rows' inverse block stages inside modup_ip_blk was
+  // measured slower on cfg2, 8.91 vs 8.77 ms: it lengthens the special-target
+  // CTAs by as much as the standalone ntt_blk_inv costs.)
   dispatch_logn(c, [&](auto L1, auto) {
-    modup_ip_n<decltype(L1)::value>(c, B, m, mid, c1, c1_stride, perm, key, key_shoup, acc, sp);
+    modup_ip_n<decltype(L1)::value>(c, B, m, mid, c1, c1_stride, perm, key, key_shoup, acc);
   });
   (void)sigma;  // two-pass rings permute block-locally inside modup_ip_blk
   return acc;
 }
 
 // ModDown of acc [B][2][m+1][N] into `out` (items (b, x), rows_per_item m,
-// 2 items per group) with the fused output additions.
-// sp_ready: the special rows' inverse block pass already ran inside
-// modup_ip_blk (fused ks_switch path); otherwise they are read from acc.
+// 2 items per group) with the fused output additions; c1inv: also leave the
+// next key switch's inverse block pass over out's c1 limbs there.
 void ks_moddown(lcl_context* c, const u64* acc, u32 B, u32 m, const RowMap& out,
-                const RowMap& add1, const RowMap& add2, const u32* perm, bool sp_ready,
+                const RowMap& add1, const RowMap& add2, const u32* perm,
                 u64* c1inv = nullptr) {
   const u64 N = c->N();
   const RowMap sp_in = make_map(acc + (u64)m * N, 1, N, (m + 1) * N, 1, 0, {c->full});
@@ -733,17 +714,10 @@ void ks_moddown(lcl_context* c, const u64* acc, u32 B, u32 m, const RowMap& out,
   epi.pinv = c->d_pinv + (u64)c->full * c->P();
   if (c->logn >= 13) {
     // inverse NTT of the special rows + lift into the m q-primes + forward
-    // column pass fused (the inverse block stages already ran inside
-    // modup_ip_blk when sp_ready), then the block pass with the
-    // divide-and-round epilogue
+    // column pass fused, then the block pass with the divide-and-round epilogue
     u64* mid = c->ws_mid.get((u64)B * 2 * m * N);
     const RowMap mid_map = make_map(mid, m, N, (u64)m * N, 1, 0, c->primes_0(m));
-    if (sp_ready) {
-      const RowMap sp_inv = make_map(c->ws_coefsp.get((u64)B * 2 * N), 1, N, N, 1, 0, {c->full});
-      lift_fwd_cols_preinv(c, 2 * B, sp_inv, mid_map, m);
-    } else {
-      inv_lift_fwd_cols(c, 2 * B, sp_in, mid_map, m);
-    }
+    inv_lift_fwd_cols(c, 2 * B, sp_in, mid_map, m);
     if (c1inv) {
       // also the next key switch's inverse block pass over the c1 limbs
       DivRoundInvStore ie;
@@ -776,7 +750,7 @@ void relinearize_batch(lcl_context* c, const u64* tern, u32 B, u32 m, u64* out) 
   u64* acc = ks_switch(c, d2, tern + 2ull * m * N, 3ull * m * N, B, m, nullptr, nullptr,
                        c->d_relin, c->d_relin_shoup);
   ks_moddown(c, acc, B, m, ct_map(out, m, N, 2ull * m * N), ct_map(tern, m, N, 3ull * m * N),
-             null_map(), nullptr, sp_preinverted(c, m));
+             null_map(), nullptr);
   c->counts.relinearizations += B;
   c->counts.mod_ups += B;
 }
@@ -832,7 +806,7 @@ void rotate_level(lcl_context* c, const u64* in, u32 B, u32 m, size_t step, u64*
                        c->d_rot_shoup.at(step), preinv_in);
   const RowMap inm = ct_map(in, m, N, 2ull * m * N);
   ks_moddown(c, acc, B, m, ct_map(out, m, N, 2ull * m * N), accumulate ? inm : null_map(), inm,
-             perm, sp_preinverted(c, m), preinv_out);
+             perm, preinv_out);
   c->counts.rotations += B;
   c->counts.mod_ups += B;
   if (accumulate) c->counts.additions += B;
@@ -945,7 +919,7 @@ void slot_reduce_serial(lcl_context* c, const u64* in, u32 B, u32 m, size_t widt
       const int nxt = cur < 0 ? 0 : 1 - cur;
       u64* acc = ks_ip(c, dig, B, m, rot_key(c, st), c->d_perm.at(st));
       ks_moddown(c, acc, B, m, ct_map(bufs[nxt], m, N, 2ull * m * N),
-                 ct_map(cur_ptr(), m, N, 2ull * m * N), base, c->d_perm.at(st), false);
+                 ct_map(cur_ptr(), m, N, 2ull * m * N), base, c->d_perm.at(st));
       cur = nxt;
       c->counts.rotations += B;
       c->counts.additions += B;
@@ -1948,7 +1922,7 @@ int lcl_hoisted_rotations(lcl_context* ctx, const uint64_t* d_ct, size_t batch, 
       }
       u64* acc = ks_ip(ctx, dig, B, m, key, ctx->d_perm.at(st));
       ks_moddown(ctx, acc, B, m, ct_map(o, m, N, 2ull * m * N), null_map(),
-                 ct_map(d_ct, m, N, 2ull * m * N), ctx->d_perm.at(st), false);
+                 ct_map(d_ct, m, N, 2ull * m * N), ctx->d_perm.at(st));
       ctx->counts.rotations += B;
     }
   });

@@ -19,10 +19,6 @@ namespace lcl {
 // tile of chunk c + STAGES - 1 streams into shared memory (cp.async) while
 // chunk c is being accumulated.
 // clients: [n][C][2][m][N]; tern out: [pairs][3][m][N] (pair p at out + (p - p0) * 3mN).
-__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
-  const u32 s = (u32)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
-}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n"); }
 template <int K>
 __device__ __forceinline__ void cp_async_wait() {
