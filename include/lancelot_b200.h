@@ -23,6 +23,7 @@
  *   lcl_*_pairs / _chunks    the same, one shard of pairs / chunks     distance.cpp:257-272,
  *                            (the reference's parallel_for ranges)     aggregation.cpp:211
  *   lcl_get_counts           OpCounters::snapshot                      ckks.cpp:134-156
+ *   lcl_pack_and_encrypt     pack_and_encrypt (client side)           distance.cpp:64-91
  *   lcl_decrypt / _decode    CkksContext::decrypt / decode (KGC side)  ckks.cpp:313-393,
  *   lcl_decrypt_values       + Embedding::coeffs_to_slots              encoding.cpp:118-134
  *
@@ -70,6 +71,7 @@ typedef enum {
 } lcl_status;
 
 typedef struct lcl_context lcl_context;
+typedef struct lcl_sampler lcl_sampler;
 
 typedef struct {
   uint64_t encryptions, additions, multiplications, relinearizations, rescales, rotations,
@@ -148,6 +150,30 @@ int lcl_slot_reduce(lcl_context* ctx, const uint64_t* d_ct, size_t batch, size_t
 /* ct x pt with a plaintext encoded on the host at (value, scale, level). */
 int lcl_mult_plain_const(lcl_context* ctx, const uint64_t* d_ct, size_t batch, size_t count,
                          double value, double pt_scale, uint64_t* d_out);
+
+/* Client side.
+ * lcl_derive_seed        derive_seed (sampling.cpp:24-30).
+ * lcl_sampler_*          Sampler(seed) (sampling.hpp:32-65): the reference's
+ *                        mt19937_64 stream; uniform_real draws (sampling.cpp:43-45).
+ * lcl_pack_and_encrypt   pack_and_encrypt (distance.cpp:64-91): the client's
+ *                        weights (host, dim doubles) chunked, encoded at the
+ *                        context scale and encrypted under the public key
+ *                        d_pk [2][full][N] (p0 rows then p1 rows, evaluation
+ *                        domain) into d_out [chunks][2][full][N]; consumes the
+ *                        sampler's draws exactly as the reference does, so the
+ *                        words are the reference's. encryptions += chunks. */
+uint64_t lcl_derive_seed(uint64_t root, uint64_t tag);
+int lcl_sampler_create(uint64_t seed, lcl_sampler** out);
+int lcl_sampler_destroy(lcl_sampler* s);
+int lcl_sampler_uniform_real(lcl_sampler* s, size_t count, double* out);
+int lcl_pack_and_encrypt(lcl_context* ctx, lcl_sampler* rng, const double* h_weights,
+                         size_t dim, double prescale, const uint64_t* d_pk, uint64_t* d_out);
+/* build_mask (aggregation.cpp:156-186), the KGC's selection mask: n rank rows
+ * (d_rank_rows [n][2][full][N]; unused by masked_aggregate, encrypted anyway
+ * because they consume the sampler's draws first) and n client selectors
+ * (d_selectors [n][2][full][N], all slots 1.0 for a selected client, else 0.0). */
+int lcl_build_mask(lcl_context* ctx, lcl_sampler* rng, size_t n, const size_t* selected,
+                   size_t l, const uint64_t* d_pk, uint64_t* d_rank_rows, uint64_t* d_selectors);
 
 /* KGC side, bit-identical to the reference:
  * lcl_decrypt         CkksContext::decrypt (ckks.cpp:381-388): d_pt [batch][count][N] =

@@ -554,6 +554,9 @@ void lo_ntt_tables(const lo_ctx* c, size_t i, uint64_t* root, uint64_t* root_sho
 size_t lo_key_words(const lo_ctx* c) { return c->full * 2 * (c->full + 1) * c->n; }
 const uint64_t* lo_relin_key(const lo_ctx* c) { return c->relin; }
 const uint64_t* lo_secret_key(const lo_ctx* c) { return c->sk; }
+/* PublicKey (p0, p1), full rows each, evaluation domain (ckks.cpp:208-219) */
+const uint64_t* lo_public_key_p0(const lo_ctx* c) { return c->pk0; }
+const uint64_t* lo_public_key_p1(const lo_ctx* c) { return c->pk1; }
 const uint64_t* lo_rotation_key(const lo_ctx* c, size_t step) {
   for (size_t i = 0; i < c->nrot; ++i)
     if (c->rot_step[i] == step) return c->rot_key[i];

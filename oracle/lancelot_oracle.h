@@ -77,6 +77,8 @@ size_t lo_key_words(const lo_ctx* c);   /* u64 words in one switch key */
 const uint64_t* lo_relin_key(const lo_ctx* c);
 const uint64_t* lo_rotation_key(const lo_ctx* c, size_t step); /* NULL: absent */
 const uint64_t* lo_secret_key(const lo_ctx* c); /* (full+1) rows, eval domain */
+const uint64_t* lo_public_key_p0(const lo_ctx* c); /* full rows, eval domain */
+const uint64_t* lo_public_key_p1(const lo_ctx* c);
 
 /* measure_distance_phase inputs (cli.cpp:316-329): one Sampler stream
  * derive_seed(seed, 0xAB1A7E) shared by all clients; out = [clients][C][2][L+1][N]. */

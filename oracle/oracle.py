@@ -59,7 +59,7 @@ def _lib():
     lib.lo_galois_elt.restype = C.c_uint64
     lib.lo_galois_elt.argtypes = [C.c_size_t, C.c_size_t]
     lib.lo_keygen.argtypes = [C.c_void_p, C.c_uint64, _szp, C.c_size_t]
-    for f in ("lo_relin_key", "lo_secret_key"):
+    for f in ("lo_relin_key", "lo_secret_key", "lo_public_key_p0", "lo_public_key_p1"):
         getattr(lib, f).restype = C.c_void_p
         getattr(lib, f).argtypes = [C.c_void_p]
     lib.lo_rotation_key.restype = C.c_void_p
@@ -186,6 +186,14 @@ class Oracle:
 
     def rotation_key(self, step):
         return self._key(lib().lo_rotation_key(self.h, step))
+
+    def public_key(self):
+        """(p0, p1) stacked: [2][full][N], evaluation domain."""
+        out = np.empty((2, self.full, self.N), np.uint64)
+        for x, f in enumerate((lib().lo_public_key_p0, lib().lo_public_key_p1)):
+            buf = (C.c_uint64 * (self.full * self.N)).from_address(f(self.h))
+            out[x] = np.frombuffer(buf, dtype=np.uint64).reshape(self.full, self.N)
+        return out
 
     def secret_key(self):
         ptr = lib().lo_secret_key(self.h)

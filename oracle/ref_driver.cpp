@@ -7,6 +7,7 @@
 //
 //   ref_driver gen   <options> --out DIR   dump keys, inputs, outputs, counters
 //   ref_driver bench <options> --reps R    time build_distance_matrix + masked_aggregate
+//   ref_driver encrypt --N N --dim D       time pack_and_encrypt of one client
 //   ref_driver ops   --N N --reps S        per-op latency (NTT, mult+relin+rescale,
 //                                          hoisted rotations, rotate, decrypt_values), S s per op
 //
@@ -396,6 +397,27 @@ int cmd_ops(const Opts& o) {
   return 0;
 }
 
+// pack_and_encrypt of one client's weight vector (dim uniform_real - 0.5
+// draws, as measure_distance_phase draws them), timed on this thread.
+int cmd_encrypt(const Opts& o) {
+  CkksParams p;
+  p.ring_degree = o.N;
+  p.depth = o.depth;
+  p.security = o.secure ? SecurityLevel::bits128 : SecurityLevel::none;
+  const CkksContext ctx(p);
+  Sampler key_rng(derive_seed(o.seed, 5));
+  const KeyBundle keys = ctx.generate_keys(key_rng, {});
+  Sampler rng(derive_seed(o.seed, 0xAB1A7Eu));
+  std::vector<double> w(o.dim);
+  for (double& x : w) x = rng.uniform_real() - 0.5;
+  const auto a = std::chrono::steady_clock::now();
+  const PackedWeights pw = pack_and_encrypt(ctx, w, keys.pk, rng);
+  const double s = std::chrono::duration<double>(std::chrono::steady_clock::now() - a).count();
+  std::printf("{\"N\": %zu, \"dim\": %zu, \"chunks\": %zu, \"pack_and_encrypt_s\": %.6f}\n", o.N,
+              o.dim, pw.chunk_count(), s);
+  return 0;
+}
+
 }  // namespace
 
 int main(int argc, char** argv) {
@@ -404,6 +426,7 @@ int main(int argc, char** argv) {
     if (o.cmd == "gen") return cmd_gen(o);
     if (o.cmd == "bench") return cmd_bench(o);
     if (o.cmd == "ops") return cmd_ops(o);
+    if (o.cmd == "encrypt") return cmd_encrypt(o);
     std::fprintf(stderr, "unknown command %s\n", o.cmd.c_str());
     return 2;
   } catch (const std::exception& e) {

@@ -20,6 +20,9 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <utility>
+#include <random>
+#include <thread>
 #include <tuple>
 #include <memory>
 #include <string>
@@ -29,6 +32,7 @@
 #include "common.cuh"
 #include "kernels.cuh"
 #include "decode.cuh"
+#include "encrypt.cuh"
 #include "ntt.cuh"
 
 using namespace lcl;
@@ -287,7 +291,7 @@ struct lcl_context {
   };
   std::vector<Lane> lanes;
   cudaEvent_t fork_ev = nullptr;
-  DevBuf ws_io_in, ws_io_sel, ws_io_dist, ws_io_agg, ws_dtern, ws_ptl;
+  DevBuf ws_io_in, ws_io_sel, ws_io_dist, ws_io_agg, ws_dtern, ws_ptl, ws_enc, ws_enc_in;
   // masked_aggregate's encode(1/l) plaintext, NTT'd on the device once per l
   size_t pt_l = 0;
   std::vector<u64> pt_host;
@@ -307,6 +311,44 @@ struct lcl_context {
     std::vector<u32> v(count);
     for (u32 i = 0; i < count; ++i) v[i] = i;
     return v;
+  }
+};
+
+// Sampler (sampling.hpp:32-65, sampling.cpp): the reference's deterministic
+// stream over std::mt19937_64 with its rejection-sampled bounded draws, so a
+// client's encryptions consume exactly the reference's draws.
+struct lcl_sampler {
+  std::mt19937_64 engine;
+  explicit lcl_sampler(u64 seed) : engine(seed) {}
+  u64 raw() { return engine(); }
+  u64 uniform_below(u64 bound) {  // sampling.cpp:34-41
+    if ((bound & (bound - 1)) == 0) return raw() & (bound - 1);
+    const u64 limit = ~u64{0} - (~u64{0} % bound) - 1;
+    u64 x = raw();
+    while (x > limit) x = raw();
+    return x % bound;
+  }
+  double uniform_real() { return static_cast<double>(raw() >> 11) * 0x1.0p-53; }  // :43-45
+  void ternary(size_t n, signed char* out) {  // :70-78
+    for (size_t j = 0; j < n; ++j) out[j] = (signed char)((long)uniform_below(3) - 1);
+  }
+  void sparse_ternary(size_t n, size_t weight, signed char* out) {  // :80-98
+    std::fill(out, out + n, 0);
+    std::vector<size_t> idx(n);
+    for (size_t i = 0; i < n; ++i) idx[i] = i;
+    for (size_t i = 0; i < weight; ++i) {
+      const size_t k = i + uniform_below(n - i);
+      std::swap(idx[i], idx[k]);
+      out[idx[i]] = uniform_below(2) == 0 ? 1 : -1;
+    }
+  }
+  void cbd(size_t n, int eta, signed char* out) {  // :100-112
+    const u64 mask = (eta == 32) ? ~u64{0} >> 32 : (u64{1} << eta) - 1;
+    for (size_t j = 0; j < n; ++j) {
+      const u64 bits = raw();
+      out[j] = (signed char)(__builtin_popcountll(bits & mask) -
+                             __builtin_popcountll((bits >> eta) & mask));
+    }
   }
 };
 
@@ -1176,6 +1218,132 @@ void decode_batch(lcl_context* c, u64* pt, u32 B, u32 m, double scale, double* s
   }
 }
 
+// ------------------------------------------------------------ client encryption
+// pack_and_encrypt (distance.cpp:64-91) of one client's weights: per chunk,
+// in the reference's draw order, r (sample_secret_like: sparse ternary of
+// Hamming weight 64, ckks.cpp:187-193), e0 and e1 (CBD, eta 21) from the
+// client's Sampler; the encodings (slots_to_coeffs + rounding, a pure
+// function of the weights) run on host threads meanwhile; then one batched
+// device pass lifts, transforms and combines with the public key.
+constexpr size_t kHammingWeight = 64;  // CkksParams::key_hamming_weight (ckks.hpp:48)
+constexpr int kErrorEta = 21;          // CkksParams::error_eta (ckks.hpp:50)
+constexpr double kMessageBound = 1048576.0;  // CkksParams::message_bound = 2^20
+
+// encode + encrypt (ckks.cpp:263-307, 350-379) of V value vectors, in order,
+// into out [V][2][full][N]: vec(v) -> (pointer, length) of vector v.
+template <class Vec>
+void encrypt_vectors(lcl_context* c, lcl_sampler* rng, size_t V, const Vec& vec, const u64* pk,
+                     u64* out) {
+  const size_t n = c->n;
+  const u32 m = c->full;
+  for (size_t v = 0; v < V; ++v) {  // the reference's encode checks (ckks.cpp:267-281)
+    const auto [p, len] = vec(v);
+    need(len <= n / 2, LCL_CAPACITY_ERROR, "more values than slots");
+    for (size_t i = 0; i < len; ++i)
+      need(std::isfinite(p[i]) && std::fabs(p[i]) <= kMessageBound, LCL_CAPACITY_ERROR,
+           "value outside the message bound");
+  }
+  std::vector<long long> rounded(V * n);
+  std::vector<signed char> small(V * 3 * n);
+  {
+    // encodings on worker threads (independent of the draws)
+    const unsigned nt = std::max(1u, std::min<unsigned>(std::thread::hardware_concurrency(), 16));
+    std::vector<std::thread> pool;
+    std::vector<std::string> err(nt);
+    for (unsigned t = 0; t < nt; ++t)
+      pool.emplace_back([&, t] {
+        try {
+          for (size_t v = t; v < V; v += nt) {
+            const auto [p, len] = vec(v);
+            const std::vector<long long> r = h_encode_rounded(std::vector<double>(p, p + len), n, c->scale);
+            std::copy(r.begin(), r.end(), rounded.begin() + v * n);
+          }
+        } catch (const LclError& e) {
+          err[t] = e.msg;
+        }
+      });
+    // the draws, sequentially, in the reference's order
+    for (size_t v = 0; v < V; ++v) {
+      signed char* s = small.data() + v * 3 * n;
+      if (kHammingWeight == 0)
+        rng->ternary(n, s);
+      else
+        rng->sparse_ternary(n, kHammingWeight, s);
+      rng->cbd(n, kErrorEta, s + n);
+      rng->cbd(n, kErrorEta, s + 2 * n);
+    }
+    for (auto& th : pool) th.join();
+    for (auto& e : err) need(e.empty(), LCL_CAPACITY_ERROR, e.empty() ? "" : e.c_str());
+  }
+  const u64 N = c->N();
+  const size_t batch = std::max<size_t>(1, std::min<size_t>(V, (size_t)((2ull << 30) / (4 * m * N * 8))));
+  for (size_t c0 = 0; c0 < V; c0 += batch) {
+    const u32 B = (u32)std::min(batch, V - c0);
+    u64* ws = c->ws_enc.get((u64)B * 4 * m * N);
+    long long* d_round = reinterpret_cast<long long*>(c->ws_enc_in.get((u64)B * N + (B * 3 * N + 7) / 8));
+    signed char* d_small = reinterpret_cast<signed char*>(d_round + (u64)B * N);
+    cuda_check(cudaMemcpyAsync(d_round, rounded.data() + c0 * n, (u64)B * N * 8,
+                               cudaMemcpyHostToDevice, c->stream), "h2d");
+    cuda_check(cudaMemcpyAsync(d_small, small.data() + c0 * 3 * n, (u64)B * 3 * N,
+                               cudaMemcpyHostToDevice, c->stream), "h2d");
+    const u64 total = (u64)B * m * N;
+    {
+      ProfScope ps(c, "encrypt_lift", (double)B * N * 11 + 8.0 * total * 4);
+      encrypt_lift<<<(u32)((total + 255) / 256), 256, 0, c->stream>>>(d_round, d_small, B, m,
+                                                                      c->logn, ws, c->d_primes);
+      post_launch(c);
+    }
+    const RowMap wm = make_map(ws, m, N, (u64)m * N, 1, 0, c->primes_0(m));
+    launch_fwd(c, B * 4 * m, wm, PlainLoad{wm}, PlainStore{wm});
+    {
+      ProfScope ps(c, "encrypt_combine", 8.0 * total * 8);
+      encrypt_combine<<<(u32)((total + 255) / 256), 256, 0, c->stream>>>(
+          ws, pk, B, m, c->logn, out + c0 * 2 * m * N, c->d_primes);
+      post_launch(c);
+    }
+    // the host staging must outlive the copies
+    cuda_check(cudaStreamSynchronize(c->stream), "encrypt");
+  }
+  c->counts.encryptions += V;
+}
+
+void pack_and_encrypt(lcl_context* c, lcl_sampler* rng, const double* w, size_t dim,
+                      double prescale, const u64* pk, u64* out) {
+  need(dim > 0, LCL_SHAPE_ERROR, "empty weight vector");
+  need(prescale > 0.0 && std::isfinite(prescale), LCL_PARAMETER_ERROR,
+       "prescale must be positive and finite");
+  for (size_t i = 0; i < dim; ++i) need(std::isfinite(w[i]), LCL_DATA_ERROR, "weights must be finite");
+  const size_t slots = c->n / 2;
+  const size_t C = (dim + slots - 1) / slots;
+  std::vector<double> scaled(w, w + dim);
+  for (double& v : scaled) v *= prescale;
+  encrypt_vectors(c, rng, C, [&](size_t ch) {
+    const size_t lo = ch * slots;
+    return std::pair<const double*, size_t>(scaled.data() + lo, std::min(slots, dim - lo));
+  }, pk, out);
+}
+
+// build_mask (aggregation.cpp:156-186): n rank rows (basis vectors of the
+// selected indices, in rank order) then n broadcast client selectors.
+void build_mask(lcl_context* c, lcl_sampler* rng, size_t n, const size_t* selected, size_t l,
+                const u64* pk, u64* rank_rows, u64* selectors) {
+  need(n <= c->n / 2, LCL_CAPACITY_ERROR, "more clients than mask slots");
+  for (size_t i = 0; i < l; ++i)
+    need(selected[i] < n, LCL_SHAPE_ERROR, "selected index outside the client range");
+  std::vector<double> rows(n * n, 0.0), sel(n * (c->n / 2), 0.0);
+  for (size_t r = 0; r < n && r < l; ++r) rows[r * n + selected[r]] = 1.0;
+  std::vector<bool> chosen(n, false);
+  for (size_t i = 0; i < l; ++i) chosen[selected[i]] = true;
+  for (size_t i = 0; i < n; ++i)
+    std::fill(sel.begin() + i * (c->n / 2), sel.begin() + (i + 1) * (c->n / 2), chosen[i] ? 1.0 : 0.0);
+  encrypt_vectors(c, rng, n, [&](size_t r) {
+    return std::pair<const double*, size_t>(rows.data() + r * n, n);
+  }, pk, rank_rows);
+  encrypt_vectors(c, rng, n, [&](size_t i) {
+    return std::pair<const double*, size_t>(sel.data() + i * (c->n / 2), c->n / 2);
+  }, pk, selectors);
+}
+
 void hadd_into(lcl_context* c, u64* acc, const u64* x, u32 B, u32 m) {
   const u64 N = c->N();
   const RowMap a = ct_map(acc, m, N, 2ull * m * N);
@@ -1522,7 +1690,8 @@ void free_context(lcl_context* c) {
   for (auto& kv : c->d_sigma) cudaFree(kv.second);
   for (DevBuf* b : {&c->ws_coef, &c->ws_digits, &c->ws_acc, &c->ws_coefsp, &c->ws_mid,
                     &c->ws_tern, &c->ws_ctA, &c->ws_ctB, &c->ws_ctC, &c->ws_pt, &c->ws_c1inv, &c->ws_io_in,
-                    &c->ws_io_sel, &c->ws_io_dist, &c->ws_io_agg, &c->ws_dtern, &c->ws_ptl})
+                    &c->ws_io_sel, &c->ws_io_dist, &c->ws_io_agg, &c->ws_dtern, &c->ws_ptl,
+                    &c->ws_enc, &c->ws_enc_in})
     b->release();
   for (void* p : {(void*)c->d_twist, (void*)c->d_roots, (void*)c->d_brv, (void*)c->d_slot})
     if (p) cudaFree(p);
@@ -1963,6 +2132,47 @@ int lcl_mult_plain_const(lcl_context* ctx, const uint64_t* d_ct, size_t batch, s
     post_launch(ctx);
     cuda_check(cudaStreamSynchronize(ctx->stream), "mult_plain");
     ctx->counts.multiplications += batch;
+  });
+}
+
+uint64_t lcl_derive_seed(uint64_t root, uint64_t tag) {  // sampling.cpp:24-30
+  u64 z = root + 0x9e3779b97f4a7c15ull * (tag + 1);
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  return z ^ (z >> 31);
+}
+
+int lcl_sampler_create(uint64_t seed, lcl_sampler** out) {
+  return guarded([&] {
+    need(out != nullptr, LCL_PARAMETER_ERROR, "null output");
+    *out = new lcl_sampler(seed);
+  });
+}
+
+int lcl_sampler_destroy(lcl_sampler* s) {
+  delete s;
+  return LCL_OK;
+}
+
+int lcl_sampler_uniform_real(lcl_sampler* s, size_t count, double* out) {
+  return guarded([&] {
+    for (size_t i = 0; i < count; ++i) out[i] = s->uniform_real();
+  });
+}
+
+int lcl_pack_and_encrypt(lcl_context* ctx, lcl_sampler* rng, const double* h_weights,
+                         size_t dim, double prescale, const uint64_t* d_pk, uint64_t* d_out) {
+  return guarded([&] {
+    need(rng != nullptr && d_pk != nullptr, LCL_PARAMETER_ERROR, "null sampler or key");
+    pack_and_encrypt(ctx, rng, h_weights, dim, prescale, d_pk, d_out);
+  });
+}
+
+int lcl_build_mask(lcl_context* ctx, lcl_sampler* rng, size_t n, const size_t* selected,
+                   size_t l, const uint64_t* d_pk, uint64_t* d_rank_rows, uint64_t* d_selectors) {
+  return guarded([&] {
+    need(rng != nullptr && d_pk != nullptr, LCL_PARAMETER_ERROR, "null sampler or key");
+    build_mask(ctx, rng, n, selected, l, d_pk, d_rank_rows, d_selectors);
   });
 }
 

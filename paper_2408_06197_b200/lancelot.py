@@ -136,6 +136,11 @@ def lib():
         "lcl_ntt_inverse": [_P, _P, _SZ, _SZ, C.c_int],
         "lcl_hadd": [_P, _P, _P, _SZ, _SZ, _P],
         "lcl_hsub": [_P, _P, _P, _SZ, _SZ, _P],
+        "lcl_sampler_create": [C.c_uint64, C.POINTER(C.c_void_p)],
+        "lcl_sampler_destroy": [_P],
+        "lcl_sampler_uniform_real": [_P, _SZ, _P],
+        "lcl_pack_and_encrypt": [_P, _P, _P, _SZ, C.c_double, _P, _P],
+        "lcl_build_mask": [_P, _P, _SZ, _P, _SZ, _P, _P, _P],
         "lcl_pair_partials": [_P, _P, _SZ, _SZ, _P],
         "lcl_pair_combine": [_P, _P, _SZ, _SZ],
         "lcl_pair_finish": [_P, _P, _SZ, _SZ, _SZ, C.c_int, _P],
@@ -297,6 +302,73 @@ class PackedWeights:
 
     def chunk_count(self):
         return int(self.chunks.shape[0])
+
+
+def derive_seed(root: int, tag: int) -> int:
+    """derive_seed (sampling.cpp:24-30)."""
+    lib().lcl_derive_seed.restype = C.c_uint64
+    lib().lcl_derive_seed.argtypes = [C.c_uint64, C.c_uint64]
+    return int(lib().lcl_derive_seed(root, tag))
+
+
+class Sampler:
+    """Sampler(seed) (sampling.hpp:32-65): the reference's mt19937_64 stream."""
+
+    def __init__(self, seed: int):
+        h = C.c_void_p()
+        _check(lib().lcl_sampler_create(C.c_uint64(seed), C.byref(h)))
+        self.h = h
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib().lcl_sampler_destroy(self.h)
+            self.h = None
+
+    def uniform_real(self, count: int):
+        out = np.empty(count, np.float64)
+        _check(lib().lcl_sampler_uniform_real(self.h, count, out.ctypes.data))
+        return out
+
+
+class PublicKey:
+    """PublicKey (ckks.hpp:62-66): (p0, p1) rows over the full chain,
+    evaluation domain, as one [2][full][N] array."""
+
+    def __init__(self, rows):
+        self.rows = np.ascontiguousarray(rows, dtype=np.uint64)
+        self._dev = None
+
+    def device(self):
+        if self._dev is None:
+            self._dev = to_device(self.rows)
+        return self._dev
+
+
+def pack_and_encrypt(ctx: "CkksContext", weights, pk: PublicKey, rng: Sampler,
+                     prescale: float = 1.0) -> "PackedWeights":
+    """distance.cpp:64-91 on the device: the weights chunked into slots,
+    encoded and encrypted, consuming rng's draws as the reference does."""
+    w = np.ascontiguousarray(weights, dtype=np.float64)
+    if w.size == 0:
+        raise ShapeError("empty weight vector")
+    N = ctx.params().ring_degree
+    chunks = -(-w.size // (N // 2))
+    out = ctx._empty(chunks, 2, ctx.full, N)
+    _check(lib().lcl_pack_and_encrypt(ctx.h, rng.h, w.ctypes.data, w.size, prescale,
+                                      _ptr(pk.device()), _ptr(out)))
+    return PackedWeights(out, int(w.size), prescale, ctx.scale())
+
+
+def build_mask(ctx: "CkksContext", selected, n: int, pk: PublicKey, rng: Sampler):
+    """aggregation.cpp:156-186 on the device -> (rank_rows, client selectors),
+    each [n][2][full][N]."""
+    N = ctx.params().ring_degree
+    sel = (C.c_size_t * max(1, len(selected)))(*selected)
+    rows = ctx._empty(n, 2, ctx.full, N)
+    sels = ctx._empty(n, 2, ctx.full, N)
+    _check(lib().lcl_build_mask(ctx.h, rng.h, n, sel, len(selected), _ptr(pk.device()),
+                                _ptr(rows), _ptr(sels)))
+    return rows, sels
 
 
 class SecretKey:

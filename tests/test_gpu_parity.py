@@ -301,6 +301,45 @@ def test_chunk_sharded_partials_bit_exact(name, shards):
     assert ctx.counters() == rig.meta["dist_ops"]
 
 
+@pytest.mark.parametrize("name", ["cfg1", "tiny_hoist_multikrum", "cfg2"])
+def test_pack_and_encrypt_bit_exact(name):
+    """Client side: measure_distance_phase's inputs (one
+    Sampler(derive_seed(1, 0xAB1A7E)) shared by the clients: dim uniform_real
+    draws, then pack_and_encrypt) produced through lcl_pack_and_encrypt equal
+    the reference's client ciphertexts (golden digests) word for word."""
+    L = _L()
+    rig = Rig(name, threads=8)
+    ctx = gpu_ctx(rig.N, secure=bool(rig.meta["options"]["secure"]))
+    pk = L.PublicKey(rig.oracle.public_key())
+    rng = L.Sampler(L.derive_seed(1, 0xAB1A7E))
+    ctx.reset_counters()
+    got = []
+    for i in range(rig.n):
+        w = rng.uniform_real(rig.dim) - 0.5
+        pw = L.pack_and_encrypt(ctx, w, pk, rng)
+        assert pw.chunk_count() == rig.C
+        got.append(L.to_host(pw.chunks))
+    got = np.stack(got)
+    assert np.array_equal(got, rig.clients)
+    assert ctx.counters()["encryptions"] == rig.n * rig.C
+
+
+@pytest.mark.parametrize("name", ["cfg1", "tiny_hoist_multikrum"])
+def test_build_mask_bit_exact(name):
+    """build_mask through lcl_build_mask with the protocol's mask sampler
+    (derive_seed(1, 0x3000000000000000)): the client selectors equal the
+    reference's (golden digests via the oracle) word for word."""
+    L = _L()
+    rig = Rig(name, threads=8)
+    ctx = gpu_ctx(rig.N, secure=bool(rig.meta["options"]["secure"]))
+    pk = L.PublicKey(rig.oracle.public_key())
+    rng = L.Sampler(L.derive_seed(1, 0x3000000000000000))
+    ctx.reset_counters()
+    _, sels = L.build_mask(ctx, rig.selected, rig.n, pk, rng)
+    assert np.array_equal(L.to_host(sels), rig.selectors)
+    assert ctx.counters()["encryptions"] == 2 * rig.n
+
+
 def test_shape_and_width_errors():
     L = _L()
     orc = Oracle(256, secure=False, threads=1)
