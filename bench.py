@@ -230,7 +230,12 @@ def our_arm(args, cfg):
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
-        dist.init_process_group("nccl")
+        # LCL_DIST_BACKEND / LCL_ONE_DEVICE: a test hook that runs the
+        # multi-rank orchestration as N ranks on ONE GPU over gloo (no N-GPU
+        # number is ever reported from it; see tools/gpu_multirank_smoke.sh)
+        dist.init_process_group(os.environ.get("LCL_DIST_BACKEND", "nccl"))
+    if os.environ.get("LCL_ONE_DEVICE") == "1":
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     N, n = cfg["N"], cfg["n"]
@@ -389,7 +394,7 @@ def our_arm(args, cfg):
 
     # ---- per-kernel breakdown of one profiled round (CUDA events per launch)
     with torch.cuda.stream(stream):
-        prof = profile_round(ctx, step, stream, N, m, npairs, Cc, width, n)
+        prof = profile_round(ctx, step, stream, N, m, npairs, cr1 - cr0, width, n)
 
     if rank == 0:
         cpu = cpu_baseline(cfg, args.config, args.cpu_budget_s) if world == 1 and not args.no_cpu else None
