@@ -340,6 +340,36 @@ def test_build_mask_bit_exact(name):
     assert ctx.counters()["encryptions"] == 2 * rig.n
 
 
+def test_client_and_kgc_errors():
+    """The new entry points raise the reference's exception types:
+    pack_and_encrypt DataError / CapacityError / ShapeError (distance.cpp:68-76,
+    ckks.cpp:267-281), build_mask ShapeError / CapacityError
+    (aggregation.cpp:158-163), decrypt_values KeyError for a short key."""
+    L = _L()
+    N = 1024
+    orc = Oracle(N, secure=False, threads=2)
+    orc.keygen(1, [1])
+    ctx = gpu_ctx(N)
+    pk = L.PublicKey(orc.public_key())
+    rng = L.Sampler(3)
+    with pytest.raises(L.DataError):
+        L.pack_and_encrypt(ctx, np.array([0.1, np.nan]), pk, rng)
+    with pytest.raises(L.CapacityError):
+        L.pack_and_encrypt(ctx, np.array([2.0 ** 21]), pk, rng)
+    with pytest.raises(L.ShapeError):
+        L.pack_and_encrypt(ctx, np.array([]), pk, rng)
+    with pytest.raises(L.ShapeError):
+        L.build_mask(ctx, [5], 4, pk, rng)
+    with pytest.raises(L.CapacityError):
+        L.build_mask(ctx, [0], N, pk, rng)
+    ct = L.pack_and_encrypt(ctx, np.full(10, 0.25), pk, rng)
+    short = L.SecretKey(orc.secret_key()[:2])
+    with pytest.raises(L.KeyError):
+        ctx.decrypt_values(L.Ciphertext(ct.chunks[0], ct.scale), short)
+    vals = ctx.decrypt_values(L.Ciphertext(ct.chunks[0], ct.scale), L.SecretKey(orc.secret_key()))
+    assert np.allclose(vals.cpu().numpy()[:10], 0.25, atol=1e-6)
+
+
 def test_shape_and_width_errors():
     L = _L()
     orc = Oracle(256, secure=False, threads=1)

@@ -92,3 +92,54 @@ def test_params_validation():
         L.CkksParams(ring_degree=1000).validate()
     with pytest.raises(L.ParameterError):
         L.CkksParams(scale_bits=30).validate()
+
+
+class _MT64:
+    """std::mt19937_64 (the reference Sampler's engine), restated for the test."""
+
+    def __init__(self, seed):
+        self.mt = [0] * 312
+        self.mt[0] = seed & (2 ** 64 - 1)
+        for i in range(1, 312):
+            self.mt[i] = (6364136223846793005 * (self.mt[i - 1] ^ (self.mt[i - 1] >> 62)) + i) & (
+                2 ** 64 - 1)
+        self.i = 312
+
+    def __call__(self):
+        if self.i >= 312:
+            for k in range(312):
+                y = (self.mt[k] & 0xFFFFFFFF80000000) | (self.mt[(k + 1) % 312] & 0x7FFFFFFF)
+                x = self.mt[(k + 156) % 312] ^ (y >> 1)
+                if y & 1:
+                    x ^= 0xB5026F5AA96619E9
+                self.mt[k] = x
+            self.i = 0
+        y = self.mt[self.i]
+        self.i += 1
+        y ^= (y >> 29) & 0x5555555555555555
+        y ^= (y << 17) & 0x71D67FFFEDA60000
+        y ^= (y << 37) & 0xFFF7EEE000000000
+        y ^= y >> 43
+        return y & (2 ** 64 - 1)
+
+
+def test_sampler_stream_and_derive_seed():
+    """The host Sampler behind lcl_pack_and_encrypt / lcl_build_mask is the
+    reference's (sampling.cpp): derive_seed's splitmix64 finaliser and
+    uniform_real = (raw >> 11) * 2^-53 over std::mt19937_64. Host-only: no
+    device needed."""
+    import paper_2408_06197_b200.lancelot as L
+
+    def splitmix(root, tag):
+        z = (root + 0x9E3779B97F4A7C15 * (tag + 1)) & (2 ** 64 - 1)
+        z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & (2 ** 64 - 1)
+        z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & (2 ** 64 - 1)
+        return z ^ (z >> 31)
+
+    for root, tag in [(1, 0xAB1A7E), (1, 5), (7, 0x3000000000000000)]:
+        assert L.derive_seed(root, tag) == splitmix(root, tag)
+    seed = L.derive_seed(1, 0xAB1A7E)
+    mt = _MT64(seed)
+    want = [(mt() >> 11) * 2.0 ** -53 for _ in range(1000)]
+    got = L.Sampler(seed).uniform_real(1000)
+    assert list(got) == want
