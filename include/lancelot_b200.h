@@ -172,6 +172,15 @@ int lcl_pack_and_encrypt(lcl_context* ctx, lcl_sampler* rng, const double* h_wei
  * (d_rank_rows [n][2][full][N]; unused by masked_aggregate, encrypted anyway
  * because they consume the sampler's draws first) and n client selectors
  * (d_selectors [n][2][full][N], all slots 1.0 for a selected client, else 0.0). */
+/* generate_keys (ckks.cpp:225-261) from the KGC's Sampler: d_sk [full+1][N]
+ * (SecretKey::s, evaluation domain), d_pk [2][full][N] (p0, p1), d_relin
+ * [full][2][full+1][N], d_rot [k][full][2][full+1][N] for the k distinct
+ * nonzero steps mod slots of steps[0..nsteps) in order (rot_steps[k], *n_rot
+ * = k; room for nsteps keys). Word-identical to the reference for the same
+ * Sampler state (draws on the host, transforms and products on the device). */
+int lcl_generate_keys(lcl_context* ctx, lcl_sampler* rng, const size_t* steps, size_t nsteps,
+                      uint64_t* d_sk, uint64_t* d_pk, uint64_t* d_relin, uint64_t* d_rot,
+                      size_t* rot_steps, size_t* n_rot);
 int lcl_build_mask(lcl_context* ctx, lcl_sampler* rng, size_t n, const size_t* selected,
                    size_t l, const uint64_t* d_pk, uint64_t* d_rank_rows, uint64_t* d_selectors);
 

@@ -8,11 +8,13 @@
 //   ref_driver gen   <options> --out DIR   dump keys, inputs, outputs, counters
 //   ref_driver bench <options> --reps R    time build_distance_matrix + masked_aggregate
 //   ref_driver encrypt --N N --dim D       time pack_and_encrypt of one client
+//   ref_driver keygen --N N --dim D --k K  time generate_keys (make_system's steps)
 //   ref_driver ops   --N N --reps S        per-op latency (NTT, mult+relin+rescale,
 //                                          hoisted rotations, rotate, decrypt_values), S s per op
 //
 // Options: --N --depth --clients --dim --k --seed --rule krum|multi_krum|median
 //          --select i,j,... --secure 0|1 --lazy 0|1 --inter 0|1
+#include <bit>
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
@@ -418,6 +420,25 @@ int cmd_encrypt(const Opts& o) {
   return 0;
 }
 
+// generate_keys for slot_reduce_steps(bit_ceil(min(dim, slots)), k), as
+// make_system does (protocol.cpp:277-285), timed on this thread.
+int cmd_keygen(const Opts& o) {
+  CkksParams p;
+  p.ring_degree = o.N;
+  p.depth = o.depth;
+  p.security = o.secure ? SecurityLevel::bits128 : SecurityLevel::none;
+  const CkksContext ctx(p);
+  const std::size_t width = std::bit_ceil(std::min(o.dim, ctx.slot_count()));
+  const std::vector<std::size_t> steps = slot_reduce_steps(width, o.k);
+  Sampler key_rng(derive_seed(o.seed, 5));
+  const auto a = std::chrono::steady_clock::now();
+  const KeyBundle kb = ctx.generate_keys(key_rng, steps);
+  const double s = std::chrono::duration<double>(std::chrono::steady_clock::now() - a).count();
+  std::printf("{\"N\": %zu, \"rotation_keys\": %zu, \"generate_keys_s\": %.6f}\n", o.N,
+              kb.rotations.steps.size(), s);
+  return 0;
+}
+
 }  // namespace
 
 int main(int argc, char** argv) {
@@ -427,6 +448,7 @@ int main(int argc, char** argv) {
     if (o.cmd == "bench") return cmd_bench(o);
     if (o.cmd == "ops") return cmd_ops(o);
     if (o.cmd == "encrypt") return cmd_encrypt(o);
+    if (o.cmd == "keygen") return cmd_keygen(o);
     std::fprintf(stderr, "unknown command %s\n", o.cmd.c_str());
     return 2;
   } catch (const std::exception& e) {

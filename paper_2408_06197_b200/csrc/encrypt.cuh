@@ -58,4 +58,59 @@ __global__ void __launch_bounds__(256)
   o[m * N] = add_mod(mul_mod(__ldg(pk + m * N + rem), r, P), e1, q);
 }
 
+// ---- key generation (ckks.cpp:195-261)
+// rows [R][N] of small signed integers (one value per coefficient, every row)
+// reduced into the row primes; prime of row r = prime_of(r).
+__global__ void __launch_bounds__(256)
+    lift_small(const signed char* __restrict__ small, u32 rows, u32 logn, u32 full,
+               u64* __restrict__ out, const PrimeConst* __restrict__ primes) {
+  const u64 N = 1ull << logn;
+  const u64 gid = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gid >= (u64)rows * N) return;
+  const u32 r = (u32)(gid >> logn);
+  const u64 q = primes[r <= full ? r : full].q;
+  const int v = small[gid & (N - 1)];
+  out[gid] = v >= 0 ? (u64)v : q - (u64)(-v);
+}
+
+// k0 = -a s + e over rows [R][N] (row r uses prime r; the special prime is
+// the last row); with target: row j also += theta_j * target_j,
+// theta_j = P mod q_j (make_switch_key, ckks.cpp:204-222).
+__global__ void __launch_bounds__(256)
+    key_rows(const u64* __restrict__ a, const u64* __restrict__ sk, const u64* __restrict__ e,
+             u32 rows, u32 logn, const u64* __restrict__ target, u32 j, u64 theta,
+             u64* __restrict__ k0, const PrimeConst* __restrict__ primes) {
+  const u64 N = 1ull << logn;
+  const u64 gid = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gid >= (u64)rows * N) return;
+  const u32 r = (u32)(gid >> logn);
+  const PrimeConst P = primes[r];
+  const u64 q = P.q;
+  const u64 as = mul_mod(a[gid], sk[gid], P);
+  u64 v = add_mod(as ? q - as : 0, e[gid], q);
+  if (target && r == j) v = add_mod(v, mul_mod(target[gid], theta, P), q);
+  k0[gid] = v;
+}
+
+// out[r][i] = in[r][perm[i]] (apply_galois in the evaluation domain, rns.cpp:534-547)
+__global__ void __launch_bounds__(256)
+    permute_rows(const u64* __restrict__ in, const u32* __restrict__ perm, u32 rows, u32 logn,
+                 u64* __restrict__ out) {
+  const u64 N = 1ull << logn;
+  const u64 gid = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gid >= (u64)rows * N) return;
+  const u64 r = gid >> logn;
+  out[gid] = in[(r << logn) + __ldg(perm + (gid & (N - 1)))];
+}
+
+// out = x * y pointwise over rows [R][N] (s^2 for the relinearization key)
+__global__ void __launch_bounds__(256)
+    square_rows(const u64* __restrict__ x, u32 rows, u32 logn, u64* __restrict__ out,
+                const PrimeConst* __restrict__ primes) {
+  const u64 N = 1ull << logn;
+  const u64 gid = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gid >= (u64)rows * N) return;
+  out[gid] = mul_mod(x[gid], x[gid], primes[(u32)(gid >> logn)]);
+}
+
 }  // namespace lcl

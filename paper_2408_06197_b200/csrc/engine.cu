@@ -1323,6 +1323,128 @@ void pack_and_encrypt(lcl_context* c, lcl_sampler* rng, const double* w, size_t 
   }, pk, out);
 }
 
+// generate_keys (ckks.cpp:225-261): the draws on the host in the reference's
+// order (secret, public a and e, then for every switch key and digit a and
+// e), the transforms and products on the device. Rotation keys for the
+// distinct nonzero steps mod slots, in the caller's order.
+struct KeygenScratch {
+  u64* a;
+  u64* e;
+  signed char* small;
+};
+
+void keygen_uniform(lcl_context* c, lcl_sampler* rng, u32 rows, std::vector<u64>& h) {
+  const size_t n = c->n;
+  h.resize((size_t)rows * n);
+  for (u32 r = 0; r < rows; ++r) {  // uniform_poly, row by row (sampling.cpp:47-55)
+    const u64 q = c->primes[r < c->full ? r : c->full];
+    for (size_t i = 0; i < n; ++i) h[(size_t)r * n + i] = rng->uniform_below(q);
+  }
+}
+
+// e (CBD) over `rows` rows into the evaluation domain at d_e
+void keygen_error(lcl_context* c, lcl_sampler* rng, u32 rows, const KeygenScratch& ks,
+                  std::vector<signed char>& hs) {
+  const size_t n = c->n;
+  hs.resize(n);
+  rng->cbd(n, kErrorEta, hs.data());
+  cuda_check(cudaMemcpyAsync(ks.small, hs.data(), n, cudaMemcpyHostToDevice, c->stream), "h2d");
+  const u64 tot = (u64)rows * n;
+  lift_small<<<(u32)((tot + 255) / 256), 256, 0, c->stream>>>(ks.small, rows, c->logn, c->full,
+                                                              ks.e, c->d_primes);
+  post_launch(c);
+  std::vector<u32> pr(rows);
+  for (u32 r = 0; r < rows; ++r) pr[r] = r < c->full ? r : c->full;
+  const RowMap em = make_map(ks.e, rows, c->N(), (u64)rows * c->N(), 1, 0, pr);
+  launch_fwd(c, rows, em, PlainLoad{em}, PlainStore{em});
+}
+
+// make_switch_key (ckks.cpp:195-223) of target [(full+1)][N] into key
+// [full][2][full+1][N].
+void keygen_switch_key(lcl_context* c, lcl_sampler* rng, const u64* d_target, const u64* d_sk,
+                       const KeygenScratch& ks, u64* key) {
+  const u32 full = c->full, rows = full + 1;
+  const u64 N = c->N(), tot = (u64)rows * N;
+  std::vector<u64> ha;
+  std::vector<signed char> hs;
+  for (u32 j = 0; j < full; ++j) {
+    u64* k0 = key + (u64)j * 2 * tot;
+    u64* a = k0 + tot;
+    keygen_uniform(c, rng, rows, ha);
+    cuda_check(cudaMemcpyAsync(a, ha.data(), tot * 8, cudaMemcpyHostToDevice, c->stream), "h2d");
+    keygen_error(c, rng, rows, ks, hs);
+    const u64 theta = c->primes[full] % c->primes[j];
+    key_rows<<<(u32)((tot + 255) / 256), 256, 0, c->stream>>>(a, d_sk, ks.e, rows, c->logn,
+                                                             d_target, j, theta, k0, c->d_primes);
+    post_launch(c);
+    // ha / hs are reused by the next digit: the copies must have landed
+    cuda_check(cudaStreamSynchronize(c->stream), "keygen");
+  }
+}
+
+std::vector<u32> galois_perm(size_t n, int logn, size_t step);  // rns.cpp:508-532, below
+
+size_t generate_keys(lcl_context* c, lcl_sampler* rng, const size_t* steps, size_t nsteps,
+                     u64* d_sk, u64* d_pk, u64* d_relin, u64* d_rot, size_t* rot_steps) {
+  const u32 full = c->full, rows = full + 1;
+  const size_t n = c->n;
+  const u64 N = c->N();
+  KeygenScratch ks;
+  ks.a = nullptr;
+  ks.e = c->ws_enc.get((u64)rows * N);
+  ks.small = reinterpret_cast<signed char*>(c->ws_enc_in.get((n + 7) / 8));
+  std::vector<signed char> hs(n);
+  std::vector<u64> ha;
+  // secret: sample_secret_like over full + 1 rows, then forward NTT
+  if (kHammingWeight == 0)
+    rng->ternary(n, hs.data());
+  else
+    rng->sparse_ternary(n, kHammingWeight, hs.data());
+  cuda_check(cudaMemcpyAsync(ks.small, hs.data(), n, cudaMemcpyHostToDevice, c->stream), "h2d");
+  lift_small<<<(u32)(((u64)rows * N + 255) / 256), 256, 0, c->stream>>>(ks.small, rows, c->logn,
+                                                                        full, d_sk, c->d_primes);
+  post_launch(c);
+  std::vector<u32> pr(rows);
+  for (u32 r = 0; r < rows; ++r) pr[r] = r < full ? r : full;
+  const RowMap skm = make_map(d_sk, rows, N, (u64)rows * N, 1, 0, pr);
+  launch_fwd(c, rows, skm, PlainLoad{skm}, PlainStore{skm});
+  cuda_check(cudaStreamSynchronize(c->stream), "keygen");
+  // public key: a uniform over the full q rows, e, p0 = -a s + e, p1 = a
+  keygen_uniform(c, rng, full, ha);
+  u64* p1 = d_pk + (u64)full * N;
+  cuda_check(cudaMemcpyAsync(p1, ha.data(), (u64)full * N * 8, cudaMemcpyHostToDevice, c->stream), "h2d");
+  keygen_error(c, rng, full, ks, hs);
+  key_rows<<<(u32)(((u64)full * N + 255) / 256), 256, 0, c->stream>>>(
+      p1, d_sk, ks.e, full, c->logn, nullptr, 0, 0, d_pk, c->d_primes);
+  post_launch(c);
+  cuda_check(cudaStreamSynchronize(c->stream), "keygen");
+  // relinearization key: target s^2
+  u64* tgt = c->ws_pt.get((u64)rows * N);
+  square_rows<<<(u32)(((u64)rows * N + 255) / 256), 256, 0, c->stream>>>(d_sk, rows, c->logn, tgt,
+                                                                         c->d_primes);
+  post_launch(c);
+  keygen_switch_key(c, rng, tgt, d_sk, ks, d_relin);
+  // rotation keys: target apply_galois(s, elt(step))
+  const u64 kw = (u64)full * 2 * rows * N;
+  size_t nk = 0;
+  std::vector<size_t> done;
+  u32* dperm = reinterpret_cast<u32*>(c->ws_dec.get((n + 1) / 2));
+  for (size_t i = 0; i < nsteps; ++i) {
+    const size_t st = steps[i] % (n / 2);
+    if (st == 0 || std::find(done.begin(), done.end(), st) != done.end()) continue;
+    done.push_back(st);
+    const std::vector<u32> perm = galois_perm(n, c->logn, st);
+    cuda_check(cudaMemcpyAsync(dperm, perm.data(), n * 4, cudaMemcpyHostToDevice, c->stream), "h2d");
+    permute_rows<<<(u32)(((u64)rows * N + 255) / 256), 256, 0, c->stream>>>(d_sk, dperm, rows,
+                                                                            c->logn, tgt);
+    post_launch(c);
+    keygen_switch_key(c, rng, tgt, d_sk, ks, d_rot + nk * kw);
+    if (rot_steps) rot_steps[nk] = st;
+    ++nk;
+  }
+  return nk;
+}
+
 // build_mask (aggregation.cpp:156-186): n rank rows (basis vectors of the
 // selected indices, in rank order) then n broadcast client selectors.
 void build_mask(lcl_context* c, lcl_sampler* rng, size_t n, const size_t* selected, size_t l,
@@ -2165,6 +2287,16 @@ int lcl_pack_and_encrypt(lcl_context* ctx, lcl_sampler* rng, const double* h_wei
   return guarded([&] {
     need(rng != nullptr && d_pk != nullptr, LCL_PARAMETER_ERROR, "null sampler or key");
     pack_and_encrypt(ctx, rng, h_weights, dim, prescale, d_pk, d_out);
+  });
+}
+
+int lcl_generate_keys(lcl_context* ctx, lcl_sampler* rng, const size_t* steps, size_t nsteps,
+                      uint64_t* d_sk, uint64_t* d_pk, uint64_t* d_relin, uint64_t* d_rot,
+                      size_t* rot_steps, size_t* n_rot) {
+  return guarded([&] {
+    need(rng != nullptr, LCL_PARAMETER_ERROR, "null sampler");
+    const size_t k = generate_keys(ctx, rng, steps, nsteps, d_sk, d_pk, d_relin, d_rot, rot_steps);
+    if (n_rot) *n_rot = k;
   });
 }
 

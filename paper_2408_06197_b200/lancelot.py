@@ -141,6 +141,7 @@ def lib():
         "lcl_sampler_uniform_real": [_P, _SZ, _P],
         "lcl_pack_and_encrypt": [_P, _P, _P, _SZ, C.c_double, _P, _P],
         "lcl_build_mask": [_P, _P, _SZ, _P, _SZ, _P, _P, _P],
+        "lcl_generate_keys": [_P, _P, _P, _SZ, _P, _P, _P, _P, _P, _P],
         "lcl_pair_partials": [_P, _P, _SZ, _SZ, _P],
         "lcl_pair_combine": [_P, _P, _SZ, _SZ],
         "lcl_pair_finish": [_P, _P, _SZ, _SZ, _SZ, C.c_int, _P],
@@ -357,6 +358,30 @@ def pack_and_encrypt(ctx: "CkksContext", weights, pk: PublicKey, rng: Sampler,
     _check(lib().lcl_pack_and_encrypt(ctx.h, rng.h, w.ctypes.data, w.size, prescale,
                                       _ptr(pk.device()), _ptr(out)))
     return PackedWeights(out, int(w.size), prescale, ctx.scale())
+
+
+def generate_keys(ctx: "CkksContext", rng: Sampler, steps):
+    """generate_keys (ckks.cpp:225-261) on the device from the KGC's Sampler:
+    (SecretKey, PublicKey, RelinKey, RotationKeySet) with host copies of the
+    words (word-identical to the reference for the same Sampler state)."""
+    import torch
+    N = ctx.params().ring_degree
+    full = ctx.full
+    kw = (full, 2, full + 1, N)
+    steps = list(steps)
+    sk = ctx._empty(full + 1, N)
+    pk = ctx._empty(2, full, N)
+    rl = ctx._empty(*kw)
+    rot = ctx._empty(max(1, len(steps)), *kw)
+    arr = (C.c_size_t * max(1, len(steps)))(*steps)
+    got = (C.c_size_t * max(1, len(steps)))()
+    nk = C.c_size_t()
+    _check(lib().lcl_generate_keys(ctx.h, rng.h, arr, len(steps), _ptr(sk), _ptr(pk), _ptr(rl),
+                                   _ptr(rot), got, C.byref(nk)))
+    torch.cuda.synchronize()
+    rot_h = to_host(rot)
+    keys = RotationKeySet({int(got[i]): rot_h[i] for i in range(nk.value)})
+    return SecretKey(to_host(sk)), PublicKey(to_host(pk)), RelinKey(to_host(rl)), keys
 
 
 def build_mask(ctx: "CkksContext", selected, n: int, pk: PublicKey, rng: Sampler):

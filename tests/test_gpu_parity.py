@@ -370,6 +370,27 @@ def test_client_and_kgc_errors():
     assert np.allclose(vals.cpu().numpy()[:10], 0.25, atol=1e-6)
 
 
+@pytest.mark.parametrize("name", ["cfg1", "tiny_hoist_multikrum"])
+def test_generate_keys_bit_exact(name):
+    """generate_keys on the device with make_system's key sampler
+    (derive_seed(1, 5)): secret, public, relinearization and every rotation
+    key equal the reference's (golden-pinned oracle) word for word."""
+    L = _L()
+    rig = Rig(name, threads=8)
+    ctx = gpu_ctx(rig.N, secure=bool(rig.meta["options"]["secure"]))
+    rng = L.Sampler(L.derive_seed(1, 5))
+    sk, pk, rk, keys = L.generate_keys(ctx, rng, rig.steps)
+    o = rig.oracle
+    assert np.array_equal(sk.rows, o.secret_key())
+    assert np.array_equal(pk.rows, o.public_key())
+    assert np.array_equal(np.asarray(rk.key).ravel(), np.asarray(o.relin_key()).ravel())
+    want = sorted({s % (rig.N // 2) for s in rig.steps} - {0})
+    assert sorted(keys.steps) == want
+    for st in want:
+        assert np.array_equal(np.asarray(keys.steps[st]).ravel(),
+                              np.asarray(o.rotation_key(st)).ravel()), st
+
+
 def test_shape_and_width_errors():
     L = _L()
     orc = Oracle(256, secure=False, threads=1)

@@ -1,4 +1,5 @@
-"""Client encryption: pack_and_encrypt of one client's weights
+"""Client encryption and key generation: pack_and_encrypt
+of one client's weights
 through lcl_pack_and_encrypt on one B200 (host draws + host encoding on
 worker threads + device lift / NTT / combine; wall clock of the synchronous
 call) beside the reference's pack_and_encrypt on one host thread
@@ -56,8 +57,32 @@ def main():
             row["speedup"] = ref["pack_and_encrypt_s"] / gpu_s
         rows.append(row)
         print(json.dumps(row), file=sys.stderr)
-    json.dump({"client_encrypt": rows, "device": torch.cuda.get_device_name(0)}, sys.stdout,
-              indent=1)
+    kg = []
+    for name, N, dim in SHAPES:
+        ctx = L.CkksContext(L.CkksParams(ring_degree=N))
+        width = 1 << (min(dim, N // 2) - 1).bit_length()
+        steps = L.slot_reduce_steps(width, 1)
+        L.generate_keys(ctx, L.Sampler(L.derive_seed(1, 5)), steps[:1])  # warm-up
+        t0 = time.perf_counter()
+        L.generate_keys(ctx, L.Sampler(L.derive_seed(1, 5)), steps)
+        torch.cuda.synchronize()
+        gpu_s = time.perf_counter() - t0
+        ref = None
+        drv = os.path.join(ROOT, "oracle", "_ref", "ref_driver")
+        if os.path.exists(drv):
+            env = dict(os.environ, LANCELOT_THREADS="1")
+            out = subprocess.run([drv, "keygen", "--N", str(N), "--dim", str(dim), "--k", "1",
+                                  "--secure", "1"], capture_output=True, text=True, env=env,
+                                 timeout=3600).stdout
+            ref = json.loads(out)
+        row = {"shape": name, "N": N, "rotation_keys": len(steps), "gpu_wall_s": gpu_s,
+               "reference_1_thread": ref}
+        if ref:
+            row["speedup"] = ref["generate_keys_s"] / gpu_s
+        kg.append(row)
+        print(json.dumps(row), file=sys.stderr)
+    json.dump({"client_encrypt": rows, "generate_keys": kg, "device": torch.cuda.get_device_name(0)},
+              sys.stdout, indent=1)
     print()
 
 
