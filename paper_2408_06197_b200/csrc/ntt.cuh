@@ -781,7 +781,10 @@ __global__ void __launch_bounds__(64, MINB)
   const u32 bq_count = (B + 3) >> 2;
   const u32 bq = blockIdx.x % bq_count;
   const u32 tb_ = blockIdx.x / bq_count;  // = t * N1 + blk
-  const u32 t = tb_ / N1, blk = tb_ - t * N1;
+  // the special-prime target (integer field, the slowest CTAs) is scheduled
+  // first so its CTAs overlap the q targets instead of forming the tail
+  const u32 traw = tb_ / N1, blk = tb_ - traw * N1;
+  const u32 t = traw == 0 ? (u32)M : traw - 1;
   const u32 bi_raw = bq * 4 + bw;
   const bool live = bi_raw < B;
   const u32 bi = live ? bi_raw : B - 1;
