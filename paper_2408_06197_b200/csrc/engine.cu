@@ -287,11 +287,12 @@ struct lcl_context {
   struct Lane {
     cudaStream_t stream = nullptr;
     cudaEvent_t done = nullptr;
-    DevBuf ws_coef, ws_digits, ws_acc, ws_coefsp, ws_mid, ws_ctB, ws_ctC, ws_c1inv;
+    DevBuf ws_coef, ws_digits, ws_acc, ws_coefsp, ws_mid, ws_ctA, ws_ctB, ws_ctC, ws_c1inv;
   };
   std::vector<Lane> lanes;
   cudaEvent_t fork_ev = nullptr;
-  DevBuf ws_io_in, ws_io_sel, ws_io_dist, ws_io_agg, ws_dtern, ws_ptl, ws_enc, ws_enc_in;
+  bool in_lane = false;  // work is being enqueued on a lane: no nested lanes
+  DevBuf ws_io_in, ws_io_sel, ws_io_dist, ws_io_agg, ws_dtern, ws_atern, ws_ptl, ws_enc, ws_enc_in;
   // masked_aggregate's encode(1/l) plaintext, NTT'd on the device once per l
   size_t pt_l = 0;
   std::vector<u64> pt_host;
@@ -865,6 +866,7 @@ void swap_lane(lcl_context* c, u32 g) {
   std::swap(c->ws_acc, ln.ws_acc);
   std::swap(c->ws_coefsp, ln.ws_coefsp);
   std::swap(c->ws_mid, ln.ws_mid);
+  std::swap(c->ws_ctA, ln.ws_ctA);
   std::swap(c->ws_ctB, ln.ws_ctB);
   std::swap(c->ws_ctC, ln.ws_ctC);
   std::swap(c->ws_c1inv, ln.ws_c1inv);
@@ -878,9 +880,36 @@ u32 lane_count(lcl_context* c, u32 B, u32 m) {
     const char* e = std::getenv("LCL_LANES");
     return e ? std::max(1, atoi(e)) : 0;
   }();
-  if (c->prof_on) return 1;  // per-kernel attribution needs a serial stream
+  if (c->prof_on || c->in_lane) return 1;  // serial attribution / no nesting
   const u32 want = env ? (u32)env : ((u64)B * m * c->N() <= (8ull << 20) ? 2u : 1u);
   return std::min<u32>(want, std::max<u32>(1, B / 8));
+}
+
+void ensure_lanes(lcl_context* c, u32 G) {
+  while (c->lanes.size() < G) {
+    c->lanes.emplace_back();
+    auto& ln = c->lanes.back();
+    cuda_check(cudaStreamCreateWithFlags(&ln.stream, cudaStreamNonBlocking), "lane stream");
+    cuda_check(cudaEventCreateWithFlags(&ln.done, cudaEventDisableTiming), "lane event");
+  }
+  if (!c->fork_ev) cuda_check(cudaEventCreateWithFlags(&c->fork_ev, cudaEventDisableTiming), "fork event");
+}
+
+// Runs f() with the context's stream and key-switch workspaces swapped for
+// lane g's (no nested lanes inside).
+template <class F>
+void on_lane(lcl_context* c, u32 g, F&& f) {
+  swap_lane(c, g);
+  c->in_lane = true;
+  try {
+    f();
+  } catch (...) {
+    c->in_lane = false;
+    swap_lane(c, g);
+    throw;
+  }
+  c->in_lane = false;
+  swap_lane(c, g);
 }
 
 // Runs f(first, count) for G contiguous groups of [0, B) concurrently, group g
@@ -892,13 +921,7 @@ void run_lanes(lcl_context* c, u32 B, u32 G, F&& f) {
     f(0u, B);
     return;
   }
-  while (c->lanes.size() < G) {
-    c->lanes.emplace_back();
-    auto& ln = c->lanes.back();
-    cuda_check(cudaStreamCreateWithFlags(&ln.stream, cudaStreamNonBlocking), "lane stream");
-    cuda_check(cudaEventCreateWithFlags(&ln.done, cudaEventDisableTiming), "lane event");
-  }
-  if (!c->fork_ev) cuda_check(cudaEventCreateWithFlags(&c->fork_ev, cudaEventDisableTiming), "fork event");
+  ensure_lanes(c, G);
   cuda_check(cudaEventRecord(c->fork_ev, c->stream), "fork");
   for (u32 g = 0; g < G; ++g) {
     const u32 b0 = (u32)((u64)B * g / G), b1 = (u32)((u64)B * (g + 1) / G);
@@ -1025,21 +1048,33 @@ void pair_accumulate_cfg(lcl_context* c, const u64* clients, u32 n, u32 chunks, 
 }
 
 // Pairs one accumulation launch covers: the i<j row-major range [a, b) of
-// the matrix; output index = position in the range.
+// the matrix (kind 0), or every pair (i, j), i < j, with j in [a, b) in
+// j-major order (kind 1: the pairs completed once clients [0, b) have
+// arrived, see lcl_server_round_host). Output index = position in the set.
 struct PairSet {
-  u32 a, b;
+  u32 a, b, kind;
 };
-PairSet row_range(u32 p0, u32 p1) { return PairSet{p0, p1}; }
+PairSet row_range(u32 p0, u32 p1) { return PairSet{p0, p1, 0}; }
+PairSet completed_by(u32 j0, u32 j1) { return PairSet{j0, j1, 1}; }
 
 std::vector<uint2> pair_list(u32 n, const PairSet& ps) {
   std::vector<uint2> all;
+  if (ps.kind == 1) {
+    for (u32 j = ps.a; j < ps.b && j < n; ++j)
+      for (u32 i = 0; i < j; ++i) all.push_back(make_uint2(i | (j << 16), (u32)all.size()));
+    return all;
+  }
   u32 p = 0;
   for (u32 i = 0; i < n; ++i)
     for (u32 j = i + 1; j < n; ++j, ++p)
       if (p >= ps.a && p < ps.b) all.push_back(make_uint2(i | (j << 16), p - ps.a));
   return all;
 }
-u32 pair_count(u32, const PairSet& ps) { return ps.b - ps.a; }
+u32 pair_count(u32 n, const PairSet& ps) {
+  if (ps.kind == 0) return ps.b - ps.a;
+  const u64 hi = std::min(ps.b, n), lo = std::min(ps.a, n);
+  return (u32)(hi * (hi - 1) / 2 - lo * (lo - 1) / 2);  // lo = 0: 0 * (2^64 - 1) = 0
+}
 
 // Bank-aware pair schedule for pair_accumulate_f64 (TPP = 1): the set cut
 // into CTA groups of per_cta; inside a group, every quarter warp (8 threads,
@@ -1047,7 +1082,7 @@ u32 pair_count(u32, const PairSet& ps) { return ps.b - ps.a; }
 // distinct bank groups (client k's tile row starts at 16-byte unit
 // k * CS / 2, CS / 2 odd), greedily.
 const uint2* pair_schedule(lcl_context* c, u32 n, const PairSet& ps, u32 per_cta, u32 cs_half) {
-  const auto key = std::make_tuple(n, ps.a, ps.b, per_cta * 64 + cs_half);
+  const auto key = std::make_tuple(n | (ps.kind << 31), ps.a, ps.b, per_cta * 64 + cs_half);
   auto it = c->sched.find(key);
   if (it != c->sched.end()) return it->second;
   const std::vector<uint2> all = pair_list(n, ps);
@@ -1125,6 +1160,7 @@ void pair_accumulate_launch(lcl_context* c, const u64* clients, u32 n, u32 chunk
   if (c->pair_f64 &&
       pair_accumulate_f64_cfg<8, 6, 2, false>(c, clients, n, chunks, c0, c1, ps, tern, accumulate))
     return;
+  need(ps.kind == 0, LCL_USAGE_ERROR, "j-major pair sets need the FP64 accumulation kernel");
   pair_accumulate_cfg<8, 4, 8>(c, clients, n, chunks, c0, c1, ps.a, ps.b, tern, accumulate);
 }
 
@@ -1787,7 +1823,7 @@ void build_context(lcl_context* c, size_t degree, int depth, int secure, int dev
 void free_context(lcl_context* c) {
   for (auto& ln : c->lanes) {
     for (DevBuf* b : {&ln.ws_coef, &ln.ws_digits, &ln.ws_acc, &ln.ws_coefsp, &ln.ws_mid,
-                      &ln.ws_ctB, &ln.ws_ctC, &ln.ws_c1inv})
+                      &ln.ws_ctA, &ln.ws_ctB, &ln.ws_ctC, &ln.ws_c1inv})
       b->release();
     if (ln.done) cudaEventDestroy(ln.done);
     if (ln.stream) cudaStreamDestroy(ln.stream);
@@ -1812,7 +1848,8 @@ void free_context(lcl_context* c) {
   for (auto& kv : c->d_sigma) cudaFree(kv.second);
   for (DevBuf* b : {&c->ws_coef, &c->ws_digits, &c->ws_acc, &c->ws_coefsp, &c->ws_mid,
                     &c->ws_tern, &c->ws_ctA, &c->ws_ctB, &c->ws_ctC, &c->ws_pt, &c->ws_c1inv, &c->ws_io_in,
-                    &c->ws_io_sel, &c->ws_io_dist, &c->ws_io_agg, &c->ws_dtern, &c->ws_ptl,
+                    &c->ws_io_sel, &c->ws_io_dist, &c->ws_io_agg, &c->ws_dtern, &c->ws_atern,
+                    &c->ws_ptl,
                     &c->ws_enc, &c->ws_enc_in})
     b->release();
   for (void* p : {(void*)c->d_twist, (void*)c->d_roots, (void*)c->d_brv, (void*)c->d_slot})
@@ -2455,6 +2492,112 @@ int lcl_masked_aggregate(lcl_context* ctx, const uint64_t* d_clients, const uint
   });
 }
 
+}  // extern "C"
+
+namespace {
+
+// Client-group form of the overlapped host round: the clients arrive in G
+// groups; when group g has landed, lane g runs the whole chain of the pairs
+// it completes (i < j, j in group g: contiguous in j-major order --
+// accumulation, relinearize, rescale, slot_reduce, D2H) while later groups
+// are still in flight. The aggregate ternaries accumulate group by group (the
+// tensor is a sum over clients) and are finished on the last lane. Group
+// boundaries k_g ~ n sqrt(g / G) give the lanes similar pair counts. Same
+// kernels and op counters as the serial round.
+void host_round_groups(lcl_context* ctx, const u64* h_clients, const u64* h_sel, u32 n, u32 C,
+                       size_t width, size_t k, size_t l, bool average, u64* h_dist, u64* h_agg,
+                       u64* dc, u64* ds, u64* dd, u64* da, u32 G) {
+  const u32 m = ctx->full;
+  const u64 N = ctx->N();
+  const u64 ctw = 2ull * m * N;
+  const u64 dstride = 2ull * (m - 1) * N;
+  const u64 astride = 2ull * (average ? m - 2 : m - 1) * N;
+  std::vector<u32> bound{0};
+  for (u32 g = 1; g < G; ++g) {
+    const u32 kb = (u32)std::lround(n * std::sqrt((double)g / G));
+    if (kb > bound.back() + 1 && kb < n) bound.push_back(kb);
+  }
+  bound.push_back(n);
+  G = (u32)bound.size() - 1;
+  ensure_lanes(ctx, G);
+  while (ctx->io_ev.size() < 1 + 3 * (size_t)G) {
+    cudaEvent_t e;
+    cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+    ctx->io_ev.push_back(e);
+  }
+  // events: 0 start; 1+g group g landed; 1+G+g its aggregate part; 1+2G+g lane done
+  cudaEvent_t* ev = ctx->io_ev.data();
+  const u64* d_pt = average ? agg_plaintext(ctx, l) : nullptr;
+  cuda_check(cudaEventRecord(ev[0], ctx->stream), "event");
+  cuda_check(cudaStreamWaitEvent(ctx->h2d, ev[0], 0), "wait");
+  cuda_check(cudaStreamWaitEvent(ctx->d2h, ev[0], 0), "wait");
+  for (u32 g = 0; g < G; ++g) cuda_check(cudaStreamWaitEvent(ctx->lanes[g].stream, ev[0], 0), "wait");
+  cuda_check(cudaMemcpyAsync(ds, h_sel, (u64)n * ctw * 8, cudaMemcpyHostToDevice, ctx->h2d), "h2d");
+  for (u32 g = 0; g < G; ++g) {
+    cuda_check(cudaMemcpyAsync(dc + (u64)bound[g] * C * ctw, h_clients + (u64)bound[g] * C * ctw,
+                               (u64)(bound[g + 1] - bound[g]) * C * ctw * 8,
+                               cudaMemcpyHostToDevice, ctx->h2d), "h2d group");
+    cuda_check(cudaEventRecord(ev[1 + g], ctx->h2d), "event");
+  }
+  u64* atern = ctx->ws_atern.get((u64)C * 3 * m * N);
+  const u32 P = n * (n - 1) / 2;
+  u64* tern = ctx->ws_dtern.get((u64)P * 3 * m * N);  // j-major, disjoint per group
+  u32 first = 0;  // j-major index of the group's first pair
+  for (u32 g = 0; g < G; ++g) {
+    const PairSet ps = completed_by(bound[g], bound[g + 1]);
+    const u32 B = pair_count(n, ps);
+    u64* o = dd + (u64)first * dstride;
+    u64* t = tern + (u64)first * 3 * m * N;
+    on_lane(ctx, g, [&] {
+      cuda_check(cudaStreamWaitEvent(ctx->stream, ev[1 + g], 0), "wait");
+      if (g > 0) cuda_check(cudaStreamWaitEvent(ctx->stream, ev[G + g], 0), "wait");
+      for (u32 c0 = 0; c0 < C; c0 += 32768)
+        agg_tensor(ctx, dc, ds, n, C, c0, std::min(C, c0 + 32768) - c0, bound[g], bound[g + 1],
+                   atern + (u64)c0 * 3 * m * N, g > 0);
+      if (g + 1 < G) {
+        cuda_check(cudaEventRecord(ev[1 + G + g], ctx->stream), "event");
+      } else {
+        for (u32 c0 = 0; c0 < C; c0 += sub_batch(ctx, m)) {
+          const u32 Bc = std::min(C, c0 + sub_batch(ctx, m)) - c0;
+          agg_finish(ctx, atern + (u64)c0 * 3 * m * N, Bc, average, d_pt, da + (u64)c0 * astride);
+        }
+        cuda_check(cudaEventRecord(ev[1 + G + g], ctx->stream), "event");
+        cuda_check(cudaStreamWaitEvent(ctx->d2h, ev[1 + G + g], 0), "wait");
+        cuda_check(cudaMemcpyAsync(h_agg, da, (u64)C * astride * 8, cudaMemcpyDeviceToHost,
+                                   ctx->d2h), "d2h agg");
+      }
+      if (B) {
+        pair_accumulate_launch(ctx, dc, n, C, 0, C, ps, t, false);
+        u64* ctA = ctx->ws_ctA.get((u64)B * 2 * m * N);
+        relinearize_batch(ctx, t, B, m, ctA);
+        rescale_batch(ctx, ctA, B, m, o);
+        slot_reduce_batch(ctx, o, B, m - 1, width, k, o);
+      }
+      cuda_check(cudaEventRecord(ev[1 + 2 * G + g], ctx->stream), "event");
+    });
+    cuda_check(cudaStreamWaitEvent(ctx->d2h, ev[1 + 2 * G + g], 0), "wait");
+    // j-major group order -> the matrix's row-major (i < j) slots
+    u32 q = 0;
+    for (u32 j = bound[g]; j < bound[g + 1]; ++j)
+      for (u32 i = 0; i < j; ++i, ++q) {
+        const u64 p = (u64)i * (2ull * n - i - 1) / 2 + (j - i - 1);
+        cuda_check(cudaMemcpyAsync(h_dist + p * dstride, o + (u64)q * dstride, dstride * 8,
+                                   cudaMemcpyDeviceToHost, ctx->d2h), "d2h pair");
+      }
+    first += B;
+  }
+  ctx->counts.multiplications += (u64)P * C + (u64)n * C;
+  ctx->counts.additions += (u64)P * (2ull * C - 1) + (u64)(n - 1) * C;
+  for (u32 g = 0; g < G; ++g)
+    cuda_check(cudaStreamWaitEvent(ctx->stream, ev[1 + 2 * G + g], 0), "join");
+  cuda_check(cudaStreamSynchronize(ctx->d2h), "round sync");
+  cuda_check(cudaStreamSynchronize(ctx->stream), "round sync");
+}
+
+}  // namespace
+
+extern "C" {
+
 int lcl_server_round_host(lcl_context* ctx, const uint64_t* h_clients, const uint64_t* h_sel,
                           size_t n, size_t chunks, double in_scale, size_t width, size_t k,
                           size_t l, int average, uint64_t* h_dist, uint64_t* h_agg) {
@@ -2499,6 +2642,15 @@ int lcl_server_round_host(lcl_context* ctx, const uint64_t* h_clients, const uin
     ensure_pairs(ctx, (u32)n);
     if (!ctx->h2d) cuda_check(cudaStreamCreateWithFlags(&ctx->h2d, cudaStreamNonBlocking), "stream");
     if (!ctx->d2h) cuda_check(cudaStreamCreateWithFlags(&ctx->d2h, cudaStreamNonBlocking), "stream");
+    static const int mode = [] {  // 0: chunk slices, 1: 2 client groups, G >= 2: G groups
+      const char* e = std::getenv("LCL_HOST_ROUND");
+      return e ? atoi(e) : 1;
+    }();
+    if (mode >= 1 && ctx->pair_f64 && n >= 4 && !ctx->prof_on) {
+      host_round_groups(ctx, h_clients, h_sel, (u32)n, (u32)chunks, width, k, l, average != 0,
+                        h_dist, h_agg, dc, ds, dd, da, mode == 1 ? 2u : (u32)mode);
+      return;
+    }
     const u32 C = (u32)chunks;
     const u32 slices = std::min<u32>(C, 16);
     const u32 per = (C + slices - 1) / slices;
