@@ -243,12 +243,14 @@ int lcl_masked_aggregate_chunks(lcl_context* ctx, const uint64_t* d_clients,
 /* Host-buffer variant of the server round used by the end-to-end benchmark:
  * H2D of clients + selectors, distance matrix, masked aggregate, D2H of both
  * outputs, synchronised before returning. The transfer is overlapped with
- * the computation (LCLT ingest): clients arrive in chunk slices
- * on an internal H2D stream, each slice is accumulated into every pair's
- * ternary and aggregated while the next is in flight, and the aggregate
- * chunks leave on an internal D2H stream; the words and op counters are
- * those of lcl_distance_matrix + lcl_masked_aggregate. Host buffers should be
- * pinned for full PCIe bandwidth (pageable memory works, slower). */
+ * the computation (LCLT ingest): the clients arrive in two
+ * groups on an internal H2D stream; the pairs the first group completes run
+ * their whole chain on one lane while the second group is in flight, the
+ * rest on a second lane, and results leave on an internal D2H stream as they
+ * are ready (chunk-sliced overlap for n < 4 or integer-pipe q-chains); the
+ * words and op counters are those of lcl_distance_matrix +
+ * lcl_masked_aggregate. Host buffers should be pinned for full PCIe
+ * bandwidth (pageable memory works, slower). */
 int lcl_server_round_host(lcl_context* ctx, const uint64_t* h_clients, const uint64_t* h_sel,
                           size_t n, size_t chunks, double in_scale, size_t width, size_t k,
                           size_t l, int average, uint64_t* h_dist, uint64_t* h_agg);
