@@ -443,6 +443,8 @@ def profile_round(ctx, step, stream, N, m, npairs, Cc, width, n):
     rows = _json.loads(buf.value.decode())
     peak = C.c_double()
     L._check(lib.lcl_peak_butterflies(ctx.h, C.byref(peak)))
+    peak_f = C.c_double()
+    L._check(lib.lcl_peak_butterflies_f64(ctx.h, C.byref(peak_f)))
     peaks = load_peaks()
     kernels = sorted(rows, key=lambda r: -r["ms"])
     total = sum(k["ms"] for k in kernels)
@@ -470,8 +472,11 @@ def profile_round(ctx, step, stream, N, m, npairs, Cc, width, n):
         int_roof = {"bound": "int (64-bit Shoup butterflies)", "kernel": top["name"],
                     "achieved": ach, "peak": peak.value, "unit": "Gbfly/s",
                     "frac": ach / peak.value,
-                    "peak_source": "measured live: lcl_peak_butterflies (register-resident "
-                                   "independent CT butterflies, all SMs)"}
+                    "peak_fp64": peak_f.value, "frac_fp64": ach / peak_f.value,
+                    "peak_source": "measured live: lcl_peak_butterflies / _f64 (register-resident "
+                                   "independent CT butterflies of each field, all SMs); q-chain "
+                                   "rows run on the FP64 pipe, the special prime on the integer "
+                                   "pipe, so the kernel's bound lies between the two"}
     # the pair accumulation runs on the FP64 pipe (q-chain < 2^44): 17 FP64
     # ops per pair-slot-chunk (2 DADD + 3 x (2 DFMA + 2 DADD + 1 DFMA)) against
     # 64 ops/clk/SM at the SM clock the round ran at
@@ -488,7 +493,7 @@ def profile_round(ctx, step, stream, N, m, npairs, Cc, width, n):
                      "ops": ops, "peak_source": f"64 FP64 ops/clk/SM x {sms} SMs x 1965 MHz "
                      "(4.27 pair-slots/clk/SM = 93% of it reached by tools/microbench/pair_forms.cu)"}
     return {"roofline": roof, "roofline_int": int_roof, "roofline_fp64": fp64_roof,
-            "kernels": kernels[:12], "peak_gbfly_s": peak.value}
+            "kernels": kernels[:12], "peak_gbfly_s": peak.value, "peak_gbfly_s_fp64": peak_f.value}
 
 
 TRAFFIC_CONFIG = None  # set by our_arm: the config whose ncu traffic file applies

@@ -98,6 +98,8 @@ int lcl_profile_begin(lcl_context* ctx);
 /* Integer roofline probe: forward-NTT butterflies/s (Shoup product + lazy
  * add/sub) on register-resident independent chains over the whole device. */
 int lcl_peak_butterflies(lcl_context* ctx, double* gbfly_per_s);
+/* The same probe for the FP64-pipe butterfly (the q-chain rows' field). */
+int lcl_peak_butterflies_f64(lcl_context* ctx, double* gbfly_per_s);
 int lcl_profile_end(lcl_context* ctx, char* json, size_t cap);
 
 /* ------------------------------------------------------------ keys */

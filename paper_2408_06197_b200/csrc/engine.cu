@@ -2008,6 +2008,27 @@ int lcl_peak_butterflies(lcl_context* ctx, double* gbfly_per_s) {
   });
 }
 
+int lcl_peak_butterflies_f64(lcl_context* ctx, double* gbfly_per_s) {
+  return guarded([&] {
+    const u32 blocks = 148 * 8, threads = 256, iters = 4096;
+    u64* sink = ctx->ws_pt.get((u64)blocks * threads);
+    const double q = (double)ctx->primes[1], w = std::floor(q / 3) + 7, wq = w / q;
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    lcl::peak_butterfly_f64<<<blocks, threads, 0, ctx->stream>>>(sink, 64, q, w, wq);
+    cudaEventRecord(a, ctx->stream);
+    lcl::peak_butterfly_f64<<<blocks, threads, 0, ctx->stream>>>(sink, iters, q, w, wq);
+    cudaEventRecord(b, ctx->stream);
+    cuda_check(cudaEventSynchronize(b), "peak butterfly f64");
+    float ms = 0;
+    cudaEventElapsedTime(&ms, a, b);
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    *gbfly_per_s = (double)blocks * threads * iters * 16 / (ms * 1e-3) / 1e9;
+  });
+}
+
 int lcl_profile_begin(lcl_context* ctx) {
   return guarded([&] {
     for (auto& r : ctx->prof) {

@@ -551,4 +551,26 @@ __global__ void __launch_bounds__(256) peak_butterfly(u64* __restrict__ sink, u3
   sink[blockIdx.x * blockDim.x + threadIdx.x] = s;
 }
 
+// Same probe for the FP64-pipe butterfly of ntt.cuh (FpF::ct: f_mulmod + two
+// DADD on exact integer-valued doubles), the field of the q-chain rows.
+__global__ void __launch_bounds__(256) peak_butterfly_f64(u64* __restrict__ sink, u32 iters,
+                                                          double q, double w, double wq) {
+  double x[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) x[i] = (double)((threadIdx.x * 131 + i * 977 + blockIdx.x) % 100003);
+  for (u32 it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const double t = f_mulmod(x[2 * i + 1], w, wq, q);
+      const double a = x[2 * i];
+      x[2 * i] = __dadd_rn(a, t);
+      x[2 * i + 1] = __dadd_rn(a, -t);
+    }
+  }
+  double s = 0;
+#pragma unroll
+  for (int i = 0; i < 32; ++i) s += x[i];
+  sink[blockIdx.x * blockDim.x + threadIdx.x] = (u64)__double_as_longlong(s);
+}
+
 }  // namespace lcl

@@ -170,6 +170,7 @@ def lib():
         "lcl_profile_begin": [_P],
         "lcl_profile_end": [_P, C.c_char_p, _SZ],
         "lcl_peak_butterflies": [_P, C.POINTER(C.c_double)],
+        "lcl_peak_butterflies_f64": [_P, C.POINTER(C.c_double)],
         "lcl_device_alloc": [_P, _SZ, C.POINTER(_P)],
         "lcl_device_free": [_P, _P],
         "lcl_copy_h2d": [_P, _P, _P, _SZ],
