@@ -284,11 +284,9 @@ def our_arm(args, cfg):
     lib = L.lib()
 
     if world == 1:
-        def step():
-            L._check(lib.lcl_distance_matrix(ctx.h, L._ptr(clients), n, Cc, scale, width, k, 1, 1,
-                                             L._ptr(d_dist), C.byref(osc)))
-            L._check(lib.lcl_masked_aggregate(ctx.h, L._ptr(clients), L._ptr(sel), n, Cc, scale,
-                                              scale, 1, 0, L._ptr(d_agg), C.byref(osc)))
+        def step():  # run_round steps 3 + 8: distance matrix and (concurrently) the aggregate
+            L._check(lib.lcl_server_round(ctx.h, L._ptr(clients), L._ptr(sel), n, Cc, width, k, 1, 0,
+                                          L._ptr(d_dist), L._ptr(d_agg)))
             return d_dist, d_agg
     else:
         # chunk-sharded: partial ternaries of all pairs over the local chunks,

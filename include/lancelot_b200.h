@@ -220,6 +220,13 @@ int lcl_masked_aggregate(lcl_context* ctx, const uint64_t* d_clients, const uint
  * (out [pair_end - pair_begin][2][full-1][N]) and chunks [chunk_begin,
  * chunk_end) of the aggregate. Concatenating the shards in order gives the
  * unsharded result word for word. */
+/* run_round steps 3 + 8 on device-resident inputs (protocol.cpp:430-432,
+ * 492-493): lcl_distance_matrix (per_pair, lazy, reduced) and
+ * lcl_masked_aggregate in one call, the aggregate on its own stream
+ * concurrently with the distance matrix; same words and counters. */
+int lcl_server_round(lcl_context* ctx, const uint64_t* d_clients, const uint64_t* d_sel,
+                     size_t n, size_t chunks, size_t width, size_t k, size_t l, int average,
+                     uint64_t* d_dist, uint64_t* d_agg);
 int lcl_distance_matrix_pairs(lcl_context* ctx, const uint64_t* d_clients, size_t n,
                               size_t chunks, double in_scale, size_t width, size_t k, int lazy,
                               int reduce, size_t pair_begin, size_t pair_end, uint64_t* d_out,

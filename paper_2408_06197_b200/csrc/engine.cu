@@ -287,7 +287,7 @@ struct lcl_context {
   struct Lane {
     cudaStream_t stream = nullptr;
     cudaEvent_t done = nullptr;
-    DevBuf ws_coef, ws_digits, ws_acc, ws_coefsp, ws_mid, ws_ctA, ws_ctB, ws_ctC, ws_c1inv;
+    DevBuf ws_coef, ws_digits, ws_acc, ws_coefsp, ws_mid, ws_tern, ws_ctA, ws_ctB, ws_ctC, ws_c1inv;
   };
   std::vector<Lane> lanes;
   cudaEvent_t fork_ev = nullptr;
@@ -866,6 +866,7 @@ void swap_lane(lcl_context* c, u32 g) {
   std::swap(c->ws_acc, ln.ws_acc);
   std::swap(c->ws_coefsp, ln.ws_coefsp);
   std::swap(c->ws_mid, ln.ws_mid);
+  std::swap(c->ws_tern, ln.ws_tern);
   std::swap(c->ws_ctA, ln.ws_ctA);
   std::swap(c->ws_ctB, ln.ws_ctB);
   std::swap(c->ws_ctC, ln.ws_ctC);
@@ -1823,7 +1824,7 @@ void build_context(lcl_context* c, size_t degree, int depth, int secure, int dev
 void free_context(lcl_context* c) {
   for (auto& ln : c->lanes) {
     for (DevBuf* b : {&ln.ws_coef, &ln.ws_digits, &ln.ws_acc, &ln.ws_coefsp, &ln.ws_mid,
-                      &ln.ws_ctA, &ln.ws_ctB, &ln.ws_ctC, &ln.ws_c1inv})
+                      &ln.ws_tern, &ln.ws_ctA, &ln.ws_ctB, &ln.ws_ctC, &ln.ws_c1inv})
       b->release();
     if (ln.done) cudaEventDestroy(ln.done);
     if (ln.stream) cudaStreamDestroy(ln.stream);
@@ -2510,6 +2511,33 @@ int lcl_masked_aggregate(lcl_context* ctx, const uint64_t* d_clients, const uint
       if (average) s = (s * ctx->scale) / (double)ctx->primes[ctx->full - 2];
       *out_scale = s;
     }
+  });
+}
+
+int lcl_server_round(lcl_context* ctx, const uint64_t* d_clients, const uint64_t* d_sel,
+                     size_t n, size_t chunks, size_t width, size_t k, size_t l, int average,
+                     uint64_t* d_dist, uint64_t* d_agg) {
+  return guarded([&] {
+    need(chunks >= 1, LCL_SHAPE_ERROR, "empty weight vector");
+    // masked_aggregate on its own lane, forked before the distance matrix:
+    // its HBM-bound tensor and short key-switch chain overlap the FP64-bound
+    // pair accumulation and the slot_reduce ladder on the context stream
+    // (lanes 0 and 1 stay free for slot_reduce)
+    if (ctx->prof_on) {
+      distance_matrix(ctx, d_clients, (u32)n, (u32)chunks, width, k, true, true, d_dist);
+      masked_aggregate(ctx, d_clients, d_sel, (u32)n, (u32)chunks, l, average != 0, d_agg);
+      return;
+    }
+    ensure_lanes(ctx, 3);
+    auto& ln = ctx->lanes[2];
+    cuda_check(cudaEventRecord(ctx->fork_ev, ctx->stream), "fork");
+    cuda_check(cudaStreamWaitEvent(ln.stream, ctx->fork_ev, 0), "lane wait");
+    on_lane(ctx, 2, [&] {
+      masked_aggregate(ctx, d_clients, d_sel, (u32)n, (u32)chunks, l, average != 0, d_agg);
+    });
+    cuda_check(cudaEventRecord(ln.done, ln.stream), "lane done");
+    distance_matrix(ctx, d_clients, (u32)n, (u32)chunks, width, k, true, true, d_dist);
+    cuda_check(cudaStreamWaitEvent(ctx->stream, ln.done, 0), "join");
   });
 }
 

@@ -142,6 +142,7 @@ def lib():
         "lcl_pack_and_encrypt": [_P, _P, _P, _SZ, C.c_double, _P, _P],
         "lcl_build_mask": [_P, _P, _SZ, _P, _SZ, _P, _P, _P],
         "lcl_generate_keys": [_P, _P, _P, _SZ, _P, _P, _P, _P, _P, _P],
+        "lcl_server_round": [_P, _P, _P, _SZ, _SZ, _SZ, _SZ, _SZ, C.c_int, _P, _P],
         "lcl_pair_partials": [_P, _P, _SZ, _SZ, _P],
         "lcl_pair_combine": [_P, _P, _SZ, _SZ],
         "lcl_pair_finish": [_P, _P, _SZ, _SZ, _SZ, C.c_int, _P],

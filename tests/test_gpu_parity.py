@@ -234,6 +234,39 @@ def test_decrypted_results_within_ckks_tolerance(golden):
         assert abs(v - plain) <= 1e-3 * max(1.0, abs(plain))
 
 
+def test_server_round_concurrent_bit_exact(golden):
+    """lcl_server_round (distance matrix + aggregate, the aggregate on its own
+    stream concurrently) reproduces the reference digests and counters."""
+    L = _L()
+    import torch
+    rig = golden
+    if not rig.lazy:
+        pytest.skip("the combined entry is the lazy, reduced per-pair round")
+    ctx = gpu_ctx(rig.N, secure=bool(rig.meta["options"]["secure"]))
+    ctx.use_relin_key(L.RelinKey(rig.oracle.relin_key()))
+    keys = L.RotationKeySet({s: rig.oracle.rotation_key(s) for s in rig.meta["rot_keys"]})
+    ctx.use_rotation_keys(keys, rig.steps)
+    m, N, n = rig.oracle.full, rig.N, rig.n
+    P = n * (n - 1) // 2
+    mo = m - 2 if rig.average else m - 1
+    cl = L.to_device(rig.clients)
+    sel = L.to_device(rig.selectors)
+    dd = torch.empty((P, 2, m - 1, N), dtype=torch.int64, device="cuda")
+    da = torch.empty((rig.C, 2, mo, N), dtype=torch.int64, device="cuda")
+    ctx.reset_counters()
+    L._check(L.lib().lcl_server_round(ctx.h, L._ptr(cl), L._ptr(sel), n, rig.C, rig.width, rig.k,
+                                      len(rig.selected), 1 if rig.average else 0, L._ptr(dd),
+                                      L._ptr(da)))
+    torch.cuda.synchronize()
+    got = L.to_host(dd)
+    pairs = [(i, j) for i in range(n) for j in range(i + 1, n)]
+    for p, (i, j) in enumerate(pairs):
+        assert sha(got[p]) == rig.meta["sha256"][f"dist_{i}_{j}"], (i, j)
+    assert sha(L.to_host(da)) == rig.meta["sha256"]["agg"]
+    want = {k: rig.meta["dist_ops"][k] + rig.meta["agg_ops"][k] for k in rig.meta["dist_ops"]}
+    assert ctx.counters() == want
+
+
 def test_kgc_decrypt_decode_bit_exact(golden):
     """Batched decrypt_values on the device (KGC side): every
     slot of every distance ciphertext and aggregate chunk equals the oracle's
