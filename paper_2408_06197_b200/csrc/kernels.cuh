@@ -190,14 +190,25 @@ __global__ void __launch_bounds__(MAXT, MINB)
   const uint2 sk = valid ? __ldg(sched + k) : make_uint2(0u, 0u);
   const u32 oi = (sk.x & 0xFFFFu) * CS, oj = (sk.x >> 16) * CS;
 
-  // chunk copies: n * TE 16-byte vectors, vector v by thread v mod blockDim
+  // chunk copies: n * TE 16-byte vectors, vector v by thread v mod blockDim.
+  // The first vector's addresses are computed once (every thread has at most
+  // one when n * TE <= blockDim, the common case); further ones per chunk.
   const u64* cbase = clients + (u64)r * N + a0;
+  auto vec_src = [&](u32 v, u32& soff) {
+    const u32 cl = v / TE, w = (v % TE) * 2, h = w / TE, e = w % TE;
+    soff = cl * CS + w;
+    return cbase + (u64)cl * chunks_total * ct_words + (u64)h * m * N + e;
+  };
+  const bool has0 = threadIdx.x < n * TE;
+  u32 soff0 = 0;
+  const u64* src0 = has0 ? vec_src(threadIdx.x, soff0) : cbase;
   auto issue = [&](u32 c, u32 stage) {
     if (c < c_end) {
-      for (u32 v = threadIdx.x; v < n * TE; v += blockDim.x) {
-        const u32 cl = v / TE, w = (v % TE) * 2, h = w / TE, e = w % TE;
-        cp_async16(tile + stage * tw + cl * CS + w,
-                   cbase + ((u64)cl * chunks_total + c) * ct_words + (u64)h * m * N + e);
+      if (has0) cp_async16(tile + stage * tw + soff0, src0 + (u64)c * ct_words);
+      for (u32 v = threadIdx.x + blockDim.x; v < n * TE; v += blockDim.x) {
+        u32 so;
+        const u64* g = vec_src(v, so);
+        cp_async16(tile + stage * tw + so, g + (u64)c * ct_words);
       }
     }
     cp_async_commit();
