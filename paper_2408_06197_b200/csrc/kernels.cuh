@@ -258,17 +258,33 @@ __global__ void __launch_bounds__(MAXT, MINB)
     }
   };
   if constexpr (!PF) {
+    // two chunks per barrier: chunk k lives in stage k % STAGES; the prologue
+    // fills STAGES - 2 stages, and each iteration refills the two stages the
+    // previous one consumed with chunks c + STAGES - 2 and c + STAGES - 1
+    static_assert(STAGES >= 4, "two chunks in flight per iteration");
 #pragma unroll
-    for (int s = 0; s < STAGES - 1; ++s) issue(c_begin + s, s);
-    u32 stage = 0;
-    for (u32 c = c_begin; c < c_end; ++c) {
-      cp_async_wait<STAGES - 2>();
+    for (int s = 0; s < STAGES - 2; ++s) issue(c_begin + s, s);
+    u32 stage = 0;  // stage of chunk c
+    u32 c = c_begin;
+    for (; c + 2 <= c_end; c += 2) {
+      cp_async_wait<STAGES - 4>();
       __syncthreads();
-      issue(c + STAGES - 1, stage == 0 ? STAGES - 1 : stage - 1);
+      const u32 s1 = stage + 1 == STAGES ? 0 : stage + 1;
+      issue(c + STAGES - 2, stage >= 2 ? stage - 2 : stage + STAGES - 2);
+      issue(c + STAGES - 1, stage >= 1 ? stage - 1 : STAGES - 1);
       ulonglong2 v[4][TE / 2];
       load(stage, v);
       math(v);
-      stage = stage + 1 == STAGES ? 0 : stage + 1;
+      load(s1, v);
+      math(v);
+      stage = s1 + 1 == STAGES ? 0 : s1 + 1;
+    }
+    if (c < c_end) {  // odd tail
+      cp_async_wait<0>();
+      __syncthreads();
+      ulonglong2 v[4][TE / 2];
+      load(stage, v);
+      math(v);
     }
   } else {
 #pragma unroll
