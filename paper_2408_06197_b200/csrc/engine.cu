@@ -519,11 +519,12 @@ void col_ilf_cfg(lcl_context* c, u32 src_rows, const RowMap& src, const RowMap& 
 
 // E = 16: 4 CTAs per SM (128 registers) -- measured cfg2 2.26 -> 1.95 ms,
 // cfg3 24.3 -> 17.5 ms against the unconstrained build (252 registers,
-// 3 CTAs). (E = 8 with 256-thread CTAs was faster at cfg2 but produced
-// wrong words in the cfg2 distance test; not pursued.)
+// 3 CTAs); E = 32 (N = 2^17): 2 CTAs per SM (128 registers), rotate 46.1 ->
+// 44.3 us per ciphertext. (E = 8 cannot work at N1 = 128: the two register
+// phases need E^2 >= N1, i.e. R = N1 / E <= E.)
 template <int LOGN1, int E>
 void col_ilf_n(lcl_context* c, u32 src_rows, const RowMap& src, const RowMap& dst, u32 fan) {
-  col_ilf_cfg<LOGN1, E, E == 16 ? 4 : 1>(c, src_rows, src, dst, fan);
+  col_ilf_cfg<LOGN1, E, E == 16 ? 4 : 2>(c, src_rows, src, dst, fan);
 }
 
 template <int LOGN1, class Epi>
