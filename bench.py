@@ -59,6 +59,7 @@ class ClockSampler:
         self.index = index
         self.samples = []  # (sm_mhz, max_mhz, reason_mask)
         self._stop = threading.Event()
+        self._ready = threading.Event()  # NVML initialised and sampling
         self._t = None
 
     def _run_nvml(self):
@@ -73,6 +74,7 @@ class ClockSampler:
                 self.samples.append((float(sm), float(mx), int(rs)))
             except Exception:
                 pass
+            self._ready.set()
             self._stop.wait(0.005)
         nv.nvmlShutdown()
 
@@ -86,6 +88,7 @@ class ClockSampler:
                 self.samples.append((float(out[0]), float(out[1]), int(out[2].strip(), 16)))
             except Exception:
                 pass
+            self._ready.set()
             self._stop.wait(0.05)
 
     def _run(self):
@@ -95,12 +98,18 @@ class ClockSampler:
             self._run_smi()
 
     def __enter__(self):
+        # NVML's first initialisation can take longer than a short timed
+        # region: wait until the sampler runs, then keep only samples taken
+        # from here on (the timed region)
         self._t = threading.Thread(target=self._run, daemon=True)
         self._t.start()
-        time.sleep(0.02)
+        self._ready.wait(timeout=10)
+        self.samples.clear()
         return self
 
     def __exit__(self, *a):
+        if not self.samples:  # a region shorter than one sampling period
+            time.sleep(0.06)
         self._stop.set()
         self._t.join(timeout=6)
 
