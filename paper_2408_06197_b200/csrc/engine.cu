@@ -2692,10 +2692,9 @@ int lcl_server_round_host(lcl_context* ctx, const uint64_t* h_clients, const uin
     ensure_pairs(ctx, (u32)n);
     if (!ctx->h2d) cuda_check(cudaStreamCreateWithFlags(&ctx->h2d, cudaStreamNonBlocking), "stream");
     if (!ctx->d2h) cuda_check(cudaStreamCreateWithFlags(&ctx->d2h, cudaStreamNonBlocking), "stream");
-    static const int mode = [] {  // 0: chunk slices, 1: 2 client groups, G >= 2: G groups
-      const char* e = std::getenv("LCL_HOST_ROUND");
-      return e ? atoi(e) : 1;
-    }();
+    // 0: chunk slices, 1: 2 client groups, G >= 2: G groups (read per call)
+    const char* mode_env = std::getenv("LCL_HOST_ROUND");
+    const int mode = mode_env ? atoi(mode_env) : 1;
     if (mode >= 1 && ctx->pair_f64 && n >= 4 && !ctx->prof_on) {
       host_round_groups(ctx, h_clients, h_sel, (u32)n, (u32)chunks, width, k, l, average != 0,
                         h_dist, h_agg, dc, ds, dd, da, mode == 1 ? 2u : (u32)mode);

@@ -179,12 +179,14 @@ def test_masked_aggregate_bit_exact_vs_reference(golden):
     assert agg.scale == rig.meta["agg_scale"]
 
 
-def test_host_round_overlapped_bit_exact_vs_reference(golden):
-    """lcl_server_round_host (host buffers in and out; chunk-sliced H2D
-    overlapped with the accumulation and the aggregate) against the
-    reference digests and op counters."""
+@pytest.mark.parametrize("mode", ["1", "0", "3"])
+def test_host_round_overlapped_bit_exact_vs_reference(golden, mode, monkeypatch):
+    """lcl_server_round_host (host buffers in and out; H2D overlapped with
+    the computation: 1 = two client groups on two lanes, 0 = chunk slices,
+    3 = three client groups) against the reference digests and op counters."""
     L = _L()
     import ctypes as C
+    monkeypatch.setenv("LCL_HOST_ROUND", mode)
     rig = golden
     if not rig.lazy:
         pytest.skip("the host round entry is the lazy, reduced per-pair round")
