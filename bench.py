@@ -35,7 +35,8 @@ CONFIGS = {
     "cfg1": dict(n=4, P=8192, N=8192, k=1),
     "cfg2": dict(n=10, P=272474, N=32768, k=1),
     "cfg3": dict(n=20, P=11173962, N=65536, k=1),
-    "cfg4": dict(n=50, P=11173962, N=65536, k=1),
+    # BASELINE configs[3]: Multi-Krum, l = 25 selected (n - l > 2c + 2 for c = 10)
+    "cfg4": dict(n=50, P=11173962, N=65536, k=1, rule="multi_krum", l=25),
 }
 METRIC = "Krum-round latency (ms) over encrypted updates"
 
@@ -195,7 +196,8 @@ def workload(cfg, name):
                         f"CKKS N=2^{N.bit_length() - 1}",
             "clients": cfg["n"], "params": cfg["P"], "ring_degree": N, "chunks": C,
             "pairs": cfg["n"] * (cfg["n"] - 1) // 2, "reduce_width": bit_ceil(min(cfg["P"], slots)),
-            "unfold_k": cfg["k"], "lazy_relin": True, "rule": "krum",
+            "unfold_k": cfg["k"], "lazy_relin": True, "rule": cfg.get("rule", "krum"),
+            "selected": cfg.get("l", 1),
             "l2": "flushed between steps (256 MiB write) and client data > L2"}
 
 
@@ -286,7 +288,9 @@ def our_arm(args, cfg):
     sel = residues(n, 2, m, N, row_primes=primes[:m])
     npairs = n * (n - 1) // 2
     d_dist = torch.empty(npairs, 2, m - 1, N, dtype=torch.int64, device=dev)
-    d_agg = torch.empty(Cc, 2, m - 1, N, dtype=torch.int64, device=dev)
+    l_sel = cfg.get("l", 1)
+    average = cfg.get("rule") == "multi_krum" and l_sel > 1
+    d_agg = torch.empty(Cc, 2, m - 2 if average else m - 1, N, dtype=torch.int64, device=dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     scale = ctx.scale()
     osc = C.c_double()
@@ -294,8 +298,8 @@ def our_arm(args, cfg):
 
     if world == 1:
         def step():  # run_round steps 3 + 8: distance matrix and (concurrently) the aggregate
-            L._check(lib.lcl_server_round(ctx.h, L._ptr(clients), L._ptr(sel), n, Cc, width, k, 1, 0,
-                                          L._ptr(d_dist), L._ptr(d_agg)))
+            L._check(lib.lcl_server_round(ctx.h, L._ptr(clients), L._ptr(sel), n, Cc, width, k, l_sel,
+                                          1 if average else 0, L._ptr(d_dist), L._ptr(d_agg)))
             return d_dist, d_agg
     else:
         # chunk-sharded: partial ternaries of all pairs over the local chunks,
@@ -303,7 +307,7 @@ def our_arm(args, cfg):
         # chains, local aggregate chunks, all-gather of both results
         from paper_2408_06197_b200.sharded import chunk_sharded_server_round, cuda_chunk_shard_fns
         fpart, ffin, fch, du, au = cuda_chunk_shard_fns(ctx, clients, sel, n, cr1 - cr0, scale,
-                                                        scale, width, k)
+                                                        scale, width, k, l=l_sel, average=average)
 
         def step():
             return chunk_sharded_server_round(npairs, Cc, du, au, fpart, ffin, fch)
@@ -357,47 +361,55 @@ def our_arm(args, cfg):
     # (lcl_server_round_host) on one GPU; with N > 1 GPUs, H2D of each rank's
     # chunk slice and the selectors, the sharded round and D2H of the gathered
     # outputs on every rank.
-    h_clients = torch.empty(clients.shape, dtype=torch.int64, pin_memory=True)
-    h_clients.copy_(clients.cpu())
-    h_sel = torch.empty(sel.shape, dtype=torch.int64, pin_memory=True)
-    h_sel.copy_(sel.cpu())
-    h_dist = torch.empty(d_dist.shape, dtype=torch.int64, pin_memory=True)
-    h_agg = torch.empty(d_agg.shape, dtype=torch.int64, pin_memory=True)
+    def measure_e2e():
+        h_clients = torch.empty(clients.shape, dtype=torch.int64, pin_memory=True)
+        h_clients.copy_(clients.cpu())
+        h_sel = torch.empty(sel.shape, dtype=torch.int64, pin_memory=True)
+        h_sel.copy_(sel.cpu())
+        h_dist = torch.empty(d_dist.shape, dtype=torch.int64, pin_memory=True)
+        h_agg = torch.empty(d_agg.shape, dtype=torch.int64, pin_memory=True)
 
-    def e2e_step():
-        if world == 1:
-            L._check(lib.lcl_server_round_host(ctx.h, C.c_void_p(h_clients.data_ptr()),
-                                               C.c_void_p(h_sel.data_ptr()), n, Cc, scale, width,
-                                               k, 1, 0, C.c_void_p(h_dist.data_ptr()),
-                                               C.c_void_p(h_agg.data_ptr())))
-            return
-        clients.copy_(h_clients, non_blocking=True)
-        sel.copy_(h_sel, non_blocking=True)
-        dd, aa = step()
-        h_dist.copy_(dd, non_blocking=True)
-        h_agg.copy_(aa, non_blocking=True)
+        def e2e_step():
+            if world == 1:
+                L._check(lib.lcl_server_round_host(ctx.h, C.c_void_p(h_clients.data_ptr()),
+                                                   C.c_void_p(h_sel.data_ptr()), n, Cc, scale, width,
+                                                   k, l_sel, 1 if average else 0,
+                                                   C.c_void_p(h_dist.data_ptr()),
+                                                   C.c_void_p(h_agg.data_ptr())))
+                return
+            clients.copy_(h_clients, non_blocking=True)
+            sel.copy_(h_sel, non_blocking=True)
+            dd, aa = step()
+            h_dist.copy_(dd, non_blocking=True)
+            h_agg.copy_(aa, non_blocking=True)
 
-    with torch.cuda.stream(stream):
-        e2e_step()
-        e2e_step()
-    e2e_ms = 0.0
-    e2e_steps = max(3, min(args.steps, 10))
-    with torch.cuda.stream(stream):
-        for _ in range(e2e_steps):
-            a = torch.cuda.Event(enable_timing=True)
-            b = torch.cuda.Event(enable_timing=True)
-            a.record(stream)
+        with torch.cuda.stream(stream):
             e2e_step()
-            b.record(stream)
-            b.synchronize()
-            e2e_ms += a.elapsed_time(b)
-    e2e_ms /= e2e_steps
-    if world > 1:
-        t = torch.tensor([e2e_ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_ms = float(t.item())
-    h2d = (h_clients.numel() + h_sel.numel()) * 8
-    d2h = (h_dist.numel() + h_agg.numel()) * 8
+            e2e_step()
+        e2e_ms = 0.0
+        e2e_steps = max(3, min(args.steps, 10))
+        with torch.cuda.stream(stream):
+            for _ in range(e2e_steps):
+                a = torch.cuda.Event(enable_timing=True)
+                b = torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                e2e_step()
+                b.record(stream)
+                b.synchronize()
+                e2e_ms += a.elapsed_time(b)
+        e2e_ms /= e2e_steps
+        if world > 1:
+            t = torch.tensor([e2e_ms], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_ms = float(t.item())
+        h2d = (h_clients.numel() + h_sel.numel()) * 8
+        d2h = (h_dist.numel() + h_agg.numel()) * 8
+        return e2e_ms, h2d, d2h
+
+    e2e = None
+    if not args.no_e2e:
+        e2e_ms, h2d, d2h = measure_e2e()
+        e2e = {"value": e2e_ms, "unit": "ms", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h}
 
     # ---- per-kernel breakdown of one profiled round (CUDA events per launch)
     with torch.cuda.stream(stream):
@@ -415,8 +427,7 @@ def our_arm(args, cfg):
                     "(every kernel is data-oblivious; bit-exactness is proven by tests/)",
             "config": workload(cfg, args.config),
             "clocks": clk.summary(),
-            "e2e": {"value": e2e_ms, "unit": "ms", "h2d_bytes_per_step": h2d,
-                    "d2h_bytes_per_step": d2h},
+            "e2e": e2e if e2e is not None else {"value": None, "skipped": "--no-e2e"},
             "gpu_launches": int(launches // max(1, args.steps)),
             "cuda_graph": graph is not None,
             "roofline": prof.get("roofline"),
@@ -541,6 +552,9 @@ def main():
     ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="launch the round eagerly")
+    ap.add_argument("--no-e2e", action="store_true",
+                    help="skip the host-buffer round (cfg4: its 72 GB of pinned client data "
+                         "exceed what a host should pin)")
     ap.add_argument("--cpu-budget-s", type=float, default=120.0)
     ap.add_argument("--ref-budget-s", type=float, default=240.0)
     args = ap.parse_args()
