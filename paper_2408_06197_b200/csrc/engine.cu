@@ -1543,15 +1543,34 @@ void distance_matrix(lcl_context* c, const u64* clients, u32 n, u32 chunks, size
   }
   const u32 SB = sub_batch(c, m);
   const u64 out_stride = 2ull * (m - 1) * N;
+  const u64 tern_words = 3ull * m * N;
+  // When more pairs than one key-switch sub-batch remain, the ternaries of
+  // ALL of them are accumulated in one pass over the clients (one launch,
+  // every pair group of a tile adjacent in the grid, so each client tile
+  // leaves HBM once), and only relinearisation / rescale / reduction run per
+  // sub-batch: 3 sub-batches at 50 clients would otherwise re-stream the
+  // clients 3 times with 137-pair CTAs instead of 175-pair ones.
+  const u32 PA = P - pair_begin;
+  const bool all_pairs = lazy && PA > SB && (u64)PA * tern_words * 8 <= (16ull << 30);
+  u64* tern_all = nullptr;
+  if (all_pairs) {
+    tern_all = c->ws_tern.get((u64)PA * tern_words);
+    for (u32 cb = 0; cb < chunks; cb += 32768)
+      pair_accumulate_launch(c, clients, n, chunks, cb, std::min(chunks, cb + 32768),
+                             row_range(pair_begin, P), tern_all, cb > 0);
+  }
   for (u32 p0 = pair_begin; p0 < P; p0 += SB) {
     const u32 p1 = std::min(P, p0 + SB), B = p1 - p0;
     u64* o = out + (u64)(p0 - pair_begin) * out_stride;
     u64* ctA = c->ws_ctA.get((u64)B * 2 * m * N);
     if (lazy) {
-      u64* tern = c->ws_tern.get((u64)B * 3 * m * N);
-      for (u32 cb = 0; cb < chunks; cb += 32768) {
-        pair_accumulate_launch(c, clients, n, chunks, cb, std::min(chunks, cb + 32768), row_range(p0, p1),
-                               tern, cb > 0);
+      u64* tern = tern_all ? tern_all + (u64)(p0 - pair_begin) * tern_words
+                           : c->ws_tern.get((u64)B * tern_words);
+      if (!tern_all) {
+        for (u32 cb = 0; cb < chunks; cb += 32768) {
+          pair_accumulate_launch(c, clients, n, chunks, cb, std::min(chunks, cb + 32768),
+                                 row_range(p0, p1), tern, cb > 0);
+        }
       }
       relinearize_batch(c, tern, B, m, ctA);
       rescale_batch(c, ctA, B, m, o);

@@ -484,11 +484,14 @@ def test_cuda_shards_concatenate_to_reference(name, world):
     assert sha(L.to_host(a)) == rig.meta["sha256"]["agg"]
 
 
-@pytest.mark.parametrize("pair_f64,n,C", [("1", 4, 600), ("0", 4, 600), ("1", 30, 3)])
+@pytest.mark.parametrize("pair_f64,n,C", [("1", 4, 600), ("0", 4, 600), ("1", 30, 3),
+                                           ("1", 48, 2), ("0", 48, 2)])
 def test_pair_accumulation_long_ranges_and_extremes(pair_f64, n, C, monkeypatch):
     """Lazy pair accumulation over 600 chunks (three 256-chunk passes of the
-    FP64-pipe kernel) and over 435 pairs (three CTA pair groups, 30 clients),
-    with boundary residues (all 0 against all q-1), for both arithmetic forms
+    FP64-pipe kernel), over 435 pairs (three CTA pair groups, 30 clients) and
+    over 1128 pairs (48 clients: more pairs than one key-switch sub-batch, so
+    every pair is accumulated in one pass and finished per sub-batch), with
+    boundary residues (all 0 against all q-1), for both arithmetic forms
     (LCL_PAIR_F64=1: FP64 pipe, 0: split-23 integer), word for word against
     the oracle's distance matrix."""
     L = _L()
