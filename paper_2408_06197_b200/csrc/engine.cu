@@ -1083,6 +1083,116 @@ u32 pair_count(u32 n, const PairSet& ps) {
 // one 16-byte shared-memory wavefront) gets pairs whose i's and j's fall in
 // distinct bank groups (client k's tile row starts at 16-byte unit
 // k * CS / 2, CS / 2 odd), greedily.
+// Orders one CTA's pairs so that every 8 consecutive threads (a quarter warp
+// of 16-byte shared-memory reads) touch clients of distinct bank groups
+// ((client * cs_half) mod 8) where possible; appends to out.
+void bank_order(std::vector<uint2> rem, u32 cs_half, std::vector<uint2>& out) {
+  while (!rem.empty()) {
+    int ib[8], jb[8];
+    for (int b = 0; b < 8; ++b) ib[b] = jb[b] = -1;
+    std::vector<uint2> grp, rest;
+    for (const uint2& e : rem) {
+      const int i = e.x & 0xFFFF, j = e.x >> 16;
+      const int bi = (int)((i * cs_half) % 8), bj = (int)((j * cs_half) % 8);
+      if (grp.size() < 8 && (ib[bi] < 0 || ib[bi] == i) && (jb[bj] < 0 || jb[bj] == j)) {
+        ib[bi] = i;
+        jb[bj] = j;
+        grp.push_back(e);
+      } else {
+        rest.push_back(e);
+      }
+    }
+    while (grp.size() < 8 && !rest.empty()) {  // no conflict-free pair left: accept one
+      grp.push_back(rest.front());
+      rest.erase(rest.begin());
+    }
+    out.insert(out.end(), grp.begin(), grp.end());
+    rem.swap(rest);
+  }
+}
+
+// Client-blocked pair groups for the full pair set of n clients: clients in
+// blocks of kPairBlock; one group per off-diagonal block pair (I < J: all
+// pairs across, 2 blocks staged) and one per two diagonal blocks (the pairs
+// inside each), so a CTA stages <= 2 * kPairBlock clients per chunk instead
+// of all n. Device layout: [groups * per_cta] uint2 entries (local client
+// indices, output pair index; .y = ~0 pads), then [groups * nl] u16 client
+// lists (padded with the group's first client).
+constexpr u32 kPairBlock = 13;  // 13 x 13 = 169 pairs <= 192 threads
+struct BlockedSchedule {
+  const uint2* sched;
+  const unsigned short* clist;
+  u32 groups, per_cta, nl;
+};
+BlockedSchedule pair_schedule_blocked(lcl_context* c, u32 n, u32 cs_half) {
+  std::vector<std::vector<u32>> blocks;
+  for (u32 b0 = 0; b0 < n; b0 += kPairBlock) {
+    blocks.emplace_back();
+    for (u32 i = b0; i < std::min(n, b0 + kPairBlock); ++i) blocks.back().push_back(i);
+  }
+  std::vector<std::vector<u32>> cls;  // clients of each group
+  const u32 nb = (u32)blocks.size();
+  for (u32 I = 0; I < nb; ++I)
+    for (u32 J = I + 1; J < nb; ++J) {
+      cls.push_back(blocks[I]);
+      cls.back().insert(cls.back().end(), blocks[J].begin(), blocks[J].end());
+    }
+  std::vector<u32> diag_groups;  // index into cls of groups made of diagonal blocks
+  for (u32 I = 0; I < nb; I += 2) {
+    diag_groups.push_back((u32)cls.size());
+    cls.push_back(blocks[I]);
+    if (I + 1 < nb) cls.back().insert(cls.back().end(), blocks[I + 1].begin(), blocks[I + 1].end());
+  }
+  // pairs of each group, output index = row-major pair number
+  std::vector<std::vector<uint2>> prs(cls.size());
+  std::vector<u32> blk(n);
+  for (u32 I = 0; I < nb; ++I)
+    for (u32 i : blocks[I]) blk[i] = I;
+  auto group_of = [&](u32 I, u32 J) {  // I <= J
+    if (I == J) return diag_groups[I / 2];
+    return I * nb - I * (I + 1) / 2 + (J - I - 1);
+  };
+  auto local = [&](u32 g, u32 i) {
+    return (u32)(std::find(cls[g].begin(), cls[g].end(), i) - cls[g].begin());
+  };
+  u32 p = 0;
+  for (u32 i = 0; i < n; ++i)
+    for (u32 j = i + 1; j < n; ++j, ++p) {
+      const u32 g = group_of(blk[i], blk[j]);
+      prs[g].push_back(make_uint2(local(g, i) | (local(g, j) << 16), p));
+    }
+  u32 per_cta = 0, nl = 0;
+  for (size_t g = 0; g < cls.size(); ++g) {
+    per_cta = std::max<u32>(per_cta, (u32)prs[g].size());
+    nl = std::max<u32>(nl, (u32)cls[g].size());
+  }
+  const u32 groups = (u32)cls.size();
+  const auto key = std::make_tuple(n | (1u << 30), 0u, 0u, cs_half);
+  auto it = c->sched.find(key);
+  if (it != c->sched.end()) {
+    return {it->second, reinterpret_cast<const unsigned short*>(it->second + (size_t)groups * per_cta), groups,
+            per_cta, nl};
+  }
+  std::vector<uint2> out;
+  for (u32 g = 0; g < groups; ++g) {
+    const size_t before = out.size();
+    bank_order(prs[g], cs_half, out);
+    out.resize(before + per_cta, make_uint2(0u, ~0u));
+  }
+  std::vector<unsigned short> cl((size_t)groups * nl);
+  for (u32 g = 0; g < groups; ++g)
+    for (u32 t = 0; t < nl; ++t) cl[(size_t)g * nl + t] = (unsigned short)(t < cls[g].size() ? cls[g][t] : cls[g][0]);
+  const size_t sbytes = out.size() * sizeof(uint2);
+  uint2* d = nullptr;
+  cuda_check(cudaMalloc(&d, sbytes + cl.size() * sizeof(unsigned short)), "schedule alloc");
+  cuda_check(cudaMemcpy(d, out.data(), sbytes, cudaMemcpyHostToDevice), "schedule upload");
+  cuda_check(cudaMemcpy(reinterpret_cast<char*>(d) + sbytes, cl.data(), cl.size() * sizeof(unsigned short),
+                        cudaMemcpyHostToDevice),
+             "schedule upload");
+  c->sched[key] = d;
+  return {d, reinterpret_cast<const unsigned short*>(d + (size_t)groups * per_cta), groups, per_cta, nl};
+}
+
 const uint2* pair_schedule(lcl_context* c, u32 n, const PairSet& ps, u32 per_cta, u32 cs_half) {
   const auto key = std::make_tuple(n | (ps.kind << 31), ps.a, ps.b, per_cta * 64 + cs_half);
   auto it = c->sched.find(key);
@@ -1091,29 +1201,8 @@ const uint2* pair_schedule(lcl_context* c, u32 n, const PairSet& ps, u32 per_cta
   std::vector<uint2> out;
   out.reserve(all.size());
   for (size_t g0 = 0; g0 < all.size(); g0 += per_cta) {
-    std::vector<uint2> rem(all.begin() + g0, all.begin() + std::min(all.size(), (size_t)g0 + per_cta));
-    while (!rem.empty()) {
-      int ib[8], jb[8];
-      for (int b = 0; b < 8; ++b) ib[b] = jb[b] = -1;
-      std::vector<uint2> grp, rest;
-      for (const uint2& e : rem) {
-        const int i = e.x & 0xFFFF, j = e.x >> 16;
-        const int bi = (int)((i * cs_half) % 8), bj = (int)((j * cs_half) % 8);
-        if (grp.size() < 8 && (ib[bi] < 0 || ib[bi] == i) && (jb[bj] < 0 || jb[bj] == j)) {
-          ib[bi] = i;
-          jb[bj] = j;
-          grp.push_back(e);
-        } else {
-          rest.push_back(e);
-        }
-      }
-      while (grp.size() < 8 && !rest.empty()) {  // no conflict-free pair left: accept one
-        grp.push_back(rest.front());
-        rest.erase(rest.begin());
-      }
-      out.insert(out.end(), grp.begin(), grp.end());
-      rem.swap(rest);
-    }
+    bank_order(std::vector<uint2>(all.begin() + g0, all.begin() + std::min(all.size(), (size_t)g0 + per_cta)),
+               cs_half, out);
   }
   uint2* d = nullptr;
   cuda_check(cudaMalloc(&d, out.size() * sizeof(uint2)), "schedule alloc");
@@ -1127,14 +1216,32 @@ template <int TE, int STAGES, int MINB, bool PF>
 bool pair_accumulate_f64_cfg(lcl_context* c, const u64* clients, u32 n, u32 chunks, u32 c0,
                              u32 c1, const PairSet& ps, u64* tern, bool accumulate) {
   constexpr int MAXT = 192;
+  static_assert(kPairBlock * kPairBlock <= MAXT, "an off-diagonal block pair fills one CTA");
   const u32 m = c->full;
   const u32 pairs = pair_count(n, ps);
-  const u32 groups = (pairs + MAXT - 1) / MAXT;
-  const u32 per_cta = (pairs + groups - 1) / groups;
+  // client-blocked groups once n exceeds two blocks and the set is the whole
+  // matrix (LCL_PAIR_BLOCKED=0 turns them off)
+  const char* eb = std::getenv("LCL_PAIR_BLOCKED");
+  const bool blocked = ps.kind == 0 && ps.a == 0 && ps.b >= n * (n - 1) / 2 && n > 2 * kPairBlock + 1 &&
+                       !(eb && eb[0] == '0');
+  u32 groups = (pairs + MAXT - 1) / MAXT;
+  u32 per_cta = (pairs + groups - 1) / groups;
+  u32 nl = n, sched_len = pairs;
+  const uint2* sched = nullptr;
+  const unsigned short* clist = nullptr;
+  if (blocked) {
+    const BlockedSchedule bs = pair_schedule_blocked(c, n, TE + 1);
+    sched = bs.sched;
+    clist = bs.clist;
+    groups = bs.groups;
+    per_cta = bs.per_cta;
+    nl = bs.nl;
+    sched_len = groups * per_cta;
+  }
   const u32 threads = std::max<u32>(64, ((per_cta + 31) / 32) * 32);
-  const size_t smem = (size_t)STAGES * n * (2 * TE + 2) * 8;
+  const size_t smem = (size_t)STAGES * nl * (2 * TE + 2) * 8;
   if (smem > 100 * 1024) return false;
-  const uint2* sched = pair_schedule(c, n, ps, per_cta, TE + 1);
+  if (!blocked) sched = pair_schedule(c, n, ps, per_cta, TE + 1);
   const u64 tiles = (u64)m * c->n / TE;
   allow_smem(pair_accumulate_f64<TE, STAGES, MAXT, MINB, PF>, smem);
   for (u32 cb = c0; cb < c1; cb += 256) {  // exact for 256 chunks per pass
@@ -1143,8 +1250,8 @@ bool pair_accumulate_f64_cfg(lcl_context* c, const u64* clients, u32 n, u32 chun
     ProfScope ps(c, "pair_accumulate",
                  8.0 * c->N() * m * (2.0 * n * (ce - cb) * groups + 3.0 * pairs * (acc ? 2 : 1)));
     pair_accumulate_f64<TE, STAGES, MAXT, MINB, PF><<<(u32)(tiles * groups), threads, smem, c->stream>>>(
-        clients, n, cb, ce, chunks, m, c->logn, sched, pairs, groups, per_cta, tern, acc ? 1 : 0,
-        c->d_primes);
+        clients, n, cb, ce, chunks, m, c->logn, sched, sched_len, groups, per_cta, tern, acc ? 1 : 0,
+        c->d_primes, clist, nl);
     post_launch(c);
   }
   return true;

@@ -173,10 +173,11 @@ __global__ void __launch_bounds__(MAXT, MINB)
     pair_accumulate_f64(const u64* __restrict__ clients, u32 n, u32 c_begin, u32 c_end,
                         u32 chunks_total, u32 m, u32 logn, const uint2* __restrict__ sched,
                         u32 pairs, u32 groups, u32 pairs_per_cta, u64* __restrict__ tern,
-                        int accumulate, const PrimeConst* __restrict__ primes) {
+                        int accumulate, const PrimeConst* __restrict__ primes,
+                        const unsigned short* __restrict__ clist, u32 nl) {
   static_assert(TE % 2 == 0, "slots are read from shared memory in 16-byte pairs");
   constexpr int CS = 2 * TE + 2;  // words per client: CS / 2 odd spreads clients over bank groups
-  extern __shared__ u64 tile[];   // [STAGES][n][CS]
+  extern __shared__ u64 tile[];   // [STAGES][nl][CS]
   const u32 N = 1u << logn;
   const u32 tiles_per_row = N / TE;
   const u32 g = blockIdx.x % groups;
@@ -184,28 +185,34 @@ __global__ void __launch_bounds__(MAXT, MINB)
   const u32 r = tix / tiles_per_row;
   const u32 a0 = (tix - r * tiles_per_row) * TE;
   const u64 ct_words = 2ull * m * N;
-  const u32 tw = n * CS;
+  // clients staged by this CTA: all n (clist == nullptr), or the nl clients
+  // of its client-blocked pair group, clist[g * nl ..]
+  if (!clist) nl = n;
+  const unsigned short* gl = clist ? clist + (size_t)g * nl : nullptr;
+  const u32 tw = nl * CS;
   const u32 k = g * pairs_per_cta + threadIdx.x;
-  const bool valid = threadIdx.x < pairs_per_cta && k < pairs;
-  const uint2 sk = valid ? __ldg(sched + k) : make_uint2(0u, 0u);
+  // schedule entries with .y == ~0 pad a group to pairs_per_cta
+  const uint2 sk = threadIdx.x < pairs_per_cta && k < pairs ? __ldg(sched + k) : make_uint2(0u, ~0u);
+  const bool valid = sk.y != ~0u;
   const u32 oi = (sk.x & 0xFFFFu) * CS, oj = (sk.x >> 16) * CS;
 
-  // chunk copies: n * TE 16-byte vectors, vector v by thread v mod blockDim.
+  // chunk copies: nl * TE 16-byte vectors, vector v by thread v mod blockDim.
   // The first vector's addresses are computed once (every thread has at most
-  // one when n * TE <= blockDim, the common case); further ones per chunk.
+  // one when nl * TE <= blockDim, the common case); further ones per chunk.
   const u64* cbase = clients + (u64)r * N + a0;
   auto vec_src = [&](u32 v, u32& soff) {
     const u32 cl = v / TE, w = (v % TE) * 2, h = w / TE, e = w % TE;
     soff = cl * CS + w;
-    return cbase + (u64)cl * chunks_total * ct_words + (u64)h * m * N + e;
+    const u32 gc = gl ? (u32)__ldg(gl + cl) : cl;
+    return cbase + (u64)gc * chunks_total * ct_words + (u64)h * m * N + e;
   };
-  const bool has0 = threadIdx.x < n * TE;
+  const bool has0 = threadIdx.x < nl * TE;
   u32 soff0 = 0;
   const u64* src0 = has0 ? vec_src(threadIdx.x, soff0) : cbase;
   auto issue = [&](u32 c, u32 stage) {
     if (c < c_end) {
       if (has0) cp_async16(tile + stage * tw + soff0, src0 + (u64)c * ct_words);
-      for (u32 v = threadIdx.x + blockDim.x; v < n * TE; v += blockDim.x) {
+      for (u32 v = threadIdx.x + blockDim.x; v < nl * TE; v += blockDim.x) {
         u32 so;
         const u64* g = vec_src(v, so);
         cp_async16(tile + stage * tw + so, g + (u64)c * ct_words);
