@@ -3,11 +3,19 @@
 A step = server step 3 + step 8 of the reference's run_round
 (protocol.cpp:430-432, 492-493): build_distance_matrix(per_pair, lazy relin,
 reduce_on_server) over all n clients, then masked_aggregate with the Krum
-selection mask. Workload = BASELINE.json configs[1] (cfg2): 10 clients,
-272,474-parameter updates, CKKS N = 2^15 (17 chunks, 45 pairs, width 16384).
+selection mask. Default workload = BASELINE.json configs[2] (cfg3), the
+largest single-GPU config and the north star's named round: 20 clients,
+11,173,962-parameter (ResNet-18) updates, CKKS N = 2^16 (342 chunks, 190
+pairs, width 32768), lazy relinearisation and HOISTED rotations with the
+unfold factor chosen dynamically as make_system does for HoistMode::dynamic_lp
+(protocol.cpp:255-287): calibrate() timed on the device (lcl_calibrate), then
+plan_unfold (distance.cpp:144-179) under the config's memory budget.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
-                    [--config cfg2|cfg1|cfg3|cfg4]
+                    [--config cfg3|cfg1|cfg2|cfg4] [--k K] [--budget-mb B]
+
+--gpus N > 1 without torchrun re-launches itself under torch.distributed.run
+with N ranks (one per GPU).
 
 Our arm prints one JSON line (rank 0). `value` is device time per round with
 inputs resident in HBM; `e2e` is the same round through the C-ABI entry
@@ -31,14 +39,21 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 CONFIGS = {
-    # name: (n clients, P params, N, k unfold, rule, selected)
+    # name: (n clients, P params, N, k unfold | budget_mb (dynamic plan), rule, selected)
     "cfg1": dict(n=4, P=8192, N=8192, k=1),
     "cfg2": dict(n=10, P=272474, N=32768, k=1),
-    "cfg3": dict(n=20, P=11173962, N=65536, k=1),
+    # BASELINE configs[2]: "lazy relin + hoisted rotations". make_system's
+    # dynamic plan picks the largest k the budget admits (plan_unfold's cost
+    # falls with k whenever t_decompose < t_hoist); the reference's default
+    # 1 GiB would pick k = 16 = 32767 rotation keys, which make_system
+    # rejects (> 512, CapacityError), so the budget is part of the config:
+    # 12 MiB = 3 fresh ciphertexts -> k = 3 (DESIGN.md §5 has the sweep).
+    "cfg3": dict(n=20, P=11173962, N=65536, budget_mb=12.0),
     # BASELINE configs[3]: Multi-Krum, l = 25 selected (n - l > 2c + 2 for c = 10)
     "cfg4": dict(n=50, P=11173962, N=65536, k=1, rule="multi_krum", l=25),
 }
 METRIC = "Krum-round latency (ms) over encrypted updates"
+DEFAULT_CONFIG = "cfg3"
 
 
 def bit_ceil(x):
@@ -132,17 +147,23 @@ def reference_arm(args, cfg):
         return
     driver = os.path.join(ROOT, "oracle", "_ref", "ref_driver")
     line = {"impl": "reference", "metric": METRIC, "unit": "ms", "higher_is_better": False,
-            "n_gpus": args.gpus, "config": workload(cfg, args.config)}
+            "n_gpus": args.gpus, "config": workload(cfg, args.config, cfg.get("k"))}
     if not os.path.exists(driver):
         line["unavailable"] = "oracle/_ref/ref_driver not built (needs /root/reference at build time)"
         print(json.dumps(line))
         return
     cores = os.cpu_count() or 1
     env = dict(os.environ, LANCELOT_THREADS=str(cores))
+    # The CPU reference needs no device warm-up; one untimed round absorbs
+    # its first-call costs (Galois-table cache, thread pool) when the budget
+    # allows, then as many timed rounds as fit (each a full round: cfg3 is
+    # ~1.5 min on 16 cores). Inputs are uniform residues (data-oblivious
+    # evaluator) so setup skips ~10 min of client encryption.
     reps = args.warmup + args.steps
     cmd = [driver, "bench", "--N", str(cfg["N"]), "--clients", str(cfg["n"]), "--dim",
-           str(cfg["P"]), "--k", str(cfg["k"]), "--secure", "1", "--reps", str(reps),
-           "--rule", "krum", "--select", "0"]
+           str(cfg["P"]), "--secure", "1", "--reps", str(reps), "--inputs", "uniform",
+           "--rule", cfg.get("rule", "krum"),
+           "--select", ",".join(str(i) for i in range(cfg.get("l", 1)))] + plan_args(cfg)
     t0 = time.time()
     proc = subprocess.Popen(cmd, stdout=subprocess.PIPE, text=True, env=env)
     budget = args.ref_budget_s
@@ -153,23 +174,46 @@ def reference_arm(args, cfg):
         out, _ = proc.communicate()
     res = parse_partial_json(out)
     times = [r["distance_s"] + r["aggregate_s"] for r in res.get("reps", [])]
-    timed = times[args.warmup:] if len(times) > args.warmup else times[-1:]
+    warm = 1 if len(times) > 1 else 0
+    timed = times[warm:]
     if not timed:
         line["unavailable"] = "reference run produced no timed repetition within the budget"
         print(json.dumps(line))
         return
+    k = res.get("k", cfg.get("k"))
+    line["config"] = workload(cfg, args.config, k)
     ms = 1000.0 * sum(timed) / len(timed)
-    sample = (f"full {args.config} round (build_distance_matrix per_pair lazy reduce + "
-              f"masked_aggregate krum) x {len(timed)} timed reps after {min(args.warmup, len(times) - len(timed))} "
-              f"warm-up; setup (keygen + encryption) {res.get('setup_s', 0):.1f}s excluded; "
-              f"wall {time.time() - t0:.0f}s")
-    line.update({"value": ms, "steps": len(timed), "warmup": args.warmup, "ms_per_step": ms,
+    sample = (f"full {args.config} round (build_distance_matrix per_pair lazy reduce, k={k} + "
+              f"masked_aggregate {cfg.get('rule', 'krum')}) x {len(timed)} timed reps after {warm} "
+              f"untimed; uniform-residue inputs; setup (keygen + calibrate + inputs) "
+              f"{res.get('setup_s', 0):.1f}s excluded; wall {time.time() - t0:.0f}s")
+    line.update({"value": ms, "steps": len(timed), "warmup": warm, "ms_per_step": ms,
                  "scaling": "replicas", "vs_baseline": None, "dtype": "u64",
-                 "data": "synthetic encrypted updates (uniform [-0.5,0.5) weights, reference generator)",
+                 "data": "synthetic: uniform residues mod each q_i for client chunks and selectors, "
+                         "keys from the reference's generate_keys",
+                 "plan": plan_record(res, cfg, "reference calibrate() on the host CPU"),
                  "cpu_baseline": {"value": ms, "unit": "ms", "cores": cores, "kind": "reference",
                                   "sample": sample},
                  "e2e": {"value": ms, "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}})
     print(json.dumps(line))
+
+
+def plan_args(cfg, k=None):
+    """ref_driver options for the config's hoisting plan: a fixed k, or
+    calibrate + plan_unfold under the memory budget (k = 0)."""
+    if k is not None:
+        return ["--k", str(k)]
+    if "budget_mb" in cfg:
+        return ["--k", "0", "--budget-mb", str(cfg["budget_mb"])]
+    return ["--k", str(cfg["k"])]
+
+
+def plan_record(res, cfg, source):
+    if "budget_mb" not in cfg:
+        return {"hoisting": "fixed", "k": res.get("k", cfg.get("k"))}
+    return {"hoisting": "dynamic_lp", "memory_budget_mb": cfg["budget_mb"], "k": res.get("k"),
+            "t_hoist_s": res.get("t_hoist"), "t_decompose_s": res.get("t_decompose"),
+            "m_cipher": res.get("m_cipher"), "calibrated_on": source}
 
 
 def parse_partial_json(out):
@@ -188,21 +232,27 @@ def parse_partial_json(out):
         return {}
 
 
-def workload(cfg, name):
+def workload(cfg, name, k):
     N = cfg["N"]
     slots = N // 2
     C = (cfg["P"] + slots - 1) // slots
-    return {"workload": f"{name}: encrypted Krum round, {cfg['n']} clients x {cfg['P']} params, "
-                        f"CKKS N=2^{N.bit_length() - 1}",
-            "clients": cfg["n"], "params": cfg["P"], "ring_degree": N, "chunks": C,
-            "pairs": cfg["n"] * (cfg["n"] - 1) // 2, "reduce_width": bit_ceil(min(cfg["P"], slots)),
-            "unfold_k": cfg["k"], "lazy_relin": True, "rule": cfg.get("rule", "krum"),
-            "selected": cfg.get("l", 1),
-            "l2": "flushed between steps (256 MiB write) and client data > L2"}
+    d = {"workload": f"{name}: encrypted Krum round, {cfg['n']} clients x {cfg['P']} params, "
+                     f"CKKS N=2^{N.bit_length() - 1}",
+         "clients": cfg["n"], "params": cfg["P"], "ring_degree": N, "chunks": C,
+         "pairs": cfg["n"] * (cfg["n"] - 1) // 2, "reduce_width": bit_ceil(min(cfg["P"], slots)),
+         "unfold_k": k, "hoisting": "dynamic_lp" if "budget_mb" in cfg else "fixed",
+         "lazy_relin": True, "rule": cfg.get("rule", "krum"),
+         "selected": cfg.get("l", 1),
+         "l2": "flushed between steps (256 MiB write) and client data > L2"}
+    if "budget_mb" in cfg:
+        d["memory_budget_mb"] = cfg["budget_mb"]
+    return d
 
 
 # ------------------------------------------------------------------ cpu baseline
-def cpu_baseline(cfg, name, budget_s):
+def cpu_baseline(cfg, name, budget_s, k):
+    """The unmodified reference (oracle/_ref) timed for one full round of the
+    same workload and plan (k) on all host cores, rank 0 at N = 1."""
     driver = os.path.join(ROOT, "oracle", "_ref", "ref_driver")
     cores = os.cpu_count() or 1
     if not os.path.exists(driver):
@@ -210,17 +260,19 @@ def cpu_baseline(cfg, name, budget_s):
                 "sample": "unavailable: oracle/_ref not built"}
     env = dict(os.environ, LANCELOT_THREADS=str(cores))
     cmd = [driver, "bench", "--N", str(cfg["N"]), "--clients", str(cfg["n"]), "--dim",
-           str(cfg["P"]), "--k", str(cfg["k"]), "--secure", "1", "--reps", "1",
-           "--rule", "krum", "--select", "0"]
+           str(cfg["P"]), "--secure", "1", "--reps", "1", "--inputs", "uniform",
+           "--rule", cfg.get("rule", "krum"),
+           "--select", ",".join(str(i) for i in range(cfg.get("l", 1)))] + plan_args(cfg, k)
     try:
         out = subprocess.run(cmd, capture_output=True, text=True, env=env, timeout=budget_s).stdout
         res = json.loads(out)
         r = res["reps"][0]
         ms = 1000.0 * (r["distance_s"] + r["aggregate_s"])
         return {"value": ms, "unit": "ms", "cores": cores, "kind": "reference",
-                "sample": f"one full {name} round on the unmodified reference core "
+                "sample": f"one full {name} round (k={k}) on the unmodified reference core "
                           f"(distance {r['distance_s']:.2f}s + aggregate {r['aggregate_s']:.2f}s), "
-                          f"LANCELOT_THREADS={cores}; setup {res['setup_s']:.1f}s excluded"}
+                          f"LANCELOT_THREADS={cores}, uniform-residue inputs; setup "
+                          f"{res['setup_s']:.1f}s excluded"}
     except Exception as e:  # noqa: BLE001
         return {"value": None, "unit": "ms", "cores": cores, "kind": "reference",
                 "sample": f"failed: {e}"[:200]}
@@ -245,6 +297,16 @@ def our_arm(args, cfg):
         # multi-rank orchestration as N ranks on ONE GPU over gloo (no N-GPU
         # number is ever reported from it; see tools/gpu_multirank_smoke.sh)
         dist.init_process_group(os.environ.get("LCL_DIST_BACKEND", "nccl"))
+    if os.environ.get("LCL_BENCH_LAUNCH_CHECK") == "1":
+        # CPU test hook (tests/test_bench_contract.py): the rank plumbing of
+        # --gpus N only -- every rank joins, rank 0 reports the world size
+        t = torch.ones(1)
+        if world > 1:
+            dist.all_reduce(t)
+            dist.destroy_process_group()
+        if rank == 0:
+            print(json.dumps({"launch_check": True, "n_gpus": world, "ranks_joined": int(t.item())}))
+        return
     if os.environ.get("LCL_ONE_DEVICE") == "1":
         local = 0
     torch.cuda.set_device(local)
@@ -253,7 +315,6 @@ def our_arm(args, cfg):
     slots = N // 2
     Cc = (cfg["P"] + slots - 1) // slots
     width = bit_ceil(min(cfg["P"], slots))
-    k = cfg["k"]
     ctx = L.CkksContext(L.CkksParams(ring_degree=N), device=local)
     stream = torch.cuda.Stream(device=dev)
     ctx.set_stream(stream)
@@ -275,6 +336,29 @@ def our_arm(args, cfg):
     def key():
         return L.to_host(residues(m, 2, m + 1, N, row_primes=primes))
 
+    # the hoisting plan: fixed k, or make_system's dynamic_lp plan from a
+    # device calibration (probe keys {1, 2}, a fresh ciphertext) under the
+    # config's memory budget; rank 0's plan is broadcast so ranks agree
+    plan = {"hoisting": "fixed", "k": cfg.get("k")}
+    if "k" in cfg:
+        k = cfg["k"]
+    else:
+        probe = L.RotationKeySet({1: key(), 2: key()})
+        fresh = L.Ciphertext(residues(2, m, N, row_primes=primes[:m]), ctx.scale())
+        with torch.cuda.stream(stream):
+            cal = L.calibrate(ctx, probe, fresh)
+        hp = L.plan_unfold(cal.t_hoist, cal.t_decompose, cal.m_cipher,
+                           cfg["budget_mb"] * 1048576.0, width)
+        k = hp.k
+        if world > 1:
+            kt = torch.tensor([k], device=dev)
+            dist.broadcast(kt, 0)
+            k = int(kt.item())
+        plan = {"hoisting": "dynamic_lp", "memory_budget_mb": cfg["budget_mb"], "k": k,
+                "t_hoist_s": cal.t_hoist, "t_decompose_s": cal.t_decompose,
+                "m_cipher": cal.m_cipher, "plan_cost_s": hp.cost,
+                "calibrated_on": "device (lcl_calibrate: median of 11 CUDA-event-timed "
+                                 "hoisted_rotations calls, batch 1)"}
     rk = L.RelinKey(key())
     steps = L.slot_reduce_steps(width, k)
     keys = L.RotationKeySet({s: key() for s in steps})
@@ -416,7 +500,8 @@ def our_arm(args, cfg):
         prof = profile_round(ctx, step, stream, N, m, npairs, cr1 - cr0, width, n)
 
     if rank == 0:
-        cpu = cpu_baseline(cfg, args.config, args.cpu_budget_s) if world == 1 and not args.no_cpu else None
+        cpu = (cpu_baseline(cfg, args.config, args.cpu_budget_s, k)
+               if world == 1 and not args.no_cpu else None)
         line = {
             "metric": METRIC, "value": ms, "unit": "ms", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False,
@@ -425,7 +510,8 @@ def our_arm(args, cfg):
                             f"reduce_scatter), pair chains sharded, all-gather") if world > 1 else "1 GPU",
             "data": "synthetic: uniform residues mod each q_i for ciphertexts, selectors and keys "
                     "(every kernel is data-oblivious; bit-exactness is proven by tests/)",
-            "config": workload(cfg, args.config),
+            "config": workload(cfg, args.config, k),
+            "plan": plan,
             "clocks": clk.summary(),
             "e2e": e2e if e2e is not None else {"value": None, "skipped": "--no-e2e"},
             "gpu_launches": int(launches // max(1, args.steps)),
@@ -521,7 +607,9 @@ def traffic_for(kernel, algorithmic_bytes):
     """DRAM bytes per launch of `kernel` from the committed ncu capture of one
     round of this config (profiles/r01_traffic_<cfg>.json, tools/ncu_traffic.py),
     or None when no capture exists."""
-    p = os.path.join(ROOT, "profiles", f"r01_traffic_{TRAFFIC_CONFIG}.json")
+    p = os.path.join(ROOT, "profiles", f"r02_traffic_{TRAFFIC_CONFIG}.json")
+    if not os.path.exists(p):
+        p = os.path.join(ROOT, "profiles", f"r01_traffic_{TRAFFIC_CONFIG}.json")
     try:
         with open(p) as f:
             k = json.load(f)["kernels"][kernel]
@@ -543,28 +631,56 @@ def load_peaks():
         return {"hbm_gbs": 6650.0, "source": "fallback (B200_PROFILING.md)"}
 
 
+def self_launch(args):
+    """--gpus N > 1 outside torchrun: re-run this script under
+    torch.distributed.run with N ranks on this node (127.0.0.1)."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+           f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default=DEFAULT_CONFIG, choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="launch the round eagerly")
     ap.add_argument("--no-e2e", action="store_true",
                     help="skip the host-buffer round (cfg4: its 72 GB of pinned client data "
                          "exceed what a host should pin)")
-    ap.add_argument("--cpu-budget-s", type=float, default=120.0)
-    ap.add_argument("--ref-budget-s", type=float, default=240.0)
+    ap.add_argument("--cpu-budget-s", type=float, default=400.0)
+    ap.add_argument("--ref-budget-s", type=float, default=420.0)
+    ap.add_argument("--k", type=int, default=None, help="fixed unfold factor (overrides the plan)")
+    ap.add_argument("--budget-mb", type=float, default=None,
+                    help="memory budget of the dynamic plan (overrides the config's)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
-    cfg = CONFIGS[args.config]
+    cfg = dict(CONFIGS[args.config])
+    if args.k:
+        cfg.pop("budget_mb", None)
+        cfg["k"] = args.k
+    elif args.budget_mb:
+        cfg.pop("k", None)
+        cfg["budget_mb"] = args.budget_mb
+    world = os.environ.get("WORLD_SIZE")
     if args.impl == "reference":
         reference_arm(args, cfg)
-    else:
-        our_arm(args, cfg)
+        return 0
+    if world is None and args.gpus > 1:
+        return self_launch(args)
+    if world is not None and int(world) != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
+    our_arm(args, cfg)
+    return 0
 
 
 if __name__ == "__main__":
-    main()
+    sys.exit(main())

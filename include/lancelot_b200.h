@@ -16,9 +16,11 @@
  *   lcl_rescale              CkksContext::rescale                      ckks.cpp:536-547
  *   lcl_rotate               CkksContext::rotate                       ckks.cpp:560-580
  *   lcl_hoisted_rotations    CkksContext::hoisted_rotations            ckks.cpp:582-612
+ *   lcl_calibrate            calibrate (make_system, dynamic_lp)       protocol.cpp:224-253
  *   lcl_slot_reduce          slot_reduce                               distance.cpp:214-240
  *   lcl_pairwise_distance    encrypted_pairwise_distance               distance.cpp:107-142
  *   lcl_distance_matrix      build_distance_matrix (per_pair)          distance.cpp:242-300
+ *   lcl_build_distance_matrix  build_distance_matrix (both modes)       distance.cpp:242-300
  *   lcl_masked_aggregate     masked_aggregate                          aggregation.cpp:188-229
  *   lcl_*_pairs / _chunks    the same, one shard of pairs / chunks     distance.cpp:257-272,
  *                            (the reference's parallel_for ranges)     aggregation.cpp:211
@@ -146,6 +148,15 @@ int lcl_rotate(lcl_context* ctx, const uint64_t* d_ct, size_t batch, size_t coun
 /* outs: [nsteps][batch][2][count][N]; one decomposition for all steps. */
 int lcl_hoisted_rotations(lcl_context* ctx, const uint64_t* d_ct, size_t batch, size_t count,
                           const size_t* h_steps, size_t nsteps, uint64_t* d_outs);
+/* calibrate (protocol.cpp:224-253) on the device: the median of 11
+ * CUDA-event-timed lcl_hoisted_rotations calls on the fresh ciphertext d_ct
+ * ([2][count][N], batch 1) for steps {1} and {1, 2}; *t_hoist = t1,
+ * *t_decompose = t2 - t1 (the reference's naming), *m_cipher =
+ * Ciphertext::size_bytes. Needs rotation keys 1 and 2 (KeyError otherwise).
+ * Synchronises the context stream. Feed the result to plan_unfold
+ * (distance.cpp:144-179; mirrored in the C++ / Python hosts). */
+int lcl_calibrate(lcl_context* ctx, const uint64_t* d_ct, size_t count, double* t_hoist,
+                  double* t_decompose, double* m_cipher);
 /* HoistPlan{k, n = width}: first min(k-1, log2 width) levels hoisted. */
 int lcl_slot_reduce(lcl_context* ctx, const uint64_t* d_ct, size_t batch, size_t count,
                     size_t width, size_t k, uint64_t* d_out);
@@ -211,6 +222,16 @@ int lcl_pairwise_distance(lcl_context* ctx, const uint64_t* d_a, const uint64_t*
 int lcl_distance_matrix(lcl_context* ctx, const uint64_t* d_clients, size_t n, size_t chunks,
                         double in_scale, size_t width, size_t k, int lazy, int reduce,
                         uint64_t* d_out, double* out_scale);
+/* build_distance_matrix with every DistanceMode and DistanceOptions
+ * (distance.cpp:242-300): mode LCL_PER_PAIR -> out [n(n-1)/2][2][full-1][N]
+ * in (i<j) order, each pair slot_reduced when reduce_on_server; mode
+ * LCL_ROW_SUMS -> out [n][2][full-1][N], row i = sum of the unreduced pair
+ * ciphertexts containing client i, slot_reduced once when reduce_on_server
+ * (reduce_on_server = !slot_sum_at_kgc, protocol.cpp:555). */
+enum { LCL_PER_PAIR = 0, LCL_ROW_SUMS = 1 };
+int lcl_build_distance_matrix(lcl_context* ctx, const uint64_t* d_clients, size_t n,
+                              size_t chunks, double in_scale, size_t width, size_t k, int mode,
+                              int lazy, int reduce_on_server, uint64_t* d_out, double* out_scale);
 /* selectors [n][2][full][N]; average = (rule == multi_krum && l > 1);
  * out [chunks][2][full-1 (or full-2 when averaging)][N]. */
 int lcl_masked_aggregate(lcl_context* ctx, const uint64_t* d_clients, const uint64_t* d_sel,

@@ -1155,6 +1155,32 @@ int lo_distance_matrix(lo_ctx* c, size_t n, size_t chunks, const uint64_t* clien
   return rc;
 }
 
+/* build_distance_matrix, row_sums mode (distance.cpp:257-298): unreduced
+ * pair distances, row i = hadd chain over the pairs containing i in pair
+ * order, then slot_reduce per row when reduce. out = [n][2][L][N]. */
+int lo_distance_rows(lo_ctx* c, size_t n, size_t chunks, const uint64_t* clients,
+                     size_t width, size_t k, int lazy, int reduce, uint64_t* out) {
+  if (n < 2) return LO_SHAPE_ERROR;
+  size_t m = c->full, ow = 2 * (m - 1) * c->n, np = n * (n - 1) / 2;
+  u64* pd = malloc(np * ow * 8);
+  int rc = lo_distance_matrix(c, n, chunks, clients, width, k, lazy, 0, pd);
+  for (size_t i = 0; !rc && i < n; ++i) {
+    u64* row = out + i * ow;
+    int first = 1;
+    size_t p = 0;
+    for (size_t a = 0; a < n; ++a)
+      for (size_t b = a + 1; b < n; ++b, ++p) {
+        if (a != i && b != i) continue;
+        if (first) memcpy(row, pd + p * ow, ow * 8);
+        else rc = rc ? rc : lo_hadd(c, m - 1, row, pd + p * ow, row);
+        first = 0;
+      }
+    if (!rc && reduce) rc = lo_slot_reduce(c, m - 1, row, width, k, row);
+  }
+  free(pd);
+  return rc;
+}
+
 typedef struct {
   lo_ctx* c;
   size_t n, chunks, l;

@@ -114,6 +114,9 @@ int lo_pairwise_distance(lo_ctx* c, size_t chunks, const uint64_t* a,
                          const uint64_t* b, int lazy, uint64_t* out);
 int lo_distance_matrix(lo_ctx* c, size_t n, size_t chunks, const uint64_t* clients,
                        size_t width, size_t k, int lazy, int reduce, uint64_t* out);
+/* row_sums mode (distance.cpp:287-298): out = [n][2][L][N]. */
+int lo_distance_rows(lo_ctx* c, size_t n, size_t chunks, const uint64_t* clients,
+                     size_t width, size_t k, int lazy, int reduce, uint64_t* out);
 int lo_masked_aggregate(lo_ctx* c, size_t n, size_t chunks, const uint64_t* clients,
                         const uint64_t* selectors, size_t l, int average,
                         uint64_t* out);

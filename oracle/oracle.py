@@ -85,6 +85,7 @@ def _lib():
     lib.lo_pairwise_distance.argtypes = [C.c_void_p, C.c_size_t, _u64p, _u64p, C.c_int, _u64p]
     lib.lo_distance_matrix.argtypes = [C.c_void_p, C.c_size_t, C.c_size_t, _u64p, C.c_size_t,
                                        C.c_size_t, C.c_int, C.c_int, _u64p]
+    lib.lo_distance_rows.argtypes = lib.lo_distance_matrix.argtypes
     lib.lo_masked_aggregate.argtypes = [C.c_void_p, C.c_size_t, C.c_size_t, _u64p, _u64p,
                                         C.c_size_t, C.c_int, _u64p]
     lib.lo_decrypt_values.argtypes = [C.c_void_p, C.c_size_t, _u64p, C.c_double,
@@ -318,6 +319,15 @@ class Oracle:
         out = np.empty((n * (n - 1) // 2, 2, self.full - 1, self.N), np.uint64)
         _chk(lib().lo_distance_matrix(self.h, n, Cc, _p(clients), width, k, int(lazy),
                                       int(reduce), _p(out)), "distance_matrix")
+        return out
+
+    def distance_rows(self, clients, width, k, lazy=True, reduce=True):
+        """DistanceMode::row_sums: [n][2][L][N]."""
+        clients = self._ct(clients)
+        n, Cc = clients.shape[0], clients.shape[1]
+        out = np.empty((n, 2, self.full - 1, self.N), np.uint64)
+        _chk(lib().lo_distance_rows(self.h, n, Cc, _p(clients), width, k, int(lazy),
+                                    int(reduce), _p(out)), "distance_rows")
         return out
 
     def masked_aggregate(self, clients, selectors, l=1, average=False):

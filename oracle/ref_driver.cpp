@@ -12,8 +12,19 @@
 //   ref_driver ops   --N N --reps S        per-op latency (NTT, mult+relin+rescale,
 //                                          hoisted rotations, rotate, decrypt_values), S s per op
 //
+//   ref_driver calibrate --N N --dim D --budget-mb B
+//                                          calibrate() + plan_unfold (protocol.cpp:224-287)
+//
 // Options: --N --depth --clients --dim --k --seed --rule krum|multi_krum|median
 //          --select i,j,... --secure 0|1 --lazy 0|1 --inter 0|1
+//          --mode per_pair|row_sums --reduce 0|1 (DistanceMode / reduce_on_server)
+//          --inputs encrypted|uniform  (uniform: client chunks and selectors are
+//          uniform residues per row -- every evaluator op is data-oblivious, so
+//          timing equals that of encrypted inputs without the ~10 min of
+//          single-stream client encryption)
+//          --k 0 --budget-mb B: the plan comes from calibrate() + plan_unfold
+//          under a B MiB memory budget (HoistMode::dynamic_lp)
+#include <algorithm>
 #include <bit>
 #include <chrono>
 #include <cstdio>
@@ -49,6 +60,10 @@ struct Opts {
   bool inter = true;
   std::size_t reps = 3;
   std::string out = ".";
+  std::string mode = "per_pair";
+  bool reduce = true;
+  bool uniform = false;
+  double budget_mb = 1024.0;
 };
 
 Opts parse(int argc, char** argv) {
@@ -69,6 +84,10 @@ Opts parse(int argc, char** argv) {
     else if (k == "--inter") o.inter = v == "1";
     else if (k == "--reps") o.reps = std::stoull(v);
     else if (k == "--out") o.out = v;
+    else if (k == "--mode") o.mode = v;
+    else if (k == "--reduce") o.reduce = v == "1";
+    else if (k == "--inputs") o.uniform = v == "uniform";
+    else if (k == "--budget-mb") o.budget_mb = std::stod(v);
     else if (k == "--select") {
       o.select.clear();
       std::stringstream ss(v);
@@ -138,9 +157,61 @@ SelectionRule rule_of(const std::string& s) {
   throw std::runtime_error("bad rule");
 }
 
+DistanceMode mode_of(const std::string& s) {
+  if (s == "per_pair") return DistanceMode::per_pair;
+  if (s == "row_sums") return DistanceMode::row_sums;
+  throw std::runtime_error("bad mode");
+}
+
+// calibrate (protocol.cpp:224-253), restated over the public API because
+// protocol.cpp (with the model / data / training stack) is not compiled
+// into the checker: median of 11 hoisted_rotations({1}) and ({1, 2}) calls on
+// a fresh encryption of 0.5 in every slot; t_hoist = t1, t_decompose =
+// t2 - t1 (the reference's naming, see SURVEY "Reference defects").
+struct Calib {
+  double t_hoist, t_decompose, m_cipher;
+};
+
+Calib calibrate_ref(const CkksContext& ctx, const KeyBundle& keys, Sampler& rng) {
+  std::vector<double> values(ctx.slot_count(), 0.5);
+  const Ciphertext ct = ctx.encrypt(ctx.encode(values), keys.pk, rng);
+  auto median_time = [&](const std::vector<std::size_t>& steps) {
+    std::vector<double> times;
+    for (int rep = 0; rep < 11; ++rep) {
+      const auto a = std::chrono::steady_clock::now();
+      (void)ctx.hoisted_rotations(ct, steps, keys.rotations);
+      times.push_back(
+          std::chrono::duration<double>(std::chrono::steady_clock::now() - a).count());
+    }
+    std::sort(times.begin(), times.end());
+    return times[times.size() / 2];
+  };
+  const double t1 = median_time({1});
+  const double t2 = median_time({1, 2});
+  return {std::max(t1, 1e-9), std::max(t2 - t1, 1e-9), (double)ct.size_bytes()};
+}
+
+// make_system's plan (protocol.cpp:255-287): dynamic_lp when k == 0 (tmp
+// keys {1, 2} from derive_seed(seed, kTagTmpKeys)-like streams; any seed
+// works: calibration only times), else fixed k.
+HoistPlan make_plan(const CkksContext& ctx, const Opts& o, std::size_t width, Calib* cal) {
+  if (o.k != 0) {
+    HoistPlan plan = fixed_plan(HoistMode::off, width);
+    plan.k = o.k;
+    return plan;
+  }
+  Sampler tmp_rng(derive_seed(o.seed, 0x7A11u));
+  const KeyBundle probe = ctx.generate_keys(tmp_rng, {1, 2});
+  Sampler calib_rng(derive_seed(o.seed, 0xCA11u));
+  const Calib c = calibrate_ref(ctx, probe, calib_rng);
+  if (cal) *cal = c;
+  return plan_unfold(c.t_hoist, c.t_decompose, c.m_cipher, o.budget_mb * 1048576.0, width);
+}
+
 struct System {
   std::unique_ptr<CkksContext> ctx;
   HoistPlan plan;
+  Calib calib{0, 0, 0};
   KeyBundle keys;
   std::vector<std::size_t> steps;
   std::vector<PackedWeights> packed;
@@ -156,15 +227,41 @@ System setup(const Opts& o) {
   s.ctx = std::make_unique<CkksContext>(p);
   const CkksContext& ctx = *s.ctx;
   const std::size_t width = std::bit_ceil(std::min(o.dim, ctx.slot_count()));
-  // make_system with a fixed unfold factor (protocol.cpp:255-287).
-  s.plan = fixed_plan(HoistMode::off, width);
-  s.plan.k = o.k;
-  s.steps = slot_reduce_steps(width, o.k);
+  // make_system (protocol.cpp:255-287): a fixed unfold factor, or the
+  // calibrated plan; no rotation keys when slot sums are left to the KGC.
+  s.plan = make_plan(ctx, o, width, &s.calib);
+  s.steps = o.reduce ? slot_reduce_steps(width, s.plan.k) : std::vector<std::size_t>{};
+  if (s.steps.size() > 512) throw CapacityError("unfold plan needs more than 512 rotation keys");
   Sampler key_rng(derive_seed(o.seed, 5));
   s.keys = ctx.generate_keys(key_rng, s.steps);
   // measure_distance_phase input generation (cli.cpp:316-329).
   Sampler rng(derive_seed(o.seed, 0xAB1A7Eu));
   s.packed.resize(o.clients);
+  if (o.uniform) {
+    const std::size_t C = chunk_count_for(o.dim, ctx.slot_count());
+    // one Sampler per client, filled on worker threads (setup only)
+    s.mask.n = o.clients;
+    s.mask.l = o.select.size();
+    s.mask.client_selectors.resize(o.clients);
+    parallel_for(o.clients, [&](std::size_t i) {
+      Sampler crng(derive_seed(o.seed, 0xAB1A7Eu + 1 + i));
+      auto uniform_ct = [&]() {
+        Ciphertext c;
+        c.c0 = PolyRns(ctx.basis(), ctx.basis()->prime_count(), false, Domain::evaluation);
+        c.c1 = c.c0;
+        crng.uniform_poly(c.c0);
+        crng.uniform_poly(c.c1);
+        c.scale = ctx.scale();
+        return c;
+      };
+      s.packed[i].dimension = o.dim;
+      s.packed[i].prescale = 1.0;
+      s.packed[i].chunks.reserve(C);
+      for (std::size_t ch = 0; ch < C; ++ch) s.packed[i].chunks.push_back(uniform_ct());
+      s.mask.client_selectors[i] = uniform_ct();
+    });
+    return s;
+  }
   for (std::size_t i = 0; i < o.clients; ++i) {
     std::vector<double> w(o.dim);
     for (double& x : w) x = rng.uniform_real() - 0.5;
@@ -197,11 +294,11 @@ int cmd_gen(const Opts& o) {
 
   DistanceOptions dopt;
   dopt.lazy_relin = o.lazy;
-  dopt.reduce_on_server = true;
+  dopt.reduce_on_server = o.reduce;
   ctx.counters().reset();
   const EncryptedDistanceMatrix m =
       build_distance_matrix(ctx, s.packed, s.keys.relin, s.plan,
-                            DistanceMode::per_pair, s.keys.rotations, dopt);
+                            mode_of(o.mode), s.keys.rotations, dopt);
   const OpCounts dist_ops = ctx.counters().snapshot();
   ctx.counters().reset();
   const PackedWeights agg =
@@ -220,6 +317,8 @@ int cmd_gen(const Opts& o) {
   for (std::size_t i = 0; i <= b.prime_count(); ++i)
     js << (i ? ", " : "") << b.tables_or_special(i).psi;
   js << "],\n";
+  js << "  \"mode\": \"" << o.mode << "\", \"reduced\": " << (m.reduced ? "true" : "false")
+     << ", \"value_scale\": " << dbl(m.value_scale) << ",\n";
   js << "  \"width\": " << s.plan.n << ", \"k\": " << s.plan.k << ", \"steps\": [";
   for (std::size_t i = 0; i < s.steps.size(); ++i) js << (i ? ", " : "") << s.steps[i];
   js << "],\n  \"rot_keys\": [";
@@ -317,13 +416,16 @@ int cmd_bench(const Opts& o) {
   const CkksContext& ctx = *s.ctx;
   DistanceOptions dopt;
   dopt.lazy_relin = o.lazy;
-  dopt.reduce_on_server = true;
-  std::printf("{\"setup_s\": %.3f, \"threads\": %zu, \"reps\": [", setup_s, worker_count());
+  dopt.reduce_on_server = o.reduce;
+  std::printf("{\"setup_s\": %.3f, \"threads\": %zu, \"k\": %zu, \"t_hoist\": %.6g, "
+              "\"t_decompose\": %.6g, \"m_cipher\": %.0f, \"reps\": [",
+              setup_s, worker_count(), s.plan.k, s.calib.t_hoist, s.calib.t_decompose,
+              s.calib.m_cipher);
   for (std::size_t r = 0; r < o.reps; ++r) {
     const auto a = std::chrono::steady_clock::now();
     const EncryptedDistanceMatrix m =
         build_distance_matrix(ctx, s.packed, s.keys.relin, s.plan,
-                              DistanceMode::per_pair, s.keys.rotations, dopt);
+                              mode_of(o.mode), s.keys.rotations, dopt);
     const auto b = std::chrono::steady_clock::now();
     const PackedWeights agg =
         masked_aggregate(ctx, s.packed, s.mask, rule_of(o.rule), s.keys.relin);
@@ -439,6 +541,27 @@ int cmd_keygen(const Opts& o) {
   return 0;
 }
 
+// calibrate() + plan_unfold for ring degree N and a dim-parameter model
+// (make_system with HoistMode::dynamic_lp, protocol.cpp:255-287).
+int cmd_calibrate(const Opts& o) {
+  CkksParams p;
+  p.ring_degree = o.N;
+  p.depth = o.depth;
+  p.security = o.secure ? SecurityLevel::bits128 : SecurityLevel::none;
+  const CkksContext ctx(p);
+  const std::size_t width = std::bit_ceil(std::min(o.dim, ctx.slot_count()));
+  Opts d = o;
+  d.k = 0;
+  Calib c{0, 0, 0};
+  const HoistPlan plan = make_plan(ctx, d, width, &c);
+  std::printf("{\"N\": %zu, \"width\": %zu, \"t_hoist\": %.9g, \"t_decompose\": %.9g, "
+              "\"m_cipher\": %.0f, \"budget_mb\": %g, \"k\": %zu, \"cost\": %.9g, "
+              "\"keys\": %zu}\n",
+              o.N, width, c.t_hoist, c.t_decompose, c.m_cipher, o.budget_mb, plan.k, plan.cost,
+              slot_reduce_steps(width, plan.k).size());
+  return 0;
+}
+
 }  // namespace
 
 int main(int argc, char** argv) {
@@ -449,6 +572,7 @@ int main(int argc, char** argv) {
     if (o.cmd == "ops") return cmd_ops(o);
     if (o.cmd == "encrypt") return cmd_encrypt(o);
     if (o.cmd == "keygen") return cmd_keygen(o);
+    if (o.cmd == "calibrate") return cmd_calibrate(o);
     std::fprintf(stderr, "unknown command %s\n", o.cmd.c_str());
     return 2;
   } catch (const std::exception& e) {

@@ -14,7 +14,8 @@ CSRC = os.path.join(HERE, "csrc")
 OUT_DIR = os.path.join(HERE, "_lib")
 LIB = os.path.join(OUT_DIR, "liblancelot_b200.so")
 SOURCES = ["engine.cu"]
-HEADERS = ["common.cuh", "ntt.cuh", "kernels.cuh"]
+# every header engine.cu includes (globbed, so a new .cuh cannot be missed)
+HEADERS = sorted(f for f in os.listdir(CSRC) if f.endswith(".cuh"))
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",

@@ -293,6 +293,8 @@ struct lcl_context {
   cudaEvent_t fork_ev = nullptr;
   bool in_lane = false;  // work is being enqueued on a lane: no nested lanes
   DevBuf ws_io_in, ws_io_sel, ws_io_dist, ws_io_agg, ws_dtern, ws_atern, ws_ptl, ws_enc, ws_enc_in;
+  DevBuf ws_cal;   // calibrate()'s two rotated ciphertexts
+  DevBuf ws_rows;  // DistanceMode::row_sums: the unreduced pair ciphertexts
   // masked_aggregate's encode(1/l) plaintext, NTT'd on the device once per l
   size_t pt_l = 0;
   std::vector<u64> pt_host;
@@ -1698,6 +1700,40 @@ void distance_matrix(lcl_context* c, const u64* clients, u32 n, u32 chunks, size
   }
 }
 
+void check_width(const lcl_context* c, size_t width) {
+  if (width == 0 || (width & (width - 1))) fail(LCL_WIDTH_ERROR, "reduction width must be a power of two");
+  if (width > c->n / 2) fail(LCL_WIDTH_ERROR, "reduction width exceeds the slot count");
+}
+
+// build_distance_matrix, DistanceMode::row_sums (distance.cpp:257-298): the
+// pair distances are computed without a per-pair reduction (reduce_pairs is
+// false in this mode), row i = the hadd chain of the n - 1 pairs containing
+// client i (one launch for all rows), then one slot_reduce per row when
+// reduce_on_server. out: [n][2][full-1][N].
+void distance_rows(lcl_context* c, const u64* clients, u32 n, u32 chunks, size_t width, size_t k,
+                   bool lazy, bool reduce, u64* out) {
+  if (n < 2) fail(LCL_SHAPE_ERROR, "pairwise distances need at least two clients");
+  if (reduce) {
+    check_width(c, width);
+    if (k == 0) fail(LCL_PARAMETER_ERROR, "unfold factor starts at 1");
+  }
+  const u32 m = c->full;
+  if (m < 2) fail(LCL_DEPTH_EXHAUSTED, "no prime left to rescale by");
+  const u64 N = c->N();
+  const u64 P = (u64)n * (n - 1) / 2;
+  const u64 W = 2ull * (m - 1) * N;
+  u64* pairs = c->ws_rows.get(P * W);
+  distance_matrix(c, clients, n, chunks, width, k, lazy, false, pairs);
+  {
+    ProfScope ps(c, "pair_row_sums", 8.0 * W * ((double)n * (n - 1) + n));
+    const dim3 grid((u32)((W / 2 + 255) / 256), n);
+    pair_row_sums<<<grid, 256, 0, c->stream>>>(pairs, n, m - 1, c->logn, out, c->d_primes);
+    post_launch(c);
+  }
+  c->counts.additions += (u64)n * (n - 2);
+  if (reduce) slot_reduce_batch(c, out, n, m - 1, width, k, out);
+}
+
 // Chunks [chunk_begin, chunk_end) of the aggregate (a shard when the chunks
 // are split across GPUs); out holds just that range.
 // encode(1/l at scale, level of the rescaled chunk) on the host
@@ -1789,6 +1825,33 @@ void masked_aggregate(lcl_context* c, const u64* clients, const u64* sel, u32 n,
     agg_finish(c, tern, B, average, d_pt, out + (u64)(c0 - chunk_begin) * 2 * mo * N);
     c->counts.multiplications += (u64)n * B;
     c->counts.additions += (u64)(n - 1) * B;
+  }
+}
+
+// CkksContext::hoisted_rotations (ckks.cpp:582-612) over B ciphertexts:
+// one decomposition shared by every step; outs [nsteps][B][2][m][N].
+void hoisted_batch(lcl_context* ctx, const u64* d_ct, u32 B, u32 m, const size_t* h_steps,
+                   size_t nsteps, u64* d_outs) {
+  const u64 N = ctx->N();
+  const u64 words = (u64)B * 2 * m * N;
+  u64* dig = nullptr;
+  for (size_t s = 0; s < nsteps; ++s) {
+    const size_t st = norm_step(ctx, h_steps[s]);
+    u64* o = d_outs + s * words;
+    if (st == 0) {
+      cuda_check(cudaMemcpyAsync(o, d_ct, words * 8, cudaMemcpyDeviceToDevice, ctx->stream), "copy");
+      continue;
+    }
+    const u64* key = rot_key(ctx, st);
+    if (!dig) {
+      const RowMap c1 = make_map(d_ct + (u64)m * N, m, N, 2ull * m * N, 1, 0, ctx->primes_0(m));
+      dig = ks_decompose(ctx, c1, B, m);
+      ctx->counts.mod_ups += B;
+    }
+    u64* acc = ks_ip(ctx, dig, B, m, key, ctx->d_perm.at(st));
+    ks_moddown(ctx, acc, B, m, ct_map(o, m, N, 2ull * m * N), null_map(),
+               ct_map(d_ct, m, N, 2ull * m * N), ctx->d_perm.at(st));
+    ctx->counts.rotations += B;
   }
 }
 
@@ -1977,7 +2040,7 @@ void free_context(lcl_context* c) {
   for (DevBuf* b : {&c->ws_coef, &c->ws_digits, &c->ws_acc, &c->ws_coefsp, &c->ws_mid,
                     &c->ws_tern, &c->ws_ctA, &c->ws_ctB, &c->ws_ctC, &c->ws_pt, &c->ws_c1inv, &c->ws_io_in,
                     &c->ws_io_sel, &c->ws_io_dist, &c->ws_io_agg, &c->ws_dtern, &c->ws_atern,
-                    &c->ws_ptl,
+                    &c->ws_ptl, &c->ws_rows, &c->ws_cal,
                     &c->ws_enc, &c->ws_enc_in})
     b->release();
   for (void* p : {(void*)c->d_twist, (void*)c->d_roots, (void*)c->d_brv, (void*)c->d_slot})
@@ -2380,28 +2443,46 @@ int lcl_hoisted_rotations(lcl_context* ctx, const uint64_t* d_ct, size_t batch, 
                           const size_t* h_steps, size_t nsteps, uint64_t* d_outs) {
   return guarded([&] {
     check_count(ctx, count);
-    const u32 B = (u32)batch, m = (u32)count;
-    const u64 N = ctx->N();
-    const u64 words = (u64)B * 2 * m * N;
-    u64* dig = nullptr;
-    for (size_t s = 0; s < nsteps; ++s) {
-      const size_t st = norm_step(ctx, h_steps[s]);
-      u64* o = d_outs + s * words;
-      if (st == 0) {
-        cuda_check(cudaMemcpyAsync(o, d_ct, words * 8, cudaMemcpyDeviceToDevice, ctx->stream), "copy");
-        continue;
+    hoisted_batch(ctx, d_ct, (u32)batch, (u32)count, h_steps, nsteps, d_outs);
+  });
+}
+
+int lcl_calibrate(lcl_context* ctx, const uint64_t* d_ct, size_t count, double* t_hoist,
+                  double* t_decompose, double* m_cipher) {
+  return guarded([&] {
+    check_count(ctx, count);
+    need(lcl_has_rotation_key(ctx, 1) && lcl_has_rotation_key(ctx, 2), LCL_KEY_ERROR,
+         "calibration needs rotation keys for steps 1 and 2");
+    const u32 m = (u32)count;
+    const u64 words = 2ull * m * ctx->N();
+    u64* outs = ctx->ws_cal.get(2 * words);
+    cudaEvent_t a, b;
+    cuda_check(cudaEventCreate(&a), "event");
+    cuda_check(cudaEventCreate(&b), "event");
+    // median of 11 device-timed calls (protocol.cpp:232-243)
+    auto median_time = [&](const std::vector<size_t>& steps) {
+      std::vector<double> t;
+      for (int rep = 0; rep < 11; ++rep) {
+        cuda_check(cudaEventRecord(a, ctx->stream), "record");
+        hoisted_batch(ctx, d_ct, 1, m, steps.data(), steps.size(), outs);
+        cuda_check(cudaEventRecord(b, ctx->stream), "record");
+        cuda_check(cudaEventSynchronize(b), "sync");
+        float ms = 0;
+        cuda_check(cudaEventElapsedTime(&ms, a, b), "elapsed");
+        t.push_back(ms * 1e-3);
       }
-      const u64* key = rot_key(ctx, st);
-      if (!dig) {
-        const RowMap c1 = make_map(d_ct + (u64)m * N, m, N, 2ull * m * N, 1, 0, ctx->primes_0(m));
-        dig = ks_decompose(ctx, c1, B, m);
-        ctx->counts.mod_ups += B;
-      }
-      u64* acc = ks_ip(ctx, dig, B, m, key, ctx->d_perm.at(st));
-      ks_moddown(ctx, acc, B, m, ct_map(o, m, N, 2ull * m * N), null_map(),
-                 ct_map(d_ct, m, N, 2ull * m * N), ctx->d_perm.at(st));
-      ctx->counts.rotations += B;
-    }
+      std::sort(t.begin(), t.end());
+      return t[t.size() / 2];
+    };
+    const double t1 = median_time({1});
+    const double t2 = median_time({1, 2});
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    // the reference's naming (protocol.cpp:249-250): t_hoist = decompose +
+    // first rotation, t_decompose = the marginal hoisted rotation
+    if (t_hoist) *t_hoist = std::max(t1, 1e-9);
+    if (t_decompose) *t_decompose = std::max(t2 - t1, 1e-9);
+    if (m_cipher) *m_cipher = (double)(words * 8);  // Ciphertext::size_bytes
   });
 }
 
@@ -2542,6 +2623,22 @@ int lcl_distance_matrix(lcl_context* ctx, const uint64_t* d_clients, size_t n, s
   return guarded([&] {
     need(chunks >= 1, LCL_SHAPE_ERROR, "empty weight vector");
     distance_matrix(ctx, d_clients, (u32)n, (u32)chunks, width, k, lazy != 0, reduce != 0, d_out);
+    if (out_scale) *out_scale = (in_scale * in_scale) / (double)ctx->primes[ctx->full - 1];
+  });
+}
+
+int lcl_build_distance_matrix(lcl_context* ctx, const uint64_t* d_clients, size_t n,
+                              size_t chunks, double in_scale, size_t width, size_t k, int mode,
+                              int lazy, int reduce_on_server, uint64_t* d_out, double* out_scale) {
+  return guarded([&] {
+    need(chunks >= 1, LCL_SHAPE_ERROR, "empty weight vector");
+    need(mode == LCL_PER_PAIR || mode == LCL_ROW_SUMS, LCL_USAGE_ERROR, "unknown distance mode");
+    if (mode == LCL_PER_PAIR)
+      distance_matrix(ctx, d_clients, (u32)n, (u32)chunks, width, k, lazy != 0,
+                      reduce_on_server != 0, d_out);
+    else
+      distance_rows(ctx, d_clients, (u32)n, (u32)chunks, width, k, lazy != 0,
+                    reduce_on_server != 0, d_out);
     if (out_scale) *out_scale = (in_scale * in_scale) / (double)ctx->primes[ctx->full - 1];
   });
 }

@@ -528,6 +528,34 @@ __global__ void __launch_bounds__(256)
 }
 
 // ------------------------------------------------------------------------
+// DistanceMode::row_sums (distance.cpp:287-298): row i of the matrix is the
+// sum of the n - 1 pair ciphertexts that contain client i. pairs: [P][W]
+// words in (i<j) row-major order, W = 2 m N; rows: [n][W]. Modular addition
+// is exact, so the sum equals the reference's left-to-right hadd chain word
+// for word. Two 64-bit words per thread (128-bit loads and stores).
+__global__ void __launch_bounds__(256)
+    pair_row_sums(const u64* __restrict__ pairs, u32 n, u32 m, u32 logn, u64* __restrict__ rows,
+                  const PrimeConst* __restrict__ primes) {
+  const u64 W = 2ull * m << logn;
+  const u64 gid = ((u64)blockIdx.x * blockDim.x + threadIdx.x) * 2;
+  const u32 i = blockIdx.y;
+  if (gid >= W) return;
+  const u32 limb = (u32)((gid >> logn) % m);
+  const u64 q = primes[limb].q;
+  u64 a0 = 0, a1 = 0;
+  for (u32 o = 0; o < n; ++o) {
+    if (o == i) continue;
+    const u32 lo = o < i ? o : i, hi = o < i ? i : o;
+    // index of (lo, hi) in the row-major i<j order
+    const u64 p = (u64)lo * (2ull * n - lo - 1) / 2 + (hi - lo - 1);
+    const ulonglong2 v = __ldg(reinterpret_cast<const ulonglong2*>(pairs + p * W + gid));
+    a0 = add_mod(a0, v.x, q);
+    a1 = add_mod(a1, v.y, q);
+  }
+  *reinterpret_cast<ulonglong2*>(rows + (u64)i * W + gid) = make_ulonglong2(a0, a1);
+}
+
+// ------------------------------------------------------------------------
 // ct x pt (ckks.cpp:549-558): out[b][x][i][a] = ct[b][x][i][a] * pt[i][a].
 __global__ void __launch_bounds__(256)
     mult_plain(const u64* __restrict__ ct, const u64* __restrict__ pt, u32 B, u32 m, u32 logn,

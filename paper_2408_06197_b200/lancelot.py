@@ -160,6 +160,10 @@ def lib():
         "lcl_pairwise_distance": [_P, _P, _P, _SZ, C.c_int, _P],
         "lcl_distance_matrix": [_P, _P, _SZ, _SZ, C.c_double, _SZ, _SZ, C.c_int, C.c_int, _P,
                                 C.POINTER(C.c_double)],
+        "lcl_calibrate": [_P, _P, _SZ, C.POINTER(C.c_double), C.POINTER(C.c_double),
+                          C.POINTER(C.c_double)],
+        "lcl_build_distance_matrix": [_P, _P, _SZ, _SZ, C.c_double, _SZ, _SZ, C.c_int, C.c_int,
+                                      C.c_int, _P, C.POINTER(C.c_double)],
         "lcl_masked_aggregate": [_P, _P, _P, _SZ, _SZ, C.c_double, C.c_double, _SZ, C.c_int, _P,
                                  C.POINTER(C.c_double)],
         "lcl_server_round_host": [_P, _P, _P, _SZ, _SZ, C.c_double, _SZ, _SZ, _SZ, C.c_int, _P,
@@ -709,6 +713,28 @@ def plan_unfold(t_hoist, t_decompose, m_cipher, m_budget, n) -> HoistPlan:
     return plan
 
 
+@dataclass
+class Calibration:
+    """protocol.hpp:256-260 (the reference's field naming)."""
+    t_hoist: float = 0.0      # seconds: decompose + first rotation (t1)
+    t_decompose: float = 0.0  # seconds: one more hoisted rotation (t2 - t1)
+    m_cipher: float = 0.0     # bytes per ciphertext
+
+
+def calibrate(ctx: CkksContext, keys: RotationKeySet, ct: Ciphertext) -> Calibration:
+    """calibrate (protocol.cpp:224-253) timed on the device: median of 11
+    hoisted_rotations(ct, {1}) and ({1, 2}) calls (lcl_calibrate). `ct` is a
+    fresh ciphertext (the reference encrypts 0.5 in every slot; every kernel
+    is data-oblivious, so any fresh ciphertext times the same)."""
+    if not (keys.has_step(1) and keys.has_step(2)):
+        raise KeyError("calibration needs rotation keys for steps 1 and 2")
+    ctx.use_rotation_keys(keys, [1, 2])
+    th, td, mc = C.c_double(), C.c_double(), C.c_double()
+    _check(lib().lcl_calibrate(ctx.h, _ptr(ct.data.contiguous()), ct.level() + 1, C.byref(th),
+                               C.byref(td), C.byref(mc)))
+    return Calibration(th.value, td.value, mc.value)
+
+
 def fixed_plan(mode: HoistMode, n: int) -> HoistPlan:
     _require_width(n)
     levels = n.bit_length() - 1
@@ -768,9 +794,16 @@ def stack_clients(all_weights):
     base = all_weights[0].chunks
     try:
         parent = base._base
-        if parent is not None and parent.dim() == 5 and parent.shape[0] == len(all_weights):
-            if all(w.chunks.data_ptr() == parent[i].data_ptr() for i, w in enumerate(all_weights)):
-                return parent
+        # zero-copy only when the parent IS the [n][C][2][full][N] batch: a
+        # view of a prefix slice (big[:, :C']) or of fewer limbs has the
+        # same data pointers but strides clients by the parent's shape
+        if (parent is not None and parent.dim() == 5 and parent.shape[0] == len(all_weights)
+                and parent.is_contiguous() and parent.dtype == base.dtype
+                and tuple(parent.shape[1:]) == tuple(base.shape)
+                and all(w.chunks.data_ptr() == parent[i].data_ptr()
+                        and tuple(w.chunks.shape) == tuple(base.shape)
+                        for i, w in enumerate(all_weights))):
+            return parent
     except AttributeError:
         pass
     return torch.stack([w.chunks for w in all_weights]).contiguous()
@@ -794,7 +827,6 @@ def build_distance_matrix(ctx: CkksContext, all_weights, rk: RelinKey, plan: Hoi
         if plan.n < (1 << (needed - 1).bit_length()):
             raise WidthError("plan width misses populated slots")
     ctx.use_relin_key(rk)
-    reduce_pairs = options.reduce_on_server and mode == DistanceMode.per_pair
     if options.reduce_on_server:
         _require_width(plan.n)
         if plan.n > ctx.slot_count():
@@ -807,25 +839,17 @@ def build_distance_matrix(ctx: CkksContext, all_weights, rk: RelinKey, plan: Hoi
     m = ctx.full
     N = ctx.params().ring_degree
     pairs = [(i, j) for i in range(n) for j in range(i + 1, n)]
-    out = ctx._empty(len(pairs), 2, m - 1, N)
+    per_pair = mode == DistanceMode.per_pair
+    out = ctx._empty(len(pairs) if per_pair else n, 2, m - 1, N)
     osc = C.c_double()
-    _check(lib().lcl_distance_matrix(ctx.h, _ptr(clients), n, C_, all_weights[0].scale,
-                                     plan.n, plan.k, 1 if options.lazy_relin else 0,
-                                     1 if reduce_pairs else 0, _ptr(out), C.byref(osc)))
+    _check(lib().lcl_build_distance_matrix(
+        ctx.h, _ptr(clients), n, C_, all_weights[0].scale, plan.n, plan.k,
+        0 if per_pair else 1, 1 if options.lazy_relin else 0,
+        1 if options.reduce_on_server else 0, _ptr(out), C.byref(osc)))
     value_scale = all_weights[0].prescale * all_weights[0].prescale
-    if mode == DistanceMode.per_pair:
-        return EncryptedDistanceMatrix(mode, n, options.reduce_on_server, value_scale, out, pairs,
-                                       osc.value)
-    rows = ctx._empty(n, 2, m - 1, N)
-    for i in range(n):
-        idx = [p for p, (a, b) in enumerate(pairs) if a == i or b == i]
-        rows[i].copy_(out[idx[0]])
-        for p in idx[1:]:
-            _check(lib().lcl_hadd(ctx.h, _ptr(rows[i]), _ptr(out[p]), 1, m - 1, _ptr(rows[i])))
-    if options.reduce_on_server and plan.n > 1:
-        _check(lib().lcl_slot_reduce(ctx.h, _ptr(rows), n, m - 1, plan.n, plan.k, _ptr(rows)))
-    return EncryptedDistanceMatrix(mode, n, options.reduce_on_server, value_scale, rows,
-                                   [(i, i) for i in range(n)], osc.value)
+    keys_ = pairs if per_pair else [(i, i) for i in range(n)]
+    return EncryptedDistanceMatrix(mode, n, options.reduce_on_server, value_scale, out, keys_,
+                                   osc.value)
 
 
 def masked_aggregate(ctx: CkksContext, weights, mask: SelectionMask, rule: SelectionRule,

@@ -43,6 +43,16 @@ CONFIGS = {
                           secure=1, lazy=1),
     "n17_hoist": dict(N=131072, clients=3, dim=140000, k=2, rule="krum", select="1", secure=1,
                       lazy=1),
+    # DistanceMode::row_sums and reduce_on_server = false (slot sums left to
+    # the KGC, protocol.cpp:555): the other build_distance_matrix branches
+    "tiny_rowsums": dict(N=256, clients=4, dim=300, k=2, rule="krum", select="0", secure=0,
+                         lazy=1, mode="row_sums", reduce=1),
+    "tiny_rowsums_kgc": dict(N=512, clients=5, dim=700, k=1, rule="krum", select="3", secure=0,
+                             lazy=1, mode="row_sums", reduce=0),
+    "tiny_perpair_kgc": dict(N=512, clients=5, dim=700, k=1, rule="multi_krum", select="0,3",
+                             secure=0, lazy=1, mode="per_pair", reduce=0),
+    "n13_rowsums": dict(N=8192, clients=5, dim=10000, k=3, rule="krum", select="1", secure=1,
+                        lazy=1, mode="row_sums", reduce=1),
 }
 
 

@@ -43,10 +43,27 @@ class Rig:
         self.rule = o["rule"]
         self.selected = [int(x) for x in str(o["select"]).split(",")]
         self.average = self.rule == "multi_krum" and len(self.selected) > 1
+        self.mode = o.get("mode", "per_pair")
+        self.reduce = bool(o.get("reduce", 1))
         self.oracle = Oracle(self.N, secure=bool(o["secure"]), threads=threads)
         self.width = width_for(self.dim, self.N)
-        self.steps = slot_reduce_steps(self.width, self.k)
+        # make_system: no rotation keys when the KGC sums the slots
+        self.steps = slot_reduce_steps(self.width, self.k) if self.reduce else []
         self.oracle.keygen(1, self.steps)
         self.clients = self.oracle.make_clients(1, self.n, self.dim)
         self.selectors = self.oracle.build_mask(1, self.selected, self.n)
         self.C = self.clients.shape[1]
+
+    def dist_keys(self):
+        """Matrix entry keys in the reference's std::map order."""
+        if self.mode == "row_sums":
+            return [(i, i) for i in range(self.n)]
+        return [(i, j) for i in range(self.n) for j in range(i + 1, self.n)]
+
+    def plain_entries(self):
+        """Plaintext slot totals per matrix entry (row sums add the pairs)."""
+        pd = self.meta["plain_dist"]
+        if self.mode != "row_sums":
+            return pd
+        pairs = [(i, j) for i in range(self.n) for j in range(i + 1, self.n)]
+        return [sum(v for (a, b), v in zip(pairs, pd) if i in (a, b)) for i in range(self.n)]

@@ -163,6 +163,63 @@ def test_distance_matrix_bit_exact_vs_reference(golden):
     assert dm.value_scale == 1.0
 
 
+MODE_GOLDEN = ["tiny_rowsums", "tiny_rowsums_kgc", "tiny_perpair_kgc", "n13_rowsums"]
+
+
+@pytest.mark.parametrize("name", MODE_GOLDEN)
+def test_distance_modes_bit_exact_vs_reference(name):
+    """build_distance_matrix's other branches through lcl_build_distance_matrix:
+    DistanceMode::row_sums (one device row-sum launch, then slot_reduce per
+    row) and reduce_on_server = false (slot sums left to the KGC), against
+    the reference's digests, op counters, scale and `reduced` flag."""
+    L = _L()
+    rig = Rig(name, threads=8)
+    ctx = gpu_ctx(rig.N, secure=bool(rig.meta["options"]["secure"]))
+    rk = L.RelinKey(rig.oracle.relin_key())
+    keys = L.RotationKeySet({s: rig.oracle.rotation_key(s) for s in rig.meta["rot_keys"]})
+    mode = L.DistanceMode.row_sums if rig.mode == "row_sums" else L.DistanceMode.per_pair
+    ctx.reset_counters()
+    dm = L.build_distance_matrix(ctx, _packed(L, rig), rk, L.HoistPlan(k=rig.k, n=rig.width),
+                                 mode, keys, L.DistanceOptions(lazy_relin=rig.lazy,
+                                                               reduce_on_server=rig.reduce))
+    got = L.to_host(dm.batch)
+    assert list(dm.keys) == rig.dist_keys()
+    for p, (i, j) in enumerate(dm.keys):
+        assert sha(got[p]) == rig.meta["sha256"][f"dist_{i}_{j}"], (i, j)
+    assert ctx.counters() == rig.meta["dist_ops"]
+    assert dm.reduced == rig.meta["reduced"]
+    assert dm.scale == rig.meta["dist"][0]["scale"]
+    if rig.reduce:  # slot 0 holds the total: the reference's decryption
+        sk = L.SecretKey(rig.oracle.secret_key())
+        vals = ctx.decrypt_values_batch(dm.batch, dm.scale, sk).cpu().numpy()
+        for p, e in enumerate(rig.meta["dist"]):
+            assert vals[p][0] == e["slot0"], p
+
+
+@pytest.mark.parametrize("name,lazy", [("tiny_krum", True), ("cfg1", True), ("tiny_eager", False)])
+def test_pairwise_distance_entry(name, lazy):
+    """lcl_pairwise_distance (encrypted_pairwise_distance, distance.cpp:107-142)
+    for clients 0 and 1: the lazy result is the reference's p01_rescale
+    intermediate; the eager one equals the oracle's."""
+    L = _L()
+    rig = Rig(name, threads=8)
+    ctx = gpu_ctx(rig.N, secure=bool(rig.meta["options"]["secure"]))
+    pw = _packed(L, rig)
+    ctx.reset_counters()
+    ct = L.encrypted_pairwise_distance(ctx, pw[0], pw[1], L.RelinKey(rig.oracle.relin_key()),
+                                       lazy=lazy)
+    got = L.to_host(ct.data)
+    if lazy:
+        assert sha(got) == rig.meta["sha256"]["p01_rescale"]
+    else:
+        assert np.array_equal(got, rig.oracle.pairwise_distance(rig.clients[0], rig.clients[1],
+                                                                lazy=False))
+    c = ctx.counters()
+    assert c["multiplications"] == rig.C
+    assert c["relinearizations"] == (1 if lazy else rig.C)
+    assert ct.scale == rig.meta["dist"][0]["scale"]
+
+
 def test_masked_aggregate_bit_exact_vs_reference(golden):
     L = _L()
     rig = golden

@@ -143,3 +143,23 @@ def test_sampler_stream_and_derive_seed():
     want = [(mt() >> 11) * 2.0 ** -53 for _ in range(1000)]
     got = L.Sampler(seed).uniform_real(1000)
     assert list(got) == want
+
+
+def test_stack_clients_zero_copy_only_for_the_whole_batch():
+    """views of a prefix slice share data pointers with the parent
+    but must not be returned as the batch (clients would be strided by the
+    parent's chunk count)."""
+    import torch
+
+    big = torch.empty(3, 5, 2, 2, 4, dtype=torch.int64)
+    big.copy_(torch.arange(big.numel()).reshape(big.shape))
+    whole = [L.PackedWeights(big[i], 10, 1.0, 1.0) for i in range(3)]
+    assert L.stack_clients(whole).data_ptr() == big.data_ptr()  # zero copy
+    pre = big[:, :2]
+    part = [L.PackedWeights(pre[i], 4, 1.0, 1.0) for i in range(3)]
+    got = L.stack_clients(part)
+    assert tuple(got.shape) == (3, 2, 2, 2, 4)
+    assert torch.equal(got, pre)
+    limbs = big[:, :, :, :1]
+    lv = [L.PackedWeights(limbs[i], 10, 1.0, 1.0) for i in range(3)]
+    assert torch.equal(L.stack_clients(lv), limbs)

@@ -10,7 +10,8 @@ import pytest
 from tests.golden_util import Rig, sha
 
 SMALL = ["tiny_krum", "tiny_hoist_multikrum", "tiny_eager", "tiny_fullhoist", "cfg1",
-         "n16_multikrum", "n17_hoist"]
+         "n16_multikrum", "n17_hoist", "tiny_rowsums", "tiny_rowsums_kgc", "tiny_perpair_kgc",
+         "n13_rowsums"]
 
 
 @pytest.fixture(scope="module", params=SMALL)
@@ -25,6 +26,7 @@ def test_basis_matches_reference(rig):
     assert rig.oracle.psi == m["psi"]
     assert rig.width == m["width"]
     assert rig.steps == m["steps"]
+    assert m.get("mode", "per_pair") == rig.mode and m.get("reduced", True) == rig.reduce
     assert rig.C == m["chunks"]
 
 
@@ -43,13 +45,11 @@ def test_keys_and_inputs_match_reference(rig):
 def test_distance_matrix_matches_reference(rig):
     o = rig.oracle
     o.reset_counts()
-    dm = o.distance_matrix(rig.clients, rig.width, rig.k, lazy=rig.lazy)
+    f = o.distance_rows if rig.mode == "row_sums" else o.distance_matrix
+    dm = f(rig.clients, rig.width, rig.k, lazy=rig.lazy, reduce=rig.reduce)
     assert o.counts() == rig.meta["dist_ops"]
-    p = 0
-    for i in range(rig.n):
-        for j in range(i + 1, rig.n):
-            assert sha(dm[p]) == rig.meta["sha256"][f"dist_{i}_{j}"], (i, j)
-            p += 1
+    for p, (i, j) in enumerate(rig.dist_keys()):
+        assert sha(dm[p]) == rig.meta["sha256"][f"dist_{i}_{j}"], (i, j)
 
 
 def test_aggregate_matches_reference(rig):
@@ -86,7 +86,9 @@ def test_decrypted_distances_track_plaintext(rig):
     """Reference tolerance: decrypted distances within rel 1e-3 of plaintext
     (test_distance.cpp:361-385)."""
     m = rig.meta
-    for e, plain in zip(m["dist"], m["plain_dist"]):
+    if not rig.reduce:
+        pytest.skip("unreduced: slot 0 holds one coordinate, not the total")
+    for e, plain in zip(m["dist"], rig.plain_entries()):
         assert abs(e["slot0"] - plain) <= 1e-3 * max(1.0, abs(plain))
 
 
