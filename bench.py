@@ -596,6 +596,15 @@ def profile_round(ctx, step, stream, N, m, npairs, Cc, width, n):
                      "peak": pk_peak, "unit": "Tops/s", "frac": ach / pk_peak,
                      "ops": ops, "peak_source": f"64 FP64 ops/clk/SM x {sms} SMs x 1965 MHz "
                      "(4.27 pair-slots/clk/SM = 93% of it reached by tools/microbench/pair_forms.cu)"}
+    if top["name"] == "pair_accumulate" and fp64_roof is not None:
+        # the top kernel is bound by the FP64 pipe, not HBM (its traffic is
+        # the compulsory client bytes, ~19 % of HBM at cfg3): report it against
+        # that pipe, keep the HBM view beside it
+        hbm_view = roof
+        roof = dict(fp64_roof)
+        roof.update({"bound": "fp64", "traffic": hbm_view.get("traffic"),
+                     "avg_launch_ms": hbm_view["avg_launch_ms"],
+                     "share_of_round": hbm_view["share_of_round"], "hbm_view": hbm_view})
     return {"roofline": roof, "roofline_int": int_roof, "roofline_fp64": fp64_roof,
             "kernels": kernels[:12], "peak_gbfly_s": peak.value, "peak_gbfly_s_fp64": peak_f.value}
 
@@ -657,7 +666,7 @@ def main():
                     help="skip the host-buffer round (cfg4: its 72 GB of pinned client data "
                          "exceed what a host should pin)")
     ap.add_argument("--cpu-budget-s", type=float, default=400.0)
-    ap.add_argument("--ref-budget-s", type=float, default=420.0)
+    ap.add_argument("--ref-budget-s", type=float, default=250.0)
     ap.add_argument("--k", type=int, default=None, help="fixed unfold factor (overrides the plan)")
     ap.add_argument("--budget-mb", type=float, default=None,
                     help="memory budget of the dynamic plan (overrides the config's)")

@@ -25,6 +25,9 @@
  *   lcl_*_pairs / _chunks    the same, one shard of pairs / chunks     distance.cpp:257-272,
  *                            (the reference's parallel_for ranges)     aggregation.cpp:211
  *   lcl_get_counts           OpCounters::snapshot                      ckks.cpp:134-156
+ *   lcl_deserialize          CkksContext::deserialize (LCLT ingest)    ckks.cpp:640-678
+ *   lcl_serialize            CkksContext::serialize                    ckks.cpp:614-638
+ *   lcl_server_round_lclt    run_round steps 3 + 8 from received blobs protocol.cpp:419-432
  *   lcl_pack_and_encrypt     pack_and_encrypt (client side)           distance.cpp:64-91
  *   lcl_decrypt / _decode    CkksContext::decrypt / decode (KGC side)  ckks.cpp:313-393,
  *   lcl_decrypt_values       + Embedding::coeffs_to_slots              encoding.cpp:118-134
@@ -284,6 +287,45 @@ int lcl_masked_aggregate_chunks(lcl_context* ctx, const uint64_t* d_clients,
 int lcl_server_round_host(lcl_context* ctx, const uint64_t* h_clients, const uint64_t* h_sel,
                           size_t n, size_t chunks, double in_scale, size_t width, size_t k,
                           size_t l, int average, uint64_t* h_dist, uint64_t* h_agg);
+
+/* ------------------------------------------------------------ LCLT ingest
+ * The wire format of CkksContext::serialize / deserialize (ckks.cpp:614-678)
+ * and the protocol's .lclt dumps (protocol.cpp:346-360): a 13-byte header
+ * ("LCLT", u16 version 1, u32 ring degree, u8 level, u8 scale bits, u8 limb
+ * count) followed by the c0 then c1 rows as little-endian u64. A batch of
+ * blobs of blob_bytes each sits at a fixed `stride` (>= blob_bytes) in host
+ * memory. Header checks run on the host, the residue checks (v < q_i) and
+ * the unaligned unpack on the device.
+ *
+ * lcl_deserialize  CkksContext::deserialize, batched: `count` blobs ->
+ *                  d_out [count][2][limbs][N]; *scale = 2^scale_bits. Errors
+ *                  (DataError) exactly as the reference: "not a ciphertext
+ *                  blob", "unsupported ciphertext format version", "ciphertext
+ *                  ring degree does not match the context", "ciphertext level
+ *                  inconsistent with the modulus chain", "ciphertext blob
+ *                  length mismatch", "residue outside its modulus". Blobs of
+ *                  one batch must share level (ShapeError) and scale
+ *                  (AlignmentError). Synchronises.
+ * lcl_serialize    CkksContext::serialize, batched: d_ct [count][2][limbs][N]
+ *                  at `scale` -> blobs at `stride` in h_blobs (ParameterError
+ *                  when log2(scale) rounds outside 1..255). Synchronises.
+ * lcl_server_round_lclt  lcl_server_round_host fed with the blobs the server
+ *                  receives (run_round step 3 deserializes every chunk,
+ *                  protocol.cpp:419-429): client i chunk c at h_client_blobs +
+ *                  (i * chunks + c) * stride, selector i at h_sel_blobs + i *
+ *                  stride, all fresh (top-level). The blob bytes are copied
+ *                  verbatim and unpacked on the device inside the overlapped
+ *                  H2D pipeline; *dist_scale / *agg_scale receive the output
+ *                  scales. Synchronises. */
+int lcl_deserialize(lcl_context* ctx, const uint8_t* h_blobs, size_t blob_bytes, size_t stride,
+                    size_t count, uint64_t* d_out, double* scale);
+int lcl_serialize(lcl_context* ctx, const uint64_t* d_ct, size_t count, size_t limbs,
+                  double scale, uint8_t* h_blobs, size_t stride);
+int lcl_server_round_lclt(lcl_context* ctx, const uint8_t* h_client_blobs,
+                          const uint8_t* h_sel_blobs, size_t blob_bytes, size_t stride, size_t n,
+                          size_t chunks, size_t width, size_t k, size_t l, int average,
+                          uint64_t* h_dist, uint64_t* h_agg, double* dist_scale,
+                          double* agg_scale);
 
 #ifdef __cplusplus
 }

@@ -350,6 +350,16 @@ int cmd_gen(const Opts& o) {
   }
   js << "],\n";
   {
+    // the LCLT wire bytes (CkksContext::serialize) of client 0's first chunk
+    // and of the first matrix entry, for the ingest parity tests
+    const auto b0 = ctx.serialize(s.packed[0].chunks[0]);
+    std::ofstream(d + "/lclt_client_0_0.bin", std::ios::binary)
+        .write(reinterpret_cast<const char*>(b0.data()), (std::streamsize)b0.size());
+    const auto b1 = ctx.serialize(m.entries.begin()->second);
+    std::ofstream(d + "/lclt_dist_first.bin", std::ios::binary)
+        .write(reinterpret_cast<const char*>(b1.data()), (std::streamsize)b1.size());
+  }
+  {
     std::vector<const Ciphertext*> v;
     for (const auto& c : agg.chunks) v.push_back(&c);
     dump_ct(d + "/agg.bin", v);

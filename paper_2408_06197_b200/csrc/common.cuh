@@ -13,6 +13,7 @@
 
 typedef uint64_t u64;
 typedef unsigned int u32;
+typedef uint8_t u8;
 
 #define LCL_MAXP 16  // q primes + special supported by one context
 

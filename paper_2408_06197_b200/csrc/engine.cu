@@ -272,6 +272,7 @@ struct lcl_context {
   std::map<size_t, u64*> d_rot;
   std::map<size_t, u64*> d_rot_shoup;
   std::map<size_t, u32*> d_perm;
+  std::map<size_t, u32*> d_blkmap;  // two-pass rings: source block -> output block of the perm
   std::map<size_t, u32*> d_sigma;  // coefficient-domain automorphism (src | neg << 31)
   lcl_counts counts{};
   u64 launches = 0;
@@ -294,7 +295,8 @@ struct lcl_context {
   bool in_lane = false;  // work is being enqueued on a lane: no nested lanes
   DevBuf ws_io_in, ws_io_sel, ws_io_dist, ws_io_agg, ws_dtern, ws_atern, ws_ptl, ws_enc, ws_enc_in;
   DevBuf ws_cal;   // calibrate()'s two rotated ciphertexts
-  DevBuf ws_rows;  // DistanceMode::row_sums: the unreduced pair ciphertexts
+  DevBuf ws_rows;  // DistanceMode::row_sums
+  DevBuf ws_stage, ws_stage_sel, ws_err;  // LCLT blob staging + unpack error words: the unreduced pair ciphertexts
   // masked_aggregate's encode(1/l) plaintext, NTT'd on the device once per l
   size_t pt_l = 0;
   std::vector<u64> pt_host;
@@ -743,6 +745,67 @@ u64* ks_switch(lcl_context* c, const RowMap& in, const u64* c1, u64 c1_stride, u
   return acc;
 }
 
+// Hoisted key switches (hoisted_rotations, ckks.cpp:582-612) of the c1 limbs
+// of B items (map `in`; c1 / c1_stride address the same limbs) for every
+// rotation step of `steps`: the ModUp inverse NTT + lift + column pass runs
+// once, then one modup_ip_hoist launch per group of <= kHoistMax steps
+// transforms the digits' blocks once and forms every step's inner product;
+// each(step index, acc [B][2][m+1][N]) then runs that step's ModDown.
+// Rings below 2^13 or more than 4 live limbs use the materialised digits.
+const u64* rot_key(lcl_context* c, size_t step);
+
+template <class Each>
+void ks_hoisted(lcl_context* c, const RowMap& in, const u64* c1, u64 c1_stride, u32 B, u32 m,
+                const std::vector<size_t>& steps, Each&& each) {
+  const u64 N = c->N();
+  if (c->logn < 13 || m > 4) {
+    u64* dig = ks_decompose(c, in, B, m);
+    for (size_t s = 0; s < steps.size(); ++s)
+      each(s, ks_ip(c, dig, B, m, rot_key(c, steps[s]), c->d_perm.at(steps[s])));
+    return;
+  }
+  u64* mid = c->ws_digits.get((u64)B * m * m * N);
+  std::vector<u32> dp(m * m);
+  for (u32 j = 0; j < m; ++j)
+    for (u32 tp = 0; tp < m; ++tp) {
+      const u32 t = tp < j ? tp : tp + 1;
+      dp[j * m + tp] = t < m ? t : c->full;
+    }
+  inv_lift_fwd_cols(c, B * m, in, make_map(mid, m * m, N, (u64)m * m * N, 1, 0, dp), m);
+  const u64 acc_step = (u64)B * 2 * (m + 1) * N;
+  const size_t G = std::min<size_t>(steps.size(), kHoistMax);
+  u64* acc = c->ws_acc.get(G * acc_step);
+  for (size_t s0 = 0; s0 < steps.size(); s0 += kHoistMax) {
+    const u32 ns = (u32)std::min<size_t>(kHoistMax, steps.size() - s0);
+    HoistSteps hs{};
+    for (u32 i = 0; i < ns; ++i) {
+      const size_t st = steps[s0 + i];
+      hs.perm[i] = c->d_perm.at(st);
+      hs.blkmap[i] = c->d_blkmap.at(st);
+      hs.key[i] = rot_key(c, st);
+      hs.key_aux[i] = c->d_rot_shoup.at(st);
+    }
+    const double rb = 8.0 * N;
+    ProfScope ps(c, "modup_ip_hoist",
+                 rb * ((double)B * m * m + (double)B * m + 2.0 * ns * m * (m + 1) +
+                       2.0 * ns * B * (m + 1)),
+                 0.5 * N * B * m * m * 8);
+    dispatch_logn(c, [&](auto L1, auto) {
+      constexpr int LOGN1 = decltype(L1)::value;
+      const u32 grid = ((B + 3) / 4) * (m + 1) * (1u << LOGN1);
+#define LCL_HOIST(MM)                                                                        \
+  case MM:                                                                                   \
+    modup_ip_hoist<LOGN1, MM><<<grid, 64, 0, c->stream>>>(B, mid, c1, c1_stride, hs, ns,      \
+                                                          c->full, acc, acc_step, tabs(c));  \
+    break;
+      switch (m) { LCL_HOIST(1) LCL_HOIST(2) LCL_HOIST(3) LCL_HOIST(4) }
+#undef LCL_HOIST
+    });
+    post_launch(c);
+    for (u32 i = 0; i < ns; ++i) each(s0 + i, acc + i * acc_step);
+  }
+}
+
 // ModDown of acc [B][2][m+1][N] into `out` (items (b, x), rows_per_item m,
 // 2 items per group) with the fused output additions; c1inv: also leave the
 // next key switch's inverse block pass over out's c1 limbs there.
@@ -980,19 +1043,18 @@ void slot_reduce_serial(lcl_context* c, const u64* in, u32 B, u32 m, size_t widt
   if (unf >= 1) {
     // hoisted batch: one decomposition of in.c1, every step reuses it.
     const RowMap c1 = make_map(in + (u64)m * N, m, N, 2ull * m * N, 1, 0, c->primes_0(m));
-    u64* dig = ks_decompose(c, c1, B, m);
     c->counts.mod_ups += B;
     const RowMap base = ct_map(in, m, N, 2ull * m * N);
-    for (size_t u = 1; u < (size_t{1} << unf); ++u) {
-      const size_t st = norm_step(c, u);
+    std::vector<size_t> hsteps;
+    for (size_t u = 1; u < (size_t{1} << unf); ++u) hsteps.push_back(norm_step(c, u));
+    ks_hoisted(c, c1, in + (u64)m * N, 2ull * m * N, B, m, hsteps, [&](size_t i, u64* acc) {
       const int nxt = cur < 0 ? 0 : 1 - cur;
-      u64* acc = ks_ip(c, dig, B, m, rot_key(c, st), c->d_perm.at(st));
       ks_moddown(c, acc, B, m, ct_map(bufs[nxt], m, N, 2ull * m * N),
-                 ct_map(cur_ptr(), m, N, 2ull * m * N), base, c->d_perm.at(st));
+                 ct_map(cur_ptr(), m, N, 2ull * m * N), base, c->d_perm.at(hsteps[i]));
       cur = nxt;
       c->counts.rotations += B;
       c->counts.additions += B;
-    }
+    });
   }
   // each level leaves its output's c1 inverse block pass for the next one
   // (two-pass rings); one buffer suffices: a level's column pass has read it
@@ -1834,25 +1896,35 @@ void hoisted_batch(lcl_context* ctx, const u64* d_ct, u32 B, u32 m, const size_t
                    size_t nsteps, u64* d_outs) {
   const u64 N = ctx->N();
   const u64 words = (u64)B * 2 * m * N;
-  u64* dig = nullptr;
+  std::vector<size_t> ks;     // nonzero steps, in order
+  std::vector<size_t> where;  // their output slots
   for (size_t s = 0; s < nsteps; ++s) {
     const size_t st = norm_step(ctx, h_steps[s]);
-    u64* o = d_outs + s * words;
     if (st == 0) {
-      cuda_check(cudaMemcpyAsync(o, d_ct, words * 8, cudaMemcpyDeviceToDevice, ctx->stream), "copy");
+      cuda_check(cudaMemcpyAsync(d_outs + s * words, d_ct, words * 8, cudaMemcpyDeviceToDevice,
+                                 ctx->stream), "copy");
       continue;
     }
-    const u64* key = rot_key(ctx, st);
-    if (!dig) {
-      const RowMap c1 = make_map(d_ct + (u64)m * N, m, N, 2ull * m * N, 1, 0, ctx->primes_0(m));
-      dig = ks_decompose(ctx, c1, B, m);
-      ctx->counts.mod_ups += B;
+    if (!ctx->d_rot.count(st)) {
+      // the reference throws here, after counting the decomposition and the
+      // rotations of the steps before this one (ckks.cpp:595-611)
+      if (!ks.empty()) {
+        ctx->counts.mod_ups += B;
+        ctx->counts.rotations += (u64)B * ks.size();
+      }
+      fail(LCL_KEY_ERROR, "no rotation key for the requested step");
     }
-    u64* acc = ks_ip(ctx, dig, B, m, key, ctx->d_perm.at(st));
-    ks_moddown(ctx, acc, B, m, ct_map(o, m, N, 2ull * m * N), null_map(),
-               ct_map(d_ct, m, N, 2ull * m * N), ctx->d_perm.at(st));
-    ctx->counts.rotations += B;
+    ks.push_back(st);
+    where.push_back(s);
   }
+  if (ks.empty()) return;
+  const RowMap c1 = make_map(d_ct + (u64)m * N, m, N, 2ull * m * N, 1, 0, ctx->primes_0(m));
+  ctx->counts.mod_ups += B;
+  ks_hoisted(ctx, c1, d_ct + (u64)m * N, 2ull * m * N, B, m, ks, [&](size_t i, u64* acc) {
+    ks_moddown(ctx, acc, B, m, ct_map(d_outs + where[i] * words, m, N, 2ull * m * N), null_map(),
+               ct_map(d_ct, m, N, 2ull * m * N), ctx->d_perm.at(ks[i]));
+    ctx->counts.rotations += B;
+  });
 }
 
 }  // namespace
@@ -2036,11 +2108,13 @@ void free_context(lcl_context* c) {
   for (auto& kv : c->d_rot) cudaFree(kv.second);
   for (auto& kv : c->d_rot_shoup) cudaFree(kv.second);
   for (auto& kv : c->d_perm) cudaFree(kv.second);
+  for (auto& kv : c->d_blkmap) cudaFree(kv.second);
   for (auto& kv : c->d_sigma) cudaFree(kv.second);
   for (DevBuf* b : {&c->ws_coef, &c->ws_digits, &c->ws_acc, &c->ws_coefsp, &c->ws_mid,
                     &c->ws_tern, &c->ws_ctA, &c->ws_ctB, &c->ws_ctC, &c->ws_pt, &c->ws_c1inv, &c->ws_io_in,
                     &c->ws_io_sel, &c->ws_io_dist, &c->ws_io_agg, &c->ws_dtern, &c->ws_atern,
-                    &c->ws_ptl, &c->ws_rows, &c->ws_cal,
+                    &c->ws_ptl, &c->ws_rows, &c->ws_cal, &c->ws_stage, &c->ws_stage_sel,
+                    &c->ws_err,
                     &c->ws_enc, &c->ws_enc_in})
     b->release();
   for (void* p : {(void*)c->d_twist, (void*)c->d_roots, (void*)c->d_brv, (void*)c->d_slot})
@@ -2302,6 +2376,18 @@ int lcl_upload_rotation_key(lcl_context* ctx, size_t step, const uint64_t* h_key
       cuda_check(cudaMalloc(&dp, p.size() * 4), "perm alloc");
       cuda_check(cudaMemcpy(dp, p.data(), p.size() * 4, cudaMemcpyHostToDevice), "perm upload");
       ctx->d_perm[step] = dp;
+      if (ctx->logn >= 13) {
+        // the evaluation-domain permutation is block-local (block_gather):
+        // output block b reads only source block p[256 b] >> 8
+        const size_t nb = ctx->n >> 8;
+        std::vector<u32> bm(nb, 0xFFFFFFFFu);
+        for (size_t b = 0; b < nb; ++b) bm[p[b << 8] >> 8] = (u32)b;
+        for (u32 v : bm) need(v != 0xFFFFFFFFu, LCL_PARAMETER_ERROR, "Galois permutation is not block-local");
+        u32* db = nullptr;
+        cuda_check(cudaMalloc(&db, nb * 4), "blkmap alloc");
+        cuda_check(cudaMemcpy(db, bm.data(), nb * 4, cudaMemcpyHostToDevice), "blkmap upload");
+        ctx->d_blkmap[step] = db;
+      }
       const std::vector<u32> sg = galois_sigma(ctx->n, step);
       u32* ds = nullptr;
       cuda_check(cudaMalloc(&ds, sg.size() * 4), "sigma alloc");
@@ -2769,6 +2855,90 @@ int lcl_server_round(lcl_context* ctx, const uint64_t* d_clients, const uint64_t
 
 namespace {
 
+// ------------------------------------------------------------ LCLT ingest
+// CkksContext::deserialize's header checks (ckks.cpp:640-660), on the host
+// (13 bytes per blob); the payload's residue checks run on the device
+// (lclt_unpack). Returns the limb count; *scale = 2^scale_bits.
+u32 lclt_header(const lcl_context* c, const uint8_t* b, size_t size, double* scale) {
+  static const uint8_t magic[4] = {'L', 'C', 'L', 'T'};
+  if (size < 13 || std::memcmp(b, magic, 4) != 0) fail(LCL_DATA_ERROR, "not a ciphertext blob");
+  if ((u32)(b[4] | (b[5] << 8)) != 1) fail(LCL_DATA_ERROR, "unsupported ciphertext format version");
+  const u64 n = (u64)b[6] | ((u64)b[7] << 8) | ((u64)b[8] << 16) | ((u64)b[9] << 24);
+  if (n != c->N()) fail(LCL_DATA_ERROR, "ciphertext ring degree does not match the context");
+  const u32 level = b[10], scale_bits = b[11], count = b[12];
+  if (level > c->full - 1 || count != level + 1)
+    fail(LCL_DATA_ERROR, "ciphertext level inconsistent with the modulus chain");
+  if (size != 13 + 2ull * count * n * 8) fail(LCL_DATA_ERROR, "ciphertext blob length mismatch");
+  if (scale) *scale = std::pow(2.0, (double)scale_bits);
+  return count;
+}
+
+// Where a host round's inputs come from: limb-major words (the reference's
+// PolyRns rows), or LCLT blobs as the server receives them (run_round step
+// 3 deserializes every chunk, protocol.cpp:419-429). Blob (i, c) of the
+// clients sits at blobs + (i * C + c) * stride, selector i at sel_blobs + i *
+// stride. Blob bytes are copied verbatim into a device staging buffer and
+// unpacked + range-checked by lclt_unpack on the copy stream, so
+// deserialization rides the same overlapped H2D pipeline as plain words.
+struct Ingest {
+  const u64* words = nullptr;
+  const u64* sel_words = nullptr;
+  const uint8_t* blobs = nullptr;
+  const uint8_t* sel_blobs = nullptr;
+  u64 stride = 0;
+  u8* stage = nullptr;
+  u8* sel_stage = nullptr;
+  u32* err = nullptr;  // device: first bad blob + 1 (clients), selectors use err + 1
+
+  void unpack(lcl_context* c, const u8* st, u32 cols, u32 r0, u32 r1, u32 c0, u32 c1, u64* out,
+              u32* e, cudaStream_t s) const {
+    const u32 m = c->full;
+    const u64 W = 2ull * m * c->N();
+    const dim3 grid((u32)((W + 255) / 256), (r1 - r0) * (c1 - c0));
+    if (!grid.y) return;
+    lclt_unpack<<<grid, 256, 0, s>>>(st, stride, cols, r0, c0, c1 - c0, m, c->logn, out, e,
+                                     c->d_primes);
+    count_launch(c);
+    cuda_check(cudaGetLastError(), "lclt_unpack");
+  }
+  // clients [i0, i1), every chunk
+  void rows(lcl_context* c, u64* dc, u32 i0, u32 i1, u32 C, cudaStream_t s) const {
+    const u64 ctw = 2ull * c->full * c->N();
+    if (words) {
+      cuda_check(cudaMemcpyAsync(dc + (u64)i0 * C * ctw, words + (u64)i0 * C * ctw,
+                                 (u64)(i1 - i0) * C * ctw * 8, cudaMemcpyHostToDevice, s), "h2d");
+      return;
+    }
+    cuda_check(cudaMemcpyAsync(stage + (u64)i0 * C * stride, blobs + (u64)i0 * C * stride,
+                               (u64)(i1 - i0) * C * stride, cudaMemcpyHostToDevice, s), "h2d blobs");
+    unpack(c, stage, C, i0, i1, 0, C, dc, err, s);
+  }
+  // chunks [c0, c1) of all n clients
+  void slice(lcl_context* c, u64* dc, u32 n, u32 C, u32 c0, u32 c1, cudaStream_t s) const {
+    const u64 ctw = 2ull * c->full * c->N();
+    if (words) {
+      cuda_check(cudaMemcpy2DAsync(dc + (u64)c0 * ctw, (u64)C * ctw * 8, words + (u64)c0 * ctw,
+                                   (u64)C * ctw * 8, (u64)(c1 - c0) * ctw * 8, n,
+                                   cudaMemcpyHostToDevice, s), "h2d slice");
+      return;
+    }
+    cuda_check(cudaMemcpy2DAsync(stage + (u64)c0 * stride, (u64)C * stride, blobs + (u64)c0 * stride,
+                                 (u64)C * stride, (u64)(c1 - c0) * stride, n,
+                                 cudaMemcpyHostToDevice, s), "h2d blob slice");
+    unpack(c, stage, C, 0, n, c0, c1, dc, err, s);
+  }
+  void sel(lcl_context* c, u64* ds, u32 n, cudaStream_t s) const {
+    const u64 ctw = 2ull * c->full * c->N();
+    if (sel_words) {
+      cuda_check(cudaMemcpyAsync(ds, sel_words, (u64)n * ctw * 8, cudaMemcpyHostToDevice, s), "h2d");
+      return;
+    }
+    cuda_check(cudaMemcpyAsync(sel_stage, sel_blobs, (u64)n * stride, cudaMemcpyHostToDevice, s),
+               "h2d sel blobs");
+    unpack(c, sel_stage, 1, 0, n, 0, 1, ds, err + 1, s);
+  }
+};
+
 // Client-group form of the overlapped host round: the clients arrive in G
 // groups; when group g has landed, lane g runs the whole chain of the pairs
 // it completes (i < j, j in group g: contiguous in j-major order --
@@ -2777,12 +2947,11 @@ namespace {
 // tensor is a sum over clients) and are finished on the last lane. Group
 // boundaries k_g ~ n sqrt(g / G) give the lanes similar pair counts. Same
 // kernels and op counters as the serial round.
-void host_round_groups(lcl_context* ctx, const u64* h_clients, const u64* h_sel, u32 n, u32 C,
+void host_round_groups(lcl_context* ctx, const Ingest& in, u32 n, u32 C,
                        size_t width, size_t k, size_t l, bool average, u64* h_dist, u64* h_agg,
                        u64* dc, u64* ds, u64* dd, u64* da, u32 G) {
   const u32 m = ctx->full;
   const u64 N = ctx->N();
-  const u64 ctw = 2ull * m * N;
   const u64 dstride = 2ull * (m - 1) * N;
   const u64 astride = 2ull * (average ? m - 2 : m - 1) * N;
   std::vector<u32> bound{0};
@@ -2805,11 +2974,9 @@ void host_round_groups(lcl_context* ctx, const u64* h_clients, const u64* h_sel,
   cuda_check(cudaStreamWaitEvent(ctx->h2d, ev[0], 0), "wait");
   cuda_check(cudaStreamWaitEvent(ctx->d2h, ev[0], 0), "wait");
   for (u32 g = 0; g < G; ++g) cuda_check(cudaStreamWaitEvent(ctx->lanes[g].stream, ev[0], 0), "wait");
-  cuda_check(cudaMemcpyAsync(ds, h_sel, (u64)n * ctw * 8, cudaMemcpyHostToDevice, ctx->h2d), "h2d");
+  in.sel(ctx, ds, n, ctx->h2d);
   for (u32 g = 0; g < G; ++g) {
-    cuda_check(cudaMemcpyAsync(dc + (u64)bound[g] * C * ctw, h_clients + (u64)bound[g] * C * ctw,
-                               (u64)(bound[g + 1] - bound[g]) * C * ctw * 8,
-                               cudaMemcpyHostToDevice, ctx->h2d), "h2d group");
+    in.rows(ctx, dc, bound[g], bound[g + 1], C, ctx->h2d);
     cuda_check(cudaEventRecord(ev[1 + g], ctx->h2d), "event");
   }
   u64* atern = ctx->ws_atern.get((u64)C * 3 * m * N);
@@ -2867,14 +3034,11 @@ void host_round_groups(lcl_context* ctx, const u64* h_clients, const u64* h_sel,
   cuda_check(cudaStreamSynchronize(ctx->stream), "round sync");
 }
 
-}  // namespace
-
-extern "C" {
-
-int lcl_server_round_host(lcl_context* ctx, const uint64_t* h_clients, const uint64_t* h_sel,
-                          size_t n, size_t chunks, double in_scale, size_t width, size_t k,
-                          size_t l, int average, uint64_t* h_dist, uint64_t* h_agg) {
-  return guarded([&] {
+// lcl_server_round_host / lcl_server_round_lclt: H2D (words or LCLT blobs),
+// the round, D2H; see the header.
+void server_round_host(lcl_context* ctx, const Ingest& in, size_t n, size_t chunks, size_t width,
+                       size_t k, size_t l, int average, uint64_t* h_dist, uint64_t* h_agg) {
+  {
     const u32 m = ctx->full;
     const u64 N = ctx->N();
     const u64 ctw = 2ull * m * N;  // words per ciphertext
@@ -2888,9 +3052,10 @@ int lcl_server_round_host(lcl_context* ctx, const uint64_t* h_clients, const uin
     u64* dd = ctx->ws_io_dist.get(dw);
     u64* da = ctx->ws_io_agg.get(aw);
     const bool overlap = n >= 2 && n <= 65535 && m >= 2 && chunks >= 2 && P <= sub_batch(ctx, m);
+    (void)sw;
     if (!overlap) {
-      cuda_check(cudaMemcpyAsync(dc, h_clients, cw * 8, cudaMemcpyHostToDevice, ctx->stream), "h2d");
-      cuda_check(cudaMemcpyAsync(ds, h_sel, sw * 8, cudaMemcpyHostToDevice, ctx->stream), "h2d");
+      in.rows(ctx, dc, 0, (u32)n, (u32)chunks, ctx->stream);
+      in.sel(ctx, ds, (u32)n, ctx->stream);
       distance_matrix(ctx, dc, (u32)n, (u32)chunks, width, k, true, true, dd);
       masked_aggregate(ctx, dc, ds, (u32)n, (u32)chunks, l, average != 0, da);
       cuda_check(cudaMemcpyAsync(h_dist, dd, dw * 8, cudaMemcpyDeviceToHost, ctx->stream), "d2h");
@@ -2919,7 +3084,7 @@ int lcl_server_round_host(lcl_context* ctx, const uint64_t* h_clients, const uin
     const char* mode_env = std::getenv("LCL_HOST_ROUND");
     const int mode = mode_env ? atoi(mode_env) : 1;
     if (mode >= 1 && ctx->pair_f64 && n >= 4 && !ctx->prof_on) {
-      host_round_groups(ctx, h_clients, h_sel, (u32)n, (u32)chunks, width, k, l, average != 0,
+      host_round_groups(ctx, in, (u32)n, (u32)chunks, width, k, l, average != 0,
                         h_dist, h_agg, dc, ds, dd, da, mode == 1 ? 2u : (u32)mode);
       return;
     }
@@ -2937,16 +3102,13 @@ int lcl_server_round_host(lcl_context* ctx, const uint64_t* h_clients, const uin
     cuda_check(cudaEventRecord(start, ctx->stream), "event");
     cuda_check(cudaStreamWaitEvent(ctx->h2d, start, 0), "wait");
     cuda_check(cudaStreamWaitEvent(ctx->d2h, start, 0), "wait");
-    cuda_check(cudaMemcpyAsync(ds, h_sel, sw * 8, cudaMemcpyHostToDevice, ctx->h2d), "h2d");
+    in.sel(ctx, ds, (u32)n, ctx->h2d);
     u64* tern = ctx->ws_dtern.get((u64)P * 3 * m * N);
     u32 s = 0;
     for (u32 c0 = 0; c0 < C; c0 += per, ++s) {
       const u32 c1 = std::min(C, c0 + per);
       // clients' chunks [c0, c1): n rows of (c1 - c0) ciphertexts, pitch C
-      cuda_check(cudaMemcpy2DAsync(dc + (u64)c0 * ctw, (u64)C * ctw * 8, h_clients + (u64)c0 * ctw,
-                                   (u64)C * ctw * 8, (u64)(c1 - c0) * ctw * 8, n,
-                                   cudaMemcpyHostToDevice, ctx->h2d),
-                 "h2d slice");
+      in.slice(ctx, dc, (u32)n, C, c0, c1, ctx->h2d);
       cuda_check(cudaEventRecord(ev[2 * s], ctx->h2d), "event");
       cuda_check(cudaStreamWaitEvent(ctx->stream, ev[2 * s], 0), "wait");
       pair_accumulate_launch(ctx, dc, (u32)n, C, c0, c1, row_range(0, P), tern, c0 > 0);
@@ -2968,7 +3130,126 @@ int lcl_server_round_host(lcl_context* ctx, const uint64_t* h_clients, const uin
     cuda_check(cudaMemcpyAsync(h_dist, dd, dw * 8, cudaMemcpyDeviceToHost, ctx->d2h), "d2h");
     cuda_check(cudaStreamSynchronize(ctx->d2h), "round sync");
     cuda_check(cudaStreamSynchronize(ctx->stream), "round sync");
+  }
+}
+
+// Validates the headers of a batch of LCLT blobs on the host: all at the
+// same limb count (returned) and scale (*scale).
+u32 lclt_batch_headers(const lcl_context* c, const uint8_t* blobs, size_t blob_bytes,
+                       size_t stride, size_t count, double* scale) {
+  need(stride >= blob_bytes, LCL_SHAPE_ERROR, "blob stride shorter than a blob");
+  u32 m = 0;
+  for (size_t i = 0; i < count; ++i) {
+    double sc = 0;
+    const u32 mi = lclt_header(c, blobs + i * stride, blob_bytes, &sc);
+    if (i == 0) {
+      m = mi;
+      *scale = sc;
+    }
+    need(mi == m, LCL_SHAPE_ERROR, "blobs of one batch differ in level");
+    need(sc == *scale, LCL_ALIGNMENT_ERROR, "operand scales diverge");
+  }
+  return m;
+}
+
+// Reads back the unpack kernels' first-bad-blob words (synchronises).
+void lclt_check(lcl_context* c, const u32* d_err, int words) {
+  u32 h[2] = {0, 0};
+  cuda_check(cudaMemcpy(h, d_err, (size_t)words * 4, cudaMemcpyDeviceToHost), "err readback");
+  for (int i = 0; i < words; ++i)
+    if (h[i]) fail(LCL_DATA_ERROR, "residue outside its modulus");
+}
+
+}  // namespace
+
+extern "C" {
+
+int lcl_server_round_host(lcl_context* ctx, const uint64_t* h_clients, const uint64_t* h_sel,
+                          size_t n, size_t chunks, double in_scale, size_t width, size_t k,
+                          size_t l, int average, uint64_t* h_dist, uint64_t* h_agg) {
+  return guarded([&] {
+    Ingest in;
+    in.words = h_clients;
+    in.sel_words = h_sel;
+    server_round_host(ctx, in, n, chunks, width, k, l, average, h_dist, h_agg);
     (void)in_scale;
+  });
+}
+
+int lcl_server_round_lclt(lcl_context* ctx, const uint8_t* h_client_blobs,
+                          const uint8_t* h_sel_blobs, size_t blob_bytes, size_t stride, size_t n,
+                          size_t chunks, size_t width, size_t k, size_t l, int average,
+                          uint64_t* h_dist, uint64_t* h_agg, double* dist_scale,
+                          double* agg_scale) {
+  return guarded([&] {
+    need(chunks >= 1, LCL_SHAPE_ERROR, "empty weight vector");
+    double w_scale = 0, s_scale = 0;
+    const u32 m = lclt_batch_headers(ctx, h_client_blobs, blob_bytes, stride, n * chunks, &w_scale);
+    const u32 ms = lclt_batch_headers(ctx, h_sel_blobs, blob_bytes, stride, n, &s_scale);
+    need(m == ctx->full && ms == ctx->full, LCL_SHAPE_ERROR,
+         "client updates and selectors must be fresh (top-level) ciphertexts");
+    Ingest in;
+    in.blobs = h_client_blobs;
+    in.sel_blobs = h_sel_blobs;
+    in.stride = stride;
+    // staging: the blob bytes verbatim (+16: the funnel shift's last load)
+    in.stage = reinterpret_cast<u8*>(ctx->ws_stage.get((n * chunks * stride + 16 + 7) / 8));
+    in.sel_stage = reinterpret_cast<u8*>(ctx->ws_stage_sel.get((n * stride + 16 + 7) / 8));
+    in.err = reinterpret_cast<u32*>(ctx->ws_err.get(1));
+    cuda_check(cudaMemsetAsync(in.err, 0, 8, ctx->stream), "err reset");
+    server_round_host(ctx, in, n, chunks, width, k, l, average, h_dist, h_agg);
+    lclt_check(ctx, in.err, 2);
+    const u32 full = ctx->full;
+    if (dist_scale) *dist_scale = (w_scale * w_scale) / (double)ctx->primes[full - 1];
+    if (agg_scale) {
+      double sc = (w_scale * s_scale) / (double)ctx->primes[full - 1];
+      if (average) sc = (sc * ctx->scale) / (double)ctx->primes[full - 2];
+      *agg_scale = sc;
+    }
+  });
+}
+
+int lcl_deserialize(lcl_context* ctx, const uint8_t* h_blobs, size_t blob_bytes, size_t stride,
+                    size_t count, uint64_t* d_out, double* scale) {
+  return guarded([&] {
+    if (!count) return;
+    double sc = 0;
+    lclt_batch_headers(ctx, h_blobs, blob_bytes, stride, count, &sc);
+    u8* st = reinterpret_cast<u8*>(ctx->ws_stage.get((count * stride + 16 + 7) / 8));
+    u32* err = reinterpret_cast<u32*>(ctx->ws_err.get(1));
+    cuda_check(cudaMemsetAsync(err, 0, 8, ctx->stream), "err reset");
+    cuda_check(cudaMemcpyAsync(st, h_blobs, count * stride, cudaMemcpyHostToDevice, ctx->stream),
+               "h2d blobs");
+    const u32 m = h_blobs[12];
+    const u64 W = 2ull * m * ctx->N();
+    const dim3 grid((u32)((W + 255) / 256), (u32)count);
+    lclt_unpack<<<grid, 256, 0, ctx->stream>>>(st, stride, (u32)count, 0, 0, (u32)count, m,
+                                               ctx->logn, d_out, err, ctx->d_primes);
+    post_launch(ctx);
+    cuda_check(cudaStreamSynchronize(ctx->stream), "deserialize sync");
+    lclt_check(ctx, err, 1);
+    if (scale) *scale = sc;
+  });
+}
+
+int lcl_serialize(lcl_context* ctx, const uint64_t* d_ct, size_t count, size_t limbs,
+                  double scale, uint8_t* h_blobs, size_t stride) {
+  return guarded([&] {
+    check_count(ctx, limbs);
+    const long long sb = std::llround(std::log2(scale));
+    need(sb >= 1 && sb <= 255, LCL_PARAMETER_ERROR, "scale exponent does not fit the header");
+    const u64 W = 2ull * limbs * ctx->N();
+    const u64 bytes = 13 + 8 * W;
+    need(stride >= bytes, LCL_SHAPE_ERROR, "blob stride shorter than a blob");
+    if (!count) return;
+    u8* st = reinterpret_cast<u8*>(ctx->ws_stage.get((count * stride + 7) / 8));
+    const dim3 grid((u32)((W + 255) / 256), (u32)count);
+    lclt_pack<<<grid, 256, 0, ctx->stream>>>(d_ct, (u32)limbs, ctx->logn, (u32)limbs - 1, (u32)sb,
+                                             stride, st);
+    post_launch(ctx);
+    cuda_check(cudaMemcpyAsync(h_blobs, st, count * stride, cudaMemcpyDeviceToHost, ctx->stream),
+               "d2h blobs");
+    cuda_check(cudaStreamSynchronize(ctx->stream), "serialize sync");
   });
 }
 

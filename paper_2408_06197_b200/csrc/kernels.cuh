@@ -528,6 +528,62 @@ __global__ void __launch_bounds__(256)
 }
 
 // ------------------------------------------------------------------------
+// LCLT wire format (CkksContext::serialize / deserialize, ckks.cpp:614-678):
+// a 13-byte header (magic "LCLT", u16 version, u32 ring degree, u8 level,
+// u8 scale bits, u8 limb count) then the c0 rows and the c1 rows as
+// little-endian u64 -- so every payload word sits 5 bytes off an 8-byte
+// boundary. Blob (r, c) of an [rows][cols] batch starts at byte
+// (r * cols + c) * stride of `blobs` (the host layout, copied verbatim);
+// ciphertext (r, c) lands at (r * cols + c) * 2 m N words of `out`. Items
+// (r, c0 .. c1) of rows r0 .. r1 are unpacked: each thread funnel-shifts two
+// aligned 8-byte loads per word, checks the residue against its prime
+// (deserialize's "residue outside its modulus") and records the first bad
+// blob in *err (atomicMin of blob index + 1 over a zero-initialised word).
+__global__ void __launch_bounds__(256)
+    lclt_unpack(const u8* __restrict__ blobs, u64 stride, u32 cols, u32 r0, u32 c0, u32 ncols,
+                u32 m, u32 logn, u64* __restrict__ out, u32* __restrict__ err,
+                const PrimeConst* __restrict__ primes) {
+  const u64 W = 2ull * m << logn;
+  const u64 k = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= W) return;
+  const u32 r = r0 + blockIdx.y / ncols, c = c0 + blockIdx.y % ncols;
+  const u64 item = (u64)r * cols + c;
+  const u64 byte = item * stride + 13 + 8 * k;
+  const u64* w = reinterpret_cast<const u64*>(blobs) + (byte >> 3);
+  const u32 sh = (u32)(byte & 7) * 8;
+  const u64 lo = __ldg(w);
+  const u64 v = sh ? (lo >> sh) | (__ldg(w + 1) << (64 - sh)) : lo;
+  const u32 limb = (u32)((k >> logn) % m);
+  if (v >= primes[limb].q) atomicMin(err, (u32)item + 1);
+  out[item * W + k] = v;
+}
+
+// serialize (ckks.cpp:614-638): ciphertexts [items][2][m][N] -> blobs at
+// `stride` bytes with the LCLT header; one thread per 8 payload bytes,
+// thread 0 of each blob also writes the header. Byte stores (the payload is
+// 5 bytes off alignment); the blob bytes leave the device with one copy.
+__global__ void __launch_bounds__(256)
+    lclt_pack(const u64* __restrict__ ct, u32 m, u32 logn, u32 level, u32 scale_bits,
+              u64 stride, u8* __restrict__ blobs) {
+  const u64 W = 2ull * m << logn;
+  const u64 k = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  const u64 item = blockIdx.y;
+  u8* b = blobs + item * stride;
+  if (k == 0) {
+    const u32 n = 1u << logn;
+    const u8 hdr[13] = {'L', 'C', 'L', 'T', 1, 0, (u8)n, (u8)(n >> 8), (u8)(n >> 16),
+                        (u8)(n >> 24), (u8)level, (u8)scale_bits, (u8)m};
+#pragma unroll
+    for (int i = 0; i < 13; ++i) b[i] = hdr[i];
+  }
+  if (k >= W) return;
+  const u64 v = __ldg(ct + item * W + k);
+  u8* p = b + 13 + 8 * k;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) p[i] = (u8)(v >> (8 * i));
+}
+
+// ------------------------------------------------------------------------
 // DistanceMode::row_sums (distance.cpp:287-298): row i of the matrix is the
 // sum of the n - 1 pair ciphertexts that contain client i. pairs: [P][W]
 // words in (i<j) row-major order, W = 2 m N; rows: [n][W]. Modular addition

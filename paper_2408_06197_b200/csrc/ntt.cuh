@@ -797,6 +797,117 @@ __global__ void __launch_bounds__(64, MINB)
                                   c1_stride, perm, key, key_aux, full, acc, tb);
 }
 
+// Hoisted rotations (ckks.cpp:582-612) fused like modup_ip_blk: ONE ModUp
+// block pass feeds the inner products of up to kHoistMax rotation steps.
+// A 16-thread group owns SOURCE block sb of target row t of item b: it runs
+// the block stages of the M digits once (the identity digit t == j is the
+// input limb's block, unpermuted) and keeps them in shared memory; then for
+// every step s the Galois permutation maps source block sb onto exactly one
+// output block ob = blkmap_s[sb] (block-local, see block_gather), whose
+// elements are gathered from the staged digits, multiplied by the step's
+// key words and accumulated over the digits in registers. The m(m+1) digit
+// rows never reach HBM and are transformed once for all the steps.
+//   mid: [B][M][M][N] (as modup_ip_blk); acc: step s at acc + s * acc_step,
+//   [B][2][M+1][N] each.
+constexpr int kHoistMax = 8;
+struct HoistSteps {
+  const u32* perm[kHoistMax];
+  const u32* blkmap[kHoistMax];
+  const u64* key[kHoistMax];
+  const u64* key_aux[kHoistMax];
+};
+
+template <class F, int LOGN1, int M>
+__device__ __forceinline__ void modup_ip_hoist_body(u32 bi, bool live, u32 t, u32 sb, u32 pi,
+                                                    u32 l, u64* s, u64 (*sd)[256 + 16],
+                                                    ulonglong2* stw, const u64* mid,
+                                                    const u64* c1, u64 c1_stride,
+                                                    const HoistSteps& hs, u32 nsteps, u32 full,
+                                                    u64* acc, u64 acc_step, const NttTabs& tb) {
+  const u32 n = 1u << tb.logn;
+  const PrimeConst P = tb.primes[pi];
+  const typename F::K K = F::konst(P);
+  const u64 kstride = (u64)(full + 1) * n;
+  stage_blk_tw<F>(stw, F::table(tb, false, pi), 1u << LOGN1, sb, threadIdx.x, 64);
+  __syncthreads();
+  const SmemTw<F> twa{stw};
+#pragma unroll 1
+  for (int j = 0; j < M; ++j) {
+    if (t == (u32)j) {
+      const u64* src = c1 + (u64)bi * c1_stride + (u64)j * n + (sb << 8);
+#pragma unroll
+      for (int e = 0; e < 16; ++e) sd[j][pad16(l + 16 * e)] = F::bits(F::from_u64(__ldg(src + l + 16 * e)));
+    } else {
+      const u32 tp = t < (u32)j ? t : t - 1;
+      const u64* src = mid + (((u64)bi * M + j) * M + tp) * n + (sb << 8);
+      typename F::T x[16];
+#pragma unroll
+      for (int e = 0; e < 16; ++e) x[e] = F::unbits(src[l + 16 * e]);
+      u64 o[16];
+      blk_fwd_body<F>(x, o, s, twa, l, K, [](typename F::T v) { return F::bits(v); });
+#pragma unroll
+      for (int e = 0; e < 16; ++e) sd[j][pad16(l + 16 * e)] = o[e];
+    }
+  }
+  __syncwarp();
+  if (!live) return;
+#pragma unroll 1
+  for (u32 st = 0; st < nsteps; ++st) {
+    const u32 ob = __ldg(hs.blkmap[st] + sb);
+    const u32* perm = hs.perm[st];
+    const u64* k0 = hs.key[st] + (u64)pi * n;
+    const u64* ks0 = hs.key_aux[st] + (u64)pi * n;
+    u64* o0 = acc + st * acc_step + ((u64)bi * 2 * (M + 1) + t) * n;
+    u64* o1 = o0 + (u64)(M + 1) * n;
+#pragma unroll 4
+    for (int e = 0; e < 16; ++e) {
+      const u32 a = (ob << 8) + l + 16 * e;
+      const u32 si = pad16(__ldg(perm + a) & 255u);
+      u64 a0 = 0, a1 = 0;
+#pragma unroll
+      for (int j = 0; j < M; ++j) {
+        const u64 off = (2ull * j) * kstride + a;
+        const typename F::T x = F::unbits(sd[j][si]);
+        const u64 kw0 = IpOps<F>::kRawKey ? __ldg(k0 + off) : 0;
+        const u64 kw1 = IpOps<F>::kRawKey ? __ldg(k0 + off + kstride) : 0;
+        const u64 p0 = IpOps<F>::mul(x, kw0, __ldg(ks0 + off), K);
+        const u64 p1 = IpOps<F>::mul(x, kw1, __ldg(ks0 + off + kstride), K);
+        a0 = j ? IpOps<F>::add(a0, p0) : p0;
+        a1 = j ? IpOps<F>::add(a1, p1) : p1;
+      }
+      o0[a] = F::canon(F::unbits(a0), K);
+      o1[a] = F::canon(F::unbits(a1), K);
+    }
+  }
+}
+
+template <int LOGN1, int M, int MINB = 6>
+__global__ void __launch_bounds__(64, MINB)
+    modup_ip_hoist(u32 B, const u64* __restrict__ mid, const u64* __restrict__ c1, u64 c1_stride,
+                   const __grid_constant__ HoistSteps hs, u32 nsteps, u32 full,
+                   u64* __restrict__ acc, u64 acc_step, const __grid_constant__ NttTabs tb) {
+  constexpr int N1 = 1 << LOGN1;
+  __shared__ u64 sm[4][256 + 16];
+  __shared__ u64 sd[4][M][256 + 16];  // the group's M transformed digit blocks
+  __shared__ ulonglong2 stw[kBlkTw];
+  const u32 l = threadIdx.x & 15, bw = threadIdx.x >> 4;
+  const u32 bq_count = (B + 3) >> 2;
+  const u32 bq = blockIdx.x % bq_count;
+  const u32 tb_ = blockIdx.x / bq_count;
+  const u32 traw = tb_ / N1, sb = tb_ - traw * N1;
+  const u32 t = traw == 0 ? (u32)M : traw - 1;  // special-prime target first
+  const u32 bi_raw = bq * 4 + bw;
+  const bool live = bi_raw < B;
+  const u32 bi = live ? bi_raw : B - 1;
+  const u32 pi = t < (u32)M ? t : full;
+  if (row_fp(tb, pi))
+    modup_ip_hoist_body<FpF, LOGN1, M>(bi, live, t, sb, pi, l, sm[bw], sd[bw], stw, mid, c1,
+                                       c1_stride, hs, nsteps, full, acc, acc_step, tb);
+  else
+    modup_ip_hoist_body<IntF, LOGN1, M>(bi, live, t, sb, pi, l, sm[bw], sd[bw], stw, mid, c1,
+                                        c1_stride, hs, nsteps, full, acc, acc_step, tb);
+}
+
 // Block pass, inverse: GS stages m = N/2 .. N1 (local m' = 128 .. 1). Input:
 // fully reduced words; output: the field's lazy words for the column pass.
 template <class F, int LOGN1>

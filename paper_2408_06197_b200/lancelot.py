@@ -160,6 +160,10 @@ def lib():
         "lcl_pairwise_distance": [_P, _P, _P, _SZ, C.c_int, _P],
         "lcl_distance_matrix": [_P, _P, _SZ, _SZ, C.c_double, _SZ, _SZ, C.c_int, C.c_int, _P,
                                 C.POINTER(C.c_double)],
+        "lcl_deserialize": [_P, _P, _SZ, _SZ, _SZ, _P, C.POINTER(C.c_double)],
+        "lcl_serialize": [_P, _P, _SZ, _SZ, C.c_double, _P, _SZ],
+        "lcl_server_round_lclt": [_P, _P, _P, _SZ, _SZ, _SZ, _SZ, _SZ, _SZ, _SZ, C.c_int, _P, _P,
+                                  C.POINTER(C.c_double), C.POINTER(C.c_double)],
         "lcl_calibrate": [_P, _P, _SZ, C.POINTER(C.c_double), C.POINTER(C.c_double),
                           C.POINTER(C.c_double)],
         "lcl_build_distance_matrix": [_P, _P, _SZ, _SZ, C.c_double, _SZ, _SZ, C.c_int, C.c_int,
@@ -611,6 +615,42 @@ class CkksContext:
         _check(lib().lcl_decrypt_values(self.h, _ptr(cts.contiguous()), B, m, scale, _ptr(dsk),
                                         _ptr(out)))
         return out
+
+    # ---- LCLT wire format (ckks.cpp:614-678)
+    def blob_bytes(self, limbs=None) -> int:
+        m = self.full if limbs is None else limbs
+        return 13 + 16 * m * self._params.ring_degree
+
+    def serialize_batch(self, cts, scale: float, stride=None):
+        """CkksContext::serialize for a batch [B][2][m][N] -> uint8 [B][stride]."""
+        B, _, m, N = (int(x) for x in cts.shape)
+        stride = stride or self.blob_bytes(m)
+        out = np.zeros((B, stride), np.uint8)
+        _check(lib().lcl_serialize(self.h, _ptr(cts.contiguous()), B, m, scale,
+                                   out.ctypes.data, stride))
+        return out
+
+    def serialize(self, ct: Ciphertext) -> bytes:
+        return self.serialize_batch(ct.data.reshape(1, *ct.data.shape), ct.scale)[0].tobytes()
+
+    def deserialize_batch(self, blobs, blob_bytes=None):
+        """CkksContext::deserialize for blobs uint8 [B][stride] -> (device
+        [B][2][m][N], scale); DataError exactly as the reference."""
+        blobs = np.ascontiguousarray(blobs, dtype=np.uint8)
+        B, stride = blobs.shape
+        blob_bytes = stride if blob_bytes is None else blob_bytes
+        m = int(blobs[0, 12]) if B and stride >= 13 else self.full
+        m = max(1, min(m, self.full))
+        out = self._empty(B, 2, m, self._params.ring_degree)
+        sc = C.c_double()
+        _check(lib().lcl_deserialize(self.h, blobs.ctypes.data, blob_bytes, stride, B, _ptr(out),
+                                     C.byref(sc)))
+        return out, sc.value
+
+    def deserialize(self, data: bytes) -> Ciphertext:
+        arr = np.frombuffer(bytes(data), np.uint8).reshape(1, -1)
+        out, sc = self.deserialize_batch(arr)
+        return Ciphertext(out[0], sc)
 
     def hmult_triple(self, a: Ciphertext, b: Ciphertext) -> TernaryCiphertext:
         """ckks.cpp:417-439 (Karatsuba; scale = product)."""

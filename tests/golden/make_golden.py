@@ -51,6 +51,11 @@ CONFIGS = {
                              lazy=1, mode="row_sums", reduce=0),
     "tiny_perpair_kgc": dict(N=512, clients=5, dim=700, k=1, rule="multi_krum", select="0,3",
                              secure=0, lazy=1, mode="per_pair", reduce=0),
+    # BASELINE configs[2] exactly as benchmarked: 20 clients x 11,173,962
+    # params (342 chunks: the pair kernel's 256-chunk passes re-enter), N =
+    # 2^16, lazy relin, hoisted rotations at the bench plan's k = 3
+    "cfg3_hoist": dict(N=65536, clients=20, dim=11173962, k=3, rule="krum", select="0",
+                       secure=1, lazy=1),
     "n13_rowsums": dict(N=8192, clients=5, dim=10000, k=3, rule="krum", select="1", secure=1,
                         lazy=1, mode="row_sums", reduce=1),
 }

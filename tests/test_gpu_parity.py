@@ -117,6 +117,45 @@ def test_evaluator_matches_oracle(evalrig):
         ctx.rotate(rs, 5, keys)
 
 
+@pytest.mark.parametrize("N", [8192, 16384])
+def test_fused_hoisted_key_switch_matches_oracle(N):
+    """modup_ip_hoist (one ModUp block pass shared by up to 8 steps; 15
+    steps = two launches): hoisted_rotations on a batch of 2 fresh (m = 4)
+    and rescaled (m = 3) ciphertexts, zero / repeated / beyond-slots steps,
+    and slot_reduce with k = 5 (15 hoisted steps), word for word."""
+    L = _L()
+    import ctypes as C
+    import torch
+    orc = Oracle(N, secure=False, threads=8)
+    width = 4096
+    steps = slot_reduce_steps(width, 5)
+    orc.keygen(3, steps)
+    cl = orc.make_clients(3, 2, N)  # 2 clients x 2 chunks
+    ctx = gpu_ctx(N)
+    keys = L.RotationKeySet({s_: orc.rotation_key(s_) for s_ in steps})
+    ctx.use_rotation_keys(keys, steps)
+    hs = [1, 2, 3, 0, 7, 9, 15, 4, 5, 6, 11, 3, N // 2 + 1]
+    cts = [cl[0, 0], cl[1, 1]]
+    for m in (4, 3):
+        if m == 3:
+            cts = [orc.rescale(x) for x in cts]
+        d = L.to_device(np.stack(cts))
+        outs = torch.empty((len(hs), 2, 2, m, N), dtype=torch.int64, device="cuda")
+        arr = (C.c_size_t * len(hs))(*hs)
+        L._check(L.lib().lcl_hoisted_rotations(ctx.h, L._ptr(d), 2, m, arr, len(hs), L._ptr(outs)))
+        got = L.to_host(outs)
+        for b in range(2):
+            want = orc.hoisted_rotations(cts[b], hs)
+            for i, st in enumerate(hs):
+                assert np.array_equal(got[i, b], want[i]), (m, b, st)
+    rs = L.Ciphertext(L.to_device(cts[0]), orc.scale)
+    for k in (5, 4):
+        got = L.slot_reduce(ctx, rs, L.HoistPlan(k=k, n=width), keys)
+        assert np.array_equal(L.to_host(got.data), orc.slot_reduce(cts[0], width, k)), k
+    with pytest.raises(L.KeyError):
+        ctx.hoisted_rotations(rs, [1, 2, 17], keys)
+
+
 def test_mult_plain_matches_oracle(evalrig):
     L = _L()
     N, orc, steps, clients = evalrig
@@ -579,3 +618,71 @@ def test_pair_accumulation_long_ranges_and_extremes(pair_f64, n, C, blocked, mon
                                  L.DistanceMode.per_pair, keys, L.DistanceOptions())
     want = orc.distance_matrix(clients, width, 1)
     assert np.array_equal(L.to_host(dm.batch), want)
+
+
+def test_cfg3_benchmark_round_bit_exact_vs_reference():
+    """BASELINE configs[2] exactly as bench.py times it: 20 clients x
+    11,173,962 params (342 chunks), N = 2^16, lazy relin, hoisted rotations
+    at the bench plan's k = 3 (fused modup_ip_hoist), Krum mask. Keys,
+    client ciphertexts and the mask are produced on the device from the
+    reference's seeds (word-identical: their digests are checked against the
+    reference's own dump), then the distance matrix, the aggregate, the op
+    counters and every decrypted slot-0 distance are checked against the
+    reference run (tests/golden/cfg3_hoist.json)."""
+    import hashlib
+    import os
+
+    import torch
+
+    L = _L()
+    from tests.golden_util import load
+    meta = load("cfg3_hoist")
+    o = meta["options"]
+    N, n, dim, k = o["N"], o["clients"], o["dim"], o["k"]
+    d = meta["sha256"]
+
+    def dsha(t):
+        h = hashlib.sha256()
+        h.update(t.cpu().numpy().tobytes())
+        return h.hexdigest()
+
+    ctx = gpu_ctx(N, secure=True)
+    width = 1 << (min(dim, N // 2) - 1).bit_length()
+    assert L.slot_reduce_steps(width, k) == meta["steps"]
+    sk, pk, rk, keys = L.generate_keys(ctx, L.Sampler(L.derive_seed(1, 5)), meta["steps"])
+    assert sha(np.asarray(rk.key)) == d["relin"]
+    rng = L.Sampler(L.derive_seed(1, 0xAB1A7E))
+    C_ = -(-dim // (N // 2))
+    assert C_ == meta["chunks"] == 342
+    big = torch.empty((n, C_, 2, ctx.full, N), dtype=torch.int64, device="cuda")
+    for i in range(n):
+        w = rng.uniform_real(dim) - 0.5
+        pw = L.pack_and_encrypt(ctx, w, pk, rng)
+        big[i].copy_(pw.chunks)
+        del pw
+        assert dsha(big[i]) == d[f"client_{i}"], i
+    _, sels = L.build_mask(ctx, [0], n, pk, L.Sampler(L.derive_seed(1, 0x3000000000000000)))
+    for i in range(n):
+        assert dsha(sels[i]) == d[f"sel_{i}"], i
+    pws = [L.PackedWeights(big[i], dim, 1.0, ctx.scale()) for i in range(n)]
+    assert L.stack_clients(pws).data_ptr() == big.data_ptr()
+    ctx.reset_counters()
+    dm = L.build_distance_matrix(ctx, pws, rk, L.HoistPlan(k=k, n=width),
+                                 L.DistanceMode.per_pair, keys, L.DistanceOptions())
+    torch.cuda.synchronize()
+    assert ctx.counters() == meta["dist_ops"]
+    for p, (i, j) in enumerate(dm.keys):
+        assert dsha(dm.batch[p]) == d[f"dist_{i}_{j}"], (i, j)
+    vals = ctx.decrypt_values_batch(dm.batch, dm.scale, sk).cpu().numpy()
+    for p, e in enumerate(meta["dist"]):
+        assert vals[p][0] == e["slot0"], p
+        assert abs(vals[p][0] - meta["plain_dist"][p]) <= 1e-3 * max(1.0, abs(meta["plain_dist"][p]))
+    mask = L.SelectionMask(n, 1, sels, ctx.scale())
+    ctx.reset_counters()
+    agg = L.masked_aggregate(ctx, pws, mask, L.SelectionRule.krum, rk)
+    torch.cuda.synchronize()
+    assert ctx.counters() == meta["agg_ops"]
+    assert dsha(agg.chunks) == d["agg"]
+    assert agg.scale == meta["agg_scale"]
+    del big
+    torch.cuda.empty_cache()
