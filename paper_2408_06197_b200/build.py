@@ -45,7 +45,7 @@ def build_cpp_driver(verbose: bool = False) -> str:
     if os.path.exists(CPP_DRIVER) and all(
             os.path.getmtime(CPP_DRIVER) > os.path.getmtime(x) for x in hdrs + [CPP_SRC, LIB]):
         return CPP_DRIVER
-    cmd = ["g++", "-std=c++17", "-O2", "-I", os.path.join(os.path.dirname(HERE), "include"),
+    cmd = ["g++", "-std=c++17", "-O2", "-pthread", "-I", os.path.join(os.path.dirname(HERE), "include"),
            CPP_SRC, "-o", CPP_DRIVER, "-L", OUT_DIR, "-llancelot_b200", "-Wl,-rpath,$ORIGIN"]
     if verbose:
         print(" ".join(cmd))

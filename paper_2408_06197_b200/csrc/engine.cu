@@ -2888,7 +2888,7 @@ struct Ingest {
   u64 stride = 0;
   u8* stage = nullptr;
   u8* sel_stage = nullptr;
-  u32* err = nullptr;  // device: first bad blob + 1 (clients), selectors use err + 1
+  u32* err = nullptr;  // device: first bad blob (UINT_MAX: none); selectors use err + 1
 
   void unpack(lcl_context* c, const u8* st, u32 cols, u32 r0, u32 r1, u32 c0, u32 c1, u64* out,
               u32* e, cudaStream_t s) const {
@@ -3154,10 +3154,10 @@ u32 lclt_batch_headers(const lcl_context* c, const uint8_t* blobs, size_t blob_b
 
 // Reads back the unpack kernels' first-bad-blob words (synchronises).
 void lclt_check(lcl_context* c, const u32* d_err, int words) {
-  u32 h[2] = {0, 0};
+  u32 h[2] = {0xFFFFFFFFu, 0xFFFFFFFFu};
   cuda_check(cudaMemcpy(h, d_err, (size_t)words * 4, cudaMemcpyDeviceToHost), "err readback");
   for (int i = 0; i < words; ++i)
-    if (h[i]) fail(LCL_DATA_ERROR, "residue outside its modulus");
+    if (h[i] != 0xFFFFFFFFu) fail(LCL_DATA_ERROR, "residue outside its modulus");
 }
 
 }  // namespace
@@ -3196,7 +3196,7 @@ int lcl_server_round_lclt(lcl_context* ctx, const uint8_t* h_client_blobs,
     in.stage = reinterpret_cast<u8*>(ctx->ws_stage.get((n * chunks * stride + 16 + 7) / 8));
     in.sel_stage = reinterpret_cast<u8*>(ctx->ws_stage_sel.get((n * stride + 16 + 7) / 8));
     in.err = reinterpret_cast<u32*>(ctx->ws_err.get(1));
-    cuda_check(cudaMemsetAsync(in.err, 0, 8, ctx->stream), "err reset");
+    cuda_check(cudaMemsetAsync(in.err, 0xFF, 8, ctx->stream), "err reset");
     server_round_host(ctx, in, n, chunks, width, k, l, average, h_dist, h_agg);
     lclt_check(ctx, in.err, 2);
     const u32 full = ctx->full;
@@ -3217,7 +3217,7 @@ int lcl_deserialize(lcl_context* ctx, const uint8_t* h_blobs, size_t blob_bytes,
     lclt_batch_headers(ctx, h_blobs, blob_bytes, stride, count, &sc);
     u8* st = reinterpret_cast<u8*>(ctx->ws_stage.get((count * stride + 16 + 7) / 8));
     u32* err = reinterpret_cast<u32*>(ctx->ws_err.get(1));
-    cuda_check(cudaMemsetAsync(err, 0, 8, ctx->stream), "err reset");
+    cuda_check(cudaMemsetAsync(err, 0xFF, 8, ctx->stream), "err reset");
     cuda_check(cudaMemcpyAsync(st, h_blobs, count * stride, cudaMemcpyHostToDevice, ctx->stream),
                "h2d blobs");
     const u32 m = h_blobs[12];

@@ -538,7 +538,7 @@ __global__ void __launch_bounds__(256)
 // (r, c0 .. c1) of rows r0 .. r1 are unpacked: each thread funnel-shifts two
 // aligned 8-byte loads per word, checks the residue against its prime
 // (deserialize's "residue outside its modulus") and records the first bad
-// blob in *err (atomicMin of blob index + 1 over a zero-initialised word).
+// blob in *err (atomicMin over a word initialised to UINT_MAX).
 __global__ void __launch_bounds__(256)
     lclt_unpack(const u8* __restrict__ blobs, u64 stride, u32 cols, u32 r0, u32 c0, u32 ncols,
                 u32 m, u32 logn, u64* __restrict__ out, u32* __restrict__ err,
@@ -554,7 +554,7 @@ __global__ void __launch_bounds__(256)
   const u64 lo = __ldg(w);
   const u64 v = sh ? (lo >> sh) | (__ldg(w + 1) << (64 - sh)) : lo;
   const u32 limb = (u32)((k >> logn) % m);
-  if (v >= primes[limb].q) atomicMin(err, (u32)item + 1);
+  if (v >= primes[limb].q) atomicMin(err, (u32)item);
   out[item * W + k] = v;
 }
 

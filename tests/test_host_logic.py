@@ -25,12 +25,47 @@ def test_library_exports_every_declared_symbol():
         assert hasattr(bound, n)
 
 
-def test_cpp_mirror_header_names_match_reference_api():
-    with open(os.path.join(ROOT, "include", "lancelot_b200.hpp")) as f:
-        hpp = f.read()
-    for sym in ("build_distance_matrix", "masked_aggregate", "slot_reduce_steps", "HoistPlan",
-                "WidthError", "KeyError", "ShapeError", "DepthExhaustedError"):
-        assert sym in hpp
+def test_cpp_mirror_plan_logic_matches_reference():
+    """plan_unfold / fixed_plan / slot_reduce_steps of the C++ mirror
+    (compiled here, no device) agree with the Python mirror (which the
+    reference's test_distance.cpp cases below pin)."""
+    import subprocess
+    import tempfile
+
+    prog = r"""
+#include <cstdio>
+#include "lancelot_b200.hpp"
+namespace L = lancelot_b200;
+int main() {
+  const double cases[][5] = {{0.17, 0.072, 4194304, 12582912, 32768}, {1e-4, 9e-5, 4194304, 1073741824, 32768},
+                             {2.0, 1.0, 1.0, 3.0, 1024}, {1.0, 1.0, 1.0, 100.0, 256}};
+  for (const auto& c : cases) {
+    const L::HoistPlan p = L::plan_unfold(c[0], c[1], c[2], c[3], (std::size_t)c[4]);
+    std::printf("%zu %.17g %zu\n", p.k, p.cost, L::slot_reduce_steps(p.n, p.k).size());
+  }
+  std::printf("%zu\n", L::fixed_plan(L::HoistMode::full, 4096).k);
+  try { L::plan_unfold(1, 1, 2, 1, 8); } catch (const L::InfeasibleError&) { std::printf("infeasible\n"); }
+  try { L::fixed_plan(L::HoistMode::dynamic_lp, 8); } catch (const L::UsageError&) { std::printf("usage\n"); }
+  return 0;
+}
+"""
+    with tempfile.TemporaryDirectory() as d:
+        src = os.path.join(d, "p.cpp")
+        with open(src, "w") as f:
+            f.write(prog)
+        exe = os.path.join(d, "p")
+        subprocess.run(["g++", "-std=c++17", "-I", os.path.join(ROOT, "include"), src, "-o", exe,
+                        "-L", os.path.dirname(L.LIB_PATH), "-llancelot_b200",
+                        f"-Wl,-rpath,{os.path.dirname(L.LIB_PATH)}"], check=True)
+        lines = subprocess.run([exe], capture_output=True, text=True, check=True).stdout.split("\n")
+    for line, c in zip(lines, [(0.17, 0.072, 4194304, 12582912, 32768),
+                               (1e-4, 9e-5, 4194304, 1073741824, 32768),
+                               (2.0, 1.0, 1.0, 3.0, 1024), (1.0, 1.0, 1.0, 100.0, 256)]):
+        k, cost, nsteps = line.split()
+        p = L.plan_unfold(*c[:4], int(c[4]))
+        assert int(k) == p.k and float(cost) == p.cost
+        assert int(nsteps) == len(L.slot_reduce_steps(p.n, p.k))
+    assert lines[4] == "13" and lines[5] == "infeasible" and lines[6] == "usage"
 
 
 def test_no_cpu_fallback_without_device():
