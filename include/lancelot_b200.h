@@ -215,6 +215,21 @@ int lcl_decode(lcl_context* ctx, uint64_t* d_pt, size_t batch, size_t count, dou
 int lcl_decrypt_values(lcl_context* ctx, const uint64_t* d_ct, size_t batch, size_t count,
                        double scale, const uint64_t* d_sk, double* d_slots);
 
+/* KGC distance table: table_from_matrix (aggregation.cpp:242-258)
+ * and totals_from_matrix (:260-277) over the device matrix entries d_entries
+ * [entries][2][count][N] at `scale`: every entry decrypted (lcl_decrypt_values),
+ * its value = slot 0 if `reduced` else the left-to-right sum of all slots,
+ * max(0, value / value_scale). h_table [n][n] symmetric with a zero diagonal
+ * (per_pair entries in (i<j) order); h_totals [n]: row sums of that table
+ * (mode LCL_PER_PAIR) or the row_sums entries themselves (LCL_ROW_SUMS).
+ * Synchronises. */
+int lcl_table_from_matrix(lcl_context* ctx, const uint64_t* d_entries, size_t n, size_t count,
+                          double scale, int reduced, double value_scale, const uint64_t* d_sk,
+                          double* h_table);
+int lcl_totals_from_matrix(lcl_context* ctx, const uint64_t* d_entries, size_t n, int mode,
+                           size_t count, double scale, int reduced, double value_scale,
+                           const uint64_t* d_sk, double* h_totals);
+
 /* ------------------------------------------------------------ hot path */
 /* a, b: [chunks][2][full][N]; out: [2][full-1][N]. lazy != 0 -> one relin. */
 int lcl_pairwise_distance(lcl_context* ctx, const uint64_t* d_a, const uint64_t* d_b,

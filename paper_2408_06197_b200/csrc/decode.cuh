@@ -168,4 +168,22 @@ __global__ void __launch_bounds__(256)
   out[gid] = buckets[b * h + __ldg(slot_index + (gid & (h - 1)))].x;
 }
 
+// KGC distance entries (aggregation.cpp:232-258): the decrypted value of a
+// matrix entry is slot 0 when the server reduced it, else the left-to-right
+// sum of every slot (std::accumulate's order, round-to-nearest adds), then
+// max(0, v / value_scale). One thread per entry.
+__global__ void __launch_bounds__(128)
+    entry_values(const double* __restrict__ slots, u32 B, u32 h, int reduced, double value_scale,
+                 double* __restrict__ out) {
+  const u32 b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  const double* s = slots + (u64)b * h;
+  double v = s[0];
+  if (!reduced) {
+    v = 0.0;
+    for (u32 i = 0; i < h; ++i) v = __dadd_rn(v, s[i]);
+  }
+  out[b] = fmax(0.0, __ddiv_rn(v, value_scale));
+}
+
 }  // namespace lcl

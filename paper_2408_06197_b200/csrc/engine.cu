@@ -296,6 +296,7 @@ struct lcl_context {
   DevBuf ws_io_in, ws_io_sel, ws_io_dist, ws_io_agg, ws_dtern, ws_atern, ws_ptl, ws_enc, ws_enc_in;
   DevBuf ws_cal;   // calibrate()'s two rotated ciphertexts
   DevBuf ws_rows;  // DistanceMode::row_sums
+  DevBuf ws_slots;  // KGC: decoded slots + entry values
   DevBuf ws_stage, ws_stage_sel, ws_err;  // LCLT blob staging + unpack error words: the unreduced pair ciphertexts
   // masked_aggregate's encode(1/l) plaintext, NTT'd on the device once per l
   size_t pt_l = 0;
@@ -2114,7 +2115,7 @@ void free_context(lcl_context* c) {
                     &c->ws_tern, &c->ws_ctA, &c->ws_ctB, &c->ws_ctC, &c->ws_pt, &c->ws_c1inv, &c->ws_io_in,
                     &c->ws_io_sel, &c->ws_io_dist, &c->ws_io_agg, &c->ws_dtern, &c->ws_atern,
                     &c->ws_ptl, &c->ws_rows, &c->ws_cal, &c->ws_stage, &c->ws_stage_sel,
-                    &c->ws_err,
+                    &c->ws_err, &c->ws_slots,
                     &c->ws_enc, &c->ws_enc_in})
     b->release();
   for (void* p : {(void*)c->d_twist, (void*)c->d_roots, (void*)c->d_brv, (void*)c->d_slot})
@@ -2686,6 +2687,69 @@ int lcl_decrypt_values(lcl_context* ctx, const uint64_t* d_ct, size_t batch, siz
     u64* pt = ctx->ws_pt.get((u64)batch * count * ctx->N());
     decrypt_batch(ctx, d_ct, (u32)batch, (u32)count, d_sk, pt);
     decode_batch(ctx, pt, (u32)batch, (u32)count, scale, d_slots);
+  });
+}
+
+// table_from_matrix / totals_from_matrix (aggregation.cpp:242-277) on the
+// device: decrypt_values of every entry, entry_values, then the host fills
+// the symmetric table (per_pair) or the totals (row_sums) in the reference's
+// order.
+static void entry_values_batch(lcl_context* ctx, const uint64_t* d_entries, size_t entries,
+                               size_t count, double scale, int reduced, double value_scale,
+                               const uint64_t* d_sk, std::vector<double>& vals) {
+  check_count(ctx, count);
+  need(d_sk != nullptr, LCL_KEY_ERROR, "null secret key");
+  need(value_scale != 0.0, LCL_PARAMETER_ERROR, "zero value scale");
+  vals.assign(entries, 0.0);
+  if (!entries) return;
+  const u32 h = (u32)(ctx->n / 2);
+  u64* pt = ctx->ws_pt.get((u64)entries * count * ctx->N());
+  double* slots = reinterpret_cast<double*>(ctx->ws_slots.get((u64)entries * h + entries));
+  double* dv = slots + (u64)entries * h;
+  decrypt_batch(ctx, d_entries, (u32)entries, (u32)count, d_sk, pt);
+  decode_batch(ctx, pt, (u32)entries, (u32)count, scale, slots);
+  entry_values<<<(u32)((entries + 127) / 128), 128, 0, ctx->stream>>>(
+      slots, (u32)entries, h, reduced, value_scale, dv);
+  post_launch(ctx);
+  cuda_check(cudaMemcpyAsync(vals.data(), dv, entries * 8, cudaMemcpyDeviceToHost, ctx->stream),
+             "d2h values");
+  cuda_check(cudaStreamSynchronize(ctx->stream), "values sync");
+}
+
+int lcl_table_from_matrix(lcl_context* ctx, const uint64_t* d_entries, size_t n, size_t count,
+                          double scale, int reduced, double value_scale, const uint64_t* d_sk,
+                          double* h_table) {
+  return guarded([&] {
+    std::vector<double> v;
+    entry_values_batch(ctx, d_entries, n * (n - 1) / 2, count, scale, reduced, value_scale, d_sk, v);
+    for (size_t i = 0; i < n * n; ++i) h_table[i] = 0.0;
+    size_t p = 0;
+    for (size_t i = 0; i < n; ++i)
+      for (size_t j = i + 1; j < n; ++j, ++p) h_table[i * n + j] = h_table[j * n + i] = v[p];
+  });
+}
+
+int lcl_totals_from_matrix(lcl_context* ctx, const uint64_t* d_entries, size_t n, int mode,
+                           size_t count, double scale, int reduced, double value_scale,
+                           const uint64_t* d_sk, double* h_totals) {
+  return guarded([&] {
+    need(mode == LCL_PER_PAIR || mode == LCL_ROW_SUMS, LCL_USAGE_ERROR, "unknown distance mode");
+    std::vector<double> v;
+    if (mode == LCL_ROW_SUMS) {
+      entry_values_batch(ctx, d_entries, n, count, scale, reduced, value_scale, d_sk, v);
+      for (size_t i = 0; i < n; ++i) h_totals[i] = v[i];
+      return;
+    }
+    entry_values_batch(ctx, d_entries, n * (n - 1) / 2, count, scale, reduced, value_scale, d_sk, v);
+    std::vector<double> t(n * n, 0.0);
+    size_t p = 0;
+    for (size_t i = 0; i < n; ++i)
+      for (size_t j = i + 1; j < n; ++j, ++p) t[i * n + j] = t[j * n + i] = v[p];
+    for (size_t i = 0; i < n; ++i) {  // std::accumulate over the row, left to right
+      double a = 0.0;
+      for (size_t j = 0; j < n; ++j) a += t[i * n + j];
+      h_totals[i] = a;
+    }
   });
 }
 

@@ -164,6 +164,9 @@ def lib():
         "lcl_serialize": [_P, _P, _SZ, _SZ, C.c_double, _P, _SZ],
         "lcl_server_round_lclt": [_P, _P, _P, _SZ, _SZ, _SZ, _SZ, _SZ, _SZ, _SZ, C.c_int, _P, _P,
                                   C.POINTER(C.c_double), C.POINTER(C.c_double)],
+        "lcl_table_from_matrix": [_P, _P, _SZ, _SZ, C.c_double, C.c_int, C.c_double, _P, _P],
+        "lcl_totals_from_matrix": [_P, _P, _SZ, C.c_int, _SZ, C.c_double, C.c_int, C.c_double, _P,
+                                   _P],
         "lcl_calibrate": [_P, _P, _SZ, C.POINTER(C.c_double), C.POINTER(C.c_double),
                           C.POINTER(C.c_double)],
         "lcl_build_distance_matrix": [_P, _P, _SZ, _SZ, C.c_double, _SZ, _SZ, C.c_int, C.c_int,
@@ -890,6 +893,36 @@ def build_distance_matrix(ctx: CkksContext, all_weights, rk: RelinKey, plan: Hoi
     keys_ = pairs if per_pair else [(i, i) for i in range(n)]
     return EncryptedDistanceMatrix(mode, n, options.reduce_on_server, value_scale, out, keys_,
                                    osc.value)
+
+
+@dataclass
+class DistanceTable:
+    """aggregation.hpp:30-35: the KGC's plaintext distance table."""
+    n: int
+    d: np.ndarray  # [n][n] float64
+
+
+def table_from_matrix(ctx: CkksContext, m: "EncryptedDistanceMatrix", sk: "SecretKey"):
+    """aggregation.cpp:242-258 on the device (decrypt_values of every entry)."""
+    if m.mode != DistanceMode.per_pair:
+        raise UsageError("pair entries required to rebuild the full table")
+    count = int(m.batch.shape[2])
+    out = np.zeros((m.n, m.n), np.float64)
+    _check(lib().lcl_table_from_matrix(ctx.h, _ptr(m.batch.contiguous()), m.n, count, m.scale,
+                                       1 if m.reduced else 0, m.value_scale,
+                                       _ptr(sk.device_rows(count)), out.ctypes.data))
+    return DistanceTable(m.n, out)
+
+
+def totals_from_matrix(ctx: CkksContext, m: "EncryptedDistanceMatrix", sk: "SecretKey"):
+    """aggregation.cpp:260-277: per-row totals from either matrix mode."""
+    count = int(m.batch.shape[2])
+    out = np.zeros(m.n, np.float64)
+    _check(lib().lcl_totals_from_matrix(ctx.h, _ptr(m.batch.contiguous()), m.n,
+                                        0 if m.mode == DistanceMode.per_pair else 1, count,
+                                        m.scale, 1 if m.reduced else 0, m.value_scale,
+                                        _ptr(sk.device_rows(count)), out.ctypes.data))
+    return out
 
 
 def masked_aggregate(ctx: CkksContext, weights, mask: SelectionMask, rule: SelectionRule,

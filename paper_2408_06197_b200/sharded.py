@@ -76,10 +76,12 @@ def aligned_range(total: int, world: int, rank: int):
     return min(total, per * rank), min(total, per * (rank + 1))
 
 
-def _reduce_scatter_sum(dist, t, total, world, rank, group):
+def _reduce_scatter_sum(dist, t, total, world, rank, group, async_op=False):
     """Integer SUM of every rank's [total, ...] tensor, rank r keeping block r
     (aligned_range). NCCL reduce_scatter on B200; all_reduce + slice under
-    gloo, which has no reduce_scatter."""
+    gloo, which has no reduce_scatter. async_op: returns (work, result()) so
+    the caller can overlap independent work with the collective (NCCL runs
+    it on its own stream after the partials are ready)."""
     torch = __import__("torch")
     per = -(-total // world)
     pad = torch.zeros((per * world,) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
@@ -87,10 +89,36 @@ def _reduce_scatter_sum(dist, t, total, world, rank, group):
     b, e = aligned_range(total, world, rank)
     if dist.get_backend(group) == "nccl":
         out = torch.empty((per,) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
-        dist.reduce_scatter_tensor(out, pad, op=dist.ReduceOp.SUM, group=group)
-        return out[: e - b]
-    dist.all_reduce(pad, op=dist.ReduceOp.SUM, group=group)
-    return pad[b:e]
+        w = dist.reduce_scatter_tensor(out, pad, op=dist.ReduceOp.SUM, group=group,
+                                       async_op=async_op)
+        res = lambda: out[: e - b]  # noqa: E731
+    else:
+        w = dist.all_reduce(pad, op=dist.ReduceOp.SUM, group=group, async_op=async_op)
+        res = lambda: pad[b:e]  # noqa: E731
+    if not async_op:
+        return res()
+    return w, res
+
+
+def _gather_async(dist, local, total, unit_shape, world, group, aligned):
+    """all_gather of uneven shards started asynchronously; result() joins."""
+    torch = __import__("torch")
+    per = -(-total // world)
+    pad = torch.zeros((per,) + tuple(unit_shape), dtype=local.dtype, device=local.device)
+    pad[: local.shape[0]] = local
+    bufs = [torch.empty_like(pad) for _ in range(world)]
+    w = dist.all_gather(bufs, pad, group=group, async_op=True)
+
+    def result():
+        w.wait()
+        if aligned:
+            return torch.cat(bufs, dim=0)[:total]
+        parts = []
+        for r in range(world):
+            b, e = shard_range(total, world, r)
+            parts.append(bufs[r][: e - b])
+        return torch.cat(parts, dim=0)
+    return result
 
 
 def _gather_aligned(dist, local, total, unit_shape, world, group):
@@ -120,13 +148,17 @@ def chunk_sharded_server_round(n_pairs, n_chunks, dist_unit_shape, agg_unit_shap
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
     t = compute_partials()
-    summed = _reduce_scatter_sum(dist, t, n_pairs, world, rank, group)
-    p0, p1 = aligned_range(n_pairs, world, rank)
-    d_local = finish_pairs(p0, p1, summed, world)
+    # the reduce_scatter of the partials overlaps the chunk-local aggregate
+    # (independent of it), and the aggregate's all-gather overlaps the
+    # key-switch chains of this rank's pairs
+    work, summed = _reduce_scatter_sum(dist, t, n_pairs, world, rank, group, async_op=True)
     a_local = compute_chunks()
+    a_full = _gather_async(dist, a_local, n_chunks, agg_unit_shape, world, group, aligned=False)
+    work.wait()
+    p0, p1 = aligned_range(n_pairs, world, rank)
+    d_local = finish_pairs(p0, p1, summed(), world)
     d_full = _gather_aligned(dist, d_local, n_pairs, dist_unit_shape, world, group)
-    a_full = _gather(dist, a_local, n_chunks, agg_unit_shape, world, rank, group)
-    return d_full, a_full
+    return d_full, a_full()
 
 
 def cuda_chunk_shard_fns(ctx, local_clients, selectors, n, local_chunks, scale, sel_scale, width,

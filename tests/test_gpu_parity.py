@@ -235,6 +235,48 @@ def test_distance_modes_bit_exact_vs_reference(name):
             assert vals[p][0] == e["slot0"], p
 
 
+@pytest.mark.parametrize("name", ["tiny_krum", "cfg1", "tiny_perpair_kgc", "tiny_rowsums",
+                                  "tiny_rowsums_kgc", "n13_rowsums"])
+def test_kgc_distance_table_and_totals(name):
+    """table_from_matrix / totals_from_matrix (aggregation.cpp:242-277) on
+    the device: reduced entries give the reference's decrypted slot 0 (golden)
+    / value_scale clamped at 0; unreduced ones the left-to-right sum of the
+    oracle-decrypted slots; totals are the rows' left-to-right sums."""
+    L = _L()
+    rig = Rig(name, threads=8)
+    ctx = gpu_ctx(rig.N, secure=bool(rig.meta["options"]["secure"]))
+    mode = L.DistanceMode.row_sums if rig.mode == "row_sums" else L.DistanceMode.per_pair
+    dm = L.build_distance_matrix(ctx, _packed(L, rig), L.RelinKey(rig.oracle.relin_key()),
+                                 L.HoistPlan(k=rig.k, n=rig.width), mode,
+                                 L.RotationKeySet({s: rig.oracle.rotation_key(s)
+                                                   for s in rig.meta["rot_keys"]}),
+                                 L.DistanceOptions(reduce_on_server=rig.reduce))
+    sk = L.SecretKey(rig.oracle.secret_key())
+    words = L.to_host(dm.batch)
+    want = []
+    for p in range(len(dm.keys)):
+        if rig.reduce:
+            v = rig.meta["dist"][p]["slot0"]
+        else:
+            v = np.add.accumulate(rig.oracle.decrypt_values(words[p], dm.scale))[-1]
+        want.append(max(0.0, v / dm.value_scale))
+    totals = L.totals_from_matrix(ctx, dm, sk)
+    if mode == L.DistanceMode.per_pair:
+        t = L.table_from_matrix(ctx, dm, sk)
+        for p, (i, j) in enumerate(dm.keys):
+            assert t.d[i][j] == want[p] and t.d[j][i] == want[p]
+        assert all(t.d[i][i] == 0.0 for i in range(rig.n))
+        for i in range(rig.n):
+            acc = 0.0
+            for j in range(rig.n):
+                acc += t.d[i][j]
+            assert totals[i] == acc
+    else:
+        with pytest.raises(L.UsageError):
+            L.table_from_matrix(ctx, dm, sk)
+        assert list(totals) == want
+
+
 @pytest.mark.parametrize("name,lazy", [("tiny_krum", True), ("cfg1", True), ("tiny_eager", False)])
 def test_pairwise_distance_entry(name, lazy):
     """lcl_pairwise_distance (encrypted_pairwise_distance, distance.cpp:107-142)
