@@ -41,6 +41,13 @@ typedef unsigned __int128 u128;
 
 namespace {
 
+// CTAs/SM bound of ntt_blk_fwd<DivRoundInvStore>. At 16 (64 registers) it
+// spills 276 B per thread; 12 (80 registers, 12 B spill) and 10 measured
+// slower at cfg3 (9.51 / 10.26 vs 9.25 ms): the spills stay in L1.
+#ifndef LCL_INV_MINB
+#define LCL_INV_MINB 16
+#endif
+
 // ------------------------------------------------------------ errors
 thread_local std::string g_last_error;
 
@@ -453,7 +460,8 @@ void fwd2(lcl_context* c, u32 rows, const RowMap& mid, const Loader& ld, const E
     ProfScope ps(c, std::is_same<Epi, DivRoundStore>::value ? "ntt_blk_fwd<divround>" : "ntt_blk_fwd",
                  rb * (store_rows(epi, rows) + (std::is_same<Epi, PlainStore>::value ? rows : 0)),
                  bpr * rows * 8);
-    ntt_blk_fwd<LOGN1, Epi, 16><<<rows * N1 / 4, 64, 0, c->stream>>>(mid, epi, tabs(c));
+    constexpr int kMinB = std::is_same<Epi, DivRoundInvStore>::value ? LCL_INV_MINB : 16;
+  ntt_blk_fwd<LOGN1, Epi, kMinB><<<rows * N1 / 4, 64, 0, c->stream>>>(mid, epi, tabs(c));
   }
   post_launch(c, 2);
 }
@@ -544,7 +552,8 @@ void blk_fwd_n(lcl_context* c, u32 rows, const RowMap& mid, const Epi& epi) {
   // 16 CTAs per SM (64-register cap): measured cfg2 1.87 -> 1.49 ms, cfg3
   // 15.65 -> 11.44 ms against the unconstrained build (128 registers); the
   // same cap on ntt_blk_inv and a 10-CTA cap on modup_ip_blk were slower
-  ntt_blk_fwd<LOGN1, Epi, 16><<<rows * N1 / 4, 64, 0, c->stream>>>(mid, epi, tabs(c));
+  constexpr int kMinB = std::is_same<Epi, DivRoundInvStore>::value ? LCL_INV_MINB : 16;
+  ntt_blk_fwd<LOGN1, Epi, kMinB><<<rows * N1 / 4, 64, 0, c->stream>>>(mid, epi, tabs(c));
 }
 
 // Calls f(LOGN1, E) with compile-time constants for the two-pass ring sizes.
@@ -1189,7 +1198,7 @@ struct BlockedSchedule {
   const unsigned short* clist;
   u32 groups, per_cta, nl;
 };
-BlockedSchedule pair_schedule_blocked(lcl_context* c, u32 n, u32 cs_half) {
+BlockedSchedule pair_schedule_blocked(lcl_context* c, u32 n, u32 cs_half, const PairSet& ps) {
   std::vector<std::vector<u32>> blocks;
   for (u32 b0 = 0; b0 < n; b0 += kPairBlock) {
     blocks.emplace_back();
@@ -1220,19 +1229,39 @@ BlockedSchedule pair_schedule_blocked(lcl_context* c, u32 n, u32 cs_half) {
   auto local = [&](u32 g, u32 i) {
     return (u32)(std::find(cls[g].begin(), cls[g].end(), i) - cls[g].begin());
   };
-  u32 p = 0;
+  // output index of pair (i, j) in the set, or -1 (row-major range [a, b),
+  // or the j-major pairs of clients j in [a, b))
+  auto out_index = [&](u64 i, u64 j, u64 p) -> long long {
+    if (ps.kind == 0) return p >= ps.a && p < ps.b ? (long long)(p - ps.a) : -1;
+    if (j < ps.a || j >= ps.b) return -1;
+    return (long long)(j * (j - 1) / 2 - (u64)ps.a * (ps.a ? ps.a - 1 : 0) / 2 + i);
+  };
+  u64 p = 0;
   for (u32 i = 0; i < n; ++i)
     for (u32 j = i + 1; j < n; ++j, ++p) {
+      const long long o = out_index(i, j, p);
+      if (o < 0) continue;
       const u32 g = group_of(blk[i], blk[j]);
-      prs[g].push_back(make_uint2(local(g, i) | (local(g, j) << 16), p));
+      prs[g].push_back(make_uint2(local(g, i) | (local(g, j) << 16), (u32)o));
     }
+  {  // only groups with pairs of the set launch
+    std::vector<std::vector<u32>> c2;
+    std::vector<std::vector<uint2>> p2;
+    for (size_t g = 0; g < cls.size(); ++g)
+      if (!prs[g].empty()) {
+        c2.push_back(cls[g]);
+        p2.push_back(prs[g]);
+      }
+    cls.swap(c2);
+    prs.swap(p2);
+  }
   u32 per_cta = 0, nl = 0;
   for (size_t g = 0; g < cls.size(); ++g) {
     per_cta = std::max<u32>(per_cta, (u32)prs[g].size());
     nl = std::max<u32>(nl, (u32)cls[g].size());
   }
   const u32 groups = (u32)cls.size();
-  const auto key = std::make_tuple(n | (1u << 30), 0u, 0u, cs_half);
+  const auto key = std::make_tuple(n | (1u << 30) | (ps.kind << 31), ps.a, ps.b, cs_half);
   auto it = c->sched.find(key);
   if (it != c->sched.end()) {
     return {it->second, reinterpret_cast<const unsigned short*>(it->second + (size_t)groups * per_cta), groups,
@@ -1284,18 +1313,19 @@ bool pair_accumulate_f64_cfg(lcl_context* c, const u64* clients, u32 n, u32 chun
   static_assert(kPairBlock * kPairBlock <= MAXT, "an off-diagonal block pair fills one CTA");
   const u32 m = c->full;
   const u32 pairs = pair_count(n, ps);
-  // client-blocked groups once n exceeds two blocks and the set is the whole
-  // matrix (LCL_PAIR_BLOCKED=0 turns them off)
+  // client-blocked groups once n exceeds two blocks, for any pair set (whole
+  // matrix, a sub-batch or shard range, or a host-round group), so a CTA
+  // never stages more than 2 * kPairBlock clients (LCL_PAIR_BLOCKED=0 turns
+  // them off)
   const char* eb = std::getenv("LCL_PAIR_BLOCKED");
-  const bool blocked = ps.kind == 0 && ps.a == 0 && ps.b >= n * (n - 1) / 2 && n > 2 * kPairBlock + 1 &&
-                       !(eb && eb[0] == '0');
+  const bool blocked = n > 2 * kPairBlock + 1 && !(eb && eb[0] == '0');
   u32 groups = (pairs + MAXT - 1) / MAXT;
   u32 per_cta = (pairs + groups - 1) / groups;
   u32 nl = n, sched_len = pairs;
   const uint2* sched = nullptr;
   const unsigned short* clist = nullptr;
   if (blocked) {
-    const BlockedSchedule bs = pair_schedule_blocked(c, n, TE + 1);
+    const BlockedSchedule bs = pair_schedule_blocked(c, n, TE + 1, ps);
     sched = bs.sched;
     clist = bs.clist;
     groups = bs.groups;

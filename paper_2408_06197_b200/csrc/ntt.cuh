@@ -688,13 +688,30 @@ struct IpOps<FpF> {
   }
 };
 
+// LCL_MODUP_KEYS selects how the key words reach the inner product:
+//   0  __ldg per element (L1 serves the CTA's 4 groups);
+//   1  as 0, plus cp.async.bulk.prefetch.L2 of digit j+1's key rows and mid
+//      block while digit j transforms;
+//   2  TMA: the (target row, block) key rows of digit j are bulk-copied into
+//      shared memory (cp.async.bulk + mbarrier) by one thread, overlapping
+//      digit j's block stages; the buffer is refilled for j+1 after a CTA
+//      barrier.
+// Measured at cfg3 (modup_ip_blk<perm>, 13 levels x 190 ciphertexts): 0
+// 12.77 ms, 1 12.80, 2 13.31 -- the key words are L2 hits shared by the
+// CTA's 4 groups, and the 8 KB staging buffer costs one CTA per SM (6 vs 7),
+// so 0 is the default; 1 and 2 stay parity-tested (tools/build_variant.sh).
+#ifndef LCL_MODUP_KEYS
+#define LCL_MODUP_KEYS 0
+#endif
+
 template <class F, int LOGN1, int M>
 __device__ __forceinline__ void modup_ip_body(u32 bi, bool live, u32 t, u32 blk, u32 pi, u32 l,
                                               u64* s, u64* s0acc, u64* s1acc, ulonglong2* stw,
                                               const u64* mid,
                                               const u64* c1, u64 c1_stride, const u32* perm,
                                               const u64* key, const u64* key_aux, u32 full,
-                                              u64* acc, const NttTabs& tb) {
+                                              u64* acc, const NttTabs& tb, u64 (*skey)[256],
+                                              u64* kbar) {
   const u32 n = 1u << tb.logn;
   const PrimeConst P = tb.primes[pi];
   const typename F::K K = F::konst(P);
@@ -703,12 +720,33 @@ __device__ __forceinline__ void modup_ip_body(u32 bi, bool live, u32 t, u32 blk,
   // rotation: output block blk of every digit comes from block src_blk of the
   // unpermuted digit (block-local Galois permutation, see block_gather)
   const u32 src_blk = perm ? (__ldg(perm + (blk << 8)) >> 8) : blk;
+  constexpr u32 kRows = IpOps<F>::kRawKey ? 4 : 2;  // key rows the field reads per digit
+  auto key_rows = [&](int j, u32 r) -> const u64* {
+    const u64 off = (2ull * j + (r & 1)) * kstride + (u64)pi * n + (blk << 8);
+    return (IpOps<F>::kRawKey && r < 2 ? key : key_aux) + off;
+  };
+  if constexpr (LCL_MODUP_KEYS == 2) {
+    if (threadIdx.x == 0) {
+      mbar_init(kbar, 1);
+      mbar_expect_tx(kbar, kRows * 2048);
+      for (u32 r = 0; r < kRows; ++r) bulk_g2s(skey[r], key_rows(0, r), 2048, kbar);
+    }
+  }
   // the CTA's 4 groups share (target row, block): its twiddles are staged once
   stage_blk_tw<F>(stw, F::table(tb, false, pi), 1u << LOGN1, src_blk, threadIdx.x, 64);
   __syncthreads();
   const SmemTw<F> twa{stw};
 #pragma unroll 1
   for (int j = 0; j < M; ++j) {
+    if constexpr (LCL_MODUP_KEYS == 1) {
+      if (j + 1 < M) {
+        if (threadIdx.x < kRows) bulk_prefetch_l2(key_rows(j + 1, threadIdx.x), 2048);
+        if (l == 0 && t != (u32)(j + 1)) {
+          const u32 tp = t < (u32)(j + 1) ? t : t - 1;
+          bulk_prefetch_l2(mid + (((u64)bi * M + j + 1) * M + tp) * n + (src_blk << 8), 2048);
+        }
+      }
+    }
     typename F::T x[16];
     if (t == (u32)j) {
       const u64* src = c1 + (u64)bi * c1_stride + (u64)j * n + (src_blk << 8);
@@ -738,20 +776,41 @@ __device__ __forceinline__ void modup_ip_body(u32 bi, bool live, u32 t, u32 blk,
         for (int e = 0; e < 16; ++e) x[e] = F::unbits(o[e]);
       }
     }
-    const u64* k0 = key + (2ull * j) * kstride + (u64)pi * n;
-    const u64* k1 = k0 + kstride;
-    const u64* ks0 = key_aux + (2ull * j) * kstride + (u64)pi * n;
-    const u64* ks1 = ks0 + kstride;
+    if constexpr (LCL_MODUP_KEYS == 2) {
+      mbar_wait(kbar, (u32)j & 1u);
+      constexpr u32 A = IpOps<F>::kRawKey ? 2 : 0;  // shared rows of the Shoup / double words
 #pragma unroll
-    for (int e = 0; e < 16; ++e) {
-      const u32 a = a0 + 16 * e;
-      const u64 kw0 = IpOps<F>::kRawKey ? __ldg(k0 + a) : 0;
-      const u64 kw1 = IpOps<F>::kRawKey ? __ldg(k1 + a) : 0;
-      const u64 p0 = IpOps<F>::mul(x[e], kw0, __ldg(ks0 + a), K);
-      const u64 p1 = IpOps<F>::mul(x[e], kw1, __ldg(ks1 + a), K);
-      const u32 si = l + 16 * e;
-      s0acc[si] = j ? IpOps<F>::add(s0acc[si], p0) : p0;
-      s1acc[si] = j ? IpOps<F>::add(s1acc[si], p1) : p1;
+      for (int e = 0; e < 16; ++e) {
+        const u32 si = l + 16 * e;
+        const u64 kw0 = IpOps<F>::kRawKey ? skey[0][si] : 0;
+        const u64 kw1 = IpOps<F>::kRawKey ? skey[1][si] : 0;
+        const u64 p0 = IpOps<F>::mul(x[e], kw0, skey[A][si], K);
+        const u64 p1 = IpOps<F>::mul(x[e], kw1, skey[A + 1][si], K);
+        s0acc[si] = j ? IpOps<F>::add(s0acc[si], p0) : p0;
+        s1acc[si] = j ? IpOps<F>::add(s1acc[si], p1) : p1;
+      }
+      __syncthreads();  // every group has read digit j's keys
+      if (j + 1 < M && threadIdx.x == 0) {
+        fence_proxy_async();
+        mbar_expect_tx(kbar, kRows * 2048);
+        for (u32 r = 0; r < kRows; ++r) bulk_g2s(skey[r], key_rows(j + 1, r), 2048, kbar);
+      }
+    } else {
+      const u64* k0 = key + (2ull * j) * kstride + (u64)pi * n;
+      const u64* k1 = k0 + kstride;
+      const u64* ks0 = key_aux + (2ull * j) * kstride + (u64)pi * n;
+      const u64* ks1 = ks0 + kstride;
+#pragma unroll
+      for (int e = 0; e < 16; ++e) {
+        const u32 a = a0 + 16 * e;
+        const u64 kw0 = IpOps<F>::kRawKey ? __ldg(k0 + a) : 0;
+        const u64 kw1 = IpOps<F>::kRawKey ? __ldg(k1 + a) : 0;
+        const u64 p0 = IpOps<F>::mul(x[e], kw0, __ldg(ks0 + a), K);
+        const u64 p1 = IpOps<F>::mul(x[e], kw1, __ldg(ks1 + a), K);
+        const u32 si = l + 16 * e;
+        s0acc[si] = j ? IpOps<F>::add(s0acc[si], p0) : p0;
+        s1acc[si] = j ? IpOps<F>::add(s1acc[si], p1) : p1;
+      }
     }
   }
   if (!live) return;
@@ -775,6 +834,13 @@ __global__ void __launch_bounds__(64, MINB)
   __shared__ u64 sm[4][256 + 16];
   __shared__ u64 sacc[4][2][256];  // lazy accumulators, coalesced order
   __shared__ ulonglong2 stw[kBlkTw];
+#if LCL_MODUP_KEYS == 2
+  __shared__ alignas(128) u64 skey[4][256];  // digit j's key rows (TMA)
+  __shared__ u64 kbar;
+#else
+  u64(*skey)[256] = nullptr;
+  u64* kbar_p = nullptr;
+#endif
   const u32 l = threadIdx.x & 15, bw = threadIdx.x >> 4;
   // the 4 groups of a CTA take 4 consecutive ciphertexts of the same
   // (target row, block): the key words they share are served from L1
@@ -789,12 +855,15 @@ __global__ void __launch_bounds__(64, MINB)
   const bool live = bi_raw < B;
   const u32 bi = live ? bi_raw : B - 1;
   const u32 pi = t < (u32)M ? t : full;
+#if LCL_MODUP_KEYS == 2
+  u64* kbar_p = &kbar;
+#endif
   if (row_fp(tb, pi))
     modup_ip_body<FpF, LOGN1, M>(bi, live, t, blk, pi, l, sm[bw], sacc[bw][0], sacc[bw][1], stw, mid, c1,
-                                 c1_stride, perm, key, key_aux, full, acc, tb);
+                                 c1_stride, perm, key, key_aux, full, acc, tb, skey, kbar_p);
   else
     modup_ip_body<IntF, LOGN1, M>(bi, live, t, blk, pi, l, sm[bw], sacc[bw][0], sacc[bw][1], stw, mid, c1,
-                                  c1_stride, perm, key, key_aux, full, acc, tb);
+                                  c1_stride, perm, key, key_aux, full, acc, tb, skey, kbar_p);
 }
 
 // Hoisted rotations (ckks.cpp:582-612) fused like modup_ip_blk: ONE ModUp

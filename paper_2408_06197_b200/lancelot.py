@@ -32,7 +32,8 @@ from enum import Enum
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "_lib", "liblancelot_b200.so")
+# LCL_LIB_PATH: an alternative in-tree build for A/B experiments (tools/)
+LIB_PATH = os.environ.get("LCL_LIB_PATH") or os.path.join(HERE, "_lib", "liblancelot_b200.so")
 
 
 # --------------------------------------------------------------- errors

@@ -662,6 +662,52 @@ def test_pair_accumulation_long_ranges_and_extremes(pair_f64, n, C, blocked, mon
     assert np.array_equal(L.to_host(dm.batch), want)
 
 
+@pytest.mark.parametrize("n", [60, 190])
+def test_pair_ranges_of_many_clients(n):
+    """Client-blocked pair groups for ANY pair set: pair
+    sub-ranges of 60 and 190 clients (lcl_distance_matrix_pairs, unreduced:
+    accumulation + relinearize + rescale) and the whole 190-client matrix's
+    lazy partials (lcl_pair_partials) equal the oracle's -- a CTA never stages
+    more than 26 clients, so there is no client-count limit (formerly
+    'too many clients for one tile' from 178 clients)."""
+    L = _L()
+    import ctypes as C
+    import torch
+    N = 256
+    orc = Oracle(N, secure=False, threads=8)
+    orc.keygen(3, [])
+    rng = np.random.default_rng(n)
+    m = orc.full
+    Cc = 2
+    clients = np.zeros((n, Cc, 2, m, N), np.uint64)
+    for r in range(m):
+        clients[:, :, :, r] = rng.integers(0, orc.primes[r], size=(n, Cc, 2, N), dtype=np.uint64)
+    ctx = L.CkksContext(L.CkksParams(ring_degree=N, security=L.SecurityLevel.none))
+    ctx.use_relin_key(L.RelinKey(orc.relin_key()))
+    dev = L.to_device(clients)
+    P = n * (n - 1) // 2
+    osc = C.c_double()
+    for a, b in ((0, 37), (P // 3, P // 3 + 500), (P - 70, P)):
+        out = torch.empty((b - a, 2, m - 1, N), dtype=torch.int64, device="cuda")
+        L._check(L.lib().lcl_distance_matrix_pairs(ctx.h, L._ptr(dev), n, Cc, orc.scale, 1, 1, 1, 0,
+                                                   a, b, L._ptr(out), C.byref(osc)))
+        got = L.to_host(out)
+        pairs = [(i, j) for i in range(n) for j in range(i + 1, n)][a:b]
+        for q in range(0, b - a, 23):
+            i, j = pairs[q]
+            assert np.array_equal(got[q], orc.pairwise_distance(clients[i], clients[j])), (a, q)
+    if n == 190:
+        t = torch.empty((P, 3, m, N), dtype=torch.int64, device="cuda")
+        L._check(L.lib().lcl_pair_partials(ctx.h, L._ptr(dev), n, Cc, L._ptr(t)))
+        got = L.to_host(t)
+        pairs = [(i, j) for i in range(n) for j in range(i + 1, n)]
+        for q in range(0, P, 997):
+            i, j = pairs[q]
+            acc = orc.hsquare(orc.hsub(clients[i, 0], clients[j, 0]))
+            orc.lazy_accumulate(acc, orc.hsquare(orc.hsub(clients[i, 1], clients[j, 1])))
+            assert np.array_equal(got[q], acc), q
+
+
 def test_cfg3_benchmark_round_bit_exact_vs_reference():
     """BASELINE configs[2] exactly as bench.py times it: 20 clients x
     11,173,962 params (342 chunks), N = 2^16, lazy relin, hoisted rotations

@@ -1,7 +1,7 @@
 """Summarise an ncu --set full report: per launch duration, DRAM traffic,
 pipe utilisation, occupancy and the top warp stall reasons.
 
-    python tools/ncu_summary.py gpurun_out/prof.ncu-rep [--md]
+    python tools/ncu_summary.py gpurun_out/prof.ncu-rep|raw.csv [--md]
 """
 import csv
 import subprocess
@@ -25,8 +25,11 @@ STALLS = "smsp__average_warps_issue_stalled_"
 
 
 def load(path):
-    out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True,
-                         text=True, check=True).stdout
+    if path.endswith(".csv"):  # an exported `--page raw --csv` listing
+        out = open(path).read()
+    else:
+        out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True,
+                             text=True, check=True).stdout
     rows = list(csv.reader(out.splitlines()))
     return rows[0], rows[1], rows[2:]
 

@@ -23,6 +23,8 @@ def bench_name(kernel):
     k = kernel.split("(")[0].replace("void ", "").replace("lcl::", "").strip()
     base = k.split("<")[0]
     if base == "ntt_blk_fwd":
+        if "DivRoundInvStore" in k:
+            return "ntt_blk_fwd<divround+inv>"
         return "ntt_blk_fwd<divround>" if "DivRoundStore" in k else "ntt_blk_fwd"
     if base.startswith("pair_accumulate"):
         return "pair_accumulate"
