@@ -43,6 +43,13 @@ struct NttTabs {
   const double2* twf;     // (psi^brv, psi^brv / q) as doubles
   const double2* itwf;
   const PrimeConst* primes;
+  // Block-pass twiddles re-ordered per 256-point block (two-pass rings):
+  // btw[p][b][pos], pos = blk_tw_pos(lm, g, l), so the 16 lanes of a block
+  // read 16 consecutive entries at every stage (see ntt.cuh GlobalTw).
+  const ulonglong2* btw;
+  const ulonglong2* bitw;
+  const double2* btwf;
+  const double2* bitwf;
   u32 fp_mask;
   u32 logn;
 };

@@ -14,6 +14,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <array>
 #include <cmath>
 #include <complex>
 #include <cstdio>
@@ -44,6 +45,14 @@ namespace {
 // CTAs/SM bound of ntt_blk_fwd<DivRoundInvStore>. At 16 (64 registers) it
 // spills 276 B per thread; 12 (80 registers, 12 B spill) and 10 measured
 // slower at cfg3 (9.51 / 10.26 vs 9.25 ms): the spills stay in L1.
+// CTAs/SM bound of the fused column pass at E = 16. With the source tile
+// parked in shared memory (LCL_COL_VSMEM, 64 KB per CTA) 3 CTAs fit, at 80
+// registers and no spill: cfg3 column passes 17.43 -> 16.98 ms against
+// 4 CTAs at 64 registers with 900 B of spill loads per thread (2 CTAs at
+// 128 registers: 17.77 ms).
+#ifndef LCL_COL_MINB
+#define LCL_COL_MINB 3
+#endif
 #ifndef LCL_INV_MINB
 #define LCL_INV_MINB 16
 #endif
@@ -266,6 +275,11 @@ struct lcl_context {
   ulonglong2* d_itw = nullptr;
   double2* d_twf = nullptr;   // (w, w / q) doubles for FP64 rows
   double2* d_itwf = nullptr;
+  // block-ordered copies for the 256-point block passes (ntt.cuh blk_tw_pos)
+  ulonglong2* d_btw = nullptr;
+  ulonglong2* d_bitw = nullptr;
+  double2* d_btwf = nullptr;
+  double2* d_bitwf = nullptr;
   u32 fp_mask = 0;            // primes whose rows run on the FP64 pipe
   bool pair_f64 = false;      // q-chain below 2^44: pair accumulation on the FP64 pipe
   u64* d_smod = nullptr;
@@ -375,6 +389,10 @@ NttTabs tabs(const lcl_context* c) {
   t.itw = c->d_itw;
   t.twf = c->d_twf;
   t.itwf = c->d_itwf;
+  t.btw = c->d_btw;
+  t.bitw = c->d_bitw;
+  t.btwf = c->d_btwf;
+  t.bitwf = c->d_bitwf;
   t.primes = c->d_primes;
   t.fp_mask = c->fp_mask;
   t.logn = (u32)c->logn;
@@ -520,7 +538,7 @@ void blk_inv_n(lcl_context* c, u32 rows, const RowMap& in, const RowMap& out) {
 template <int LOGN1, int E, int MINB>
 void col_ilf_cfg(lcl_context* c, u32 src_rows, const RowMap& src, const RowMap& dst, u32 fan) {
   constexpr int N1 = 1 << LOGN1;
-  constexpr size_t smem = (size_t)N1 * 16 * 8;
+  constexpr size_t smem = (size_t)N1 * 16 * 8 * (LCL_COL_VSMEM && E == 16 ? 2 : 1);
   static bool once = (allow_smem(ntt_col_inv_lift_fwd<LOGN1, E, MINB>, smem), true);
   (void)once;
   const u32 groups = (u32)(c->n >> LOGN1) >> 4;
@@ -537,7 +555,7 @@ void col_ilf_cfg(lcl_context* c, u32 src_rows, const RowMap& src, const RowMap& 
 // phases need E^2 >= N1, i.e. R = N1 / E <= E.)
 template <int LOGN1, int E>
 void col_ilf_n(lcl_context* c, u32 src_rows, const RowMap& src, const RowMap& dst, u32 fan) {
-  col_ilf_cfg<LOGN1, E, E == 16 ? 4 : 2>(c, src_rows, src, dst, fan);
+  col_ilf_cfg<LOGN1, E, E == 16 ? LCL_COL_MINB : 2>(c, src_rows, src, dst, fan);
 }
 
 template <int LOGN1, class Epi>
@@ -624,7 +642,11 @@ void modup_ip_launch(lcl_context* c, u32 B, const u64* mid, const u64* c1, u64 c
   ProfScope ps(c, perm ? "modup_ip_blk<perm>" : "modup_ip_blk",
                rb * ((double)B * M * M + B * M + 4.0 * M * (M + 1) + 2.0 * B * (M + 1)),
                0.5 * c->N() * B * M * M * 8);
-  modup_ip_blk<LOGN1, M><<<((B + 3) / 4) * (M + 1) * N1, 64, 0, c->stream>>>(
+  constexpr size_t smem = modup_smem_bytes(LCL_MODUP_G);
+  static bool once = (allow_smem(modup_ip_blk<LOGN1, M>, smem), true);
+  (void)once;
+  modup_ip_blk<LOGN1, M><<<((B + LCL_MODUP_G - 1) / LCL_MODUP_G) * (M + 1) * N1, 16 * LCL_MODUP_G, smem,
+                           c->stream>>>(
       B, mid, c1, c1_stride, perm, key, key_shoup, c->full, acc, tabs(c));
 }
 
@@ -796,6 +818,7 @@ void ks_hoisted(lcl_context* c, const RowMap& in, const u64* c1, u64 c1_stride, 
       hs.key_aux[i] = c->d_rot_shoup.at(st);
     }
     const double rb = 8.0 * N;
+    {  // (scope: the launch only, not the ModDowns below)
     ProfScope ps(c, "modup_ip_hoist",
                  rb * ((double)B * m * m + (double)B * m + 2.0 * ns * m * (m + 1) +
                        2.0 * ns * B * (m + 1)),
@@ -811,6 +834,7 @@ void ks_hoisted(lcl_context* c, const RowMap& in, const u64* c1, u64 c1_stride, 
       switch (m) { LCL_HOIST(1) LCL_HOIST(2) LCL_HOIST(3) LCL_HOIST(4) }
 #undef LCL_HOIST
     });
+    }
     post_launch(c);
     for (u32 i = 0; i < ns; ++i) each(s0 + i, acc + i * acc_step);
   }
@@ -1357,7 +1381,11 @@ bool pair_accumulate_f64_cfg(lcl_context* c, const u64* clients, u32 n, u32 chun
 // <4,8,2,true> 30.0, <2,8,4,false> 45.7; split-23 integer kernel 50.3; a
 // warp-specialised variant -- producer warp, full/empty mbarriers, no CTA
 // barrier -- ran 29.6 ms with cp.async and 55 ms with 64-byte TMA bulk
-// copies, which are issue-bound at this row size),
+// copies, which are issue-bound at this row size; round 2: a client-quad
+// form (a thread owns a 2 x 2 block of pairs {i1,i2} x {j1,j2}, half the
+// staged words per pair-slot for the same FP64 work) ran 35.6 ms with one
+// slot per thread (400 threads, 1 CTA/SM) and 36.3 ms with two (128
+// registers, 2 CTAs/SM) against 25.4 ms -- parity-green, not kept),
 // else the split-23 integer kernel.
 void pair_accumulate_launch(lcl_context* c, const u64* clients, u32 n, u32 chunks, u32 c0,
                             u32 c1, const PairSet& ps, u64* tern, bool accumulate) {
@@ -2102,6 +2130,33 @@ void build_context(lcl_context* c, size_t degree, int depth, int secure, int dev
   cuda_check(cudaMemcpy(c->d_itw, itw.data(), P * n * sizeof(ulonglong2), cudaMemcpyHostToDevice), "upload");
   cuda_check(cudaMemcpy(c->d_twf, twf.data(), P * n * sizeof(double2), cudaMemcpyHostToDevice), "upload");
   cuda_check(cudaMemcpy(c->d_itwf, itwf.data(), P * n * sizeof(double2), cudaMemcpyHostToDevice), "upload");
+  if (c->logn >= 13) {
+    // block-ordered tables: block b (N1 = n / 256 blocks) holds
+    // root[(N1 + b) 2^lm + i] at blk_tw_pos(lm, i mod 2^(lm-4), i div 2^(lm-4))
+    // (lm >= 4), 2^lm - 1 + i (lm < 4); entry 255 of each block is unused
+    const size_t n1 = n >> 8;
+    std::vector<ulonglong2> btw(P * n, make_ulonglong2(0, 0)), bitw(P * n, make_ulonglong2(0, 0));
+    std::vector<double2> btwf(P * n, make_double2(0, 0)), bitwf(P * n, make_double2(0, 0));
+    for (u32 i = 0; i < P; ++i)
+      for (size_t b = 0; b < n1; ++b)
+        for (int lm = 0; lm < 8; ++lm)
+          for (u32 x = 0; x < (1u << lm); ++x) {
+            const u32 pos = lm < 4 ? blk_tw_pos(lm, x, 0) : blk_tw_pos(lm, x & ((1u << (lm - 4)) - 1), x >> (lm - 4));
+            const size_t src = i * n + (n1 + b) * ((size_t)1 << lm) + x, dst = i * n + b * 256 + pos;
+            btw[dst] = tw[src];
+            bitw[dst] = itw[src];
+            btwf[dst] = twf[src];
+            bitwf[dst] = itwf[src];
+          }
+    cuda_check(cudaMalloc(&c->d_btw, P * n * sizeof(ulonglong2)), "alloc");
+    cuda_check(cudaMalloc(&c->d_bitw, P * n * sizeof(ulonglong2)), "alloc");
+    cuda_check(cudaMalloc(&c->d_btwf, P * n * sizeof(double2)), "alloc");
+    cuda_check(cudaMalloc(&c->d_bitwf, P * n * sizeof(double2)), "alloc");
+    cuda_check(cudaMemcpy(c->d_btw, btw.data(), P * n * sizeof(ulonglong2), cudaMemcpyHostToDevice), "upload");
+    cuda_check(cudaMemcpy(c->d_bitw, bitw.data(), P * n * sizeof(ulonglong2), cudaMemcpyHostToDevice), "upload");
+    cuda_check(cudaMemcpy(c->d_btwf, btwf.data(), P * n * sizeof(double2), cudaMemcpyHostToDevice), "upload");
+    cuda_check(cudaMemcpy(c->d_bitwf, bitwf.data(), P * n * sizeof(double2), cudaMemcpyHostToDevice), "upload");
+  }
   c->fp_mask = fp_rows(c->primes);
   {
     // pair_accumulate_f64 needs |x - y| < 2^44 for every q-chain residue
@@ -2130,6 +2185,10 @@ void free_context(lcl_context* c) {
   cudaFree(c->d_itw);
   cudaFree(c->d_twf);
   cudaFree(c->d_itwf);
+  cudaFree(c->d_btw);
+  cudaFree(c->d_bitw);
+  cudaFree(c->d_btwf);
+  cudaFree(c->d_bitwf);
   cudaFree(c->d_smod);
   cudaFree(c->d_pinv);
   cudaFree(c->d_pairs);

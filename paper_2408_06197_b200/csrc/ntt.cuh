@@ -55,6 +55,9 @@ struct IntF {
   __device__ static __forceinline__ TwPtr table(const NttTabs& t, bool inv, u32 pi) {
     return (inv ? t.itw : t.tw) + ((u64)pi << t.logn);
   }
+  __device__ static __forceinline__ TwPtr btable(const NttTabs& t, bool inv, u32 pi) {
+    return (inv ? t.bitw : t.btw) + ((u64)pi << t.logn);
+  }
   __device__ static __forceinline__ Tw ld(TwPtr t, u32 idx) {
     const ulonglong2 v = __ldg(t + idx);
     return Tw{v.x, v.y};
@@ -104,6 +107,9 @@ struct FpF {
   __device__ static __forceinline__ K konst(const PrimeConst& P) { return K{P.qf, P.qinvf, P.q}; }
   __device__ static __forceinline__ TwPtr table(const NttTabs& t, bool inv, u32 pi) {
     return (inv ? t.itwf : t.twf) + ((u64)pi << t.logn);
+  }
+  __device__ static __forceinline__ TwPtr btable(const NttTabs& t, bool inv, u32 pi) {
+    return (inv ? t.bitwf : t.btwf) + ((u64)pi << t.logn);
   }
   __device__ static __forceinline__ Tw ld(TwPtr t, u32 idx) {
     const double2 v = __ldg(t + idx);
@@ -460,34 +466,40 @@ __global__ void __launch_bounds__(16 * ((1 << LOGN1) / E))
     col_fwd_body<IntF, LOGN1, E>(out, ld, tb, sm, r, j, c, k, pi);
 }
 
-// Block-pass twiddles in shared memory. Block b's 8 local stages use
-// root[(N1 + b) 2^lm + i], i < 2^lm, lm = 0..7: 255 entries, staged once per
-// CTA at slot 2^lm - 1 + i by all its threads (every group of the CTA works
-// on block b of a row of the same prime), so the stages read them with
-// shared-memory latency instead of an L1/L2 round trip per stage.
-constexpr int kBlkTw = 256;  // staged entries per CTA (255 used)
+// Block-pass twiddles. Block b's 8 local stages use root[(N1 + b) 2^lm + i],
+// i < 2^lm, lm = 0..7 (255 entries). In the first 4 stages (lane l holds
+// elements l + 16 e) i = g is the same for all 16 lanes; in the last 4 (lane l
+// holds 16 l + e) lane l needs i = l 2^(lm-4) + g, g < 2^(lm-4), so in the
+// reference's order the 16 lanes would read entries 2^(lm-4) apart -- up to a
+// 16-way shared-memory bank conflict (16 distinct L1 lines from global) at
+// lm = 7. The context therefore keeps a block-ordered copy of the table
+// (NttTabs::btw..): per block 256 entries, entry (lm, g) of lane l at
+//   lm < 4:  2^lm - 1 + g                          (uniform: broadcast)
+//   lm >= 4: 15 + (2^(lm-4) - 1 + g) * 16 + l      (16 consecutive entries)
+// so every stage reads one contiguous 256-byte run per 16 lanes.
+__host__ __device__ __forceinline__ u32 blk_tw_pos(int lm, u32 g, u32 l) {
+  return lm < 4 ? (1u << lm) - 1 + g : 15 + ((1u << (lm - 4)) - 1 + g) * 16 + l;
+}
+constexpr int kBlkTw = 256;  // entries per block (255 used)
+// The CTA's block table (4 KB, contiguous) staged into shared memory once.
 template <class F>
-__device__ __forceinline__ void stage_blk_tw(ulonglong2* stw, typename F::TwPtr tw, u32 n1, u32 b,
-                                             u32 tid, u32 nthr) {
-  const ulonglong2* t = reinterpret_cast<const ulonglong2*>(tw);
-  for (u32 k = tid; k < 255; k += nthr) {
-    const u32 lm = 31 - __clz(k + 1);
-    stw[k] = __ldg(t + (n1 + b) * (1u << lm) + (k + 1 - (1u << lm)));
-  }
+__device__ __forceinline__ void stage_blk_tw(ulonglong2* stw, typename F::TwPtr btab_block, u32 tid,
+                                             u32 nthr) {
+  const ulonglong2* t = reinterpret_cast<const ulonglong2*>(btab_block);
+  for (u32 k = tid; k < (u32)kBlkTw; k += nthr) stw[k] = __ldg(t + k);
 }
 template <class F>
-struct GlobalTw {  // root[(N1 + b) 2^lm + i] straight from the table (L1 / L2)
+struct GlobalTw {  // the block's 256 block-ordered entries straight from the table (L1 / L2)
   typename F::TwPtr tw;
-  u32 base;  // N1 + b
-  __device__ __forceinline__ typename F::Tw operator()(int lm, u32 i) const {
-    return F::ld(tw, base * (1u << lm) + i);
+  __device__ __forceinline__ typename F::Tw operator()(int lm, u32 g, u32 l) const {
+    return F::ld(tw, blk_tw_pos(lm, g, l));
   }
 };
 template <class F>
 struct SmemTw {
   const ulonglong2* stw;
-  __device__ __forceinline__ typename F::Tw operator()(int lm, u32 i) const {
-    const ulonglong2 v = stw[(1u << lm) - 1 + i];
+  __device__ __forceinline__ typename F::Tw operator()(int lm, u32 g, u32 l) const {
+    const ulonglong2 v = stw[blk_tw_pos(lm, g, l)];
     typename F::Tw w;
     if constexpr (std::is_same<F, FpF>::value) {
       w.w = __longlong_as_double((long long)v.x);
@@ -510,7 +522,7 @@ __device__ __forceinline__ void blk_fwd_body(typename F::T (&x)[16], u64 (&o)[16
                                              const Fin& fin) {
   static_for<0, 4, 1>([&](auto LM) {
     constexpr int lm = decltype(LM)::value;
-    ct_stage<F, 16, (16 >> (lm + 1))>(x, [&](int gi) { return twa(lm, (u32)gi); }, K);
+    ct_stage<F, 16, (16 >> (lm + 1))>(x, [&](int gi) { return twa(lm, (u32)gi, l); }, K);
   });
 #pragma unroll
   for (int e = 0; e < 16; ++e) s[l + 16 * e + e] = F::bits(x[e]);
@@ -520,7 +532,7 @@ __device__ __forceinline__ void blk_fwd_body(typename F::T (&x)[16], u64 (&o)[16
   static_for<4, 8, 1>([&](auto LM) {
     constexpr int lm = decltype(LM)::value;
     constexpr int d = 256 >> (lm + 1);
-    ct_stage<F, 16, d>(x, [&](int gi) { return twa(lm, (16 * l + gi * 2 * d) >> (8 - lm)); }, K);
+    ct_stage<F, 16, d>(x, [&](int gi) { return twa(lm, (u32)gi, l); }, K);
   });
   __syncwarp();
 #pragma unroll
@@ -545,7 +557,7 @@ __device__ __forceinline__ void blk_inv_body(typename F::T (&x)[16], u64* s, con
   static_for<7, 3, -1>([&](auto LM) {
     constexpr int lm = decltype(LM)::value;
     constexpr int d = 256 >> (lm + 1);
-    gs_stage<F, 16, d>(x, [&](int gi) { return twa(lm, (16 * l + gi * 2 * d) >> (8 - lm)); }, K);
+    gs_stage<F, 16, d>(x, [&](int gi) { return twa(lm, (u32)gi, l); }, K);
   });
   F::gs_fix(x, K);
   __syncwarp();
@@ -557,7 +569,7 @@ __device__ __forceinline__ void blk_inv_body(typename F::T (&x)[16], u64* s, con
   __syncwarp();
   static_for<3, -1, -1>([&](auto LM) {
     constexpr int lm = decltype(LM)::value;
-    gs_stage<F, 16, (16 >> (lm + 1))>(x, [&](int gi) { return twa(lm, (u32)gi); }, K);
+    gs_stage<F, 16, (16 >> (lm + 1))>(x, [&](int gi) { return twa(lm, (u32)gi, l); }, K);
   });
   F::gs_fix(x, K);
 }
@@ -590,7 +602,7 @@ __device__ __forceinline__ void blk_fwd_kernel_body(const RowMap& in, const Epi&
 #pragma unroll
   for (int e = 0; e < 16; ++e) x[e] = F::unbits(src[l + 16 * e]);
   u64 o[16];
-  const GlobalTw<F> twa{F::table(tb, false, pi), (1u << LOGN1) + b};
+  const GlobalTw<F> twa{F::btable(tb, false, pi) + b * kBlkTw};
   blk_fwd_body<F>(x, o, s, twa, l, K, [&](typename F::T v) -> u64 {
     if (std::is_same<F, FpF>::value || Epi::kNeedsReduced) return F::canon(v, K);
     return F::bits(v);
@@ -618,7 +630,7 @@ __device__ __forceinline__ void blk_fwd_kernel_body(const RowMap& in, const Epi&
       __syncwarp();  // s[] (permuted add2 staging) is reused by the inverse body
 #pragma unroll
       for (int e = 0; e < 16; ++e) x[e] = F::from_u64(o[e]);
-      blk_inv_body<F>(x, s, GlobalTw<F>{F::table(tb, true, pi), (1u << LOGN1) + b}, l, K);
+      blk_inv_body<F>(x, s, GlobalTw<F>{F::btable(tb, true, pi) + b * kBlkTw}, l, K);
       u64* dst = row_ptr(epi.inv_out, r) + (b << 8);
 #pragma unroll
       for (int e = 0; e < 16; ++e) dst[l + 16 * e] = F::bits(x[e]);
@@ -627,9 +639,13 @@ __device__ __forceinline__ void blk_fwd_kernel_body(const RowMap& in, const Epi&
 }
 
 // Block pass, forward: 256-point blocks, 16 threads per block, 16 elements per
-// thread, 4 consecutive blocks of one row per CTA. (Staging the twiddles in
-// shared memory with 4 same-prime rows per CTA was measured slower here:
-// cfg2 ntt_blk_fwd<divround> 1.55 -> 1.88 ms.)
+// thread, 4 consecutive blocks of one row per CTA. (4 same-prime rows per CTA
+// sharing block b's twiddles through L1 was measured slower at cfg3, also
+// with the conflict-free block-ordered table: ntt_blk_fwd<divround+inv>
+// 7.99 -> 12.18 ms, <divround> 4.58 -> 5.38, ntt_blk_inv 3.99 -> 4.05; most
+// of that was the 16-lane __syncwarp mask the divergent groups needed:
+// with the full-warp barrier kept, <divround+inv> alone costs 7.99 vs 11.86 ms
+// with the half-warp mask.)
 template <int LOGN1, class Epi, int MINB = 1>
 __global__ void __launch_bounds__(64, MINB)
     ntt_blk_fwd(const __grid_constant__ RowMap in, const __grid_constant__ Epi epi,
@@ -703,6 +719,12 @@ struct IpOps<FpF> {
 #ifndef LCL_MODUP_KEYS
 #define LCL_MODUP_KEYS 0
 #endif
+// (Measured and rejected at cfg3, modup_ip_blk<perm>, 13 levels: a register
+// software pipeline loading digit j + 1's block while digit j computes,
+// 12.84 -> 13.47 ms at 6 CTAs/SM and 14.62 at 8; 2 or 4 ciphertext quads per
+// CTA so the staged twiddles are reused, 12.93 / 12.95 ms; after the
+// block-ordered twiddles (11.48 ms), the accumulators in registers instead
+// of shared memory, 13.09 ms at 6 CTAs/SM and 14.80 at 8.)
 
 template <class F, int LOGN1, int M>
 __device__ __forceinline__ void modup_ip_body(u32 bi, bool live, u32 t, u32 blk, u32 pi, u32 l,
@@ -733,7 +755,7 @@ __device__ __forceinline__ void modup_ip_body(u32 bi, bool live, u32 t, u32 blk,
     }
   }
   // the CTA's 4 groups share (target row, block): its twiddles are staged once
-  stage_blk_tw<F>(stw, F::table(tb, false, pi), 1u << LOGN1, src_blk, threadIdx.x, 64);
+  stage_blk_tw<F>(stw, F::btable(tb, false, pi) + src_blk * kBlkTw, threadIdx.x, blockDim.x);
   __syncthreads();
   const SmemTw<F> twa{stw};
 #pragma unroll 1
@@ -824,16 +846,27 @@ __device__ __forceinline__ void modup_ip_body(u32 bi, bool live, u32 t, u32 blk,
   }
 }
 
-template <int LOGN1, int M, int MINB = 8>
-__global__ void __launch_bounds__(64, MINB)
+// LCL_MODUP_G: 16-lane groups (ciphertexts) per CTA; MINB keeps 128
+// registers. 8 groups (4 CTAs / SM, 16 warps, 53 KB shared) against 4 (7
+// CTAs / SM: shared-memory bound, 14 warps): cfg3 modup_ip_blk<perm>
+// 11.28 -> 10.53 ms, relinearisation 3.44 -> 3.29 ms.
+#ifndef LCL_MODUP_G
+#define LCL_MODUP_G 8
+#endif
+constexpr size_t modup_smem_bytes(int G) { return (size_t)G * (256 + 16 + 512) * 8 + kBlkTw * 16; }
+template <int LOGN1, int M, int G = LCL_MODUP_G, int MINB = 32 / G>
+__global__ void __launch_bounds__(16 * G, MINB)
     modup_ip_blk(u32 B, const u64* __restrict__ mid, const u64* __restrict__ c1, u64 c1_stride,
                  const u32* __restrict__ perm, const u64* __restrict__ key,
                  const u64* __restrict__ key_aux, u32 full, u64* __restrict__ acc,
                  const __grid_constant__ NttTabs tb) {
   constexpr int N1 = 1 << LOGN1;
-  __shared__ u64 sm[4][256 + 16];
-  __shared__ u64 sacc[4][2][256];  // lazy accumulators, coalesced order
-  __shared__ ulonglong2 stw[kBlkTw];
+  // dynamic shared memory (modup_smem_bytes): [G][272] block transposes,
+  // [G][2][256] lazy accumulators (coalesced order), the block's twiddles
+  extern __shared__ u64 dyn_sm[];
+  u64(*sm)[256 + 16] = reinterpret_cast<u64(*)[256 + 16]>(dyn_sm);
+  u64(*sacc)[2][256] = reinterpret_cast<u64(*)[2][256]>(dyn_sm + G * (256 + 16));
+  ulonglong2* stw = reinterpret_cast<ulonglong2*>(dyn_sm + G * (256 + 16 + 512));
 #if LCL_MODUP_KEYS == 2
   __shared__ alignas(128) u64 skey[4][256];  // digit j's key rows (TMA)
   __shared__ u64 kbar;
@@ -842,22 +875,25 @@ __global__ void __launch_bounds__(64, MINB)
   u64* kbar_p = nullptr;
 #endif
   const u32 l = threadIdx.x & 15, bw = threadIdx.x >> 4;
-  // the 4 groups of a CTA take 4 consecutive ciphertexts of the same
-  // (target row, block): the key words they share are served from L1
-  const u32 bq_count = (B + 3) >> 2;
+  // the G groups of a CTA take G consecutive ciphertexts of the same
+  // (target row, block): the key words they share are served from L1 and
+  // the block's twiddles are staged once
+  const u32 bq_count = (B + G - 1) / G;
   const u32 bq = blockIdx.x % bq_count;
   const u32 tb_ = blockIdx.x / bq_count;  // = t * N1 + blk
   // the special-prime target (integer field, the slowest CTAs) is scheduled
   // first so its CTAs overlap the q targets instead of forming the tail
   const u32 traw = tb_ / N1, blk = tb_ - traw * N1;
   const u32 t = traw == 0 ? (u32)M : traw - 1;
-  const u32 bi_raw = bq * 4 + bw;
-  const bool live = bi_raw < B;
-  const u32 bi = live ? bi_raw : B - 1;
   const u32 pi = t < (u32)M ? t : full;
 #if LCL_MODUP_KEYS == 2
   u64* kbar_p = &kbar;
 #endif
+  // groups past the batch redo item B - 1 without storing (the block stages
+  // use warp-wide barriers)
+  const u32 bi_raw = bq * G + bw;
+  const bool live = bi_raw < B;
+  const u32 bi = live ? bi_raw : B - 1;
   if (row_fp(tb, pi))
     modup_ip_body<FpF, LOGN1, M>(bi, live, t, blk, pi, l, sm[bw], sacc[bw][0], sacc[bw][1], stw, mid, c1,
                                  c1_stride, perm, key, key_aux, full, acc, tb, skey, kbar_p);
@@ -897,7 +933,7 @@ __device__ __forceinline__ void modup_ip_hoist_body(u32 bi, bool live, u32 t, u3
   const PrimeConst P = tb.primes[pi];
   const typename F::K K = F::konst(P);
   const u64 kstride = (u64)(full + 1) * n;
-  stage_blk_tw<F>(stw, F::table(tb, false, pi), 1u << LOGN1, sb, threadIdx.x, 64);
+  stage_blk_tw<F>(stw, F::btable(tb, false, pi) + sb * kBlkTw, threadIdx.x, 64);
   __syncthreads();
   const SmemTw<F> twa{stw};
 #pragma unroll 1
@@ -988,7 +1024,7 @@ __device__ __forceinline__ void blk_inv_kernel_body(const RowMap& in, const RowM
   typename F::T x[16];
 #pragma unroll
   for (int e = 0; e < 16; ++e) x[e] = F::from_u64(src[l + 16 * e]);
-  blk_inv_body<F>(x, s, GlobalTw<F>{F::table(tb, true, pi), (1u << LOGN1) + b}, l, K);
+  blk_inv_body<F>(x, s, GlobalTw<F>{F::btable(tb, true, pi) + b * kBlkTw}, l, K);
   u64* dst = row_ptr(out, r) + (b << 8);
 #pragma unroll
   for (int e = 0; e < 16; ++e) dst[l + 16 * e] = F::bits(x[e]);
@@ -1089,8 +1125,14 @@ __device__ __forceinline__ typename Fd::T lift_to(typename Fs::T v, u64 qs_half,
   }
 }
 
-template <class Fs, class Fd, int LOGN1, int E>
-__device__ __forceinline__ void col_lift_fwd(const typename Fs::T (&v)[E], const RowMap& dst, u32 rd,
+// LCL_COL_VSMEM: the coefficient-domain source tile v is parked in a second
+// shared-memory tile (thread-private slots, no barrier) across the fan-out
+// instead of registers, so the register cap does not spill it to local memory.
+#ifndef LCL_COL_VSMEM
+#define LCL_COL_VSMEM 1
+#endif
+template <class Fs, class Fd, int LOGN1, int E, class VSrc>
+__device__ __forceinline__ void col_lift_fwd(const VSrc& v, const RowMap& dst, u32 rd,
                                              u32 pd, u64 qs_half, u64 corr, const NttTabs& tb,
                                              u64* sm, u32 j, u32 c, u32 k) {
   constexpr int N1 = 1 << LOGN1;
@@ -1101,7 +1143,7 @@ __device__ __forceinline__ void col_lift_fwd(const typename Fs::T (&v)[E], const
   const typename Fd::TwPtr tw = Fd::table(tb, false, pd);
   typename Fd::T x[E];
 #pragma unroll
-  for (int e = 0; e < E; ++e) x[e] = lift_to<Fs, Fd>(v[e], qs_half, corr, D);
+  for (int e = 0; e < E; ++e) x[e] = lift_to<Fs, Fd>(v(e), qs_half, corr, D);
   col_fwd_phase1<Fd, LOGN1, E>(x, tw, K);
   __syncthreads();  // the previous user of sm[] is done
 #pragma unroll
@@ -1145,15 +1187,24 @@ __device__ __forceinline__ void col_ilf_body(const RowMap& src, const RowMap& ds
     }
   }
   const u64 qs_half = __ldg(&tb.primes[ps].half);
+  u64* vs = sm + N1 * 16;  // LCL_COL_VSMEM (E = 16): thread-private slots (k + R e) * 16 + c
+  if constexpr (LCL_COL_VSMEM && E == 16) {
+#pragma unroll
+    for (int e = 0; e < E; ++e) vs[(k + R * e) * 16 + c] = Fs::bits(v[e]);
+  }
+  const auto vget = [&](int e) -> typename Fs::T {
+    if constexpr (LCL_COL_VSMEM && E == 16) return Fs::unbits(vs[(k + R * e) * 16 + c]);
+    else return v[e];
+  };
 #pragma unroll 1
   for (u32 f = 0; f < fan; ++f) {
     const u32 rd = rs * fan + f;
     const u32 pd = row_prime(dst, rd);
     const u64 corr = __ldg(&tb.primes[pd].q) - __ldg(smod + ps * nprimes + pd);
     if (row_fp(tb, pd))
-      col_lift_fwd<Fs, FpF, LOGN1, E>(v, dst, rd, pd, qs_half, corr, tb, sm, j, c, k);
+      col_lift_fwd<Fs, FpF, LOGN1, E>(vget, dst, rd, pd, qs_half, corr, tb, sm, j, c, k);
     else
-      col_lift_fwd<Fs, IntF, LOGN1, E>(v, dst, rd, pd, qs_half, corr, tb, sm, j, c, k);
+      col_lift_fwd<Fs, IntF, LOGN1, E>(vget, dst, rd, pd, qs_half, corr, tb, sm, j, c, k);
   }
 }
 

@@ -623,7 +623,8 @@ def test_cuda_shards_concatenate_to_reference(name, world):
 
 
 @pytest.mark.parametrize("pair_f64,n,C,blocked", [("1", 4, 600, "1"), ("0", 4, 600, "1"), ("1", 30, 3, "1"),
-                                                   ("1", 48, 2, "1"), ("1", 48, 2, "0"), ("0", 48, 2, "1")])
+                                                   ("1", 7, 5, "1"), ("1", 48, 2, "1"), ("1", 48, 2, "0"),
+                                                   ("0", 48, 2, "1")])
 def test_pair_accumulation_long_ranges_and_extremes(pair_f64, n, C, blocked, monkeypatch):
     """Lazy pair accumulation over 600 chunks (three 256-chunk passes of the
     FP64-pipe kernel), over 435 pairs (three CTA pair groups, 30 clients) and
@@ -631,8 +632,8 @@ def test_pair_accumulation_long_ranges_and_extremes(pair_f64, n, C, blocked, mon
     every pair is accumulated in one pass and finished per sub-batch; with
     client-blocked pair groups above 27 clients, LCL_PAIR_BLOCKED=0 the flat
     ones), with boundary residues (all 0 against all q-1), for both arithmetic forms
-    (LCL_PAIR_F64=1: FP64 pipe, 0: split-23 integer), word for word against
-    the oracle's distance matrix."""
+    (LCL_PAIR_F64=1: FP64 pipe, 0: split-23 integer), odd n included, word
+    for word against the oracle's distance matrix."""
     L = _L()
     monkeypatch.setenv("LCL_PAIR_F64", pair_f64)
     monkeypatch.setenv("LCL_PAIR_BLOCKED", blocked)

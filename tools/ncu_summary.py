@@ -20,6 +20,10 @@ METRICS = [
     ("regs", "launch__registers_per_thread"),
     ("warp_insts_M", "smsp__inst_executed.sum"),
     ("l2_hit_pct", "lts__t_sector_hit_rate.pct"),
+    ("fp64_pipe_pct", "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"),
+    ("l1_data_pipe_pct", "l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed"),
+    ("smem_wavefronts_M", "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum"),
+    ("smem_conflicts_M", "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum"),
 ]
 STALLS = "smsp__average_warps_issue_stalled_"
 
@@ -61,7 +65,7 @@ def main():
                     v = v / 1e3
                 if u == "msecond" and label == "time_us":
                     v = v * 1e3
-                if label == "warp_insts_M":
+                if label in ("warp_insts_M", "smem_wavefronts_M", "smem_conflicts_M"):
                     v = v / 1e6
                 parts.append(f"{label}={v:.1f}")
         print("   " + " ".join(parts))
