@@ -45,6 +45,17 @@ namespace {
 // CTAs/SM bound of ntt_blk_fwd<DivRoundInvStore>. At 16 (64 registers) it
 // spills 276 B per thread; 12 (80 registers, 12 B spill) and 10 measured
 // slower at cfg3 (9.51 / 10.26 vs 9.25 ms): the spills stay in L1.
+// Divide-and-round block passes with TMA-staged operands (ntt_blk_fwd_dr_tma)
+// and their CTAs/SM bound (33 KB of shared memory per CTA: at most 6).
+// Measured at cfg3: <divround+inv> 7.99 -> 13.90 ms, <divround> 4.61 -> 7.89
+// (12 warps/SM instead of 32: the staging buffers cost more occupancy than
+// the early loads buy), so the register-load kernel stays the default.
+#ifndef LCL_DR_TMA
+#define LCL_DR_TMA 0
+#endif
+#ifndef LCL_DR_MINB
+#define LCL_DR_MINB 6
+#endif
 // CTAs/SM bound of the fused column pass at E = 16. With the source tile
 // parked in shared memory (LCL_COL_VSMEM, 64 KB per CTA) 3 CTAs fit, at 80
 // registers and no spill: cfg3 column passes 17.43 -> 16.98 ms against
@@ -570,8 +581,16 @@ void blk_fwd_n(lcl_context* c, u32 rows, const RowMap& mid, const Epi& epi) {
   // 16 CTAs per SM (64-register cap): measured cfg2 1.87 -> 1.49 ms, cfg3
   // 15.65 -> 11.44 ms against the unconstrained build (128 registers); the
   // same cap on ntt_blk_inv and a 10-CTA cap on modup_ip_blk were slower
-  constexpr int kMinB = std::is_same<Epi, DivRoundInvStore>::value ? LCL_INV_MINB : 16;
-  ntt_blk_fwd<LOGN1, Epi, kMinB><<<rows * N1 / 4, 64, 0, c->stream>>>(mid, epi, tabs(c));
+  if constexpr (LCL_DR_TMA && (std::is_same<Epi, DivRoundStore>::value ||
+                               std::is_same<Epi, DivRoundInvStore>::value)) {
+    constexpr size_t smem = 4 * kDrGroupWords * 8;
+    static bool once = (allow_smem(ntt_blk_fwd_dr_tma<LOGN1, Epi, LCL_DR_MINB>, smem), true);
+    (void)once;
+    ntt_blk_fwd_dr_tma<LOGN1, Epi, LCL_DR_MINB><<<rows * N1 / 4, 64, smem, c->stream>>>(mid, epi, tabs(c));
+  } else {
+    constexpr int kMinB = std::is_same<Epi, DivRoundInvStore>::value ? LCL_INV_MINB : 16;
+    ntt_blk_fwd<LOGN1, Epi, kMinB><<<rows * N1 / 4, 64, 0, c->stream>>>(mid, epi, tabs(c));
+  }
 }
 
 // Calls f(LOGN1, E) with compile-time constants for the two-pass ring sizes.

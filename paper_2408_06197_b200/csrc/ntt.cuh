@@ -72,24 +72,26 @@ struct IntF {
     x = a + t;
     y = a + (k.four_q - t);
   }
-  // Inverse GS butterfly: x, y in [0, 2q) -> x', y' in [0, 2q).
+  // Inverse GS butterfly: x, y in [0, 4q) -> x', y' in [0, 4q) (the
+  // truncated-quotient Shoup product lands in [0, 4q) too).
   __device__ static __forceinline__ void gs(T& x, T& y, Tw w, const K& k) {
     const u64 a = x, b = y;
     const u64 s = a + b;
-    x = s >= k.two_q ? s - k.two_q : s;
-    y = mul_shoup_lazy(a - b + k.two_q, w.w, w.ws, k.q);
+    x = s >= k.four_q ? s - k.four_q : s;
+    y = mul_shoup_lazy4(a + (k.four_q - b), w.w, w.ws, k.q);
   }
   template <int E>
-  __device__ static __forceinline__ void gs_fix(T (&)[E], const K&) {}  // GS stays in [0, 2q)
+  __device__ static __forceinline__ void gs_fix(T (&)[E], const K&) {}  // GS stays in [0, 4q)
   __device__ static __forceinline__ T from_u64(u64 v) { return v; }
   __device__ static __forceinline__ u64 bits(T v) { return v; }
   __device__ static __forceinline__ T unbits(u64 v) { return v; }
   __device__ static __forceinline__ u64 canon(T v, const K& k) { return reduce62(v, k.q, k.mu62); }
-  // Last inverse stage with N^-1 folded in: fully reduced outputs.
+  // Last inverse stage with N^-1 folded in: fully reduced outputs (inputs
+  // in [0, 4q)).
   __device__ static __forceinline__ void inv_last(T& a, T& b, const PrimeConst& P) {
     const u64 x = a, y = b;
     a = mul_shoup(x + y, P.n_inv, P.n_inv_shoup, P.q);
-    b = mul_shoup(x - y + P.two_q, P.w1n, P.w1n_shoup, P.q);
+    b = mul_shoup(x - y + 2 * P.two_q, P.w1n, P.w1n_shoup, P.q);
   }
   __device__ static __forceinline__ u64 canon_last(T v, const K&) { return v; }
 };
@@ -661,6 +663,88 @@ __global__ void __launch_bounds__(64, MINB)
     blk_fwd_kernel_body<FpF, LOGN1>(in, epi, tb, sm[bw], r, b, l, pi);
   else
     blk_fwd_kernel_body<IntF, LOGN1>(in, epi, tb, sm[bw], r, b, l, pi);
+}
+
+// Divide-and-round block pass with its operands staged by TMA. The 16-lane
+// group of block b issues, from one lane, cp.async.bulk copies of every
+// 2 KB block it needs -- the ModDown column-pass output (mid), the key-switch
+// accumulator x, add1 and add2's (Galois-)source block -- onto one mbarrier
+// before it does anything else, so the epilogue's loads are in flight during
+// the block stages instead of being issued (and waited for) after them.
+// Shared memory per group: [272] mid (later the transpose buffer), [256] x,
+// [256] add1, [256] add2, mbarrier.
+constexpr int kDrGroupWords = 272 + 3 * 256 + 2;
+template <class F, int LOGN1, class Epi>
+__device__ __forceinline__ void blk_fwd_dr_tma_body(const RowMap& in, const Epi& epi, const NttTabs& tb,
+                                                    u64* g, u32 r, u32 b, u32 l, u32 pi) {
+  const PrimeConst P = tb.primes[pi];
+  const typename F::K K = F::konst(P);
+  const auto row = epi.bind(r, pi, P);
+  u64* smid = g;
+  u64* sx = g + 272;
+  u64* sa1 = sx + 256;
+  u64* sa2 = sa1 + 256;
+  u64* bar = sa2 + 256;
+  const u32 bo = b << 8;
+  if (l == 0) {
+    mbar_init(bar, 1);
+    mbar_expect_tx(bar, 2048u * (2 + (row.a1 ? 1 : 0) + (row.a2 ? 1 : 0)));
+    bulk_g2s(smid, row_ptr(in, r) + bo, 2048, bar);
+    bulk_g2s(sx, row.x + bo, 2048, bar);
+    if (row.a1) bulk_g2s(sa1, row.a1 + bo, 2048, bar);
+    if (row.a2) bulk_g2s(sa2, row.a2 + (row.perm ? (__ldg(row.perm + bo) & ~255u) : bo), 2048, bar);
+  }
+  __syncwarp();
+  mbar_wait(bar, 0);
+  typename F::T x[16];
+#pragma unroll
+  for (int e = 0; e < 16; ++e) x[e] = F::unbits(smid[l + 16 * e]);
+  __syncwarp();  // smid becomes the transpose buffer
+  u64 o[16];
+  const GlobalTw<F> twa{F::btable(tb, false, pi) + b * kBlkTw};
+  blk_fwd_body<F>(x, o, smid, twa, l, K, [&](typename F::T v) -> u64 {
+    if (std::is_same<F, FpF>::value || Epi::kNeedsReduced) return F::canon(v, K);
+    return F::bits(v);
+  });
+#pragma unroll
+  for (int e = 0; e < 16; ++e) {
+    const u32 a = l + 16 * e;
+    u64 add = row.a1 ? sa1[a] : 0;
+    if (row.a2) add = add_mod(add, sa2[row.perm ? (__ldg(row.perm + bo + a) & 255u) : a], row.q);
+    const u64 v = add_mod(mul_shoup(sx[a] + (row.q80 - o[e]), row.iv, row.ivs, row.q), add, row.q);
+    row.o[bo + a] = v;
+    o[e] = v;
+  }
+  if constexpr (Epi::kInvNext) {
+    const RowMap& om = epi.out;
+    if (((r / om.rows_per_item) % om.items_per_group) == 1) {
+      __syncwarp();
+#pragma unroll
+      for (int e = 0; e < 16; ++e) x[e] = F::from_u64(o[e]);
+      blk_inv_body<F>(x, smid, GlobalTw<F>{F::btable(tb, true, pi) + b * kBlkTw}, l, K);
+      u64* dst = row_ptr(epi.inv_out, r) + bo;
+#pragma unroll
+      for (int e = 0; e < 16; ++e) dst[l + 16 * e] = F::bits(x[e]);
+    }
+  }
+}
+
+template <int LOGN1, class Epi, int MINB>
+__global__ void __launch_bounds__(64, MINB)
+    ntt_blk_fwd_dr_tma(const __grid_constant__ RowMap in, const __grid_constant__ Epi epi,
+                       const __grid_constant__ NttTabs tb) {
+  constexpr int N1 = 1 << LOGN1;
+  extern __shared__ __align__(16) u64 dr_sm[];  // [4][kDrGroupWords]
+  const u32 l = threadIdx.x & 15, bw = threadIdx.x >> 4;
+  const u32 blk_global = blockIdx.x * 4 + bw;
+  const u32 r = blk_global / N1;
+  const u32 b = blk_global - r * N1;
+  const u32 pi = row_prime(in, r);
+  u64* g = dr_sm + bw * kDrGroupWords;
+  if (row_fp(tb, pi))
+    blk_fwd_dr_tma_body<FpF, LOGN1>(in, epi, tb, g, r, b, l, pi);
+  else
+    blk_fwd_dr_tma_body<IntF, LOGN1>(in, epi, tb, g, r, b, l, pi);
 }
 
 // ModUp block pass fused with the key inner product (ckks.cpp:464-518).
