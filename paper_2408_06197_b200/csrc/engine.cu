@@ -45,6 +45,12 @@ namespace {
 // CTAs/SM bound of ntt_blk_fwd<DivRoundInvStore>. At 16 (64 registers) it
 // spills 276 B per thread; 12 (80 registers, 12 B spill) and 10 measured
 // slower at cfg3 (9.51 / 10.26 vs 9.25 ms): the spills stay in L1.
+// modup_ip_blk as two field-specialised launches (special target on the
+// integer pipe, then the q targets on the FP64 pipe) instead of one kernel
+// carrying both fields' code.
+#ifndef LCL_MODUP_SPLIT
+#define LCL_MODUP_SPLIT 1
+#endif
 // Divide-and-round block passes with TMA-staged operands (ntt_blk_fwd_dr_tma)
 // and their CTAs/SM bound (33 KB of shared memory per CTA: at most 6).
 // Measured at cfg3: <divround+inv> 7.99 -> 13.90 ms, <divround> 4.61 -> 7.89
@@ -410,6 +416,21 @@ NttTabs tabs(const lcl_context* c) {
   return t;
 }
 
+// Field selection of a row map (ntt.cuh use_fp): 1 = every row's prime runs
+// on the FP64 pipe, 2 = every row on the integer pipe, 0 = mixed.
+int field_sel(const lcl_context* c, const RowMap& m) {
+  bool fp = false, in = false;
+  for (u32 r = 0; r < m.rows_per_item; ++r) ((c->fp_mask >> m.prime_of[r]) & 1u ? fp : in) = true;
+  return fp && !in ? 1 : (in && !fp ? 2 : 0);
+}
+// Calls f(integral_constant<FS>) for the map's field selection.
+template <class F>
+void with_fs(int fs, F&& f) {
+  if (fs == 1) f(std::integral_constant<int, 1>{});
+  else if (fs == 2) f(std::integral_constant<int, 2>{});
+  else f(std::integral_constant<int, 0>{});
+}
+
 void post_launch(lcl_context* c, u64 k = 1) {
   count_launch(c, k);
   cuda_check(cudaGetLastError(), "kernel launch");
@@ -490,7 +511,9 @@ void fwd2(lcl_context* c, u32 rows, const RowMap& mid, const Loader& ld, const E
                  rb * (store_rows(epi, rows) + (std::is_same<Epi, PlainStore>::value ? rows : 0)),
                  bpr * rows * 8);
     constexpr int kMinB = std::is_same<Epi, DivRoundInvStore>::value ? LCL_INV_MINB : 16;
-  ntt_blk_fwd<LOGN1, Epi, kMinB><<<rows * N1 / 4, 64, 0, c->stream>>>(mid, epi, tabs(c));
+  with_fs(field_sel(c, mid), [&](auto FS) {
+    ntt_blk_fwd<LOGN1, Epi, kMinB, decltype(FS)::value><<<rows * N1 / 4, 64, 0, c->stream>>>(mid, epi, tabs(c));
+  });
   }
   post_launch(c, 2);
 }
@@ -506,7 +529,9 @@ void inv2(lcl_context* c, u32 rows, const RowMap& in, const RowMap& mid, const E
   const double bpr = 0.5 * c->N();
   {
     ProfScope ps(c, "ntt_blk_inv", rb * 2.0 * rows, bpr * rows * 8);
-    ntt_blk_inv<LOGN1><<<rows * N1 / 4, 64, 0, c->stream>>>(in, mid, tabs(c));
+    with_fs(field_sel(c, in), [&](auto FS) {
+      ntt_blk_inv<LOGN1, 1, decltype(FS)::value><<<rows * N1 / 4, 64, 0, c->stream>>>(in, mid, tabs(c));
+    });
   }
   {
     ProfScope ps(c, "ntt_col_inv", rb * 2.0 * rows, bpr * rows * LOGN1);
@@ -543,20 +568,37 @@ template <int LOGN1>
 void blk_inv_n(lcl_context* c, u32 rows, const RowMap& in, const RowMap& out) {
   constexpr int N1 = 1 << LOGN1;
   ProfScope ps(c, "ntt_blk_inv", 16.0 * c->N() * rows, 0.5 * c->N() * rows * 8);
-  ntt_blk_inv<LOGN1><<<rows * N1 / 4, 64, 0, c->stream>>>(in, out, tabs(c));
+  with_fs(field_sel(c, in), [&](auto FS) {
+    ntt_blk_inv<LOGN1, 1, decltype(FS)::value><<<rows * N1 / 4, 64, 0, c->stream>>>(in, out, tabs(c));
+  });
 }
 
 template <int LOGN1, int E, int MINB>
 void col_ilf_cfg(lcl_context* c, u32 src_rows, const RowMap& src, const RowMap& dst, u32 fan) {
   constexpr int N1 = 1 << LOGN1;
   constexpr size_t smem = (size_t)N1 * 16 * 8 * (LCL_COL_VSMEM && E == 16 ? 2 : 1);
-  static bool once = (allow_smem(ntt_col_inv_lift_fwd<LOGN1, E, MINB>, smem), true);
-  (void)once;
   const u32 groups = (u32)(c->n >> LOGN1) >> 4;
   ProfScope ps(c, "ntt_col_inv_lift_fwd", 8.0 * c->N() * (src_rows + (double)src_rows * fan),
                0.5 * c->N() * LOGN1 * (src_rows + (double)src_rows * fan));
-  ntt_col_inv_lift_fwd<LOGN1, E, MINB><<<src_rows * groups, 16 * (N1 / E), smem, c->stream>>>(
-      src, dst, fan, c->d_smod, c->P(), tabs(c));
+  // field-specialised instances for the key-switch shapes: ModUp (FP64
+  // q-limb sources, mixed targets), ModDown (integer special-prime sources,
+  // FP64 targets), rescale (FP64 -> FP64), all-integer (LCL_FP64=0)
+  auto go = [&](auto FSS, auto FSD) {
+    constexpr int A = decltype(FSS)::value, B = decltype(FSD)::value;
+    static bool once = (allow_smem(ntt_col_inv_lift_fwd<LOGN1, E, MINB, A, B>, smem), true);
+    (void)once;
+    ntt_col_inv_lift_fwd<LOGN1, E, MINB, A, B><<<src_rows * groups, 16 * (N1 / E), smem, c->stream>>>(
+        src, dst, fan, c->d_smod, c->P(), tabs(c));
+  };
+  using I0 = std::integral_constant<int, 0>;
+  using I1 = std::integral_constant<int, 1>;
+  using I2 = std::integral_constant<int, 2>;
+  const int fss = field_sel(c, src), fsd = field_sel(c, dst);
+  if (fss == 1 && fsd == 0) go(I1{}, I0{});
+  else if (fss == 2 && fsd == 1) go(I2{}, I1{});
+  else if (fss == 1 && fsd == 1) go(I1{}, I1{});
+  else if (fss == 2 && fsd == 2) go(I2{}, I2{});
+  else go(I0{}, I0{});
 }
 
 // E = 16: 4 CTAs per SM (128 registers) -- measured cfg2 2.26 -> 1.95 ms,
@@ -589,7 +631,10 @@ void blk_fwd_n(lcl_context* c, u32 rows, const RowMap& mid, const Epi& epi) {
     ntt_blk_fwd_dr_tma<LOGN1, Epi, LCL_DR_MINB><<<rows * N1 / 4, 64, smem, c->stream>>>(mid, epi, tabs(c));
   } else {
     constexpr int kMinB = std::is_same<Epi, DivRoundInvStore>::value ? LCL_INV_MINB : 16;
-    ntt_blk_fwd<LOGN1, Epi, kMinB><<<rows * N1 / 4, 64, 0, c->stream>>>(mid, epi, tabs(c));
+    with_fs(field_sel(c, mid), [&](auto FS) {
+      ntt_blk_fwd<LOGN1, Epi, kMinB, decltype(FS)::value><<<rows * N1 / 4, 64, 0, c->stream>>>(mid, epi,
+                                                                                             tabs(c));
+    });
   }
 }
 
@@ -655,18 +700,32 @@ LiftLoad lift_from(lcl_context* c, const RowMap& src, u32 rows_per_item, u32 fan
 
 template <int LOGN1, int M>
 void modup_ip_launch(lcl_context* c, u32 B, const u64* mid, const u64* c1, u64 c1_stride,
-                     const u32* perm, const u64* key, const u64* key_shoup, u64* acc) {
+                     const u32* perm, const u64* key, const u64* key_aux, u64* acc) {
   constexpr int N1 = 1 << LOGN1;
   const double rb = 8.0 * c->N();
   ProfScope ps(c, perm ? "modup_ip_blk<perm>" : "modup_ip_blk",
                rb * ((double)B * M * M + B * M + 4.0 * M * (M + 1) + 2.0 * B * (M + 1)),
                0.5 * c->N() * B * M * M * 8);
   constexpr size_t smem = modup_smem_bytes(LCL_MODUP_G);
-  static bool once = (allow_smem(modup_ip_blk<LOGN1, M>, smem), true);
+  const u32 bq = (B + LCL_MODUP_G - 1) / LCL_MODUP_G;
+  const bool sp_int = !((c->fp_mask >> c->full) & 1u);
+  const bool q_fp = (c->fp_mask & ((1u << M) - 1)) == ((1u << M) - 1);
+  if (LCL_MODUP_SPLIT && sp_int && q_fp) {
+    // the special target (integer field) then the M q targets (FP64 field)
+    static bool once = (allow_smem(modup_ip_blk<LOGN1, M, 2>, smem), allow_smem(modup_ip_blk<LOGN1, M, 1>, smem),
+                        true);
+    (void)once;
+    modup_ip_blk<LOGN1, M, 2><<<bq * N1, 16 * LCL_MODUP_G, smem, c->stream>>>(
+        B, mid, c1, c1_stride, perm, key, key_aux, c->full, acc, tabs(c), 0);
+    modup_ip_blk<LOGN1, M, 1><<<bq * M * N1, 16 * LCL_MODUP_G, smem, c->stream>>>(
+        B, mid, c1, c1_stride, perm, key, key_aux, c->full, acc, tabs(c), 1);
+    count_launch(c);
+    return;
+  }
+  static bool once = (allow_smem(modup_ip_blk<LOGN1, M, 0>, smem), true);
   (void)once;
-  modup_ip_blk<LOGN1, M><<<((B + LCL_MODUP_G - 1) / LCL_MODUP_G) * (M + 1) * N1, 16 * LCL_MODUP_G, smem,
-                           c->stream>>>(
-      B, mid, c1, c1_stride, perm, key, key_shoup, c->full, acc, tabs(c));
+  modup_ip_blk<LOGN1, M, 0><<<bq * (M + 1) * N1, 16 * LCL_MODUP_G, smem, c->stream>>>(
+      B, mid, c1, c1_stride, perm, key, key_aux, c->full, acc, tabs(c), 0);
 }
 
 template <int LOGN1>

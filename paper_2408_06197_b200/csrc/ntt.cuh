@@ -37,6 +37,16 @@
 namespace lcl {
 
 __device__ __forceinline__ bool row_fp(const NttTabs& t, u32 pi) { return (t.fp_mask >> pi) & 1u; }
+// Field selection of a launch (template argument FS): 0 = per row at run
+// time, 1 = every row on the FP64 pipe, 2 = every row on the integer pipe.
+// A launch whose rows share one field compiles only that field's code (the
+// two-field kernels are 80-140 KB of SASS and stalled on instruction fetch).
+template <int FS>
+__device__ __forceinline__ bool use_fp(const NttTabs& t, u32 pi) {
+  if constexpr (FS == 1) return true;
+  else if constexpr (FS == 2) return false;
+  else return row_fp(t, pi);
+}
 
 // ------------------------------------------------------------ fields
 struct IntF {
@@ -648,7 +658,7 @@ __device__ __forceinline__ void blk_fwd_kernel_body(const RowMap& in, const Epi&
 // of that was the 16-lane __syncwarp mask the divergent groups needed:
 // with the full-warp barrier kept, <divround+inv> alone costs 7.99 vs 11.86 ms
 // with the half-warp mask.)
-template <int LOGN1, class Epi, int MINB = 1>
+template <int LOGN1, class Epi, int MINB = 1, int FS = 0>
 __global__ void __launch_bounds__(64, MINB)
     ntt_blk_fwd(const __grid_constant__ RowMap in, const __grid_constant__ Epi epi,
                 const __grid_constant__ NttTabs tb) {
@@ -659,7 +669,7 @@ __global__ void __launch_bounds__(64, MINB)
   const u32 r = blk_global / N1;
   const u32 b = blk_global - r * N1;
   const u32 pi = row_prime(in, r);
-  if (row_fp(tb, pi))
+  if (use_fp<FS>(tb, pi))
     blk_fwd_kernel_body<FpF, LOGN1>(in, epi, tb, sm[bw], r, b, l, pi);
   else
     blk_fwd_kernel_body<IntF, LOGN1>(in, epi, tb, sm[bw], r, b, l, pi);
@@ -938,12 +948,15 @@ __device__ __forceinline__ void modup_ip_body(u32 bi, bool live, u32 t, u32 blk,
 #define LCL_MODUP_G 8
 #endif
 constexpr size_t modup_smem_bytes(int G) { return (size_t)G * (256 + 16 + 512) * 8 + kBlkTw * 16; }
-template <int LOGN1, int M, int G = LCL_MODUP_G, int MINB = 32 / G>
+// FS (see use_fp): 0 = all M + 1 targets in one launch (t0 = 0), 2 = the
+// special target only, 1 = the M q targets only (t0 = 1): the field-split
+// launches compile one field each.
+template <int LOGN1, int M, int FS = 0, int G = LCL_MODUP_G, int MINB = 32 / G>
 __global__ void __launch_bounds__(16 * G, MINB)
     modup_ip_blk(u32 B, const u64* __restrict__ mid, const u64* __restrict__ c1, u64 c1_stride,
                  const u32* __restrict__ perm, const u64* __restrict__ key,
                  const u64* __restrict__ key_aux, u32 full, u64* __restrict__ acc,
-                 const __grid_constant__ NttTabs tb) {
+                 const __grid_constant__ NttTabs tb, u32 t0) {
   constexpr int N1 = 1 << LOGN1;
   // dynamic shared memory (modup_smem_bytes): [G][272] block transposes,
   // [G][2][256] lazy accumulators (coalesced order), the block's twiddles
@@ -967,7 +980,8 @@ __global__ void __launch_bounds__(16 * G, MINB)
   const u32 tb_ = blockIdx.x / bq_count;  // = t * N1 + blk
   // the special-prime target (integer field, the slowest CTAs) is scheduled
   // first so its CTAs overlap the q targets instead of forming the tail
-  const u32 traw = tb_ / N1, blk = tb_ - traw * N1;
+  const u32 tr = tb_ / N1, blk = tb_ - tr * N1;
+  const u32 traw = tr + t0;
   const u32 t = traw == 0 ? (u32)M : traw - 1;
   const u32 pi = t < (u32)M ? t : full;
 #if LCL_MODUP_KEYS == 2
@@ -978,7 +992,7 @@ __global__ void __launch_bounds__(16 * G, MINB)
   const u32 bi_raw = bq * G + bw;
   const bool live = bi_raw < B;
   const u32 bi = live ? bi_raw : B - 1;
-  if (row_fp(tb, pi))
+  if (use_fp<FS>(tb, pi))
     modup_ip_body<FpF, LOGN1, M>(bi, live, t, blk, pi, l, sm[bw], sacc[bw][0], sacc[bw][1], stw, mid, c1,
                                  c1_stride, perm, key, key_aux, full, acc, tb, skey, kbar_p);
   else
@@ -1114,7 +1128,7 @@ __device__ __forceinline__ void blk_inv_kernel_body(const RowMap& in, const RowM
   for (int e = 0; e < 16; ++e) dst[l + 16 * e] = F::bits(x[e]);
 }
 
-template <int LOGN1, int MINB = 1>
+template <int LOGN1, int MINB = 1, int FS = 0>
 __global__ void __launch_bounds__(64, MINB)
     ntt_blk_inv(const __grid_constant__ RowMap in, const __grid_constant__ RowMap out,
                 const __grid_constant__ NttTabs tb) {
@@ -1125,7 +1139,7 @@ __global__ void __launch_bounds__(64, MINB)
   const u32 r = blk_global / N1;
   const u32 b = blk_global - r * N1;
   const u32 pi = row_prime(in, r);
-  if (row_fp(tb, pi))
+  if (use_fp<FS>(tb, pi))
     blk_inv_kernel_body<FpF, LOGN1>(in, out, tb, sm[bw], r, b, l, pi);
   else
     blk_inv_kernel_body<IntF, LOGN1>(in, out, tb, sm[bw], r, b, l, pi);
@@ -1241,7 +1255,7 @@ __device__ __forceinline__ void col_lift_fwd(const VSrc& v, const RowMap& dst, u
   for (int e = 0; e < E; ++e) o[j + (k * E + e) * n2] = Fd::bits(x[e]);
 }
 
-template <class Fs, int LOGN1, int E>
+template <class Fs, int LOGN1, int E, int FSD>
 __device__ __forceinline__ void col_ilf_body(const RowMap& src, const RowMap& dst, u32 fan,
                                              const u64* smod, u32 nprimes, const NttTabs& tb,
                                              u64* sm, u32 rs, u32 j, u32 c, u32 k, u32 ps) {
@@ -1285,14 +1299,14 @@ __device__ __forceinline__ void col_ilf_body(const RowMap& src, const RowMap& ds
     const u32 rd = rs * fan + f;
     const u32 pd = row_prime(dst, rd);
     const u64 corr = __ldg(&tb.primes[pd].q) - __ldg(smod + ps * nprimes + pd);
-    if (row_fp(tb, pd))
+    if (use_fp<FSD>(tb, pd))
       col_lift_fwd<Fs, FpF, LOGN1, E>(vget, dst, rd, pd, qs_half, corr, tb, sm, j, c, k);
     else
       col_lift_fwd<Fs, IntF, LOGN1, E>(vget, dst, rd, pd, qs_half, corr, tb, sm, j, c, k);
   }
 }
 
-template <int LOGN1, int E, int MINB = 1>
+template <int LOGN1, int E, int MINB = 1, int FSS = 0, int FSD = 0>
 __global__ void __launch_bounds__(16 * ((1 << LOGN1) / E), MINB)
     ntt_col_inv_lift_fwd(const __grid_constant__ RowMap src, const __grid_constant__ RowMap dst,
                          u32 fan, const u64* __restrict__ smod, u32 nprimes,
@@ -1304,10 +1318,10 @@ __global__ void __launch_bounds__(16 * ((1 << LOGN1) / E), MINB)
   const u32 c = threadIdx.x & 15, k = threadIdx.x >> 4;
   const u32 j = (g << 4) + c;
   const u32 ps = row_prime(src, rs);
-  if (row_fp(tb, ps))
-    col_ilf_body<FpF, LOGN1, E>(src, dst, fan, smod, nprimes, tb, sm, rs, j, c, k, ps);
+  if (use_fp<FSS>(tb, ps))
+    col_ilf_body<FpF, LOGN1, E, FSD>(src, dst, fan, smod, nprimes, tb, sm, rs, j, c, k, ps);
   else
-    col_ilf_body<IntF, LOGN1, E>(src, dst, fan, smod, nprimes, tb, sm, rs, j, c, k, ps);
+    col_ilf_body<IntF, LOGN1, E, FSD>(src, dst, fan, smod, nprimes, tb, sm, rs, j, c, k, ps);
 }
 
 // Single-CTA transform for small rings (N <= 4096): the whole row in shared
