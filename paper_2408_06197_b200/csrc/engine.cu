@@ -47,9 +47,10 @@ namespace {
 // slower at cfg3 (9.51 / 10.26 vs 9.25 ms): the spills stay in L1.
 // modup_ip_blk as two field-specialised launches (special target on the
 // integer pipe, then the q targets on the FP64 pipe) instead of one kernel
-// carrying both fields' code.
+// carrying both fields' code: measured neutral at cfg3 (10.57 vs 10.55 ms),
+// so the single launch stays the default.
 #ifndef LCL_MODUP_SPLIT
-#define LCL_MODUP_SPLIT 1
+#define LCL_MODUP_SPLIT 0
 #endif
 // Divide-and-round block passes with TMA-staged operands (ntt_blk_fwd_dr_tma)
 // and their CTAs/SM bound (33 KB of shared memory per CTA: at most 6).
