@@ -1464,7 +1464,11 @@ bool pair_accumulate_f64_cfg(lcl_context* c, const u64* clients, u32 n, u32 chun
 // form (a thread owns a 2 x 2 block of pairs {i1,i2} x {j1,j2}, half the
 // staged words per pair-slot for the same FP64 work) ran 35.6 ms with one
 // slot per thread (400 threads, 1 CTA/SM) and 36.3 ms with two (128
-// registers, 2 CTAs/SM) against 25.4 ms -- parity-green, not kept),
+// registers, 2 CTAs/SM) against 25.4 ms -- parity-green, not kept; a
+// dual-pipe form putting 25 / 40 / 55 % of each CTA's pairs on the integer
+// multiply pipe (split-23 sums, two threads per pair, warp-uniform roles)
+// ran 34.3 / 37.1 / 37.5 ms -- the two roles' staging share one L1 and the
+// integer products cost ~2x the FP64 ones),
 // else the split-23 integer kernel.
 void pair_accumulate_launch(lcl_context* c, const u64* clients, u32 n, u32 chunks, u32 c0,
                             u32 c1, const PairSet& ps, u64* tern, bool accumulate) {
