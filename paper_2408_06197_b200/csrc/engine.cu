@@ -3233,6 +3233,8 @@ void host_round_groups(lcl_context* ctx, const Ingest& in, u32 n, u32 C,
       if (g + 1 < G) {
         cuda_check(cudaEventRecord(ev[1 + G + g], ctx->stream), "event");
       } else {
+        // (finishing the aggregate on lane 0 beside this lane's pair chain
+        // measured slower: cfg3 e2e 577.6 vs 566.2 ms at 8 groups)
         for (u32 c0 = 0; c0 < C; c0 += sub_batch(ctx, m)) {
           const u32 Bc = std::min(C, c0 + sub_batch(ctx, m)) - c0;
           agg_finish(ctx, atern + (u64)c0 * 3 * m * N, Bc, average, d_pt, da + (u64)c0 * astride);
@@ -3316,9 +3318,13 @@ void server_round_host(lcl_context* ctx, const Ingest& in, size_t n, size_t chun
     ensure_pairs(ctx, (u32)n);
     if (!ctx->h2d) cuda_check(cudaStreamCreateWithFlags(&ctx->h2d, cudaStreamNonBlocking), "stream");
     if (!ctx->d2h) cuda_check(cudaStreamCreateWithFlags(&ctx->d2h, cudaStreamNonBlocking), "stream");
-    // 0: chunk slices, 1: 2 client groups, G >= 2: G groups (read per call)
+    // 0: chunk slices, 1: 2 client groups, G >= 2: G groups (read per call).
+    // Default 8 groups: the smaller the last group, the shorter the chain
+    // left after the last byte lands -- e2e cfg3 592.5 (2 groups), 574.4 (4),
+    // 568.9 (6), 566.2 (8), 567.8 ms (10); cfg2 13.17 / 14.06 / 12.81 / 12.66
+    // / 13.55 ms.
     const char* mode_env = std::getenv("LCL_HOST_ROUND");
-    const int mode = mode_env ? atoi(mode_env) : 1;
+    const int mode = mode_env ? atoi(mode_env) : 8;
     if (mode >= 1 && ctx->pair_f64 && n >= 4 && !ctx->prof_on) {
       host_round_groups(ctx, in, (u32)n, (u32)chunks, width, k, l, average != 0,
                         h_dist, h_agg, dc, ds, dd, da, mode == 1 ? 2u : (u32)mode);

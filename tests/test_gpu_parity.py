@@ -317,11 +317,12 @@ def test_masked_aggregate_bit_exact_vs_reference(golden):
     assert agg.scale == rig.meta["agg_scale"]
 
 
-@pytest.mark.parametrize("mode", ["1", "0", "3"])
+@pytest.mark.parametrize("mode", ["1", "0", "3", "8"])
 def test_host_round_overlapped_bit_exact_vs_reference(golden, mode, monkeypatch):
     """lcl_server_round_host (host buffers in and out; H2D overlapped with
     the computation: 1 = two client groups on two lanes, 0 = chunk slices,
-    3 = three client groups) against the reference digests and op counters."""
+    3 / 8 = three / eight client groups, 8 the default) against the
+    reference digests and op counters."""
     L = _L()
     import ctypes as C
     monkeypatch.setenv("LCL_HOST_ROUND", mode)
