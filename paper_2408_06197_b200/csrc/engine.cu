@@ -1468,7 +1468,9 @@ bool pair_accumulate_f64_cfg(lcl_context* c, const u64* clients, u32 n, u32 chun
 // dual-pipe form putting 25 / 40 / 55 % of each CTA's pairs on the integer
 // multiply pipe (split-23 sums, two threads per pair, warp-uniform roles)
 // ran 34.3 / 37.1 / 37.5 ms -- the two roles' staging share one L1 and the
-// integer products cost ~2x the FP64 ones),
+// integer products cost ~2x the FP64 ones; OR-ing the exponent into the
+// staged tile once per CTA (by each vector's copying thread, before the
+// barrier) instead of once per pair ran 26.7-27.0 vs 25.5-25.7 ms),
 // else the split-23 integer kernel.
 void pair_accumulate_launch(lcl_context* c, const u64* clients, u32 n, u32 chunks, u32 c0,
                             u32 c1, const PairSet& ps, u64* tern, bool accumulate) {
