@@ -45,6 +45,12 @@ namespace {
 // CTAs/SM bound of ntt_blk_fwd<DivRoundInvStore>. At 16 (64 registers) it
 // spills 276 B per thread; 12 (80 registers, 12 B spill) and 10 measured
 // slower at cfg3 (9.51 / 10.26 vs 9.25 ms): the spills stay in L1.
+// Single rotations through modup_ip_hoist (ns = 1: digits parked in shared
+// memory, register accumulators) instead of modup_ip_blk: measured 11.81 vs
+// 10.44 ms at cfg3 (10 instead of 16 warps/SM), so off.
+#ifndef LCL_ROT_HOIST
+#define LCL_ROT_HOIST 0
+#endif
 // modup_ip_blk as two field-specialised launches (special target on the
 // integer pipe, then the q targets on the FP64 pipe) instead of one kernel
 // carrying both fields' code: measured neutral at cfg3 (10.57 vs 10.55 ms),
@@ -813,6 +819,34 @@ u64* ks_ip(lcl_context* c, const u64* dig, u32 B, u32 m, const u64* key, const u
   return acc;
 }
 
+// One modup_ip_hoist launch: the ModUp block pass of the digits in mid
+// (column-pass output, [B][m][m][N]) feeding the inner products of ns steps
+// into acc + s * acc_step ([B][2][m+1][N] each).
+void hoist_launch(lcl_context* c, u32 B, u32 m, const u64* mid, const u64* c1, u64 c1_stride,
+                  const HoistSteps& hs, u32 ns, u64* acc, u64 acc_step) {
+  const double rb = 8.0 * c->N();
+  {
+    ProfScope ps(c, ns == 1 ? "modup_ip_hoist<1>" : "modup_ip_hoist",
+                 rb * ((double)B * m * m + (double)B * m + 2.0 * ns * m * (m + 1) + 2.0 * ns * B * (m + 1)),
+                 0.5 * c->N() * B * m * m * 8);
+    dispatch_logn(c, [&](auto L1, auto) {
+      constexpr int LOGN1 = decltype(L1)::value;
+      const u32 grid = ((B + 3) / 4) * (m + 1) * (1u << LOGN1);
+#define LCL_HOIST(MM)                                                                        \
+  case MM:                                                                                   \
+    modup_ip_hoist<LOGN1, MM><<<grid, 64, 0, c->stream>>>(B, mid, c1, c1_stride, hs, ns,      \
+                                                          c->full, acc, acc_step, tabs(c));  \
+    break;
+      switch (m) {
+        LCL_HOIST(1) LCL_HOIST(2) LCL_HOIST(3) LCL_HOIST(4)
+        default: fail(LCL_PARAMETER_ERROR, "hoisted key switching supports up to 4 live limbs");
+      }
+#undef LCL_HOIST
+    });
+  }
+  post_launch(c);
+}
+
 // decompose_for_keyswitch + inner product (ckks.cpp:464-518) for the c1 / d2
 // limbs of B items: `in` maps them (rows_per_item = m); c1 / c1_stride address
 // the same limbs for the identity digits. sigma / perm: the rotation's
@@ -824,7 +858,7 @@ bool ks_fused(const lcl_context* c, u32 m) { return c->logn >= 13 && m <= 6; }
 // previous level's divide-and-round, rows [B][m][N]); fused path only.
 u64* ks_switch(lcl_context* c, const RowMap& in, const u64* c1, u64 c1_stride, u32 B, u32 m,
                const u32* sigma, const u32* perm, const u64* key, const u64* key_shoup,
-               const u64* preinv = nullptr) {
+               const u64* preinv = nullptr, const u32* blkmap = nullptr) {
   if (!ks_fused(c, m)) {
     u64* dig = ks_decompose(c, in, B, m, sigma);
     return ks_ip(c, dig, B, m, key, nullptr);
@@ -846,6 +880,17 @@ u64* ks_switch(lcl_context* c, const RowMap& in, const u64* c1, u64 c1_stride, u
   else
     inv_lift_fwd_cols(c, B * m, in, mid_map, m);
   u64* acc = c->ws_acc.get((u64)B * 2 * (m + 1) * N);
+  if (LCL_ROT_HOIST && perm && blkmap && m <= 4) {
+    // a single rotation through the hoisted kernel (digits parked in shared
+    // memory, the inner product from them with register accumulators)
+    HoistSteps hs{};
+    hs.perm[0] = perm;
+    hs.blkmap[0] = blkmap;
+    hs.key[0] = key;
+    hs.key_aux[0] = key_shoup;
+    hoist_launch(c, B, m, mid, c1, c1_stride, hs, 1, acc, (u64)B * 2 * (m + 1) * N);
+    return acc;
+  }
   // (Running the special rows' inverse block stages inside modup_ip_blk was
   // measured slower on cfg2, 8.91 vs 8.77 ms: it lengthens the special-target
   // CTAs by as much as the standalone ntt_blk_inv costs.)
@@ -896,25 +941,7 @@ void ks_hoisted(lcl_context* c, const RowMap& in, const u64* c1, u64 c1_stride, 
       hs.key[i] = rot_key(c, st);
       hs.key_aux[i] = c->d_rot_shoup.at(st);
     }
-    const double rb = 8.0 * N;
-    {  // (scope: the launch only, not the ModDowns below)
-    ProfScope ps(c, "modup_ip_hoist",
-                 rb * ((double)B * m * m + (double)B * m + 2.0 * ns * m * (m + 1) +
-                       2.0 * ns * B * (m + 1)),
-                 0.5 * N * B * m * m * 8);
-    dispatch_logn(c, [&](auto L1, auto) {
-      constexpr int LOGN1 = decltype(L1)::value;
-      const u32 grid = ((B + 3) / 4) * (m + 1) * (1u << LOGN1);
-#define LCL_HOIST(MM)                                                                        \
-  case MM:                                                                                   \
-    modup_ip_hoist<LOGN1, MM><<<grid, 64, 0, c->stream>>>(B, mid, c1, c1_stride, hs, ns,      \
-                                                          c->full, acc, acc_step, tabs(c));  \
-    break;
-      switch (m) { LCL_HOIST(1) LCL_HOIST(2) LCL_HOIST(3) LCL_HOIST(4) }
-#undef LCL_HOIST
-    });
-    }
-    post_launch(c);
+    hoist_launch(c, B, m, mid, c1, c1_stride, hs, ns, acc, acc_step);
     for (u32 i = 0; i < ns; ++i) each(s0 + i, acc + i * acc_step);
   }
 }
@@ -1025,7 +1052,8 @@ void rotate_level(lcl_context* c, const u64* in, u32 B, u32 m, size_t step, u64*
   // coefficient-domain automorphism instead.
   const u32* sigma = c->logn < 13 ? c->d_sigma.at(step) : nullptr;
   u64* acc = ks_switch(c, c1, in + (u64)m * N, 2ull * m * N, B, m, sigma, perm, key,
-                       c->d_rot_shoup.at(step), preinv_in);
+                       c->d_rot_shoup.at(step), preinv_in,
+                       c->logn >= 13 ? c->d_blkmap.at(step) : nullptr);
   const RowMap inm = ct_map(in, m, N, 2ull * m * N);
   ks_moddown(c, acc, B, m, ct_map(out, m, N, 2ull * m * N), accumulate ? inm : null_map(), inm,
              perm, preinv_out);
