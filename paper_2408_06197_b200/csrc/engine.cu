@@ -354,6 +354,8 @@ struct lcl_context {
   DevBuf ws_dec;
   // overlapped host round: H2D / D2H copy streams and per-slice events
   cudaStream_t h2d = nullptr, d2h = nullptr;
+  cudaStream_t unpk = nullptr;  // LCLT unpacking off the copy stream (host round)
+  std::vector<cudaEvent_t> unpk_ev;
   std::vector<cudaEvent_t> io_ev;
 
   u32 P() const { return full + 1; }
@@ -2306,6 +2308,8 @@ void free_context(lcl_context* c) {
   cudaFree(c->d_pinv);
   cudaFree(c->d_pairs);
   for (auto& kv : c->sched) cudaFree(kv.second);
+  if (c->unpk) cudaStreamDestroy(c->unpk);
+  for (cudaEvent_t e : c->unpk_ev) cudaEventDestroy(e);
   cudaFree(c->d_relin);
   cudaFree(c->d_relin_shoup);
   for (auto& kv : c->d_rot) cudaFree(kv.second);
@@ -3168,7 +3172,10 @@ struct Ingest {
     cuda_check(cudaGetLastError(), "lclt_unpack");
   }
   // clients [i0, i1), every chunk
-  void rows(lcl_context* c, u64* dc, u32 i0, u32 i1, u32 C, cudaStream_t s) const {
+  // clients [i0, i1), every chunk; with an unpack stream u (LCLT blobs), the
+  // copy stream records `copied` and moves on while u unpacks the group
+  void rows(lcl_context* c, u64* dc, u32 i0, u32 i1, u32 C, cudaStream_t s,
+            cudaStream_t u = nullptr, cudaEvent_t copied = nullptr) const {
     const u64 ctw = 2ull * c->full * c->N();
     if (words) {
       cuda_check(cudaMemcpyAsync(dc + (u64)i0 * C * ctw, words + (u64)i0 * C * ctw,
@@ -3177,7 +3184,11 @@ struct Ingest {
     }
     cuda_check(cudaMemcpyAsync(stage + (u64)i0 * C * stride, blobs + (u64)i0 * C * stride,
                                (u64)(i1 - i0) * C * stride, cudaMemcpyHostToDevice, s), "h2d blobs");
-    unpack(c, stage, C, i0, i1, 0, C, dc, err, s);
+    if (u) {
+      cuda_check(cudaEventRecord(copied, s), "event");
+      cuda_check(cudaStreamWaitEvent(u, copied, 0), "wait");
+    }
+    unpack(c, stage, C, i0, i1, 0, C, dc, err, u ? u : s);
   }
   // chunks [c0, c1) of all n clients
   void slice(lcl_context* c, u64* dc, u32 n, u32 C, u32 c0, u32 c1, cudaStream_t s) const {
@@ -3241,9 +3252,25 @@ void host_round_groups(lcl_context* ctx, const Ingest& in, u32 n, u32 C,
   cuda_check(cudaStreamWaitEvent(ctx->d2h, ev[0], 0), "wait");
   for (u32 g = 0; g < G; ++g) cuda_check(cudaStreamWaitEvent(ctx->lanes[g].stream, ev[0], 0), "wait");
   in.sel(ctx, ds, n, ctx->h2d);
+  // LCLT groups are unpacked on their own stream so the next group's copy
+  // starts as soon as this one's bytes are in (the unpack kernels would
+  // otherwise sit between the copies on the copy stream)
+  cudaStream_t up = nullptr;
+  if (in.blobs) {
+    if (!ctx->unpk) cuda_check(cudaStreamCreateWithFlags(&ctx->unpk, cudaStreamNonBlocking), "stream");
+    while (ctx->unpk_ev.size() < G + 1) {
+      cudaEvent_t e;
+      cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+      ctx->unpk_ev.push_back(e);
+    }
+    up = ctx->unpk;
+    // the selectors (unpacked on the copy stream) come first
+    cuda_check(cudaEventRecord(ctx->unpk_ev[G], ctx->h2d), "event");
+    cuda_check(cudaStreamWaitEvent(up, ctx->unpk_ev[G], 0), "wait");
+  }
   for (u32 g = 0; g < G; ++g) {
-    in.rows(ctx, dc, bound[g], bound[g + 1], C, ctx->h2d);
-    cuda_check(cudaEventRecord(ev[1 + g], ctx->h2d), "event");
+    in.rows(ctx, dc, bound[g], bound[g + 1], C, ctx->h2d, up, up ? ctx->unpk_ev[g] : nullptr);
+    cuda_check(cudaEventRecord(ev[1 + g], up ? up : ctx->h2d), "event");
   }
   u64* atern = ctx->ws_atern.get((u64)C * 3 * m * N);
   const u32 P = n * (n - 1) / 2;
