@@ -355,6 +355,7 @@ struct lcl_context {
   // overlapped host round: H2D / D2H copy streams and per-slice events
   cudaStream_t h2d = nullptr, d2h = nullptr;
   cudaStream_t unpk = nullptr;  // LCLT unpacking off the copy stream (host round)
+  cudaStream_t d2h_agg = nullptr;  // the aggregate's D2H, independent of the pairs' copies
   std::vector<cudaEvent_t> unpk_ev;
   std::vector<cudaEvent_t> io_ev;
 
@@ -2309,6 +2310,7 @@ void free_context(lcl_context* c) {
   cudaFree(c->d_pairs);
   for (auto& kv : c->sched) cudaFree(kv.second);
   if (c->unpk) cudaStreamDestroy(c->unpk);
+  if (c->d2h_agg) cudaStreamDestroy(c->d2h_agg);
   for (cudaEvent_t e : c->unpk_ev) cudaEventDestroy(e);
   cudaFree(c->d_relin);
   cudaFree(c->d_relin_shoup);
@@ -3250,6 +3252,7 @@ void host_round_groups(lcl_context* ctx, const Ingest& in, u32 n, u32 C,
   cuda_check(cudaEventRecord(ev[0], ctx->stream), "event");
   cuda_check(cudaStreamWaitEvent(ctx->h2d, ev[0], 0), "wait");
   cuda_check(cudaStreamWaitEvent(ctx->d2h, ev[0], 0), "wait");
+  cuda_check(cudaStreamWaitEvent(ctx->d2h_agg, ev[0], 0), "wait");
   for (u32 g = 0; g < G; ++g) cuda_check(cudaStreamWaitEvent(ctx->lanes[g].stream, ev[0], 0), "wait");
   in.sel(ctx, ds, n, ctx->h2d);
   // LCLT groups are unpacked on their own stream so the next group's copy
@@ -3268,9 +3271,21 @@ void host_round_groups(lcl_context* ctx, const Ingest& in, u32 n, u32 C,
     cuda_check(cudaEventRecord(ctx->unpk_ev[G], ctx->h2d), "event");
     cuda_check(cudaStreamWaitEvent(up, ctx->unpk_ev[G], 0), "wait");
   }
+  // LCL_TRACE_ROUND=1: print when the last byte landed, the last group was
+  // unpacked, the lanes finished and the last D2H completed (ms from start)
+  static const bool trace = std::getenv("LCL_TRACE_ROUND") != nullptr;
+  cudaEvent_t tr[6] = {};
+  if (trace) {
+    for (auto& e : tr) cuda_check(cudaEventCreate(&e), "trace event");
+    cuda_check(cudaEventRecord(tr[0], ctx->stream), "event");
+  }
   for (u32 g = 0; g < G; ++g) {
     in.rows(ctx, dc, bound[g], bound[g + 1], C, ctx->h2d, up, up ? ctx->unpk_ev[g] : nullptr);
     cuda_check(cudaEventRecord(ev[1 + g], up ? up : ctx->h2d), "event");
+  }
+  if (trace) {
+    cuda_check(cudaEventRecord(tr[1], ctx->h2d), "event");
+    cuda_check(cudaEventRecord(tr[2], up ? up : ctx->h2d), "event");
   }
   u64* atern = ctx->ws_atern.get((u64)C * 3 * m * N);
   const u32 P = n * (n - 1) / 2;
@@ -3297,9 +3312,11 @@ void host_round_groups(lcl_context* ctx, const Ingest& in, u32 n, u32 C,
           agg_finish(ctx, atern + (u64)c0 * 3 * m * N, Bc, average, d_pt, da + (u64)c0 * astride);
         }
         cuda_check(cudaEventRecord(ev[1 + G + g], ctx->stream), "event");
-        cuda_check(cudaStreamWaitEvent(ctx->d2h, ev[1 + G + g], 0), "wait");
+        // on its own stream: the D2H stream's earlier pair copies wait for
+        // the other lanes' chains, which would hold the aggregate back
+        cuda_check(cudaStreamWaitEvent(ctx->d2h_agg, ev[1 + G + g], 0), "wait");
         cuda_check(cudaMemcpyAsync(h_agg, da, (u64)C * astride * 8, cudaMemcpyDeviceToHost,
-                                   ctx->d2h), "d2h agg");
+                                   ctx->d2h_agg), "d2h agg");
       }
       if (B) {
         pair_accumulate_launch(ctx, dc, n, C, 0, C, ps, t, false);
@@ -3325,8 +3342,23 @@ void host_round_groups(lcl_context* ctx, const Ingest& in, u32 n, u32 C,
   ctx->counts.additions += (u64)P * (2ull * C - 1) + (u64)(n - 1) * C;
   for (u32 g = 0; g < G; ++g)
     cuda_check(cudaStreamWaitEvent(ctx->stream, ev[1 + 2 * G + g], 0), "join");
+  if (trace) {
+    cuda_check(cudaEventRecord(tr[3], ctx->stream), "event");
+    cuda_check(cudaEventRecord(tr[4], ctx->d2h), "event");
+    cuda_check(cudaEventRecord(tr[5], ctx->d2h_agg), "event");
+  }
+  cuda_check(cudaStreamSynchronize(ctx->d2h_agg), "round sync");
   cuda_check(cudaStreamSynchronize(ctx->d2h), "round sync");
   cuda_check(cudaStreamSynchronize(ctx->stream), "round sync");
+  if (trace) {
+    float t[5];
+    for (int i = 0; i < 5; ++i) cudaEventElapsedTime(&t[i], tr[0], tr[i + 1]);
+    std::fprintf(stderr,
+                 "host round (G=%u): last byte %.2f ms, last unpack %.2f, lanes done %.2f, pair d2h done %.2f, "
+                 "aggregate d2h done %.2f\n",
+                 G, t[0], t[1], t[2], t[3], t[4]);
+    for (auto& e : tr) cudaEventDestroy(e);
+  }
 }
 
 // lcl_server_round_host / lcl_server_round_lclt: H2D (words or LCLT blobs),
@@ -3375,6 +3407,7 @@ void server_round_host(lcl_context* ctx, const Ingest& in, size_t n, size_t chun
     ensure_pairs(ctx, (u32)n);
     if (!ctx->h2d) cuda_check(cudaStreamCreateWithFlags(&ctx->h2d, cudaStreamNonBlocking), "stream");
     if (!ctx->d2h) cuda_check(cudaStreamCreateWithFlags(&ctx->d2h, cudaStreamNonBlocking), "stream");
+    if (!ctx->d2h_agg) cuda_check(cudaStreamCreateWithFlags(&ctx->d2h_agg, cudaStreamNonBlocking), "stream");
     // 0: chunk slices, 1: 2 client groups, G >= 2: G groups (read per call).
     // Default 8 groups: the smaller the last group, the shorter the chain
     // left after the last byte lands -- e2e cfg3 592.5 (2 groups), 574.4 (4),
