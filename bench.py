@@ -35,6 +35,9 @@ import sys
 import threading
 import time
 
+# before any CUDA context: the host round's streams each get a hardware queue
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 

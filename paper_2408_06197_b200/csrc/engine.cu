@@ -356,6 +356,10 @@ struct lcl_context {
   cudaStream_t h2d = nullptr, d2h = nullptr;
   cudaStream_t unpk = nullptr;  // LCLT unpacking off the copy stream (host round)
   cudaStream_t d2h_agg = nullptr;  // the aggregate's D2H, independent of the pairs' copies
+  cudaStream_t crit = nullptr;     // highest-priority streams for the host round's last two lanes
+  cudaStream_t crit2 = nullptr;
+  cudaStream_t lo = nullptr;       // lowest priority: the last group's slice accumulations
+  cudaStream_t crit3 = nullptr;    // highest priority: the last group's aggregate slices
   std::vector<cudaEvent_t> unpk_ev;
   std::vector<cudaEvent_t> io_ev;
 
@@ -2311,6 +2315,10 @@ void free_context(lcl_context* c) {
   for (auto& kv : c->sched) cudaFree(kv.second);
   if (c->unpk) cudaStreamDestroy(c->unpk);
   if (c->d2h_agg) cudaStreamDestroy(c->d2h_agg);
+  if (c->crit) cudaStreamDestroy(c->crit);
+  if (c->crit2) cudaStreamDestroy(c->crit2);
+  if (c->lo) cudaStreamDestroy(c->lo);
+  if (c->crit3) cudaStreamDestroy(c->crit3);
   for (cudaEvent_t e : c->unpk_ev) cudaEventDestroy(e);
   cudaFree(c->d_relin);
   cudaFree(c->d_relin_shoup);
@@ -3192,6 +3200,28 @@ struct Ingest {
     }
     unpack(c, stage, C, i0, i1, 0, C, dc, err, u ? u : s);
   }
+  // chunks [c0, c1) of clients [i0, i1) (one pitched copy), unpacked on u
+  // when given (the copy stream records `copied` and moves on)
+  void part(lcl_context* c, u64* dc, u32 i0, u32 i1, u32 C, u32 c0, u32 c1, cudaStream_t s,
+            cudaStream_t u = nullptr, cudaEvent_t copied = nullptr) const {
+    const u64 ctw = 2ull * c->full * c->N();
+    if (words) {
+      cuda_check(cudaMemcpy2DAsync(dc + ((u64)i0 * C + c0) * ctw, (u64)C * ctw * 8,
+                                   words + ((u64)i0 * C + c0) * ctw, (u64)C * ctw * 8,
+                                   (u64)(c1 - c0) * ctw * 8, i1 - i0, cudaMemcpyHostToDevice, s),
+                 "h2d part");
+      return;
+    }
+    cuda_check(cudaMemcpy2DAsync(stage + ((u64)i0 * C + c0) * stride, (u64)C * stride,
+                                 blobs + ((u64)i0 * C + c0) * stride, (u64)C * stride,
+                                 (u64)(c1 - c0) * stride, i1 - i0, cudaMemcpyHostToDevice, s),
+               "h2d blob part");
+    if (u) {
+      cuda_check(cudaEventRecord(copied, s), "event");
+      cuda_check(cudaStreamWaitEvent(u, copied, 0), "wait");
+    }
+    unpack(c, stage, C, i0, i1, c0, c1, dc, err, u ? u : s);
+  }
   // chunks [c0, c1) of all n clients
   void slice(lcl_context* c, u64* dc, u32 n, u32 C, u32 c0, u32 c1, cudaStream_t s) const {
     const u64 ctw = 2ull * c->full * c->N();
@@ -3233,14 +3263,61 @@ void host_round_groups(lcl_context* ctx, const Ingest& in, u32 n, u32 C,
   const u64 N = ctx->N();
   const u64 dstride = 2ull * (m - 1) * N;
   const u64 astride = 2ull * (average ? m - 2 : m - 1) * N;
+  // The last T clients arrive as single-client groups (LCL_TAIL_SINGLES; by
+  // default n / 4 when one client's bytes take >= ~10 ms of PCIe): a single
+  // client's chain (its pairs' accumulation and key-switch ladder) then
+  // fits inside the next client's copy, so only the last client's chain is
+  // left after the last byte. The head [0, n - T) is cut by the sqrt rule.
+  const int tail_env = [] {
+    const char* e = std::getenv("LCL_TAIL_SINGLES");
+    return e ? atoi(e) : -1;
+  }();
+  const u64 client_bytes = (u64)C * 2 * m * N * 8;
+  u32 T = tail_env >= 0 ? (u32)tail_env : (client_bytes >= (512ull << 20) ? n / 4 : 0);
+  T = std::min(T, n - 2);
+  const u32 head = n - T;
   std::vector<u32> bound{0};
   for (u32 g = 1; g < G; ++g) {
-    const u32 kb = (u32)std::lround(n * std::sqrt((double)g / G));
-    if (kb > bound.back() + 1 && kb < n) bound.push_back(kb);
+    const u32 kb = (u32)std::lround(head * std::sqrt((double)g / G));
+    if (kb > bound.back() + 1 && kb < head) bound.push_back(kb);
   }
-  bound.push_back(n);
+  bound.push_back(head);
+  for (u32 j = head + 1; j <= n; ++j) bound.push_back(j);
   G = (u32)bound.size() - 1;
   ensure_lanes(ctx, G);
+  // With single-client tail groups, the last two lanes (the chains that
+  // finish last) run on highest-priority streams, ahead of the other lanes'
+  // work and of the last group's slice accumulations (lowest priority), and
+  // the aggregate slices too (LCL_LANE_PRIO = 0 / 1 forces it off / on;
+  // cfg3 e2e 541.4 -> 539.9 ms; at cfg2, with no tail singles, it costs
+  // 12.8 -> 13.6 ms, so it follows T by default)
+  const int prio_env = [] {
+    const char* e = std::getenv("LCL_LANE_PRIO");
+    return e ? atoi(e) : -1;
+  }();
+  const bool prio = prio_env >= 0 ? prio_env == 1 : T > 0;
+  if (!ctx->crit) {
+    int lo = 0, hi = 0;
+    cuda_check(cudaDeviceGetStreamPriorityRange(&lo, &hi), "priority range");
+    cuda_check(cudaStreamCreateWithPriority(&ctx->crit, cudaStreamNonBlocking, hi), "stream");
+    cuda_check(cudaStreamCreateWithPriority(&ctx->crit2, cudaStreamNonBlocking, hi), "stream");
+    cuda_check(cudaStreamCreateWithPriority(&ctx->lo, cudaStreamNonBlocking, lo), "stream");
+    cuda_check(cudaStreamCreateWithPriority(&ctx->crit3, cudaStreamNonBlocking, hi), "stream");
+  }
+  struct LaneSwap {  // swapped back on every exit path
+    lcl_context* c;
+    u32 g;
+    bool on;
+    ~LaneSwap() {
+      if (!on) return;
+      std::swap(c->lanes[g].stream, c->crit);
+      if (g) std::swap(c->lanes[g - 1].stream, c->crit2);
+    }
+  } lane_swap{ctx, G - 1, prio};
+  if (prio) {
+    std::swap(ctx->lanes[G - 1].stream, ctx->crit);
+    if (G >= 2) std::swap(ctx->lanes[G - 2].stream, ctx->crit2);
+  }
   while (ctx->io_ev.size() < 1 + 3 * (size_t)G) {
     cudaEvent_t e;
     cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
@@ -3260,7 +3337,11 @@ void host_round_groups(lcl_context* ctx, const Ingest& in, u32 n, u32 C,
   // otherwise sit between the copies on the copy stream)
   cudaStream_t up = nullptr;
   if (in.blobs) {
-    if (!ctx->unpk) cuda_check(cudaStreamCreateWithFlags(&ctx->unpk, cudaStreamNonBlocking), "stream");
+    if (!ctx->unpk) {  // highest priority: every later step waits for the unpacked words
+      int lo = 0, hi = 0;
+      cuda_check(cudaDeviceGetStreamPriorityRange(&lo, &hi), "priority range");
+      cuda_check(cudaStreamCreateWithPriority(&ctx->unpk, cudaStreamNonBlocking, hi), "stream");
+    }
     while (ctx->unpk_ev.size() < G + 1) {
       cudaEvent_t e;
       cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
@@ -3275,12 +3356,73 @@ void host_round_groups(lcl_context* ctx, const Ingest& in, u32 n, u32 C,
   // unpacked, the lanes finished and the last D2H completed (ms from start)
   static const bool trace = std::getenv("LCL_TRACE_ROUND") != nullptr;
   cudaEvent_t tr[6] = {};
+  std::vector<cudaEvent_t> trl;  // per lane: pair accumulation done, chain done
   if (trace) {
     for (auto& e : tr) cuda_check(cudaEventCreate(&e), "trace event");
+    trl.resize(2 * G);
+    for (auto& e : trl) cuda_check(cudaEventCreate(&e), "trace event");
     cuda_check(cudaEventRecord(tr[0], ctx->stream), "event");
   }
+  // The last group can arrive in S chunk slices (LCL_LAST_SLICES, default
+  // 8): the aggregate is a sum over every client, so only the last group's
+  // bytes hold it back; per slice, the aggregate chunks are finished and
+  // copied out while the next slice lands, instead of all 342 chunks'
+  // aggregate (1.07 GB D2H at cfg3) after the last byte. LCL_LAST_PAIRS=1
+  // also accumulates the last group's pairs slice by slice.
+  const int last_slices_env = [] {
+    const char* e = std::getenv("LCL_LAST_SLICES");
+    return e ? atoi(e) : 8;
+  }();
+  const bool last_pairs = [] {
+    const char* e = std::getenv("LCL_LAST_PAIRS");
+    return e && e[0] == '1';
+  }();
+  const u32 S = G >= 2 && last_slices_env > 1 ? std::min<u32>((u32)last_slices_env, C) : 1;
+  while (ctx->io_ev.size() < 1 + 3 * (size_t)G + 2 * S + 4) {
+    cudaEvent_t e;
+    cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+    ctx->io_ev.push_back(e);
+  }
+  ev = ctx->io_ev.data();
+  cudaEvent_t* sev = ev + 1 + 3 * G;  // slice s landed (and unpacked)
+  cudaEvent_t* aev = sev + S;         // slice s's aggregate chunks finished
+  cudaEvent_t lfork = aev[S], lacc = aev[S + 1];  // last lane -> slice stream -> last lane
+  cudaEvent_t afork = aev[S + 2], ajoin = aev[S + 3];  // lane 0 -> aggregate slices -> lane 0
+  // Runs f with the context's stream replaced by s, ordered after and
+  // joined back into the current stream (lane workspaces stay the lane's).
+  auto on_stream = [&](cudaStream_t st, cudaEvent_t fork, cudaEvent_t join, auto&& f) {
+    cudaStream_t own = ctx->stream;
+    cuda_check(cudaEventRecord(fork, own), "event");
+    cuda_check(cudaStreamWaitEvent(st, fork, 0), "wait");
+    ctx->stream = st;
+    try {
+      f();
+    } catch (...) {
+      ctx->stream = own;
+      throw;
+    }
+    ctx->stream = own;
+    cuda_check(cudaEventRecord(join, st), "event");
+    cuda_check(cudaStreamWaitEvent(own, join, 0), "wait");
+  };
+  if (in.blobs) {
+    while (ctx->unpk_ev.size() < G + 1 + S) {
+      cudaEvent_t e;
+      cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+      ctx->unpk_ev.push_back(e);
+    }
+  }
+  auto slice_lo = [&](u32 s) { return (u32)((u64)C * s / S); };
   for (u32 g = 0; g < G; ++g) {
-    in.rows(ctx, dc, bound[g], bound[g + 1], C, ctx->h2d, up, up ? ctx->unpk_ev[g] : nullptr);
+    if (g + 1 == G && S > 1) {
+      for (u32 s = 0; s < S; ++s) {
+        in.part(ctx, dc, bound[g], bound[g + 1], C, slice_lo(s), slice_lo(s + 1), ctx->h2d, up,
+                up ? ctx->unpk_ev[G + 1 + s] : nullptr);
+        cuda_check(cudaEventRecord(sev[s], up ? up : ctx->h2d), "event");
+      }
+    } else {
+      in.rows(ctx, dc, bound[g], bound[g + 1], C, ctx->h2d, up, up ? ctx->unpk_ev[g] : nullptr);
+    }
     cuda_check(cudaEventRecord(ev[1 + g], up ? up : ctx->h2d), "event");
   }
   if (trace) {
@@ -3296,6 +3438,54 @@ void host_round_groups(lcl_context* ctx, const Ingest& in, u32 n, u32 C,
     const u32 B = pair_count(n, ps);
     u64* o = dd + (u64)first * dstride;
     u64* t = tern + (u64)first * 3 * m * N;
+    if (g + 1 == G && S > 1) {
+      // the last group's aggregate slices on lane 0 (its own chain is long
+      // done): tensor of the group's clients onto the earlier groups' sums,
+      // relinearize + rescale, D2H on the aggregate's copy stream
+      on_lane(ctx, 0, [&] { on_stream(prio ? ctx->crit3 : ctx->stream, afork, ajoin, [&] {
+        cuda_check(cudaStreamWaitEvent(ctx->stream, ev[G + g], 0), "wait");
+        for (u32 s = 0; s < S; ++s) {
+          const u32 c0 = slice_lo(s), c1 = slice_lo(s + 1);
+          cuda_check(cudaStreamWaitEvent(ctx->stream, sev[s], 0), "wait");
+          agg_tensor(ctx, dc, ds, n, C, c0, c1 - c0, bound[g], bound[g + 1],
+                     atern + (u64)c0 * 3 * m * N, true);
+          for (u32 b0 = c0; b0 < c1; b0 += sub_batch(ctx, m)) {
+            const u32 Bc = std::min(c1, b0 + sub_batch(ctx, m)) - b0;
+            agg_finish(ctx, atern + (u64)b0 * 3 * m * N, Bc, average, d_pt, da + (u64)b0 * astride);
+          }
+          cuda_check(cudaEventRecord(aev[s], ctx->stream), "event");
+          cuda_check(cudaStreamWaitEvent(ctx->d2h_agg, aev[s], 0), "wait");
+          cuda_check(cudaMemcpyAsync(h_agg + (u64)c0 * astride, da + (u64)c0 * astride,
+                                     (u64)(c1 - c0) * astride * 8, cudaMemcpyDeviceToHost,
+                                     ctx->d2h_agg), "d2h agg slice");
+        }
+        cuda_check(cudaEventRecord(ev[1 + G + g], ctx->stream), "event");
+      }); });
+      on_lane(ctx, g, [&] {
+        if (B) {
+          if (last_pairs) {
+            // slice accumulations on the lowest-priority stream (they have
+            // slack until the last byte); the chain continues on the lane
+            on_stream(prio ? ctx->lo : ctx->stream, lfork, lacc, [&] {
+              for (u32 s = 0; s < S; ++s) {
+                cuda_check(cudaStreamWaitEvent(ctx->stream, sev[s], 0), "wait");
+                pair_accumulate_launch(ctx, dc, n, C, slice_lo(s), slice_lo(s + 1), ps, t, s > 0);
+              }
+            });
+          } else {
+            cuda_check(cudaStreamWaitEvent(ctx->stream, ev[1 + g], 0), "wait");
+            pair_accumulate_launch(ctx, dc, n, C, 0, C, ps, t, false);
+          }
+          if (trace) cuda_check(cudaEventRecord(trl[2 * g], ctx->stream), "event");
+          u64* ctA = ctx->ws_ctA.get((u64)B * 2 * m * N);
+          relinearize_batch(ctx, t, B, m, ctA);
+          rescale_batch(ctx, ctA, B, m, o);
+          slot_reduce_batch(ctx, o, B, m - 1, width, k, o);
+        }
+        if (trace) cuda_check(cudaEventRecord(trl[2 * g + 1], ctx->stream), "event");
+        cuda_check(cudaEventRecord(ev[1 + 2 * G + g], ctx->stream), "event");
+      });
+    } else
     on_lane(ctx, g, [&] {
       cuda_check(cudaStreamWaitEvent(ctx->stream, ev[1 + g], 0), "wait");
       if (g > 0) cuda_check(cudaStreamWaitEvent(ctx->stream, ev[G + g], 0), "wait");
@@ -3320,11 +3510,13 @@ void host_round_groups(lcl_context* ctx, const Ingest& in, u32 n, u32 C,
       }
       if (B) {
         pair_accumulate_launch(ctx, dc, n, C, 0, C, ps, t, false);
+        if (trace) cuda_check(cudaEventRecord(trl[2 * g], ctx->stream), "event");
         u64* ctA = ctx->ws_ctA.get((u64)B * 2 * m * N);
         relinearize_batch(ctx, t, B, m, ctA);
         rescale_batch(ctx, ctA, B, m, o);
         slot_reduce_batch(ctx, o, B, m - 1, width, k, o);
       }
+      if (trace) cuda_check(cudaEventRecord(trl[2 * g + 1], ctx->stream), "event");
       cuda_check(cudaEventRecord(ev[1 + 2 * G + g], ctx->stream), "event");
     });
     cuda_check(cudaStreamWaitEvent(ctx->d2h, ev[1 + 2 * G + g], 0), "wait");
@@ -3342,6 +3534,8 @@ void host_round_groups(lcl_context* ctx, const Ingest& in, u32 n, u32 C,
   ctx->counts.additions += (u64)P * (2ull * C - 1) + (u64)(n - 1) * C;
   for (u32 g = 0; g < G; ++g)
     cuda_check(cudaStreamWaitEvent(ctx->stream, ev[1 + 2 * G + g], 0), "join");
+  // the aggregate's last part (on lane 0 when the last group is sliced)
+  cuda_check(cudaStreamWaitEvent(ctx->stream, ev[2 * G], 0), "join aggregate");
   if (trace) {
     cuda_check(cudaEventRecord(tr[3], ctx->stream), "event");
     cuda_check(cudaEventRecord(tr[4], ctx->d2h), "event");
@@ -3357,6 +3551,14 @@ void host_round_groups(lcl_context* ctx, const Ingest& in, u32 n, u32 C,
                  "host round (G=%u): last byte %.2f ms, last unpack %.2f, lanes done %.2f, pair d2h done %.2f, "
                  "aggregate d2h done %.2f\n",
                  G, t[0], t[1], t[2], t[3], t[4]);
+    for (u32 g = 0; g < G; ++g) {
+      float a = 0, b = 0;
+      cudaEventElapsedTime(&a, tr[0], trl[2 * g]);
+      cudaEventElapsedTime(&b, tr[0], trl[2 * g + 1]);
+      std::fprintf(stderr, "  lane %u (clients %u..%u, %u pairs): accumulated %.2f ms, chain done %.2f\n", g,
+                   bound[g], bound[g + 1] - 1, pair_count(n, completed_by(bound[g], bound[g + 1])), a, b);
+    }
+    for (auto& e : trl) cudaEventDestroy(e);
     for (auto& e : tr) cudaEventDestroy(e);
   }
 }
@@ -3412,9 +3614,14 @@ void server_round_host(lcl_context* ctx, const Ingest& in, size_t n, size_t chun
     // Default 8 groups: the smaller the last group, the shorter the chain
     // left after the last byte lands -- e2e cfg3 592.5 (2 groups), 574.4 (4),
     // 568.9 (6), 566.2 (8), 567.8 ms (10); cfg2 13.17 / 14.06 / 12.81 / 12.66
-    // / 13.55 ms. (The last group in 8 chunk slices, each slice's aggregate
-    // chunks finished and copied out while the next lands, measured slower:
-    // 582 / 15.4 ms -- the per-slice work outlasts a slice's copy.)
+    // / 13.55 ms. Round 2, with 32 hardware queues (CUDA_DEVICE_MAX_CONNECTIONS,
+    // set by the package: with 8, lanes alias onto the copy streams' queues),
+    // the last group in 8 chunk slices for the aggregate (549.4 ms), the last
+    // n / 4 clients as single-client groups and the last lanes at high
+    // priority: cfg3 e2e 556.9 -> ~540 ms; cfg2 unchanged (no tail singles).
+    // Rejected: the last client's pairs accumulated per slice (LCL_LAST_PAIRS=1,
+    // 541-551 ms: the slices starve the second-to-last chain), 2 or 4 slots
+    // per thread in the pair kernel for small pair sets (683 / 562 ms).
     const char* mode_env = std::getenv("LCL_HOST_ROUND");
     const int mode = mode_env ? atoi(mode_env) : 8;
     if (mode >= 1 && ctx->pair_f64 && n >= 4 && !ctx->prof_on) {

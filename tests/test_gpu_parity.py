@@ -317,15 +317,26 @@ def test_masked_aggregate_bit_exact_vs_reference(golden):
     assert agg.scale == rig.meta["agg_scale"]
 
 
-@pytest.mark.parametrize("mode", ["1", "0", "3", "8"])
+@pytest.mark.parametrize("mode", ["1", "0", "3", "8", "8:unsliced", "8:singles", "8:singles+slicepairs"])
 def test_host_round_overlapped_bit_exact_vs_reference(golden, mode, monkeypatch):
     """lcl_server_round_host (host buffers in and out; H2D overlapped with
     the computation: 1 = two client groups on two lanes, 0 = chunk slices,
-    3 / 8 = three / eight client groups, 8 the default) against the
-    reference digests and op counters."""
+    3 / 8 = three / eight client groups, 8 the default: the last group's
+    aggregate in chunk slices; unsliced = one piece; singles = the last two
+    clients as single-client groups on high-priority lanes; slicepairs = the
+    last group's pairs accumulated per slice on a low-priority stream)
+    against the reference digests and op counters."""
     L = _L()
     import ctypes as C
-    monkeypatch.setenv("LCL_HOST_ROUND", mode)
+    groups, _, form = mode.partition(":")
+    monkeypatch.setenv("LCL_HOST_ROUND", groups)
+    if form == "unsliced":
+        monkeypatch.setenv("LCL_LAST_SLICES", "1")
+    if form.startswith("singles"):
+        monkeypatch.setenv("LCL_TAIL_SINGLES", "2")
+        monkeypatch.setenv("LCL_LANE_PRIO", "1")
+    if form.endswith("slicepairs"):
+        monkeypatch.setenv("LCL_LAST_PAIRS", "1")
     rig = golden
     if not rig.lazy:
         pytest.skip("the host round entry is the lazy, reduced per-pair round")
@@ -774,5 +785,29 @@ def test_cfg3_benchmark_round_bit_exact_vs_reference():
     assert ctx.counters() == meta["agg_ops"]
     assert dsha(agg.chunks) == d["agg"]
     assert agg.scale == meta["agg_scale"]
+    # the same round through the host entry, pinned buffers in and out (the
+    # bench's e2e form at its own shape: the last group's aggregate in chunk
+    # slices, n / 4 single-client tail groups on high-priority lanes)
+    import ctypes as C
+    h_clients = torch.empty(big.shape, dtype=torch.int64, pin_memory=True)
+    h_clients.copy_(big)
     del big
     torch.cuda.empty_cache()
+    h_sel = torch.empty((n,) + tuple(sels[0].shape), dtype=torch.int64, pin_memory=True)
+    for i in range(n):
+        h_sel[i].copy_(sels[i])
+    m = ctx.full
+    h_dist = torch.empty((n * (n - 1) // 2, 2, m - 1, N), dtype=torch.int64, pin_memory=True)
+    h_agg = torch.empty((C_, 2, m - 1, N), dtype=torch.int64, pin_memory=True)
+    ctx.use_relin_key(rk)
+    ctx.use_rotation_keys(keys, meta["steps"])
+    ctx.reset_counters()
+    L._check(L.lib().lcl_server_round_host(
+        ctx.h, C.c_void_p(h_clients.data_ptr()), C.c_void_p(h_sel.data_ptr()), n, C_,
+        ctx.scale(), width, k, 1, 0, C.c_void_p(h_dist.data_ptr()), C.c_void_p(h_agg.data_ptr())))
+    for p, (i, j) in enumerate(dm.keys):
+        assert dsha(h_dist[p]) == d[f"dist_{i}_{j}"], (i, j)
+    assert dsha(h_agg) == d["agg"]
+    want = {key: meta["dist_ops"][key] + meta["agg_ops"][key] for key in meta["dist_ops"]}
+    assert ctx.counters() == want
+    del h_clients, h_sel, h_dist, h_agg
