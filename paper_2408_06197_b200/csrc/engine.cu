@@ -1471,7 +1471,14 @@ bool pair_accumulate_f64_cfg(lcl_context* c, const u64* clients, u32 n, u32 chun
     nl = bs.nl;
     sched_len = groups * per_cta;
   }
-  const u32 threads = std::max<u32>(64, ((per_cta + 31) / 32) * 32);
+  // every warp of a CTA runs the pair math (warps of padding included), so
+  // the CTA is sized to the schedule: one warp for <= 32 pairs (a host-round
+  // group of one client) -- LCL_PAIR_MIN_THREADS (default 32; 64 before)
+  static const u32 min_threads = [] {
+    const char* e = std::getenv("LCL_PAIR_MIN_THREADS");
+    return e ? (u32)std::max(32, atoi(e)) : 32u;
+  }();
+  const u32 threads = std::max<u32>(min_threads, ((per_cta + 31) / 32) * 32);
   const size_t smem = (size_t)STAGES * nl * (2 * TE + 2) * 8;
   if (smem > 100 * 1024) return false;
   if (!blocked) sched = pair_schedule(c, n, ps, per_cta, TE + 1);
