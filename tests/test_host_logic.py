@@ -198,3 +198,20 @@ def test_stack_clients_zero_copy_only_for_the_whole_batch():
     limbs = big[:, :, :, :1]
     lv = [L.PackedWeights(limbs[i], 10, 1.0, 1.0) for i in range(3)]
     assert torch.equal(L.stack_clients(lv), limbs)
+
+
+def test_package_import_sets_32_hardware_queues():
+    """The host round runs ~16 streams; the package asks for 32 hardware
+    work queues before any CUDA context exists (an explicit setting wins)."""
+    import subprocess
+    import sys
+
+    code = ("import os; os.environ.pop('CUDA_DEVICE_MAX_CONNECTIONS', None); "
+            "import paper_2408_06197_b200; print(os.environ['CUDA_DEVICE_MAX_CONNECTIONS'])")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True, check=True)
+    assert out.stdout.strip() == "32"
+    code2 = ("import os; os.environ['CUDA_DEVICE_MAX_CONNECTIONS'] = '16'; "
+             "import paper_2408_06197_b200; print(os.environ['CUDA_DEVICE_MAX_CONNECTIONS'])")
+    out = subprocess.run([sys.executable, "-c", code2], cwd=root, capture_output=True, text=True, check=True)
+    assert out.stdout.strip() == "16"
