@@ -1444,7 +1444,7 @@ const uint2* pair_schedule(lcl_context* c, u32 n, const PairSet& ps, u32 per_cta
   return d;
 }
 
-template <int TE, int STAGES, int MINB, bool PF>
+template <int TE, int STAGES, int MINB, bool PF, int W = 1>
 bool pair_accumulate_f64_cfg(lcl_context* c, const u64* clients, u32 n, u32 chunks, u32 c0,
                              u32 c1, const PairSet& ps, u64* tern, bool accumulate) {
   constexpr int MAXT = 192;
@@ -1478,18 +1478,22 @@ bool pair_accumulate_f64_cfg(lcl_context* c, const u64* clients, u32 n, u32 chun
     const char* e = std::getenv("LCL_PAIR_MIN_THREADS");
     return e ? (u32)std::max(32, atoi(e)) : 32u;
   }();
-  const u32 threads = std::max<u32>(min_threads, ((per_cta + 31) / 32) * 32);
-  const size_t smem = (size_t)STAGES * nl * (2 * TE + 2) * 8;
+  u32 threads = std::max<u32>(min_threads, ((per_cta + 31) / 32) * 32);
+  if (W > 1) {  // W warps on a W * TE-slot tile, one warp's worth of pairs
+    if (blocked || per_cta > 32) return false;
+    threads = 32 * W;
+  }
+  const size_t smem = (size_t)STAGES * W * nl * (2 * TE + 2) * 8;
   if (smem > 100 * 1024) return false;
   if (!blocked) sched = pair_schedule(c, n, ps, per_cta, TE + 1);
-  const u64 tiles = (u64)m * c->n / TE;
-  allow_smem(pair_accumulate_f64<TE, STAGES, MAXT, MINB, PF>, smem);
+  const u64 tiles = (u64)m * c->n / (TE * W);
+  allow_smem(pair_accumulate_f64<TE, STAGES, MAXT, MINB, PF, W>, smem);
   for (u32 cb = c0; cb < c1; cb += 256) {  // exact for 256 chunks per pass
     const u32 ce = std::min(c1, cb + 256);
     const bool acc = accumulate || cb > c0;
     ProfScope ps(c, "pair_accumulate",
                  8.0 * c->N() * m * (2.0 * n * (ce - cb) * groups + 3.0 * pairs * (acc ? 2 : 1)));
-    pair_accumulate_f64<TE, STAGES, MAXT, MINB, PF><<<(u32)(tiles * groups), threads, smem, c->stream>>>(
+    pair_accumulate_f64<TE, STAGES, MAXT, MINB, PF, W><<<(u32)(tiles * groups), threads, smem, c->stream>>>(
         clients, n, cb, ce, chunks, m, c->logn, sched, sched_len, groups, per_cta, tern, acc ? 1 : 0,
         c->d_primes, clist, nl);
     post_launch(c);
@@ -1516,6 +1520,16 @@ bool pair_accumulate_f64_cfg(lcl_context* c, const u64* clients, u32 n, u32 chun
 // else the split-23 integer kernel.
 void pair_accumulate_launch(lcl_context* c, const u64* clients, u32 n, u32 chunks, u32 c0,
                             u32 c1, const PairSet& ps, u64* tern, bool accumulate) {
+  // <= 32 pairs (a host-round group of one client): 4 warps on a 32-slot
+  // tile, 256-byte copies (LCL_PAIR_W=1 turns it off)
+  const char* we = std::getenv("LCL_PAIR_W");
+  const int pw = we ? atoi(we) : 4;
+  if (c->pair_f64 && pw == 4 && c->n >= 32 * 8 &&
+      pair_accumulate_f64_cfg<8, 6, 2, false, 4>(c, clients, n, chunks, c0, c1, ps, tern, accumulate))
+    return;
+  if (c->pair_f64 && pw == 2 && c->n >= 16 * 8 &&
+      pair_accumulate_f64_cfg<8, 6, 2, false, 2>(c, clients, n, chunks, c0, c1, ps, tern, accumulate))
+    return;
   if (c->pair_f64 &&
       pair_accumulate_f64_cfg<8, 6, 2, false>(c, clients, n, chunks, c0, c1, ps, tern, accumulate))
     return;

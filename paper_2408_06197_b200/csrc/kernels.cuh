@@ -168,7 +168,13 @@ __device__ __forceinline__ u64 dmodq(double v, u64 q, const PrimeConst& P) {
 // threads by a host schedule (sched[k] = (i | j << 16, output index)) that
 // puts clients of distinct shared-memory bank groups in every quarter warp,
 // so the 16-byte tile reads are conflict-free.
-template <int TE, int STAGES, int MAXT, int MINB, bool PF>
+// W > 1 (at most 32 pairs per CTA): the CTA's tile is W * TE slots wide and
+// warp w owns slots [w TE, (w + 1) TE) of it for the same pairs, so every
+// (client, poly) piece copied per chunk is W * 64 bytes: 64-byte pieces cap
+// the staging at ~3 TB/s, 256-byte ones reach ~7 TB/s
+// (tools/microbench/stride_probe.cu) -- the case of a host-round group of
+// one client, whose few pairs leave the FP64 pipe idle.
+template <int TE, int STAGES, int MAXT, int MINB, bool PF, int W = 1>
 __global__ void __launch_bounds__(MAXT, MINB)
     pair_accumulate_f64(const u64* __restrict__ clients, u32 n, u32 c_begin, u32 c_end,
                         u32 chunks_total, u32 m, u32 logn, const uint2* __restrict__ sched,
@@ -177,42 +183,47 @@ __global__ void __launch_bounds__(MAXT, MINB)
                         const unsigned short* __restrict__ clist, u32 nl) {
   static_assert(TE % 2 == 0, "slots are read from shared memory in 16-byte pairs");
   constexpr int CS = 2 * TE + 2;  // words per client: CS / 2 odd spreads clients over bank groups
-  extern __shared__ u64 tile[];   // [STAGES][nl][CS]
+  extern __shared__ u64 tile[];   // [STAGES][W][nl][CS]
   const u32 N = 1u << logn;
-  const u32 tiles_per_row = N / TE;
+  const u32 tiles_per_row = N / (TE * W);
   const u32 g = blockIdx.x % groups;
   const u32 tix = blockIdx.x / groups;
   const u32 r = tix / tiles_per_row;
-  const u32 a0 = (tix - r * tiles_per_row) * TE;
+  const u32 a0 = (tix - r * tiles_per_row) * (TE * W);
+  const u32 sub = W > 1 ? threadIdx.x / 32 : 0;     // the thread's TE-slot sub-tile
+  const u32 pt = W > 1 ? threadIdx.x % 32 : threadIdx.x;  // its pair within the CTA
   const u64 ct_words = 2ull * m * N;
   // clients staged by this CTA: all n (clist == nullptr), or the nl clients
   // of its client-blocked pair group, clist[g * nl ..]
   if (!clist) nl = n;
   const unsigned short* gl = clist ? clist + (size_t)g * nl : nullptr;
-  const u32 tw = nl * CS;
-  const u32 k = g * pairs_per_cta + threadIdx.x;
+  const u32 tw = W * nl * CS;
+  const u32 k = g * pairs_per_cta + pt;
   // schedule entries with .y == ~0 pad a group to pairs_per_cta
-  const uint2 sk = threadIdx.x < pairs_per_cta && k < pairs ? __ldg(sched + k) : make_uint2(0u, ~0u);
+  const uint2 sk = pt < pairs_per_cta && k < pairs ? __ldg(sched + k) : make_uint2(0u, ~0u);
   const bool valid = sk.y != ~0u;
-  const u32 oi = (sk.x & 0xFFFFu) * CS, oj = (sk.x >> 16) * CS;
+  const u32 oi = (sub * nl + (sk.x & 0xFFFFu)) * CS, oj = (sub * nl + (sk.x >> 16)) * CS;
 
   // chunk copies: nl * TE 16-byte vectors, vector v by thread v mod blockDim.
   // The first vector's addresses are computed once (every thread has at most
   // one when nl * TE <= blockDim, the common case); further ones per chunk.
   const u64* cbase = clients + (u64)r * N + a0;
+  // vector v: client cl, poly h, word x of the poly's W * TE-word piece
+  // (consecutive v read consecutive 16 bytes), parked in sub-tile x / TE
   auto vec_src = [&](u32 v, u32& soff) {
-    const u32 cl = v / TE, w = (v % TE) * 2, h = w / TE, e = w % TE;
-    soff = cl * CS + w;
+    const u32 cl = v / (W * TE), rest = (v % (W * TE)) * 2;
+    const u32 h = rest / (W * TE), x = rest % (W * TE), ws = x / TE, e = x % TE;
+    soff = (ws * nl + cl) * CS + h * TE + e;
     const u32 gc = gl ? (u32)__ldg(gl + cl) : cl;
-    return cbase + (u64)gc * chunks_total * ct_words + (u64)h * m * N + e;
+    return cbase + (u64)gc * chunks_total * ct_words + (u64)h * m * N + x;
   };
-  const bool has0 = threadIdx.x < nl * TE;
+  const bool has0 = threadIdx.x < nl * TE * W;
   u32 soff0 = 0;
   const u64* src0 = has0 ? vec_src(threadIdx.x, soff0) : cbase;
   auto issue = [&](u32 c, u32 stage) {
     if (c < c_end) {
       if (has0) cp_async16(tile + stage * tw + soff0, src0 + (u64)c * ct_words);
-      for (u32 v = threadIdx.x + blockDim.x; v < nl * TE; v += blockDim.x) {
+      for (u32 v = threadIdx.x + blockDim.x; v < nl * TE * W; v += blockDim.x) {
         u32 so;
         const u64* g = vec_src(v, so);
         cp_async16(tile + stage * tw + so, g + (u64)c * ct_words);
@@ -321,7 +332,7 @@ __global__ void __launch_bounds__(MAXT, MINB)
   auto combine = [&](double h, double l) {  // h * 2^44 + l  (mod q)
     return add_mod(mul_mod(dmodq(h, q, P), w44, P), dmodq(l, q, P), q);
   };
-  u64* ob = tern + (u64)sk.y * 3 * m * N + (u64)r * N + a0;
+  u64* ob = tern + (u64)sk.y * 3 * m * N + (u64)r * N + a0 + sub * TE;
 #pragma unroll
   for (int t = 0; t < TE; ++t) {
     u64* o = ob + t;
